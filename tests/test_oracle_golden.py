@@ -1,0 +1,38 @@
+"""Pin the CPU oracle against the reference's recorded outputs (CPU only)."""
+
+import pytest
+
+from golden_io import OPTION_SETS, modules, outcome, same
+from oracle import core, disasm, validate
+
+CASES = modules()
+
+
+@pytest.mark.parametrize("rec", CASES, ids=[r["name"] for r in CASES])
+def test_oracle_decode(rec):
+    def run():
+        h, insts = core.decode_module(rec["bytes"])
+        return [list(h), [[op, len(w)] for op, w in insts]]
+    assert same(outcome(run), rec["decode"])
+
+
+@pytest.mark.parametrize("rec", CASES, ids=[r["name"] for r in CASES])
+def test_oracle_disasm(rec):
+    for key, opts in OPTION_SETS.items():
+        got = outcome(lambda: disasm.disassemble(rec["bytes"], disasm.Options(**opts)))
+        assert same(got, rec["disasm"][key]), key
+    got = outcome(lambda: disasm.disassemble(rec["bytes"], strict=True))
+    assert same(got, rec["disasm_strict"])
+
+
+@pytest.mark.parametrize("rec", CASES, ids=[r["name"] for r in CASES])
+def test_oracle_fixpoint_equals_closed_form(rec):
+    a = outcome(lambda: disasm.disassemble(rec["bytes"], closed_form=False))
+    b = outcome(lambda: disasm.disassemble(rec["bytes"], closed_form=True))
+    assert a == b
+
+
+@pytest.mark.parametrize("rec", CASES, ids=[r["name"] for r in CASES])
+def test_oracle_validate(rec):
+    got = outcome(lambda: [list(d) for d in validate.validate(rec["bytes"])])
+    assert same(got, rec["validate"])
