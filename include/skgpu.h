@@ -1,0 +1,115 @@
+/* libskgpu -- B200 (sm_100a) batch SPIR-V codec: the C-ABI drop-in boundary.
+ *
+ * The reference (spirvkit 0.1.0) is pure Python and has no FFI layer; its hot
+ * path is the Python API listed in SURVEY.md 8(b).  Each entry point below
+ * replaces the loop body of one of those functions for a whole batch of
+ * modules at once; paper_2305_09493_b200/_native.py binds them with ctypes and
+ * keeps the reference's Python signatures on top.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors),
+ *    stream-ordered on `stream` (a cudaStream_t, or NULL for the legacy
+ *    stream).  Nothing is synchronised inside the library.
+ *  - A batch is a byte arena `data` with per-module byte offset/length arrays
+ *    (int64).  Module starts SHOULD be 16-byte aligned (vectorised loads);
+ *    unaligned starts are accepted and loaded bytewise.
+ *  - Content errors (what the reference raises or reports) never fail a call:
+ *    they become per-module status codes (SKG_ST_*) plus an error record with
+ *    the exact str(exc) text.  Return values report API misuse / CUDA errors.
+ *  - Thread-safe for distinct workspaces; tables are immutable after create.
+ */
+#ifndef SKGPU_H
+#define SKGPU_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* per-module status = exception class the reference raises/reports */
+enum {
+  SKG_ST_OK = 0,
+  SKG_ST_TRUNCATED = 1,    /* TruncatedStreamError */
+  SKG_ST_NOTSPIRV = 2,     /* NotSpirvError */
+  SKG_ST_CORRUPT = 3,      /* CorruptStreamError */
+  SKG_ST_CODEC = 4,        /* CodecError */
+  SKG_ST_UNICODE = 5,      /* UnicodeDecodeError */
+  SKG_ST_KEY = 6,          /* KeyError */
+  SKG_ST_VALUE = 7,        /* ValueError */
+  SKG_ST_INTERNAL = 99     /* scratch/capacity problem: rerun with more workspace */
+};
+
+/* disassembler option bits (DisassemblerOptions, disasm.py:46-54; strict :103) */
+enum {
+  SKG_OPT_HIGHLIGHT = 1, SKG_OPT_INLINE_NAMES = 2, SKG_OPT_NO_INDENT = 4,
+  SKG_OPT_GROUP = 8, SKG_OPT_NO_HEADER = 16, SKG_OPT_STRICT = 32
+};
+
+/* one error record (256 bytes): module index, status, detail words, message */
+typedef struct skg_error {
+  int32_t module;
+  int32_t status;
+  uint32_t a, b, c, d;   /* UnicodeDecodeError: start, end, reason(1 start,2 cont,3 end), byte */
+  int32_t len;           /* message length (may exceed the stored 227 bytes) */
+  char msg[228];
+} skg_error;
+
+typedef struct skg_tables skg_tables;
+
+/* Upload a grammar table blob (paper_2305_09493_b200/tables.py) to the device.
+ * Replaces: grammar.load_pinned()/load_pinned_extended() lookups
+ * (reference grammar.py:97-154) as seen by ops.py / disasm.py / validate.py. */
+int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** out);
+void skg_tables_destroy(skg_tables* t);
+
+/* Device workspace (bytes) for a batch of n_mod modules whose largest module
+ * has max_words words.  Includes look-back state, counters and the per-warp
+ * overflow scratch of the persistent grid. */
+uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words);
+
+/* Batch disassembly.
+ * Replaces: Disassembler.to_text / disassemble_module(data, options, strict=...)
+ * (reference disasm.py:117-127, 392-398) for every module of the batch.
+ * Output: text arena `text` (capacity text_cap bytes); module m's text is
+ * text[text_off[m] : text_off[m+1]] (text_off has n_mod+1 entries).
+ * status[m] = SKG_ST_*; errors[] gets one record per failing module (up to
+ * err_cap; counters: see skg_last_counts).  If the arena is too small nothing
+ * past the capacity is written and *the required size* is text_off[n_mod]. */
+int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+               const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+               uint8_t* text, uint64_t text_cap, int64_t* text_off, int32_t* status,
+               skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
+               void* stream);
+
+/* Batch structural + capability validation.
+ * Replaces: validate_module(bytes) (reference validate.py:73-94).
+ * Output: diagnostics_text-formatted lines ("severity code location message\n")
+ * per module in the `text` arena (same offset convention as skg_disasm);
+ * non-codec exceptions that escape the reference validator are reported
+ * through status/errors exactly like skg_disasm. */
+int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                 const int64_t* mod_len, uint32_t n_mod, uint32_t max_words, uint8_t* text,
+                 uint64_t text_cap, int64_t* text_off, int32_t* status, skg_error* errors,
+                 uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* Instruction-boundary pass only (header + per-instruction offsets).
+ * Replaces: codec.decode_module (reference codec.py:199-231).
+ * inst_off receives, for module m, the word offsets of its instructions at
+ * inst_off[inst_base[m] ...]; inst_base (n_mod+1) is computed by the caller as
+ * an exclusive bound (the library writes inst_count[m]).  header: 5 words per
+ * module (byte-order normalised). */
+int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_len, uint32_t n_mod,
+               uint32_t* header, uint32_t* inst_off, const int64_t* inst_base, uint32_t* inst_count,
+               uint32_t* words_out, const int64_t* words_base, int32_t* status, skg_error* errors,
+               uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* Counters of the last call on `workspace` (device->host copy, synchronous on
+ * `stream`): number of error records wanted, and 1 if the text arena overflowed. */
+int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow, void* stream);
+
+/* Version / build info string. */
+const char* skg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

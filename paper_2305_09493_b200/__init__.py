@@ -1,0 +1,17 @@
+"""B200-native SPIR-V codec path (disassemble / validate / decode) behind the
+``spirvkit`` (arXiv 2305.09493 reference) API.  See DESIGN.md."""
+
+from .codec import ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module
+from .disasm import Disassembler, DisassemblerOptions, disassemble_batch, disassemble_module
+from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,
+                     GenerationError, GrammarError, GrammarParseError, GrammarSchemaError,
+                     IdExhaustedError, NotFoundError, NotSpirvError, ScopeError,
+                     SerializationError, SpirvKitError, SsaError, StructureError,
+                     TruncatedStreamError)
+from .grammar import (EnumerantDef, ExtInstGrammar, GrammarSpec, InstructionDef, OperandKindDef,
+                      OperandSlot, load_core_grammar, load_extended_grammar, load_pinned,
+                      load_pinned_extended, transitive_capabilities)
+from .validate import (Diagnostic, check_capability_closure, diagnostics_text, validate_batch,
+                       validate_module)
+
+__version__ = "0.1.0"

@@ -1,0 +1,278 @@
+"""ctypes binding of libskgpu.so (include/skgpu.h) + device buffer plumbing.
+
+PyTorch is used only to own device memory and streams.  There is no CPU
+fallback: if the library or a CUDA device is missing, every codec entry point
+raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+from pathlib import Path
+
+import numpy as np
+
+from . import errors as _err
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("SKGPU_LIB", _HERE / "libskgpu.so"))
+
+ST_OK, ST_TRUNCATED, ST_NOTSPIRV, ST_CORRUPT, ST_CODEC = 0, 1, 2, 3, 4
+ST_UNICODE, ST_KEY, ST_VALUE, ST_INTERNAL = 5, 6, 7, 99
+
+OPT_HIGHLIGHT, OPT_INLINE, OPT_NO_INDENT, OPT_GROUP, OPT_NO_HEADER, OPT_STRICT = 1, 2, 4, 8, 16, 32
+
+ERR_DTYPE = np.dtype([("module", "<i4"), ("status", "<i4"), ("a", "<u4"), ("b", "<u4"),
+                      ("c", "<u4"), ("d", "<u4"), ("len", "<i4"), ("msg", "S228")])
+assert ERR_DTYPE.itemsize == 256
+
+_UTF8_REASON = {1: "invalid start byte", 2: "invalid continuation byte", 3: "unexpected end of data"}
+
+
+class NativeUnavailable(RuntimeError):
+    """libskgpu.so could not be loaded or no CUDA device is present."""
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.is_file():
+        raise NativeUnavailable(f"{LIB_PATH} is missing: run __graft_entry__.build()")
+    L = ctypes.CDLL(str(LIB_PATH))
+    P, U32, U64, I32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+    L.skg_tables_create.argtypes = [P, U64, ctypes.POINTER(P)]
+    L.skg_tables_destroy.argtypes = [P]
+    L.skg_workspace_bytes.argtypes = [U32, U32]
+    L.skg_workspace_bytes.restype = U64
+    L.skg_disasm.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P]
+    L.skg_validate.argtypes = [P, P, P, P, U32, U32, P, U64, P, P, P, U32, P, U64, P]
+    L.skg_decode.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, U32, P, U64, P]
+    L.skg_last_counts.argtypes = [P, ctypes.POINTER(U32), ctypes.POINTER(U32), P]
+    L.skg_version.restype = ctypes.c_char_p
+    for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts):
+        f.restype = I32
+    _lib = L
+    return L
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the codec path runs on the GPU only")
+    return torch
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"libskgpu {what} failed with code {rc}")
+
+
+# -- grammar tables --------------------------------------------------------------
+_tables = {}
+
+
+def tables_handle(spec, ext):
+    """Device table handle for (spec, ext); packed + uploaded once per pair."""
+    from . import grammar, tables
+    spec = spec if spec is not None else grammar.load_pinned()
+    ext = ext if ext is not None else grammar.load_pinned_extended()
+    key = (id(spec), id(ext))
+    hit = _tables.get(key)
+    if hit is not None and hit[1] is spec and hit[2] is ext:
+        return hit[0]
+    _torch()
+    packed = tables.pack(spec, ext)
+    blob = np.ascontiguousarray(packed.blob, dtype=np.uint32)
+    handle = ctypes.c_void_p()
+    _check(lib().skg_tables_create(blob.ctypes.data, blob.size, ctypes.byref(handle)), "tables_create")
+    _tables[key] = (handle, spec, ext)
+    return handle
+
+
+# -- device batches ----------------------------------------------------------------
+class DeviceBatch:
+    """Modules resident in device memory: byte arena + int64 offsets/lengths."""
+
+    def __init__(self, data, off, length, max_words, total_bytes):
+        self.data, self.off, self.len = data, off, length
+        self.n = int(off.numel())
+        self.max_words = int(max_words)
+        self.total_bytes = int(total_bytes)
+
+    @classmethod
+    def from_host(cls, data: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, stream=None):
+        torch = _torch()
+        dev = torch.device("cuda")
+        d = torch.from_numpy(np.ascontiguousarray(data, dtype=np.uint8)).to(dev, non_blocking=False)
+        o = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
+        ln = torch.from_numpy(np.ascontiguousarray(lengths, dtype=np.int64)).to(dev)
+        mw = int(lengths.max()) // 4 if len(lengths) else 0
+        return cls(d, o, ln, mw, int(lengths.sum()))
+
+    @classmethod
+    def from_modules(cls, modules):
+        lengths = np.array([len(m) for m in modules], dtype=np.int64)
+        padded = (lengths + 15) // 16 * 16
+        offsets = np.zeros(len(modules), dtype=np.int64)
+        if len(modules) > 1:
+            offsets[1:] = np.cumsum(padded)[:-1]
+        buf = bytearray(int(padded.sum()) + 16)
+        for m, o in zip(modules, offsets):
+            buf[o:o + len(m)] = m
+        return cls.from_host(np.frombuffer(bytes(buf), dtype=np.uint8), offsets, lengths)
+
+
+class _Workspace:
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes):
+        torch = _torch()
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+        return self.buf
+
+
+_ws = _Workspace()
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class TextResult:
+    """Device-resident output of a batch call."""
+
+    def __init__(self, text, off, status, errors):
+        self.text, self.off, self.status, self.errors = text, off, status, errors
+
+
+def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, err_cap=None):
+    torch = _torch()
+    L = lib()
+    th = tables_handle(spec, ext)
+    n = batch.n
+    ws_bytes = int(L.skg_workspace_bytes(n, max(batch.max_words, 1)))
+    ws = _ws.get(ws_bytes)
+    cap = text_cap if text_cap is not None else 6 * batch.total_bytes + 4096
+    ecap = err_cap if err_cap is not None else max(16, min(n, 1 << 16))
+    for _ in range(3):
+        text = torch.empty(max(cap, 16), dtype=torch.uint8, device="cuda")
+        off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        errs = torch.empty(ecap * 256, dtype=torch.uint8, device="cuda")
+        if kind == "disasm":
+            rc = L.skg_disasm(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
+                              opts, batch.max_words, text.data_ptr(), cap, off.data_ptr(),
+                              status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes, _stream())
+        else:
+            rc = L.skg_validate(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
+                                batch.max_words, text.data_ptr(), cap, off.data_ptr(),
+                                status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes,
+                                _stream())
+        _check(rc, kind)
+        nerr, over = ctypes.c_uint32(), ctypes.c_uint32()
+        _check(L.skg_last_counts(ws.data_ptr(), ctypes.byref(nerr), ctypes.byref(over), _stream()), "counts")
+        if n == 0:
+            off.zero_()
+        need = int(off[n].item()) if n else 0
+        if over.value or nerr.value > ecap:
+            cap = max(cap, need + 16)
+            ecap = max(ecap, int(nerr.value))
+            continue
+        return TextResult(text[:need], off, status[:n], errs[: nerr.value * 256])
+    raise RuntimeError(f"libskgpu {kind}: output capacity retry failed")
+
+
+def run_disasm(batch, opts, spec=None, ext=None, **kw):
+    return _run_text_kernel("disasm", batch, opts, spec, ext, **kw)
+
+
+def run_validate(batch, spec=None, **kw):
+    return _run_text_kernel("validate", batch, 0, spec, None, **kw)
+
+
+def decode_errors(err_bytes: np.ndarray):
+    """module index -> exception instance, from the device error records."""
+    recs = np.frombuffer(err_bytes.tobytes(), dtype=ERR_DTYPE)
+    out = {}
+    for r in recs:
+        msg = bytes(r["msg"])[: max(0, min(int(r["len"]), 227))].decode("utf-8", "replace")
+        out[int(r["module"])] = make_exception(int(r["status"]), msg, int(r["a"]), int(r["b"]),
+                                               int(r["c"]), int(r["d"]))
+    return out
+
+
+def make_exception(status, msg, a=0, b=0, c=0, d=0):
+    if status == ST_TRUNCATED:
+        return _err.TruncatedStreamError(msg)
+    if status == ST_NOTSPIRV:
+        return _err.NotSpirvError(msg)
+    if status == ST_CORRUPT:
+        return _err.CorruptStreamError(msg)
+    if status == ST_CODEC:
+        return _err.CodecError(msg)
+    if status == ST_UNICODE:
+        obj = bytes(a) + bytes([d]) + bytes(max(0, b - a - 1))
+        return UnicodeDecodeError("utf-8", obj, a, b, _UTF8_REASON.get(c, "invalid start byte"))
+    if status == ST_KEY:
+        return KeyError(int(msg))
+    if status == ST_VALUE:
+        return ValueError(msg)
+    return RuntimeError(f"libskgpu internal error: {msg}")
+
+
+def fetch_texts(res: TextResult, n: int):
+    """Host copies: list of (text bytes | exception) per module."""
+    off = res.off.cpu().numpy()
+    status = res.status.cpu().numpy()
+    text = res.text.cpu().numpy().tobytes()
+    errs = decode_errors(res.errors.cpu().numpy()) if res.errors.numel() else {}
+    out = []
+    for m in range(n):
+        if status[m] != ST_OK:
+            out.append(errs.get(m) or make_exception(int(status[m]), "error record dropped"))
+        else:
+            out.append(text[off[m]:off[m + 1]])
+    return out
+
+
+def run_decode(data: bytes):
+    """Single-module boundary pass -> (header tuple, words array, [(start, wc)]) or raises."""
+    torch = _torch()
+    L = lib()
+    n = len(data)
+    W = n // 4
+    dev = torch.device("cuda")
+    pad = bytes(data) + b"\x00" * (-n % 16 + 16)
+    d = torch.frombuffer(bytearray(pad), dtype=torch.uint8).to(dev)
+    meta = torch.tensor([0, n, 0], dtype=torch.int64, device=dev)   # off, len, base
+    header = torch.zeros(5, dtype=torch.int32, device=dev)
+    inst_off = torch.zeros(max(W, 1), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    words = torch.zeros(max(W, 1), dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    errs = torch.zeros(256, dtype=torch.uint8, device=dev)
+    ws = _ws.get(1 << 20)
+    p = meta.data_ptr()
+    _check(L.skg_decode(d.data_ptr(), p, p + 8, 1, header.data_ptr(), inst_off.data_ptr(), p + 16,
+                        cnt.data_ptr(), words.data_ptr(), p + 16, status.data_ptr(), errs.data_ptr(), 1,
+                        ws.data_ptr(), 1 << 20, _stream()), "decode")
+    st = int(status.item())
+    if st != ST_OK:
+        raise decode_errors(errs.cpu().numpy())[0]
+    h = header.cpu().numpy().view(np.uint32)
+    k = int(cnt.item())
+    return tuple(int(x) for x in h), words.cpu().numpy().view(np.uint32)[:W], \
+        inst_off.cpu().numpy().view(np.uint32)[:k]
+
+
+__all__ = ["lib", "DeviceBatch", "run_disasm", "run_validate", "run_decode", "fetch_texts",
+           "make_exception", "NativeUnavailable", "tables_handle", "struct"]

@@ -1,0 +1,219 @@
+// C-ABI entry points of libskgpu (include/skgpu.h).
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include "../../include/skgpu.h"
+#include "skg_module.cuh"
+
+namespace skg {
+struct DisasmArgs;
+struct ValidateArgs;
+struct DecodeArgs;
+}
+
+#include "skg_disasm.cu"
+#include "skg_validate.cu"
+#include "skg_decode.cu"
+
+struct skg_tables {
+  skg::Tables t;
+  uint32_t* d_blob;
+};
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr uint32_t kSlabBytes = 24 * 1024;
+
+int g_sms = 0;
+
+int sm_count() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+uint32_t grid_blocks() {
+  // persistent grid: 2 blocks of 4 warps per SM (24 KB shared slab per warp)
+  return (uint32_t)sm_count() * 2;
+}
+
+uint64_t slot_bytes(uint32_t max_words) {
+  return (skg::worst_bytes(max_words) + 255) & ~(uint64_t)255;
+}
+
+struct WsLayout {
+  uint64_t state, counters, scratch, total, slot;
+  uint32_t n_warps;
+};
+
+WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
+  WsLayout l;
+  l.n_warps = grid_blocks() * kWarpsPerBlock;
+  l.slot = slot_bytes(max_words);
+  l.counters = 0;
+  l.state = 256;
+  l.scratch = (l.state + 8ull * (n_mod + 1) + 255) & ~255ull;
+  l.total = l.scratch + l.slot * l.n_warps;
+  return l;
+}
+
+int check(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "skgpu: CUDA error %s\n", cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skg_version(void) { return "skgpu 0.1 (sm_100a)"; }
+
+int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** out) {
+  if (!host_blob || n_words < 64 || !out) return -1;
+  if (host_blob[0] != 0x54474B53u) return -2;
+  skg_tables* t = new skg_tables();
+  if (int e = check(cudaMalloc(&t->d_blob, n_words * 4))) { delete t; return e; }
+  if (int e = check(cudaMemcpy(t->d_blob, host_blob, n_words * 4, cudaMemcpyHostToDevice))) {
+    cudaFree(t->d_blob); delete t; return e;
+  }
+  const uint32_t* h = host_blob;
+  skg::Tables& T = t->t;
+  const uint32_t* b = t->d_blob;
+  T.blob = b;
+  T.n_inst = h[2]; T.inst = b + h[3];
+  T.max_opcode = h[4]; T.opidx = reinterpret_cast<const uint16_t*>(b + h[5]);
+  T.n_kind = h[6]; T.kind = b + h[7];
+  T.n_enum = h[8]; T.enm = b + h[9];
+  T.n_slot = h[10]; T.slot = b + h[11];
+  T.str = reinterpret_cast<const uint8_t*>(b + h[12]); T.str_bytes = h[13];
+  T.n_req = h[14]; T.req = b + h[15];
+  T.n_cap = h[16]; T.cap_words = h[17];
+  T.closure = reinterpret_cast<const uint64_t*>(b + h[18]);
+  T.vsort = b + h[19]; T.n_vsort = h[20];
+  T.ext_max = (int32_t)h[21]; T.ext = b + h[22];
+  T.idref = h[23];
+  for (int j = 0; j < 5; ++j) T.width_req[j] = h[24 + j];
+  T.linkage = h[29];
+  T.ocl_off = h[30]; T.ocl_len = h[31];
+  T.req_stride = h[32];
+  T.cap_kind = h[33];
+  *out = t;
+  return 0;
+}
+
+void skg_tables_destroy(skg_tables* t) {
+  if (!t) return;
+  cudaFree(t->d_blob);
+  delete t;
+}
+
+uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words) {
+  return ws_layout(n_mod, max_words).total;
+}
+
+int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow, void* stream) {
+  uint32_t c[4];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int e = check(cudaMemcpyAsync(c, workspace, 16, cudaMemcpyDeviceToHost, s))) return e;
+  if (int e = check(cudaStreamSynchronize(s))) return e;
+  if (n_errors) *n_errors = c[1];
+  if (text_overflow) *text_overflow = c[2];
+  return 0;
+}
+
+int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+               const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+               uint8_t* text, uint64_t text_cap, int64_t* text_off, int32_t* status,
+               skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
+               void* stream) {
+  if (!t || !workspace) return -1;
+  WsLayout l = ws_layout(n_mod, max_words);
+  if (workspace_bytes < l.total) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  if (int e = check(cudaMemsetAsync(ws, 0, l.scratch, s))) return e;
+  if (n_mod == 0) return 0;
+  skg::DisasmArgs a;
+  a.T = t->t;
+  a.data = data; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod; a.opts = opts;
+  a.text = text; a.text_cap = text_cap; a.text_off = text_off; a.status = status;
+  a.state = reinterpret_cast<unsigned long long*>(ws + l.state);
+  a.ticket = reinterpret_cast<uint32_t*>(ws + l.counters);
+  a.errs = reinterpret_cast<skg::ErrRec*>(errors);
+  a.err_cap = err_cap;
+  a.gscratch = ws + l.scratch;
+  a.gslot_bytes = l.slot;
+  a.smem_slab = kSlabBytes;
+  const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  skg::disasm_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, smem, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                 const int64_t* mod_len, uint32_t n_mod, uint32_t max_words, uint8_t* text,
+                 uint64_t text_cap, int64_t* text_off, int32_t* status, skg_error* errors,
+                 uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (!t || !workspace) return -1;
+  WsLayout l = ws_layout(n_mod, max_words);
+  if (workspace_bytes < l.total) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  if (int e = check(cudaMemsetAsync(ws, 0, l.scratch, s))) return e;
+  if (n_mod == 0) return 0;
+  skg::ValidateArgs a;
+  a.T = t->t;
+  a.data = data; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod;
+  a.text = text; a.text_cap = text_cap; a.text_off = text_off; a.status = status;
+  a.state = reinterpret_cast<unsigned long long*>(ws + l.state);
+  a.ticket = reinterpret_cast<uint32_t*>(ws + l.counters);
+  a.errs = reinterpret_cast<skg::ErrRec*>(errors);
+  a.err_cap = err_cap;
+  a.gscratch = ws + l.scratch;
+  a.gslot_bytes = l.slot;
+  a.smem_slab = kSlabBytes;
+  const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(skg::validate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  skg::validate_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, smem, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_len, uint32_t n_mod,
+               uint32_t* header, uint32_t* inst_off, const int64_t* inst_base, uint32_t* inst_count,
+               uint32_t* words_out, const int64_t* words_base, int32_t* status, skg_error* errors,
+               uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (!workspace) return -1;
+  if (workspace_bytes < 256) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int e = check(cudaMemsetAsync(workspace, 0, 256, s))) return e;
+  if (n_mod == 0) return 0;
+  skg::DecodeArgs a;
+  a.data = data; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod;
+  a.header = header; a.inst_off = inst_off; a.inst_base = inst_base; a.inst_count = inst_count;
+  a.words_out = words_out; a.words_base = words_base; a.status = status;
+  a.counters = reinterpret_cast<uint32_t*>(workspace);
+  a.errs = reinterpret_cast<skg::ErrRec*>(errors);
+  a.err_cap = err_cap;
+  const uint32_t threads = 256;
+  uint32_t blocks = (n_mod + threads - 1) / threads;
+  skg::decode_kernel<<<blocks, threads, 0, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -1,0 +1,513 @@
+// Per-module device state shared by the disassembler and validator kernels.
+//
+// One warp owns one module at a time.  Its scratch (words, instruction table,
+// id hash table, ...) lives in a shared-memory slab when it fits and in a
+// per-warp global-memory slot otherwise.  Phases (all warp-synchronous):
+//   load      : 16-byte loads of the module bytes, byte-swap if big-endian
+//               (codec.py:199-216)
+//   boundary  : instruction-boundary walk with the exact wc==0 / overrun
+//               errors (codec.py:217-230)
+//   prescan   : per-instruction grammar lookup + the per-id maps the reference
+//               keeps in dicts -- type_info / value_type (last wins), first
+//               OpName, last OpExtInstImport, first definition (disasm.py:131-157,
+//               208-219; validate.py:179-192).  "First/last wins" is resolved by
+//               processing instructions in lane-strided chunks in document order
+//               and letting the lowest/highest lane of each equal-key group write.
+#pragma once
+#include "skg_walk.cuh"
+
+namespace skg {
+
+constexpr uint32_t MAGIC = 0x07230203u;
+constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// exception classes reported per module (python: _native.STATUS)
+enum : int32_t {
+  ST_OK = 0, ST_TRUNCATED = 1, ST_NOTSPIRV = 2, ST_CORRUPT = 3, ST_CODEC = 4, ST_UNICODE = 5,
+  ST_KEY = 6, ST_VALUE = 7, ST_OVERFLOW = 8, ST_ASSEMBLY = 9, ST_STRUCTURE = 10,
+  ST_SERIALIZATION = 11, ST_SCOPE = 12, ST_NOTFOUND = 13, ST_INTERNAL = 99
+};
+
+struct ErrRec {            // 256 bytes
+  int32_t module;
+  int32_t cls;
+  uint32_t a, b, c, d;     // UnicodeDecodeError: start, end, reason, byte; KeyError: key
+  int32_t len;
+  char msg[228];
+};
+
+// iflag bits
+enum : uint8_t { IF_PRESCAN_UTF8 = 1, IF_HAS_RESULT = 2, IF_EXT_KNOWN = 4, IF_FIRSTDEF = 8 };
+// hfl bits
+enum : uint8_t { HF_NAMED_D = 1, HF_P0 = 2, HF_KEPT = 4, HF_FRIENDLY = 8 };
+
+struct Mod {
+  uint8_t* base;          // scratch base (header)
+  uint32_t* w;            // words (normalised to little-endian values)
+  uint32_t W;
+  uint32_t* ioff;         // instruction start word offsets, I entries
+  uint32_t I;
+  uint16_t* idef;
+  uint8_t* iflag;
+  uint8_t* ierr;
+  uint8_t* isec;
+  uint32_t* ia;
+  uint32_t* ib;
+  uint32_t* irl;
+  uint32_t* nrec;         // 6 words per named definition
+  int32_t* pos;           // closed-form demotion array / taken set
+  uint32_t npos;
+  uint32_t* hkey;
+  uint32_t* hdef;
+  uint32_t* hti;
+  uint32_t* hvt;
+  uint32_t* hname;
+  uint32_t* himp;
+  uint32_t* hser;
+  uint32_t* hrl;
+  uint8_t* hA;
+  uint8_t* hfl;
+  uint32_t C, shift;
+  uint32_t* fill;         // in the scratch header
+  uint32_t* overflow;
+  uint32_t* top_present;  // entry for key 0xFFFFFFFF lives in the dedicated slot C
+  uint32_t major, minor, gen, bound, schema;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// bytes needed before the per-module tables: header + words + instruction offsets
+__host__ __device__ inline size_t head_bytes(uint32_t W) {
+  return 64 + align16(4ull * W) + align16(4ull * (W > 5 ? W - 5 : 1) + 4);
+}
+
+__host__ __device__ inline uint32_t table_capacity(uint32_t I) {
+  uint32_t need = I + I / 2 + 8;
+  uint32_t c = 64;
+  while (c < need) c <<= 1;
+  return c;
+}
+
+__host__ __device__ inline size_t tables_bytes(uint32_t I, uint32_t C) {
+  size_t n = 0;
+  n += align16(2ull * I) + 3 * align16(1ull * I) + 3 * align16(4ull * I);   // idef, iflag/ierr/isec, ia/ib/irl
+  n += align16(24ull * I);                                                  // nrec
+  uint32_t npos = C + I + 2 > 8 * I + 8 ? C + I + 2 : 8 * I + 8;
+  n += align16(4ull * npos);
+  n += 8 * align16(4ull * (C + 1)) + 2 * align16(C + 1);
+  return n;
+}
+
+// worst-case scratch for a module of W words (I <= W-5, table sized for W ids)
+__host__ __device__ inline size_t worst_bytes(uint32_t W) {
+  uint32_t I = W > 5 ? W - 5 : 0;
+  uint32_t C = 64;
+  while (C < 2 * W + 8) C <<= 1;
+  return head_bytes(W) + tables_bytes(I, C);
+}
+
+__device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
+  m.base = base;
+  m.fill = reinterpret_cast<uint32_t*>(base);
+  m.overflow = m.fill + 1;
+  m.top_present = m.fill + 2;
+  m.w = reinterpret_cast<uint32_t*>(base + 64);
+  m.W = W;
+  m.ioff = reinterpret_cast<uint32_t*>(base + 64 + align16(4ull * W));
+}
+
+__device__ inline void layout_tables(Mod& m, uint32_t C) {
+  uint8_t* p = m.base + head_bytes(m.W);
+  const uint32_t I = m.I;
+  auto take = [&](size_t bytes) { uint8_t* r = p; p += align16(bytes); return r; };
+  m.idef = reinterpret_cast<uint16_t*>(take(2ull * I));
+  m.iflag = take(I);
+  m.ierr = take(I);
+  m.isec = take(I);
+  m.ia = reinterpret_cast<uint32_t*>(take(4ull * I));
+  m.ib = reinterpret_cast<uint32_t*>(take(4ull * I));
+  m.irl = reinterpret_cast<uint32_t*>(take(4ull * I));
+  m.nrec = reinterpret_cast<uint32_t*>(take(24ull * I));
+  m.npos = C + I + 2 > 8 * I + 8 ? C + I + 2 : 8 * I + 8;
+  m.pos = reinterpret_cast<int32_t*>(take(4ull * m.npos));
+  m.hkey = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hdef = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hti = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hvt = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hname = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.himp = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hser = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hrl = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
+  m.hA = take(C + 1);
+  m.hfl = take(C + 1);
+  m.C = C;
+  uint32_t lg = 0;
+  while ((1u << lg) < C) ++lg;
+  m.shift = 32 - lg;
+}
+
+// -- warp helpers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t warp_incl_sum(uint32_t v) {
+  const uint32_t l = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(FULL, v, d);
+    if (l >= (uint32_t)d) v += t;
+  }
+  return v;
+}
+
+__device__ __forceinline__ int32_t warp_incl_max(int32_t v) {
+  const uint32_t l = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int32_t t = __shfl_up_sync(FULL, v, d);
+    if (l >= (uint32_t)d) v = max(v, t);
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(FULL, v, d));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// -- id hash table --------------------------------------------------------------
+__device__ __forceinline__ uint32_t ht_home(const Mod& m, uint32_t key) {
+  return (key * 0x9E3779B1u) >> m.shift;
+}
+
+__device__ inline uint32_t ht_find(const Mod& m, uint32_t key) {
+  if (key == EMPTY) return *m.top_present ? m.C : NONE32;   // dedicated slot for 0xFFFFFFFF
+  uint32_t s = ht_home(m, key);
+  for (uint32_t probe = 0; probe < m.C; ++probe) {
+    uint32_t k = m.hkey[s];
+    if (k == key) return s;
+    if (k == EMPTY) return NONE32;
+    s = (s + 1) & (m.C - 1);
+  }
+  return NONE32;
+}
+
+__device__ inline uint32_t ht_insert(const Mod& m, uint32_t key) {
+  if (key == EMPTY) {
+    *m.top_present = 1;
+    return m.C;
+  }
+  uint32_t s = ht_home(m, key);
+  for (uint32_t probe = 0; probe < m.C; ++probe) {
+    uint32_t k = m.hkey[s];
+    if (k == key) return s;
+    if (k == EMPTY) {
+      uint32_t old = atomicCAS(&m.hkey[s], EMPTY, key);
+      if (old == EMPTY) {
+        uint32_t f = atomicAdd(m.fill, 1u) + 1;
+        if (f * 4 > m.C * 3) *m.overflow = 1;
+        return s;
+      }
+      if (old == key) return s;
+    }
+    s = (s + 1) & (m.C - 1);
+  }
+  *m.overflow = 1;
+  return NONE32;
+}
+
+// -- instruction accessors ------------------------------------------------------
+__device__ __forceinline__ uint32_t inst_start(const Mod& m, uint32_t i) { return m.ioff[i]; }
+__device__ __forceinline__ uint32_t inst_nops(const Mod& m, uint32_t i) { return (m.w[m.ioff[i]] >> 16) - 1; }
+__device__ __forceinline__ uint32_t inst_opcode(const Mod& m, uint32_t i) { return m.w[m.ioff[i]] & 0xFFFF; }
+__device__ __forceinline__ const uint32_t* inst_ops(const Mod& m, uint32_t i) { return m.w + m.ioff[i] + 1; }
+
+// -- resolver (RenderContext.literal_resolver / validate._make_resolver) ---------
+struct Resolver {
+  const Mod* m;
+  const Tables* T;
+  __device__ Width rt(uint32_t id) const {
+    uint32_t s = ht_find(*m, id);
+    if (s == NONE32 || m->hti[s] == NONE32) return Width{0, false, false, false};
+    uint32_t j = m->hti[s];
+    const uint32_t* ops = inst_ops(*m, j);
+    uint32_t d = m->idef[j];
+    if (T->special(d) == SP_TYPEINT) return Width{ops[1], ops[2] == 1, false, true};
+    return Width{ops[1], false, true, true};
+  }
+  __device__ Width sel(uint32_t selector) const {
+    uint32_t s = ht_find(*m, selector);
+    if (s == NONE32 || m->hvt[s] == NONE32) return Width{0, false, false, false};
+    return rt(inst_ops(*m, m->hvt[s])[0]);
+  }
+};
+
+// -- error records --------------------------------------------------------------
+struct ErrWriter {
+  ErrRec* rec;
+  int32_t n = 0;
+  __device__ void put(uint8_t c) { if (n < (int32_t)sizeof(rec->msg) - 1) rec->msg[n] = (char)c; ++n; }
+  __device__ void putn(const uint8_t* s, uint32_t len) { for (uint32_t i = 0; i < len; ++i) put(s[i]); }
+  __device__ void fill(uint8_t c, uint32_t k) { for (uint32_t i = 0; i < k; ++i) put(c); }
+};
+
+// Batch-wide outputs common to all kernels
+struct ErrSink {
+  ErrRec* recs;
+  uint32_t* count;
+  uint32_t cap;
+  __device__ ErrRec* alloc() {
+    uint32_t k = atomicAdd(count, 1u);
+    return k < cap ? recs + k : nullptr;
+  }
+};
+
+// Compose the str(exc) text of a walk error (ops.py:351-374, codec.py:127-129,
+// ops.py:420-422, CPython UnicodeDecodeError.__str__).
+template <class S>
+__device__ inline void put_walk_error(S& s, const Tables& T, uint32_t idef, const WalkErr& e) {
+  auto opname = [&]() { s.putn(T.str + T.iname_off(idef), T.iname_len(idef)); };
+  switch (e.code) {
+    case W_EXHAUSTED: opname(); put_cstr(s, ": operand words exhausted mid-instruction"); break;
+    case W_LEFTOVER: opname(); put_cstr(s, ": "); put_u64(s, e.a); put_cstr(s, " leftover operand word(s)"); break;
+    case W_NONUL: put_cstr(s, "string literal is not NUL-terminated"); break;
+    case W_UNRESOLVED: opname(); put_cstr(s, ": cannot resolve the width of a context-dependent literal"); break;
+    case W_UNICODE:
+      put_cstr(s, "'utf-8' codec can't decode ");
+      if (e.b - e.a == 1) {
+        put_cstr(s, "byte 0x"); put_hex2_lower(s, e.d); put_cstr(s, " in position "); put_u64(s, e.a);
+      } else {
+        put_cstr(s, "bytes in position "); put_u64(s, e.a); s.put('-'); put_u64(s, e.b - 1);
+      }
+      put_cstr(s, e.c == U8_START ? ": invalid start byte"
+                  : e.c == U8_CONT ? ": invalid continuation byte" : ": unexpected end of data");
+      break;
+    case W_KEY: put_u64(s, e.a); break;
+    case W_VALUE: put_cstr(s, "negative shift count"); break;
+    default: break;
+  }
+}
+
+__device__ inline int32_t walk_status(uint32_t code) {
+  if (werr_is_codec(code)) return ST_CORRUPT;
+  if (code == W_UNICODE) return ST_UNICODE;
+  if (code == W_KEY) return ST_KEY;
+  return ST_VALUE;
+}
+
+
+
+// ---------------------------------------------------------------------------
+// load + boundary.  Returns ST_OK or an error class; on error fills `err`
+// (on lane 0).  Words are loaded into m.w (already laid out via layout_head).
+__device__ inline int32_t load_and_split(Mod& m, const uint8_t* src, uint64_t nbytes, ErrSink* es,
+                                         int32_t module) {
+  const uint32_t lane = lane_id();
+  ErrRec* err = nullptr;
+  if (nbytes % 4 != 0 || nbytes < 20) {
+    if (lane == 0 && es) err = es->alloc();
+    if (lane == 0 && err) {
+      ErrWriter ew{err};
+      put_u64(ew, nbytes);
+      put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
+      err->module = module; err->cls = ST_TRUNCATED; err->len = ew.n;
+    }
+    return ST_TRUNCATED;
+  }
+  const uint32_t W = (uint32_t)(nbytes / 4);
+  // 16-byte vector loads (module starts are 16-byte aligned in a batch)
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(m.w);
+    const uint32_t n4 = W / 4;
+    for (uint32_t k = lane; k < n4; k += 32) d4[k] = __ldg(s4 + k);
+    for (uint32_t k = n4 * 4 + lane; k < W; k += 32) m.w[k] = __ldg(reinterpret_cast<const uint32_t*>(src) + k);
+  } else {
+    for (uint32_t k = lane; k < W; k += 32) {
+      const uint8_t* p = src + 4ull * k;
+      m.w[k] = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+    }
+  }
+  __syncwarp();
+  const uint32_t w0 = m.w[0];
+  if (w0 != MAGIC) {
+    if (bswap32(w0) != MAGIC) {
+      if (lane == 0 && es) err = es->alloc();
+      if (lane == 0 && err) {
+        ErrWriter ew{err};
+        put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, w0); put_cstr(ew, " is not SPIR-V");
+        err->module = module; err->cls = ST_NOTSPIRV; err->len = ew.n;
+      }
+      return ST_NOTSPIRV;
+    }
+    for (uint32_t k = lane; k < W; k += 32) m.w[k] = bswap32(m.w[k]);
+    __syncwarp();
+  }
+  m.major = (m.w[1] >> 16) & 0xFF;
+  m.minor = (m.w[1] >> 8) & 0xFF;
+  m.gen = m.w[2];
+  m.bound = m.w[3];
+  m.schema = m.w[4];
+  // instruction-boundary walk (pointer chase: pos += wc)
+  int32_t st = ST_OK;
+  uint32_t I = 0, bad = 0;
+  if (lane == 0) {
+    uint32_t p = 5;
+    while (p < W) {
+      uint32_t wc = m.w[p] >> 16;
+      if (wc == 0) { st = ST_CORRUPT; bad = p; break; }
+      if (p + wc > W) { st = ST_TRUNCATED; bad = p; break; }
+      m.ioff[I++] = p;
+      p += wc;
+    }
+    if (st != ST_OK && es) err = es->alloc();
+    if (st != ST_OK && err) {
+      ErrWriter ew{err};
+      put_cstr(ew, "instruction at word "); put_u64(ew, bad);
+      put_cstr(ew, st == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
+      err->module = module; err->cls = st; err->len = ew.n;
+    }
+  }
+  st = __shfl_sync(FULL, st, 0);
+  m.I = __shfl_sync(FULL, I, 0);
+  __syncwarp();
+  return st;
+}
+
+__device__ inline void init_tables(Mod& m) {
+  const uint32_t lane = lane_id();
+  for (uint32_t s = lane; s <= m.C; s += 32) {
+    m.hkey[s] = EMPTY;
+    m.hdef[s] = NONE32; m.hti[s] = NONE32; m.hvt[s] = NONE32; m.hname[s] = NONE32;
+    m.himp[s] = NONE32; m.hser[s] = NONE32; m.hrl[s] = 0;
+    m.hA[s] = 0; m.hfl[s] = 0;
+  }
+  if (lane == 0) { *m.fill = 0; *m.overflow = 0; *m.top_present = 0; }
+  __syncwarp();
+}
+
+// last-writer / first-writer within a chunk for equal keys
+__device__ __forceinline__ bool group_last(bool part, uint32_t key) {
+  uint64_t k = part ? (uint64_t)key : (0x100000000ull + lane_id());
+  unsigned g = __match_any_sync(FULL, k);
+  return part && (31 - __clz(g)) == (int)lane_id();
+}
+__device__ __forceinline__ bool group_first(bool part, uint32_t key) {
+  uint64_t k = part ? (uint64_t)key : (0x100000000ull + lane_id());
+  unsigned g = __match_any_sync(FULL, k);
+  return part && (__ffs(g) - 1) == (int)lane_id();
+}
+
+// prescan: returns whether any OpName was recorded
+__device__ inline bool prescan(Mod& m, const Tables& T) {
+  const uint32_t lane = lane_id();
+  bool any_name = false;
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    const uint32_t i = base + lane;
+    const bool act = i < m.I;
+    uint32_t d = NONE32, n = 0, sp = SP_NONE;
+    const uint32_t* ops = nullptr;
+    if (act) {
+      ops = inst_ops(m, i);
+      n = inst_nops(m, i);
+      d = T.inst_of(inst_opcode(m, i));
+      m.idef[i] = d == NONE32 ? NONE16 : (uint16_t)d;
+      sp = d == NONE32 ? SP_NONE : T.special(d);
+      m.iflag[i] = 0;
+      m.ierr[i] = 0;
+    }
+    // type_info (last wins): OpTypeInt with exactly 3 words / OpTypeFloat >= 2
+    {
+      bool part = act && ((sp == SP_TYPEINT && n == 3) || (sp == SP_TYPEFLOAT && n >= 2));
+      uint32_t key = part ? ops[0] : 0;
+      uint32_t slot = part ? ht_insert(m, key) : NONE32;
+      if (group_last(part, key) && slot != NONE32) m.hti[slot] = i;
+    }
+    __syncwarp();
+    // value_type (last wins)
+    {
+      bool part = act && d != NONE32 && T.has_result(d) && T.has_rtype(d) && n >= 2;
+      uint32_t key = part ? ops[1] : 0;
+      uint32_t slot = part ? ht_insert(m, key) : NONE32;
+      if (group_last(part, key) && slot != NONE32) m.hvt[slot] = i;
+    }
+    __syncwarp();
+    // OpExtInstImport (last decodable wins) / OpName (first decodable wins)
+    {
+      bool part = act && (sp == SP_EXTINSTIMPORT || sp == SP_NAME) && n >= 2;
+      if (part) {
+        uint32_t nbytes, next;
+        if (!string_span(ops, 1, n, nbytes, next)) part = false;
+        else {
+          WalkErr e;
+          if (string_utf8(ops, 1, nbytes, e) != U8_OK) { part = false; m.iflag[i] |= IF_PRESCAN_UTF8; }
+        }
+      }
+      bool imp = part && sp == SP_EXTINSTIMPORT, nam = part && sp == SP_NAME;
+      uint32_t key = part ? ops[0] : 0;
+      uint32_t slot = part ? ht_insert(m, key) : NONE32;
+      if (group_last(imp, key) && slot != NONE32) m.himp[slot] = i;
+      if (group_first(nam, key) && slot != NONE32 && m.hname[slot] == NONE32) m.hname[slot] = i;
+      any_name |= nam;
+    }
+    __syncwarp();
+    // first definition (definition order D)
+    {
+      bool part = false;
+      uint32_t key = 0;
+      if (act && d != NONE32 && T.has_result(d)) {
+        uint32_t idx = T.has_rtype(d) ? 1 : 0;
+        if (idx < n) { part = true; key = ops[idx]; }
+      }
+      uint32_t slot = part ? ht_insert(m, key) : NONE32;
+      if (group_first(part, key) && slot != NONE32 && m.hdef[slot] == NONE32) m.hdef[slot] = i;
+    }
+    __syncwarp();
+  }
+  return __any_sync(FULL, any_name);
+}
+
+// decoupled look-back over module tickets: returns the exclusive prefix of `agg`
+// (state: bit 62 = aggregate ready, bit 63 = inclusive ready, low 62 bits value)
+__device__ inline uint64_t lookback(unsigned long long* state, uint32_t ticket, uint64_t agg) {
+  constexpr uint64_t FA = 1ull << 62, FP = 1ull << 63, VM = FA - 1;
+  const uint32_t lane = lane_id();
+  if (ticket == 0) {
+    if (lane == 0) atomicExch(state, FP | agg);
+    return 0;
+  }
+  if (lane == 0) atomicExch(state + ticket, FA | agg);
+  uint64_t excl = 0;
+  int64_t j = (int64_t)ticket - 1;
+  while (true) {
+    int64_t idx = j - (int64_t)lane;
+    uint64_t v = idx >= 0 ? *((volatile unsigned long long*)(state + idx)) : FP;
+    bool ready = (v & (FA | FP)) != 0;
+    bool incl = (v & FP) != 0;
+    unsigned not_ready = __ballot_sync(FULL, !ready);
+    unsigned incl_mask = __ballot_sync(FULL, incl);
+    // lanes up to (and including) the first inclusive one are usable if all ready
+    int first_incl = incl_mask ? __ffs(incl_mask) - 1 : 32;
+    unsigned usable = first_incl == 32 ? FULL : ((first_incl == 31) ? FULL : ((1u << (first_incl + 1)) - 1));
+    if (not_ready & usable) continue;   // spin until the window is ready
+    uint64_t part = (lane <= (uint32_t)first_incl && idx >= 0) ? (v & VM) : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(FULL, part, d);
+    excl += part;
+    if (first_incl < 32) break;
+    j -= 32;
+  }
+  if (lane == 0) atomicExch(state + ticket, FP | (excl + agg));
+  return excl;
+}
+
+}  // namespace skg

@@ -1,0 +1,115 @@
+// Device view of the grammar table blob built by paper_2305_09493_b200/tables.py.
+// One little-endian uint32 array; the header (64 words) holds counts and word
+// offsets of every section.  All lookups the reference performs through
+// Python dicts (grammar.py:97-127, ops.py:376-409) become array indexing here.
+#pragma once
+#include <cstdint>
+
+namespace skg {
+
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+constexpr uint16_t NONE16 = 0xFFFFu;
+
+// instruction special codes (tables.py SPECIAL)
+enum : uint32_t {
+  SP_NONE = 0, SP_TYPEINT = 1, SP_TYPEFLOAT = 2, SP_EXTINSTIMPORT = 3, SP_NAME = 4, SP_SWITCH = 5,
+  SP_EXTINST = 6, SP_FUNCTION = 7, SP_FUNCTIONEND = 8, SP_CAPABILITY = 9, SP_MEMORYMODEL = 10,
+  SP_ENTRYPOINT = 11, SP_LABEL = 12, SP_FUNCTIONPARAM = 13, SP_VARIABLE = 14, SP_UNDEF = 15,
+  SP_LINE = 16, SP_NOLINE = 17
+};
+enum : uint32_t { CAT_ID = 0, CAT_BITENUM = 1, CAT_VALUEENUM = 2, CAT_LITERAL = 3, CAT_COMPOSITE = 4 };
+enum : uint32_t { LIT_PLAIN = 0, LIT_STRING = 1, LIT_CTXNUM = 2, LIT_INTEGER = 3, LIT_EXTINST = 4, LIT_SPECOP = 5 };
+enum : uint32_t { IDR_ID = 0, IDR_RESULT = 1, IDR_RESULT_TYPE = 2 };
+enum : uint32_t { Q_ONE = 0, Q_OPT = 1, Q_VAR = 2 };
+constexpr uint32_t SECTION_KEEP = 255;
+
+struct Tables {
+  const uint32_t* blob;
+  uint32_t n_inst, max_opcode, n_kind, n_enum, n_slot, n_req, n_cap, cap_words, n_vsort;
+  int32_t ext_max;
+  uint32_t idref, linkage, ocl_off, ocl_len, req_stride, cap_kind;
+  uint32_t width_req[5];
+  uint32_t str_bytes;
+  const uint32_t* inst;     // 8 words / instruction
+  const uint16_t* opidx;    // max_opcode+1 entries
+  const uint32_t* kind;     // 8 words / kind
+  const uint32_t* enm;      // 8 words / enumerant
+  const uint32_t* slot;     // kind | quant<<16 | spec_tail<<24
+  const uint8_t* str;
+  const uint32_t* req;      // req_stride words / requirement
+  const uint64_t* closure;  // cap_words u64 / capability name
+  const uint32_t* vsort;    // (value, enum index) pairs
+  const uint32_t* ext;      // (name_off, name_len) per ext number
+
+  // -- instructions ----------------------------------------------------------
+  __device__ __forceinline__ uint32_t inst_of(uint32_t opcode) const {
+    if (opcode > max_opcode) return NONE32;
+    uint16_t v = __ldg(opidx + opcode);
+    return v == NONE16 ? NONE32 : v;
+  }
+  __device__ __forceinline__ const uint32_t* irec(uint32_t i) const { return inst + 8 * i; }
+  __device__ __forceinline__ uint32_t iname_off(uint32_t i) const { return __ldg(irec(i)); }
+  __device__ __forceinline__ uint32_t iname_len(uint32_t i) const { return __ldg(irec(i) + 1) & 0xFFFF; }
+  __device__ __forceinline__ uint32_t inslots(uint32_t i) const { return __ldg(irec(i) + 1) >> 16; }
+  __device__ __forceinline__ uint32_t islot_off(uint32_t i) const { return __ldg(irec(i) + 2); }
+  __device__ __forceinline__ uint32_t iflags(uint32_t i) const { return __ldg(irec(i) + 3); }
+  __device__ __forceinline__ bool has_result(uint32_t i) const { return iflags(i) & 1; }
+  __device__ __forceinline__ bool has_rtype(uint32_t i) const { return iflags(i) & 2; }
+  __device__ __forceinline__ uint32_t special(uint32_t i) const { return (iflags(i) >> 8) & 0xFF; }
+  __device__ __forceinline__ uint32_t section(uint32_t i) const { return (iflags(i) >> 16) & 0xFF; }
+  __device__ __forceinline__ uint32_t ireq(uint32_t i) const { return __ldg(irec(i) + 4); }
+
+  // -- kinds -----------------------------------------------------------------
+  __device__ __forceinline__ const uint32_t* krec(uint32_t k) const { return kind + 8 * k; }
+  __device__ __forceinline__ uint32_t kcat(uint32_t k) const { return __ldg(krec(k)) & 0xFF; }
+  __device__ __forceinline__ uint32_t ksub(uint32_t k) const { return (__ldg(krec(k)) >> 8) & 0xFF; }
+  __device__ __forceinline__ uint32_t knbases(uint32_t k) const { return __ldg(krec(k)) >> 16; }
+  __device__ __forceinline__ uint32_t kenum_off(uint32_t k) const { return __ldg(krec(k) + 1); }
+  __device__ __forceinline__ uint32_t knenum(uint32_t k) const { return __ldg(krec(k) + 2); }
+  __device__ __forceinline__ uint32_t kzero(uint32_t k) const { return __ldg(krec(k) + 3); }
+  __device__ __forceinline__ uint32_t kbase_off(uint32_t k) const { return __ldg(krec(k) + 4); }
+  __device__ __forceinline__ uint32_t kvs_off(uint32_t k) const { return __ldg(krec(k) + 5); }
+  __device__ __forceinline__ uint32_t kvs_n(uint32_t k) const { return __ldg(krec(k) + 6); }
+
+  // -- enumerants ----------------------------------------------------------------
+  __device__ __forceinline__ const uint32_t* erec(uint32_t e) const { return enm + 8 * e; }
+  __device__ __forceinline__ uint32_t evalue(uint32_t e) const { return __ldg(erec(e)); }
+  __device__ __forceinline__ uint32_t ename_off(uint32_t e) const { return __ldg(erec(e) + 1); }
+  __device__ __forceinline__ uint32_t ename_len(uint32_t e) const { return __ldg(erec(e) + 2) & 0xFFFF; }
+  __device__ __forceinline__ uint32_t enparams(uint32_t e) const { return __ldg(erec(e) + 2) >> 16; }
+  __device__ __forceinline__ uint32_t eparam_off(uint32_t e) const { return __ldg(erec(e) + 3); }
+  __device__ __forceinline__ uint32_t ereq(uint32_t e) const { return __ldg(erec(e) + 4); }
+  __device__ __forceinline__ uint32_t emerged(uint32_t e) const { return __ldg(erec(e) + 5); }
+  __device__ __forceinline__ uint32_t ecapname(uint32_t e) const { return __ldg(erec(e) + 6); }
+
+  // first enumerant of a ValueEnum kind with this value (ops.py:385-390)
+  __device__ uint32_t venum_lookup(uint32_t k, uint32_t value) const {
+    uint32_t lo = kvs_off(k), n = kvs_n(k);
+    uint32_t hi = lo + n;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      uint32_t v = __ldg(vsort + 2 * mid);
+      if (v < value) lo = mid + 1; else hi = mid;
+    }
+    if (lo < kvs_off(k) + n && __ldg(vsort + 2 * lo) == value) return __ldg(vsort + 2 * lo + 1);
+    return NONE32;
+  }
+
+  __device__ __forceinline__ uint32_t slot_kind(uint32_t s) const { return __ldg(slot + s) & 0xFFFF; }
+  __device__ __forceinline__ uint32_t slot_quant(uint32_t s) const { return (__ldg(slot + s) >> 16) & 0xFF; }
+  __device__ __forceinline__ bool slot_spec_tail(uint32_t s) const { return (__ldg(slot + s) >> 24) & 1; }
+
+  // -- requirements / capabilities ---------------------------------------------
+  __device__ __forceinline__ const uint32_t* rrec(uint32_t r) const { return req + req_stride * r; }
+
+  // -- ext instructions -------------------------------------------------------
+  __device__ __forceinline__ bool ext_name(uint32_t num, uint32_t& off, uint32_t& len) const {
+    if (ext_max < 0 || num > (uint32_t)ext_max) return false;
+    off = __ldg(ext + 2 * num);
+    if (off == NONE32) return false;
+    len = __ldg(ext + 2 * num + 1);
+    return true;
+  }
+};
+
+}  // namespace skg

@@ -1,0 +1,410 @@
+// Batch validator: binary modules -> diagnostics, bit-exact with the reference
+// validate_module (validate.py:73-296).  Output per module is the
+// diagnostics_text rendering, one "severity code location message" line per
+// diagnostic, each terminated by '\n', in validate_module's order:
+// module-level shape findings, then per instruction index i:
+//   DuplicateResultId, BoundTooSmall*      (_check_ids, validate.py:139-168)
+//   UnknownOpcode | OperandMismatch        (_check_operand_layout, :207-220)
+//   MissingCapability (instruction, operands*, width)  (_closure_diagnostics, :237-267)
+// Non-codec exceptions raised by the operand walk escape validate_module in the
+// reference; they are reported as the module status like the disassembler does.
+#include "skg_module.cuh"
+
+namespace skg {
+
+struct ValidateArgs {
+  Tables T;
+  const uint8_t* data;
+  const int64_t* mod_off;
+  const int64_t* mod_len;
+  uint32_t n_mod;
+  uint8_t* text;
+  uint64_t text_cap;
+  int64_t* text_off;
+  int32_t* status;
+  unsigned long long* state;
+  uint32_t* ticket;
+  ErrRec* errs;
+  uint32_t err_cap;
+  uint8_t* gscratch;
+  uint64_t gslot_bytes;
+  uint32_t smem_slab;
+};
+
+constexpr int MAX_CAPW = 6;
+
+template <class S>
+__device__ inline void diag_head(S& s, bool error, const char* code, uint32_t loc) {
+  put_cstr(s, error ? "error " : "warning ");
+  put_cstr(s, code);
+  s.put(' ');
+  if (loc == NONE32) put_cstr(s, "module"); else put_u64(s, loc);
+  s.put(' ');
+}
+
+__device__ inline bool unsatisfied(const Tables& T, uint32_t r, const uint64_t* eff) {
+  if (r == NONE32) return false;
+  const uint32_t* rec = T.rrec(r);
+  for (uint32_t k = 0; k < T.cap_words; ++k) {
+    uint64_t bits = (uint64_t)__ldg(rec + 2 + 2 * k) | ((uint64_t)__ldg(rec + 3 + 2 * k) << 32);
+    if (bits & eff[k]) return false;
+  }
+  return true;
+}
+
+template <class S>
+__device__ inline void put_req_repr(S& s, const Tables& T, uint32_t r) {
+  const uint32_t* rec = T.rrec(r);
+  s.putn(T.str + __ldg(rec), __ldg(rec + 1));
+}
+
+struct NullVis {
+  __device__ void id(uint32_t, uint32_t, int) {}
+  __device__ void venum(uint32_t, uint32_t, uint32_t) {}
+  __device__ void benum(uint32_t, uint32_t, bool, uint64_t) {}
+  __device__ void str(const uint32_t*, uint32_t, uint32_t) {}
+  __device__ void typed(const LitVal&) {}
+  __device__ void lit(uint32_t, uint32_t) {}
+  __device__ void comp_begin() {}
+  __device__ void comp_end() {}
+};
+
+template <class S>
+struct BoundVis : NullVis {
+  S* s;
+  uint32_t i, bound;
+  __device__ void id(uint32_t, uint32_t v, int) {
+    if (v >= bound) {
+      diag_head(*s, true, "BoundTooSmall", i);
+      s->put('%'); put_u64(*s, v); put_cstr(*s, " is not below the header bound "); put_u64(*s, bound);
+      s->put('\n');
+    }
+  }
+};
+
+template <class S>
+struct ReqVis : NullVis {
+  S* s;
+  const Tables* T;
+  const uint64_t* eff;
+  uint32_t i, d;
+  __device__ void line(uint32_t r) {
+    diag_head(*s, true, "MissingCapability", i);
+    s->putn(T->str + T->iname_off(d), T->iname_len(d));
+    put_cstr(*s, " operand requires one of ");
+    put_req_repr(*s, *T, r);
+    s->put('\n');
+  }
+  __device__ void venum(uint32_t, uint32_t, uint32_t e) {
+    if (e == NONE32) return;
+    uint32_t r = T->emerged(e);
+    if (unsatisfied(*T, r, eff)) line(r);
+  }
+  __device__ void benum(uint32_t k, uint32_t mask, bool full, uint64_t comp) {
+    if (!full) return;
+    uint32_t eo = T->kenum_off(k);
+    for (int j = 0; j < 64; ++j) {
+      if (!((comp >> j) & 1)) continue;
+      uint32_t r = T->ereq(eo + j);
+      if (unsatisfied(*T, r, eff)) line(r);
+    }
+  }
+};
+
+// all located diagnostics of instruction i; returns the walk status
+template <class S>
+__device__ inline WalkErr inst_diags(S& s, const Mod& m, const Tables& T, uint32_t i,
+                                     const uint64_t* eff) {
+  const uint32_t d = m.idef[i];
+  const uint32_t* ops = inst_ops(m, i);
+  const uint32_t n = inst_nops(m, i);
+  if (d == NONE16) {
+    diag_head(s, false, "UnknownOpcode", i);
+    put_cstr(s, "opcode "); put_u64(s, inst_opcode(m, i)); put_cstr(s, " is not in the loaded grammar\n");
+    return WalkErr{};
+  }
+  if (T.has_result(d)) {
+    uint32_t idx = T.has_rtype(d) ? 1 : 0;
+    if (idx < n) {
+      uint32_t slot = ht_find(m, ops[idx]);
+      if (slot != NONE32 && m.hdef[slot] != i) {
+        diag_head(s, true, "DuplicateResultId", i);
+        s.put('%'); put_u64(s, ops[idx]); put_cstr(s, " already defined at instruction ");
+        put_u64(s, m.hdef[slot]); s.put('\n');
+      }
+    }
+  }
+  Resolver res{&m, &T};
+  NullVis nv;
+  WalkErr e = walk(T, d, ops, n, nv, res);
+  if (e.code != W_OK && !werr_is_codec(e.code)) return e;
+  if (e.code == W_OK) {
+    BoundVis<S> bv;
+    bv.s = &s; bv.i = i; bv.bound = m.bound;
+    walk(T, d, ops, n, bv, res);
+  } else {
+    diag_head(s, true, "OperandMismatch", i);
+    put_walk_error(s, T, d, e);
+    s.put('\n');
+  }
+  const uint32_t sp = T.special(d);
+  if (sp == SP_CAPABILITY) return e;
+  uint32_t r = T.ireq(d);
+  if (unsatisfied(T, r, eff)) {
+    diag_head(s, true, "MissingCapability", i);
+    s.putn(T.str + T.iname_off(d), T.iname_len(d));
+    put_cstr(s, " requires one of ");
+    put_req_repr(s, T, r);
+    s.put('\n');
+  }
+  if (e.code != W_OK) return e;
+  ReqVis<S> rv;
+  rv.s = &s; rv.T = &T; rv.eff = eff; rv.i = i; rv.d = d;
+  walk(T, d, ops, n, rv, res);
+  uint32_t wr = NONE32;
+  if ((sp == SP_TYPEINT || sp == SP_TYPEFLOAT) && n >= 2) {
+    uint32_t wd = ops[1];
+    if (sp == SP_TYPEINT) wr = wd == 8 ? T.width_req[0] : wd == 16 ? T.width_req[1] : wd == 64 ? T.width_req[2] : NONE32;
+    else wr = wd == 16 ? T.width_req[3] : wd == 64 ? T.width_req[4] : NONE32;
+  }
+  if (unsatisfied(T, wr, eff)) {
+    diag_head(s, true, "MissingCapability", i);
+    s.putn(T.str + T.iname_off(d), T.iname_len(d));
+    put_cstr(s, " with this width requires one of ");
+    put_req_repr(s, T, wr);
+    s.put('\n');
+  }
+  return e;
+}
+
+struct Shape {
+  bool has_fn, has_cap, has_ep;
+  uint32_t n_mm;
+  bool linkage;
+};
+
+template <class S>
+__device__ inline void shape_diags(S& s, const Shape& sh) {
+  if (!sh.has_fn) { diag_head(s, true, "MissingFunction", NONE32); put_cstr(s, "module declares no function\n"); }
+  if (!sh.has_cap) { diag_head(s, true, "MissingCapability", NONE32); put_cstr(s, "module declares no capability\n"); }
+  if (sh.n_mm == 0) { diag_head(s, true, "MissingMemoryModel", NONE32); put_cstr(s, "module has no memory model\n"); }
+  else if (sh.n_mm > 1) {
+    diag_head(s, true, "MultipleMemoryModels", NONE32);
+    put_cstr(s, "module has "); put_u64(s, sh.n_mm); put_cstr(s, " memory model instructions\n");
+  }
+  if (!sh.has_ep) {
+    diag_head(s, !sh.linkage, "MissingEntryPoint", NONE32);
+    put_cstr(s, "module declares no entry point\n");
+  }
+}
+
+__global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t lane = lane_id();
+  const uint32_t warp_in_block = threadIdx.x >> 5;
+  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
+  uint8_t* slab = smem + (size_t)warp_in_block * a.smem_slab;
+  uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
+  const Tables& T = a.T;
+  ErrSink es{a.errs, a.ticket + 1, a.err_cap};
+
+  while (true) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1u);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= a.n_mod) break;
+    const int64_t nbytes = a.mod_len[t];
+    const uint8_t* src = a.data + a.mod_off[t];
+    int32_t status = ST_OK;
+    uint64_t total = 0;
+    Mod m;
+    Shape sh{};
+    uint64_t eff[MAX_CAPW] = {0, 0, 0, 0, 0, 0};
+    int32_t decode_status = ST_OK;
+    const uint32_t W = (nbytes >= 0 && nbytes % 4 == 0) ? (uint32_t)(nbytes / 4) : 0;
+    bool in_smem = head_bytes(W) <= a.smem_slab;
+    ErrRec* drec = nullptr;
+    if (!in_smem && worst_bytes(W) > a.gslot_bytes) {
+      status = ST_INTERNAL;
+      if (lane == 0 && (drec = es.alloc())) {
+        ErrWriter ew{drec};
+        put_cstr(ew, "internal: module exceeds the per-warp scratch slot");
+        drec->module = (int32_t)t; drec->cls = ST_INTERNAL; drec->len = ew.n;
+      }
+    } else {
+      layout_head(m, in_smem ? slab : gslot, W);
+      decode_status = load_and_split(m, src, (uint64_t)nbytes, nullptr, (int32_t)t);
+    }
+    if (status == ST_OK && decode_status == ST_OK) {
+      uint32_t C = table_capacity(m.I);
+      for (int attempt = 0; attempt < 3; ++attempt) {
+        if (head_bytes(m.W) + tables_bytes(m.I, C) > (in_smem ? a.smem_slab : a.gslot_bytes)) {
+          if (in_smem) {
+            Mod g;
+            layout_head(g, gslot, m.W);
+            for (uint32_t k = lane; k < m.W; k += 32) g.w[k] = m.w[k];
+            for (uint32_t k = lane; k < m.I; k += 32) g.ioff[k] = m.ioff[k];
+            g.I = m.I; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
+            __syncwarp();
+            m = g;
+            in_smem = false;
+          }
+          if (head_bytes(m.W) + tables_bytes(m.I, C) > a.gslot_bytes) { status = ST_INTERNAL; break; }
+        }
+        layout_tables(m, C);
+        init_tables(m);
+        prescan(m, T);
+        if (*m.overflow) {
+          C = C * 4;
+          while (C < 2 * m.W + 8) C <<= 1;
+          __syncwarp();
+          continue;
+        }
+        // module shape + effective capabilities (validate.py:101-136)
+        bool fn = false, cap = false, ep = false;
+        uint32_t mm = 0;
+        for (uint32_t base = 0; base < m.I; base += 32) {
+          uint32_t i = base + lane;
+          if (i >= m.I || m.idef[i] == NONE16) continue;
+          uint32_t sp = T.special(m.idef[i]);
+          fn |= sp == SP_FUNCTION;
+          ep |= sp == SP_ENTRYPOINT;
+          mm += sp == SP_MEMORYMODEL;
+          if (sp == SP_CAPABILITY) {
+            cap = true;
+            if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
+              uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
+              uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
+              if (cn != NONE32)
+                for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k) eff[k] |= __ldg(T.closure + cn * T.cap_words + k);
+            }
+          }
+        }
+        sh.has_fn = __any_sync(FULL, fn);
+        sh.has_cap = __any_sync(FULL, cap);
+        sh.has_ep = __any_sync(FULL, ep);
+        sh.n_mm = warp_sum_u32(mm);
+        for (int k = 0; k < MAX_CAPW; ++k) {
+#pragma unroll
+          for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
+        }
+        sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
+        // sizes + escaping exceptions
+        for (uint32_t base = 0; base < m.I; base += 32) {
+          uint32_t i = base + lane;
+          if (i < m.I) {
+            CountSink cs;
+            WalkErr e = inst_diags(cs, m, T, i, eff);
+            m.ierr[i] = (uint8_t)e.code;
+            m.ia[i] = cs.n;
+          }
+        }
+        __syncwarp();
+        uint32_t bad = NONE32;
+        for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
+          uint32_t i = base + lane;
+          unsigned b = __ballot_sync(FULL, i < m.I && m.ierr[i] != W_OK && !werr_is_codec(m.ierr[i]));
+          if (b) bad = base + __ffs(b) - 1;
+        }
+        if (bad != NONE32) {
+          if (lane == 0) {
+            ErrRec* rec = es.alloc();
+            CountSink cs;
+            WalkErr e = inst_diags(cs, m, T, bad, eff);
+            status = walk_status(e.code);
+            if (rec) {
+              ErrWriter ew{rec};
+              put_walk_error(ew, T, m.idef[bad], e);
+              rec->module = (int32_t)t; rec->cls = status; rec->len = ew.n;
+              rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
+            }
+          }
+          status = __shfl_sync(FULL, status, 0);
+          break;
+        }
+        CountSink hs;
+        shape_diags(hs, sh);
+        uint64_t run = hs.n;
+        for (uint32_t base = 0; base < m.I; base += 32) {
+          uint32_t i = base + lane;
+          uint32_t len = i < m.I ? m.ia[i] : 0;
+          uint32_t incl = warp_incl_sum(len);
+          if (i < m.I) m.ia[i] = (uint32_t)(run + incl - len);
+          run += __shfl_sync(FULL, incl, 31);
+        }
+        __syncwarp();
+        total = run;
+        break;
+      }
+    }
+    // the decode error of the module is its only diagnostic line
+    if (status == ST_OK && decode_status != ST_OK) {
+      const char* code = decode_status == ST_NOTSPIRV ? "NotSpirv"
+                         : decode_status == ST_TRUNCATED ? "TruncatedStream" : "CorruptStream";
+      CountSink cs;
+      diag_head(cs, true, code, NONE32);
+      ErrRec tmp;
+      // recompute the message into a local record
+      {
+        ErrWriter ew{&tmp};
+        // identical text to load_and_split's
+        if (nbytes % 4 != 0 || nbytes < 20) {
+          put_u64(ew, (uint64_t)nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
+        } else if (decode_status == ST_NOTSPIRV) {
+          put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, m.w[0]); put_cstr(ew, " is not SPIR-V");
+        } else {
+          // re-walk to find the failing position
+          uint32_t p = 5;
+          while (p < m.W) {
+            uint32_t wc = m.w[p] >> 16;
+            if (wc == 0 || p + wc > m.W) break;
+            p += wc;
+          }
+          put_cstr(ew, "instruction at word "); put_u64(ew, p);
+          put_cstr(ew, decode_status == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
+        }
+        tmp.len = ew.n;
+      }
+      total = cs.n + (uint32_t)tmp.len + 1;
+      uint64_t off = lookback(a.state, t, total);
+      if (lane == 0) {
+        a.text_off[t] = (int64_t)off;
+        a.status[t] = ST_OK;
+        if (t == a.n_mod - 1) a.text_off[a.n_mod] = (int64_t)(off + total);
+        if (off + total > a.text_cap) atomicExch(a.ticket + 2, 1u);
+        else {
+          MemSink ms(a.text + off);
+          diag_head(ms, true, code, NONE32);
+          ms.putn((const uint8_t*)tmp.msg, (uint32_t)tmp.len);
+          ms.put('\n');
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (status != ST_OK) total = 0;
+    uint64_t off = lookback(a.state, t, total);
+    if (lane == 0) {
+      a.text_off[t] = (int64_t)off;
+      a.status[t] = status;
+      if (t == a.n_mod - 1) a.text_off[a.n_mod] = (int64_t)(off + total);
+    }
+    if (status == ST_OK && total > 0) {
+      if (off + total > a.text_cap) {
+        if (lane == 0) atomicExch(a.ticket + 2, 1u);
+      } else {
+        uint8_t* out = a.text + off;
+        if (lane == 0) { MemSink ms(out); shape_diags(ms, sh); }
+        for (uint32_t base = 0; base < m.I; base += 32) {
+          uint32_t i = base + lane;
+          if (i >= m.I) continue;
+          MemSink ms(out + m.ia[i]);
+          inst_diags(ms, m, T, i, eff);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace skg

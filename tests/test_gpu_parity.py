@@ -1,0 +1,143 @@
+"""CUDA path vs. the reference's golden vectors and the CPU oracle (needs a B200)."""
+
+import random
+import struct
+
+import numpy as np
+import pytest
+
+from golden_io import OPTION_SETS, modules, outcome, same
+
+pytestmark = pytest.mark.gpu
+
+CASES = modules()
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2305_09493_b200 as sk
+    return sk
+
+
+def _as_outcome(r):
+    if isinstance(r, BaseException):
+        return {"exc": [type(r).__name__, str(r)]}
+    return {"ok": r}
+
+
+def test_disasm_golden_batch_all_options(sk):
+    datas = [r["bytes"] for r in CASES]
+    for key, opts in OPTION_SETS.items():
+        got = sk.disassemble_batch(datas, sk.DisassemblerOptions(**opts))
+        bad = [r["name"] for r, g in zip(CASES, got) if not same(_as_outcome(g), r["disasm"][key])]
+        assert not bad, f"{key}: {bad[:10]}"
+    got = sk.disassemble_batch(datas, strict=True)
+    bad = [r["name"] for r, g in zip(CASES, got) if not same(_as_outcome(g), r["disasm_strict"])]
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("rec", CASES[:40], ids=[r["name"] for r in CASES[:40]])
+def test_disassemble_module_single(sk, rec):
+    got = outcome(lambda: sk.disassemble_module(rec["bytes"]))
+    assert same(got, rec["disasm"]["default"])
+
+
+def test_validate_golden_batch(sk):
+    datas = [r["bytes"] for r in CASES]
+    got = sk.validate_batch(datas)
+    bad = []
+    for r, g in zip(CASES, got):
+        o = _as_outcome(g)
+        if "ok" in o:
+            o = {"ok": [[d.severity, d.code, d.location, d.message] for d in o["ok"]]}
+        if not same(o, r["validate"]):
+            bad.append(r["name"])
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("rec", CASES[::7], ids=[r["name"] for r in CASES[::7]])
+def test_decode_module_golden(sk, rec):
+    def run():
+        h, insts = sk.decode_module(rec["bytes"])
+        return [[h.major_version, h.minor_version, h.generator_magic, h.bound, h.schema],
+                [[i.opcode, len(i.operands)] for i in insts]]
+    assert same(outcome(run), rec["decode"])
+
+
+def test_synthetic_families_vs_oracle(sk):
+    from oracle import disasm as odis, validate as oval
+    from synth.families import FAMILIES, build_module
+    mods = [build_module(f, s) for f in FAMILIES for s in range(40)]
+    got = sk.disassemble_batch(mods)
+    assert all(g == odis.disassemble(m) for m, g in zip(mods, got))
+    opts = sk.DisassemblerOptions(highlight=True, group=True)
+    got = sk.disassemble_batch(mods, opts)
+    oo = odis.Options(highlight=True, group=True)
+    assert all(g == odis.disassemble(m, oo) for m, g in zip(mods, got))
+    vd = sk.validate_batch(mods)
+    for m, d in zip(mods, vd):
+        assert [(x.severity, x.code, x.location, x.message) for x in d] == \
+            [tuple(x) for x in oval.validate(m)]
+
+
+def _const_module(width, values):
+    """One OpTypeFloat/OpTypeInt + one OpConstant per value (raw words)."""
+    words = [0x07230203, 0x00010200, 0, len(values) + 2, 0]
+    words += [(3 << 16) | 22, 1, width]                       # OpTypeFloat %1 width
+    for k, v in enumerate(values):
+        if width == 64:
+            words += [(5 << 16) | 43, 1, k + 2, v & 0xFFFFFFFF, v >> 32]
+        else:
+            words += [(4 << 16) | 43, 1, k + 2, v]
+    return struct.pack(f"<{len(words)}I", *words)
+
+
+def _expected_floats(width, values):
+    fmt = {16: "<e", 32: "<f", 64: "<d"}[width]
+    out = []
+    for v in values:
+        raw = struct.pack("<Q" if width == 64 else "<I", v)
+        out.append(repr(struct.unpack(fmt, raw[: width // 8])[0]))
+    return out
+
+
+@pytest.mark.parametrize("width", [16, 32, 64])
+def test_float_repr_matches_cpython(sk, width):
+    rng = random.Random(width)
+    if width == 16:
+        values = list(range(65536))
+    elif width == 32:
+        values = [rng.getrandbits(32) for _ in range(200000)]
+        values += [0x00000001, 0x007FFFFF, 0x00800000, 0x7F7FFFFF, 0x3DCCCCCD, 0x80000000]
+    else:
+        values = [rng.getrandbits(64) for _ in range(200000)]
+        values += [struct.unpack("<Q", struct.pack("<d", x))[0] for x in
+                   (1e16, 9999999999999998.0, 1e-05, 0.0001, 5e-324, 1.7976931348623157e308, 0.1)]
+    chunks = [values[i:i + 4000] for i in range(0, len(values), 4000)]
+    mods = [_const_module(width, c) for c in chunks]
+    texts = sk.disassemble_batch(mods, sk.DisassemblerOptions(no_header=True, inline_names=False,
+                                                              no_indent=True))
+    for c, t in zip(chunks, texts):
+        assert not isinstance(t, BaseException), t
+        lines = t.splitlines()[1:]
+        got = [ln.split(" ")[-1] for ln in lines]
+        want = _expected_floats(width, c)
+        bad = [(hex(v), w, g) for v, w, g in zip(c, want, got) if w != g]
+        assert not bad, bad[:5]
+
+
+def test_batch_with_mixed_errors_and_sizes(sk):
+    """A large shuffled batch: results must not depend on batch position."""
+    from oracle import disasm as odis
+    rng = random.Random(5)
+    pool = [r["bytes"] for r in CASES]
+    mods = [rng.choice(pool) for _ in range(3000)]
+    got = sk.disassemble_batch(mods)
+    cache = {}
+    for m, g in zip(mods, got):
+        if m not in cache:
+            cache[m] = outcome(lambda: odis.disassemble(m))
+        assert same(_as_outcome(g), cache[m])
