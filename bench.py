@@ -1,0 +1,377 @@
+"""Benchmark: SPIR-V words/s disassembled on B200 (BASELINE.json configs[1]).
+
+Workload (N=1): a batch of 1,000,000 synthetic modules drawn (seeded) from
+10,000 builder-canonical variants of the paper's benchmark kernels (saxpy,
+matmul, DFT, n-body, Black-Scholes; synth/families.py), disassembled with the
+reference's default options.  One step = one batch pass of the CUDA
+disassembler (libskgpu skg_disasm) with the input resident in HBM.  N>1
+(torchrun, one process per GPU): every rank disassembles its own 1M-module
+batch (weak scaling, no collective on the data path); value = all ranks' words
+/ max-over-ranks time.
+
+Extra keys: roofline (HBM, algorithmic bytes 4W+T per launch), cpu_baseline
+(the reference's own CPU implementation, oracle/_ref, timed on this box's host
+cores on a bounded sample), e2e (host buffers through DisasmSession: pinned
+H2D + kernel + D2H of the text), gpu_launches, clocks.
+
+``--impl reference`` times the reference's CPU implementation instead (rank 0
+only, all host cores, bounded sample per step) and prints the same JSON line
+with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SPIR-V words/sec disassembled+assembled (1/2/4/8 B200); % of HBM roofline"
+SEED = 20261017
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# -- CPU reference (bounded sample) ------------------------------------------------
+_REF_MOD = None
+
+
+def _ref_init():
+    global _REF_MOD
+    ref = ROOT / "oracle" / "_ref"
+    if (ref / "spirvkit").is_dir():
+        sys.path.insert(0, str(ref))
+        import spirvkit
+        _REF_MOD = ("reference", spirvkit.disassemble_module)
+    else:
+        from oracle import disasm as odis
+        _REF_MOD = ("port", odis.disassemble)
+
+
+def _ref_work(mods):
+    fn = _REF_MOD[1]
+    words = 0
+    for m in mods:
+        fn(m)
+        words += len(m) // 4
+    return words
+
+
+def ref_kind():
+    return "reference" if (ROOT / "oracle" / "_ref" / "spirvkit").is_dir() else "port"
+
+
+class CpuReference:
+    """The reference disassembler on all host cores (multiprocessing)."""
+
+    def __init__(self, cores=None):
+        import multiprocessing as mp
+        self.cores = cores or len(os.sched_getaffinity(0))
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_ref_init)
+
+    def run(self, mods):
+        chunks = [mods[i::self.cores] for i in range(self.cores)]
+        t0 = time.perf_counter()
+        words = sum(self.pool.map(_ref_work, chunks))
+        return words, time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def sample_modules(batch, n):
+    idx = np.linspace(0, batch.n - 1, num=min(n, batch.n)).astype(np.int64)
+    return [batch.module(int(i)) for i in idx]
+
+
+# -- clocks ------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, name in enumerate(names):
+                if len(s) > 3 + k and s[3 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:  # noqa: BLE001
+            pass
+    return 6650.0, "fallback"
+
+
+def profile_traffic():
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:  # noqa: BLE001
+            return None
+    return None
+
+
+# -- the GPU arm ---------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    from paper_2305_09493_b200 import _native
+    from paper_2305_09493_b200.disasm import DisasmSession, DisassemblerOptions, option_bits
+    from synth.families import sample_batch
+
+    t0 = time.perf_counter()
+    batch = sample_batch(args.modules, args.variants, SEED + rank)
+    words = batch.words
+    log(f"[rank {rank}] batch: {batch.n} modules, {words} words, {batch.data.nbytes} bytes "
+        f"({time.perf_counter() - t0:.1f}s)")
+    dev = _native.DeviceBatch.from_host(batch.data, batch.offsets, batch.lengths)
+    opts = option_bits(DisassemblerOptions())
+    plan = _native.DisasmPlan(dev, opts)
+    info = plan.fit()
+    status = plan.status[: dev.n].cpu().numpy()
+    assert info["errors"] == 0 and not info["overflow"] and (status == 0).all(), info
+    text_bytes = info["text_bytes"]
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.launch()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            plan.launch()
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    total_words = words * world
+    value = total_words / (ms_step / 1e3)
+
+    # spot-check parity of the timed configuration against the oracle
+    if rank == 0:
+        from oracle import disasm as odis
+        txt = plan.text[: text_bytes].cpu().numpy()
+        span = plan.span.cpu().numpy()
+        for i in np.linspace(0, dev.n - 1, 8).astype(int):
+            got = txt[span[2 * i]:span[2 * i] + span[2 * i + 1]].tobytes().decode()
+            assert got == odis.disassemble(batch.module(int(i))), f"module {i} differs from oracle"
+
+    # e2e through the host-buffer public API
+    sess = DisasmSession()
+    sess.stage(batch.data, batch.offsets, batch.lengths)
+    sess.run_staged()
+    e2e_steps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t1 = time.perf_counter()
+    for _ in range(e2e_steps):
+        text, toff, st = sess.run_staged()
+    e2e_s = (time.perf_counter() - t1) / e2e_steps
+    et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_s = float(et.item())
+    assert len(text) == text_bytes
+    h2d = batch.data.nbytes + 16 * batch.n
+    d2h = text_bytes + 16 * batch.n + 4 * batch.n + 32
+
+    if rank != 0:
+        return None
+    peak, peak_src = peak_hbm()
+    alg_bytes = 4 * words + text_bytes
+    achieved = alg_bytes / (ms_step / 1e3) / 1e9
+    traffic = profile_traffic()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "words/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic: seeded builder-canonical paper-family modules (synth/families.py)",
+        "config": {
+            "workload": "configs[1]: batch of 1M synthetic modules (saxpy/matmul/DFT/n-body/"
+                        "Black-Scholes variants) disassembled on 1 B200, default options; "
+                        "step = disassembly only (assembler path not yet on GPU)",
+            "modules_per_gpu": batch.n, "variants": args.variants, "words_per_gpu": words,
+            "input_bytes_per_gpu": 4 * words, "text_bytes_per_gpu": text_bytes,
+            "l2": "inputs (%.2f GB) and output exceed the 126 MB L2; no flush needed" %
+                  (batch.data.nbytes / 1e9),
+            "parallelism": f"module-sharded x{world}",
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "frac_of_nominal_8TBs": achieved / 8000.0,
+        },
+        "e2e": {"value": total_words / e2e_s, "unit": "words/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "paper_2305_09493_b200.disasm.DisasmSession.run_staged"},
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        ref = CpuReference()
+        try:
+            sample = sample_modules(batch, ref.cores * args.cpu_per_core)
+            ref.run(sample[: ref.cores])          # fork + import warm-up
+            w, dt = ref.run(sample)
+        finally:
+            ref.close()
+        line["cpu_baseline"] = {"value": w / dt, "unit": "words/s", "cores": ref.cores,
+                                "kind": ref_kind(),
+                                "sample": f"{len(sample)} modules ({w} words) evenly spaced "
+                                          f"through the batch, disassemble_module each"}
+    return line
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    from synth.families import sample_batch
+    batch = sample_batch(max(2000, args.ref_modules), min(args.variants, 2000), SEED)
+    ref = CpuReference()
+    try:
+        per_step = ref.cores * args.cpu_per_core
+        sample = sample_modules(batch, batch.n)
+        words_total, t_total = 0, 0.0
+        cursor = 0
+
+        def take():
+            nonlocal cursor
+            out = [sample[(cursor + k) % len(sample)] for k in range(per_step)]
+            cursor += per_step
+            return out
+
+        for _ in range(args.warmup):
+            ref.run(take())
+        for _ in range(args.steps):
+            w, dt = ref.run(take())
+            words_total += w
+            t_total += dt
+    finally:
+        ref.close()
+    value = words_total / t_total
+    return {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: seeded builder-canonical paper-family modules (synth/families.py)",
+        "config": {"workload": "configs[1] (bounded CPU sample): reference spirvkit "
+                               "disassemble_module per module on all host cores",
+                   "modules_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "words/s", "cores": ref.cores,
+                         "kind": ref_kind(),
+                         "sample": f"{per_step} modules per step from a 2000-variant pool"},
+        "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--modules", type=int, default=1_000_000)
+    ap.add_argument("--variants", type=int, default=10_000)
+    ap.add_argument("--cpu-per-core", type=int, default=150)
+    ap.add_argument("--ref-modules", type=int, default=4000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -62,7 +62,7 @@ int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** 
 void skg_tables_destroy(skg_tables* t);
 
 /* Device workspace (bytes) for a batch of n_mod modules whose largest module
- * has max_words words.  Includes look-back state, counters and the per-warp
+ * has max_words words.  Includes the counters (ticket, errors, allocator) and the per-warp
  * overflow scratch of the persistent grid. */
 uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words);
 
@@ -70,25 +70,28 @@ uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words);
  * Replaces: Disassembler.to_text / disassemble_module(data, options, strict=...)
  * (reference disasm.py:117-127, 392-398) for every module of the batch.
  * Output: text arena `text` (capacity text_cap bytes); module m's text is
- * text[text_off[m] : text_off[m+1]] (text_off has n_mod+1 entries).
+ * text[text_span[2m] : text_span[2m] + text_span[2m+1]].  Modules reserve their
+ * bytes with an atomic bump allocator, so the arena holds the modules' texts in
+ * completion order (no inter-module ordering wait on the device).
  * status[m] = SKG_ST_*; errors[] gets one record per failing module (up to
- * err_cap; counters: see skg_last_counts).  If the arena is too small nothing
- * past the capacity is written and *the required size* is text_off[n_mod]. */
+ * err_cap; counters: see skg_last_counts).  If the arena is too small the
+ * modules that do not fit are not written, the overflow flag is set and the
+ * required size is reported by skg_last_counts. */
 int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
-               uint8_t* text, uint64_t text_cap, int64_t* text_off, int32_t* status,
+               uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
                skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
                void* stream);
 
 /* Batch structural + capability validation.
  * Replaces: validate_module(bytes) (reference validate.py:73-94).
  * Output: diagnostics_text-formatted lines ("severity code location message\n")
- * per module in the `text` arena (same offset convention as skg_disasm);
+ * per module in the `text` arena (same span convention as skg_disasm);
  * non-codec exceptions that escape the reference validator are reported
  * through status/errors exactly like skg_disasm. */
 int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                  const int64_t* mod_len, uint32_t n_mod, uint32_t max_words, uint8_t* text,
-                 uint64_t text_cap, int64_t* text_off, int32_t* status, skg_error* errors,
+                 uint64_t text_cap, int64_t* text_span, int32_t* status, skg_error* errors,
                  uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream);
 
 /* Instruction-boundary pass only (header + per-instruction offsets).
@@ -103,8 +106,10 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
                uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream);
 
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
- * `stream`): number of error records wanted, and 1 if the text arena overflowed. */
-int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow, void* stream);
+ * `stream`): number of error records wanted, 1 if the text arena overflowed,
+ * and the text bytes the batch needs (allocator cursor). */
+int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow,
+                    uint64_t* text_bytes, void* stream);
 
 /* Version / build info string. */
 const char* skg_version(void);

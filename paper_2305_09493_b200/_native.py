@@ -53,7 +53,7 @@ def lib():
     L.skg_disasm.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P]
     L.skg_validate.argtypes = [P, P, P, P, U32, U32, P, U64, P, P, P, U32, P, U64, P]
     L.skg_decode.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, U32, P, U64, P]
-    L.skg_last_counts.argtypes = [P, ctypes.POINTER(U32), ctypes.POINTER(U32), P]
+    L.skg_last_counts.argtypes = [P, ctypes.POINTER(U32), ctypes.POINTER(U32), ctypes.POINTER(U64), P]
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts):
         f.restype = I32
@@ -148,10 +148,18 @@ def _stream():
 
 
 class TextResult:
-    """Device-resident output of a batch call."""
+    """Device-resident output of a batch call: module m's text is
+    text[span[2m] : span[2m] + span[2m+1]]."""
 
-    def __init__(self, text, off, status, errors):
-        self.text, self.off, self.status, self.errors = text, off, status, errors
+    def __init__(self, text, span, status, errors):
+        self.text, self.span, self.status, self.errors = text, span, status, errors
+
+
+def last_counts(ws):
+    nerr, over, used = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint64()
+    _check(lib().skg_last_counts(ws.data_ptr(), ctypes.byref(nerr), ctypes.byref(over),
+                                 ctypes.byref(used), _stream()), "counts")
+    return int(nerr.value), bool(over.value), int(used.value)
 
 
 def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, err_cap=None):
@@ -165,29 +173,25 @@ def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, e
     ecap = err_cap if err_cap is not None else max(16, min(n, 1 << 16))
     for _ in range(3):
         text = torch.empty(max(cap, 16), dtype=torch.uint8, device="cuda")
-        off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
         status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         errs = torch.empty(ecap * 256, dtype=torch.uint8, device="cuda")
         if kind == "disasm":
             rc = L.skg_disasm(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
-                              opts, batch.max_words, text.data_ptr(), cap, off.data_ptr(),
+                              opts, batch.max_words, text.data_ptr(), cap, span.data_ptr(),
                               status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes, _stream())
         else:
             rc = L.skg_validate(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
-                                batch.max_words, text.data_ptr(), cap, off.data_ptr(),
+                                batch.max_words, text.data_ptr(), cap, span.data_ptr(),
                                 status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes,
                                 _stream())
         _check(rc, kind)
-        nerr, over = ctypes.c_uint32(), ctypes.c_uint32()
-        _check(L.skg_last_counts(ws.data_ptr(), ctypes.byref(nerr), ctypes.byref(over), _stream()), "counts")
-        if n == 0:
-            off.zero_()
-        need = int(off[n].item()) if n else 0
-        if over.value or nerr.value > ecap:
-            cap = max(cap, need + 16)
-            ecap = max(ecap, int(nerr.value))
+        nerr, over, used = last_counts(ws)
+        if over or nerr > ecap:
+            cap = max(cap, used + 16)
+            ecap = max(ecap, nerr)
             continue
-        return TextResult(text[:need], off, status[:n], errs[: nerr.value * 256])
+        return TextResult(text[:used], span[: 2 * n], status[:n], errs[: nerr * 256])
     raise RuntimeError(f"libskgpu {kind}: output capacity retry failed")
 
 
@@ -231,7 +235,7 @@ def make_exception(status, msg, a=0, b=0, c=0, d=0):
 
 def fetch_texts(res: TextResult, n: int):
     """Host copies: list of (text bytes | exception) per module."""
-    off = res.off.cpu().numpy()
+    span = res.span.cpu().numpy()
     status = res.status.cpu().numpy()
     text = res.text.cpu().numpy().tobytes()
     errs = decode_errors(res.errors.cpu().numpy()) if res.errors.numel() else {}
@@ -240,7 +244,8 @@ def fetch_texts(res: TextResult, n: int):
         if status[m] != ST_OK:
             out.append(errs.get(m) or make_exception(int(status[m]), "error record dropped"))
         else:
-            out.append(text[off[m]:off[m + 1]])
+            o = int(span[2 * m])
+            out.append(text[o:o + int(span[2 * m + 1])])
     return out
 
 
@@ -276,3 +281,62 @@ def run_decode(data: bytes):
 
 __all__ = ["lib", "DeviceBatch", "run_disasm", "run_validate", "run_decode", "fetch_texts",
            "make_exception", "NativeUnavailable", "tables_handle", "struct"]
+
+
+class DisasmPlan:
+    """Preallocated device outputs for repeated launches over one DeviceBatch.
+
+    ``launch()`` enqueues the workspace reset + ``skg_disasm`` on the current
+    stream and returns immediately (no host synchronisation), which is what the
+    benchmark times.  ``check()`` synchronises and verifies capacity/error counts.
+    """
+
+    def __init__(self, batch: DeviceBatch, opts: int, spec=None, ext=None, text_cap=None,
+                 kind: str = "disasm"):
+        torch = _torch()
+        self.kind = kind
+        self.batch, self.opts = batch, opts
+        self.th = tables_handle(spec, ext)
+        n = batch.n
+        self.ws_bytes = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        self.cap = text_cap if text_cap is not None else 6 * batch.total_bytes + 4096
+        self.text = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
+        self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
+        self.status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        self.ecap = max(16, min(n, 1 << 16))
+        self.errs = torch.empty(self.ecap * 256, dtype=torch.uint8, device="cuda")
+
+    def launch(self, stream=None):
+        b = self.batch
+        s = stream if stream is not None else _stream()
+        if self.kind == "disasm":
+            rc = lib().skg_disasm(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n,
+                                  self.opts, b.max_words, self.text.data_ptr(), self.cap,
+                                  self.span.data_ptr(), self.status.data_ptr(), self.errs.data_ptr(),
+                                  self.ecap, self.ws.data_ptr(), self.ws_bytes, s)
+        else:
+            rc = lib().skg_validate(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n,
+                                    b.max_words, self.text.data_ptr(), self.cap, self.span.data_ptr(),
+                                    self.status.data_ptr(), self.errs.data_ptr(), self.ecap,
+                                    self.ws.data_ptr(), self.ws_bytes, s)
+        _check(rc, self.kind)
+
+    def check(self):
+        nerr, over, used = last_counts(self.ws)
+        return {"errors": nerr, "overflow": over, "text_bytes": used}
+
+    def grow(self, need):
+        torch = _torch()
+        self.cap = need + 16
+        self.text = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
+
+    def fit(self):
+        """Run once and shrink/grow the text arena to the exact size needed."""
+        self.launch()
+        info = self.check()
+        if info["overflow"] or info["text_bytes"] + 16 != self.cap:
+            self.grow(info["text_bytes"])
+            self.launch()
+            info = self.check()
+        return info

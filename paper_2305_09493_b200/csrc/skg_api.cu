@@ -23,7 +23,7 @@ struct skg_tables {
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
-constexpr uint32_t kSlabBytes = 24 * 1024;
+constexpr uint32_t kSlabBytes = 18 * 1024;
 
 int g_sms = 0;
 
@@ -38,27 +38,31 @@ int sm_count() {
 }
 
 uint32_t grid_blocks() {
-  // persistent grid: 2 blocks of 4 warps per SM (24 KB shared slab per warp)
-  return (uint32_t)sm_count() * 2;
+  // persistent grid: 3 blocks of 4 warps per SM (16 KB shared slab per warp)
+  return (uint32_t)sm_count() * 3;
 }
 
-uint64_t slot_bytes(uint32_t max_words) {
-  return (skg::worst_bytes(max_words) + 255) & ~(uint64_t)255;
+uint64_t gslot_bytes(uint32_t max_words) {
+  return (skg::worst_bytes(max_words, skg::RENDER_MIN) + 255) & ~(uint64_t)255;
 }
+
+constexpr uint64_t kTextScratch = 64 * 1024;   // per-warp module text scratch
 
 struct WsLayout {
-  uint64_t state, counters, scratch, total, slot;
+  uint64_t state, counters, scratch, total, slot, gtext;
   uint32_t n_warps;
 };
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
+  (void)n_mod;
   l.n_warps = grid_blocks() * kWarpsPerBlock;
-  l.slot = slot_bytes(max_words);
+  l.slot = gslot_bytes(max_words);
   l.counters = 0;
-  l.state = 256;
-  l.scratch = (l.state + 8ull * (n_mod + 1) + 255) & ~255ull;
-  l.total = l.scratch + l.slot * l.n_warps;
+  l.state = 0;
+  l.scratch = 256;
+  l.gtext = l.scratch + l.slot * l.n_warps;
+  l.total = l.gtext + kTextScratch * l.n_warps;
   return l;
 }
 
@@ -119,19 +123,21 @@ uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words) {
   return ws_layout(n_mod, max_words).total;
 }
 
-int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow, void* stream) {
-  uint32_t c[4];
+int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow,
+                    uint64_t* text_bytes, void* stream) {
+  uint32_t c[6];
   cudaStream_t s = (cudaStream_t)stream;
-  if (int e = check(cudaMemcpyAsync(c, workspace, 16, cudaMemcpyDeviceToHost, s))) return e;
+  if (int e = check(cudaMemcpyAsync(c, workspace, 24, cudaMemcpyDeviceToHost, s))) return e;
   if (int e = check(cudaStreamSynchronize(s))) return e;
   if (n_errors) *n_errors = c[1];
   if (text_overflow) *text_overflow = c[2];
+  if (text_bytes) *text_bytes = (uint64_t)c[4] | ((uint64_t)c[5] << 32);
   return 0;
 }
 
 int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
-               uint8_t* text, uint64_t text_cap, int64_t* text_off, int32_t* status,
+               uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
                skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
                void* stream) {
   if (!t || !workspace) return -1;
@@ -144,13 +150,14 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   skg::DisasmArgs a;
   a.T = t->t;
   a.data = data; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod; a.opts = opts;
-  a.text = text; a.text_cap = text_cap; a.text_off = text_off; a.status = status;
-  a.state = reinterpret_cast<unsigned long long*>(ws + l.state);
+  a.text = text; a.text_cap = text_cap; a.text_span = text_span; a.status = status;
   a.ticket = reinterpret_cast<uint32_t*>(ws + l.counters);
   a.errs = reinterpret_cast<skg::ErrRec*>(errors);
   a.err_cap = err_cap;
   a.gscratch = ws + l.scratch;
   a.gslot_bytes = l.slot;
+  a.gtext = ws + l.gtext;
+  a.gtext_bytes = kTextScratch;
   a.smem_slab = kSlabBytes;
   const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
   static bool attr = false;
@@ -164,7 +171,7 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
 
 int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                  const int64_t* mod_len, uint32_t n_mod, uint32_t max_words, uint8_t* text,
-                 uint64_t text_cap, int64_t* text_off, int32_t* status, skg_error* errors,
+                 uint64_t text_cap, int64_t* text_span, int32_t* status, skg_error* errors,
                  uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream) {
   if (!t || !workspace) return -1;
   WsLayout l = ws_layout(n_mod, max_words);
@@ -176,8 +183,7 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   skg::ValidateArgs a;
   a.T = t->t;
   a.data = data; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod;
-  a.text = text; a.text_cap = text_cap; a.text_off = text_off; a.status = status;
-  a.state = reinterpret_cast<unsigned long long*>(ws + l.state);
+  a.text = text; a.text_cap = text_cap; a.text_span = text_span; a.status = status;
   a.ticket = reinterpret_cast<uint32_t*>(ws + l.counters);
   a.errs = reinterpret_cast<skg::ErrRec*>(errors);
   a.err_cap = err_cap;

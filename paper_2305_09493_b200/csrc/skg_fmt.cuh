@@ -240,28 +240,54 @@ SKG_HD inline void shortest_decimal(uint64_t bits, uint64_t& out_digits, int32_t
   out_exp = exp;
 }
 
-// CPython repr(float) of a double given by its bits (disasm.py:93-94).
-template <class S>
-SKG_HD inline void put_repr_double(S& s, uint64_t bits) {
-  const bool neg = bits >> 63;
-  const uint32_t e = (uint32_t)((bits >> 52) & 0x7FF);
-  const uint64_t m = bits & ((1ull << 52) - 1);
-  if (e == 0x7FF) {
-    if (m) { put_cstr(s, "nan"); return; }
-    if (neg) s.put('-');
-    put_cstr(s, "inf");
-    return;
-  }
-  if (neg) s.put('-');
-  if (e == 0 && m == 0) { put_cstr(s, "0.0"); return; }
+// CPython repr(float) pieces of a double: kind 0 finite nonzero, 1 nan, 2 inf, 3 zero.
+struct FloatParts {
   uint64_t digits;
   int32_t exp;
-  shortest_decimal(bits, digits, exp);
+  uint8_t kind;
+  bool neg;
+};
+
+SKG_HD inline FloatParts repr_parts(uint64_t bits) {
+  FloatParts p;
+  p.neg = bits >> 63;
+  const uint32_t e = (uint32_t)((bits >> 52) & 0x7FF);
+  const uint64_t m = bits & ((1ull << 52) - 1);
+  p.digits = 0; p.exp = 0;
+  if (e == 0x7FF) { p.kind = m ? 1 : 2; if (m) p.neg = false; return p; }
+  if (e == 0 && m == 0) { p.kind = 3; return p; }
+  p.kind = 0;
+  shortest_decimal(bits, p.digits, p.exp);
+  return p;
+}
+
+// length of repr() text (disasm.py:93-94 / float_repr_style 'short')
+SKG_HD inline uint32_t repr_len(const FloatParts& p) {
+  const uint32_t sgn = p.neg ? 1 : 0;
+  if (p.kind != 0) return sgn + 3;                        // nan / inf / 0.0
+  const int32_t n = (int32_t)dec_len_u64(p.digits);
+  const int32_t decpt = n + p.exp;
+  if (decpt <= -4 || decpt > 16) {
+    int32_t x = decpt - 1;
+    uint32_t xl = dec_len_u64((uint64_t)(x < 0 ? -x : x));
+    return sgn + 1 + (n > 1 ? (uint32_t)n : 0) + 2 + (xl < 2 ? 2 : xl);
+  }
+  if (decpt <= 0) return sgn + 2 + (uint32_t)(-decpt) + (uint32_t)n;
+  if (decpt < n) return sgn + (uint32_t)n + 1;
+  return sgn + (uint32_t)decpt + 2;
+}
+
+template <class S>
+SKG_HD inline void put_repr_parts(S& s, const FloatParts& p) {
+  if (p.kind == 1) { put_cstr(s, "nan"); return; }
+  if (p.neg) s.put('-');
+  if (p.kind == 2) { put_cstr(s, "inf"); return; }
+  if (p.kind == 3) { put_cstr(s, "0.0"); return; }
   char buf[20];
   int n = 0;
-  { uint64_t v = digits; do { buf[n++] = (char)('0' + v % 10); v /= 10; } while (v); }
+  { uint64_t v = p.digits; do { buf[n++] = (char)('0' + v % 10); v /= 10; } while (v); }
   // buf holds digits reversed; value = 0.d1..dn * 10^decpt
-  const int32_t decpt = n + exp;
+  const int32_t decpt = n + p.exp;
   if (decpt <= -4 || decpt > 16) {
     s.put((uint8_t)buf[n - 1]);
     if (n > 1) {
@@ -290,6 +316,12 @@ SKG_HD inline void put_repr_double(S& s, uint64_t bits) {
   for (int i = n - 1; i >= 0; --i) s.put((uint8_t)buf[i]);
   for (int32_t i = n; i < decpt; ++i) s.put('0');
   s.put('.'); s.put('0');
+}
+
+// CPython repr(float) of a double given by its bits (disasm.py:93-94).
+template <class S>
+SKG_HD inline void put_repr_double(S& s, uint64_t bits) {
+  put_repr_parts(s, repr_parts(bits));
 }
 
 // f16 / f32 bits widened to double bits (struct '<e' / '<f' unpack, codec.py:174-178)

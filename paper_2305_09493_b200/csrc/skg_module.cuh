@@ -43,68 +43,86 @@ enum : uint8_t { IF_PRESCAN_UTF8 = 1, IF_HAS_RESULT = 2, IF_EXT_KNOWN = 4, IF_FI
 enum : uint8_t { HF_NAMED_D = 1, HF_P0 = 2, HF_KEPT = 4, HF_FRIENDLY = 8 };
 
 struct Mod {
-  uint8_t* base;          // scratch base (header)
+  uint8_t* base;          // scratch base (64-byte header of counters)
   uint32_t* w;            // words (normalised to little-endian values)
   uint32_t W;
   uint32_t* ioff;         // instruction start word offsets, I entries
   uint32_t I;
+  // per instruction
   uint16_t* idef;
   uint8_t* iflag;
   uint8_t* ierr;
   uint8_t* isec;
   uint32_t* ia;
   uint32_t* ib;
-  uint32_t* irl;
-  uint32_t* nrec;         // 6 words per named definition
-  int32_t* pos;           // closed-form demotion array / taken set
-  uint32_t npos;
+  uint16_t* irl;
+  // per id "slot": direct mode slot = id (ids < bound, the canonical case);
+  // hash mode (any id >= bound seen): open addressing over hkey, slot C holds 0xFFFFFFFF
+  bool direct;
+  uint32_t S;             // number of slots
+  uint32_t C, shift;      // hash mode
   uint32_t* hkey;
-  uint32_t* hdef;
-  uint32_t* hti;
-  uint32_t* hvt;
-  uint32_t* hname;
-  uint32_t* himp;
-  uint32_t* hser;
-  uint32_t* hrl;
-  uint8_t* hA;
+  uint32_t* hdef;         // first definition (instruction index)
+  uint32_t* hti;          // type_info: last OpTypeInt/OpTypeFloat
+  uint32_t* hvt;          // value_type: last instruction with this result
+  uint32_t* hname;        // first decodable OpName
+  uint32_t* himp;         // last decodable OpExtInstImport
+  uint32_t* hser;         // friendly-name serial (NONE32: bare base)
+  uint32_t* nH;           // sanitized-name hash / prefix hash / length
+  uint32_t* nP;
+  uint32_t* nLen;
+  uint32_t* ndl;          // named definitions in D order (slots)
+  int32_t* pos;           // closed-form demotion scan, S + 2 entries
+  uint16_t* hrl;          // friendly ref length
+  uint8_t* hA;            // referenced by a decodable instruction
   uint8_t* hfl;
-  uint32_t C, shift;
-  uint32_t* fill;         // in the scratch header
+  uint8_t* hpres;         // slot in use
+  uint8_t* spill;         // global scratch for the rare sequential name-dedup path
+  uint8_t* work;          // name-resolution arrays, then the render workspace
+  uint32_t work_bytes;
+  bool work_shared;       // work region is in shared memory
+  uint32_t* fill;         // header counters
   uint32_t* overflow;
-  uint32_t* top_present;  // entry for key 0xFFFFFFFF lives in the dedicated slot C
+  uint32_t* top_present;
   uint32_t major, minor, gen, bound, schema;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// bytes needed before the per-module tables: header + words + instruction offsets
-__host__ __device__ inline size_t head_bytes(uint32_t W) {
+// Scratch layout of one module (shared slab or global slot):
+//   [64 B counters][words: W][instruction offsets: I+1][per-instruction arrays]
+//   [per-id slot arrays][work: friendly-name arrays, later the render workspace]
+__host__ __device__ inline size_t head_bytes(uint32_t W) {      // before the boundary walk
   return 64 + align16(4ull * W) + align16(4ull * (W > 5 ? W - 5 : 1) + 4);
 }
-
-__host__ __device__ inline uint32_t table_capacity(uint32_t I) {
-  uint32_t need = I + I / 2 + 8;
-  uint32_t c = 64;
-  while (c < need) c <<= 1;
-  return c;
+__host__ __device__ inline size_t head_used(uint32_t W, uint32_t I) {
+  return 64 + align16(4ull * W) + align16(4ull * (I + 1));
 }
-
-__host__ __device__ inline size_t tables_bytes(uint32_t I, uint32_t C) {
-  size_t n = 0;
-  n += align16(2ull * I) + 3 * align16(1ull * I) + 3 * align16(4ull * I);   // idef, iflag/ierr/isec, ia/ib/irl
-  n += align16(24ull * I);                                                  // nrec
-  uint32_t npos = C + I + 2 > 8 * I + 8 ? C + I + 2 : 8 * I + 8;
-  n += align16(4ull * npos);
-  n += 8 * align16(4ull * (C + 1)) + 2 * align16(C + 1);
-  return n;
+__host__ __device__ inline size_t inst_bytes(uint32_t I) {
+  return align16(2ull * I) + 3 * align16(1ull * I) + 2 * align16(4ull * I) + align16(2ull * I);
 }
-
-// worst-case scratch for a module of W words (I <= W-5, table sized for W ids)
-__host__ __device__ inline size_t worst_bytes(uint32_t W) {
-  uint32_t I = W > 5 ? W - 5 : 0;
+__host__ __device__ inline size_t slot_bytes(uint32_t S, bool hash) {
+  return (hash ? align16(4ull * S) : 0) + 6 * align16(4ull * S) + align16(2ull * S) +
+         3 * align16(1ull * S);
+}
+__host__ __device__ inline size_t names_bytes(uint32_t S) {
+  return 4 * align16(4ull * S) + align16(4ull * (S + 2));
+}
+__host__ __device__ inline size_t spill_bytes(uint32_t I) { return 32ull * I + 64; }
+__host__ __device__ inline uint32_t hash_capacity(uint32_t W) {
   uint32_t C = 64;
   while (C < 2 * W + 8) C <<= 1;
-  return head_bytes(W) + tables_bytes(I, C);
+  return C;
+}
+__host__ __device__ inline size_t work_need(uint32_t S, size_t work_min) {
+  size_t nb = names_bytes(S);
+  return nb > work_min ? nb : work_min;
+}
+// worst case for a module of W words: hash mode in the global slot
+__host__ __device__ inline size_t worst_bytes(uint32_t W, size_t work_min) {
+  uint32_t I = W > 5 ? W - 5 : 0;
+  uint32_t S = hash_capacity(W) + 1;
+  return head_bytes(W) + inst_bytes(I) + slot_bytes(S, true) + work_need(S, work_min) + spill_bytes(I);
 }
 
 __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
@@ -117,8 +135,15 @@ __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
   m.ioff = reinterpret_cast<uint32_t*>(base + 64 + align16(4ull * W));
 }
 
-__device__ inline void layout_tables(Mod& m, uint32_t C) {
-  uint8_t* p = m.base + head_bytes(m.W);
+__device__ inline size_t tables_need(const Mod& m, bool direct, uint32_t S_or_C, size_t work_min) {
+  const uint32_t S = direct ? S_or_C : S_or_C + 1;
+  return head_used(m.W, m.I) + inst_bytes(m.I) + slot_bytes(S, !direct) + work_need(S, work_min);
+}
+
+// lay out per-instruction, per-slot and work arrays after the instruction offsets
+__device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_t region_bytes,
+                                     size_t work_min) {
+  uint8_t* p = m.base + head_used(m.W, m.I);
   const uint32_t I = m.I;
   auto take = [&](size_t bytes) { uint8_t* r = p; p += align16(bytes); return r; };
   m.idef = reinterpret_cast<uint16_t*>(take(2ull * I));
@@ -127,24 +152,40 @@ __device__ inline void layout_tables(Mod& m, uint32_t C) {
   m.isec = take(I);
   m.ia = reinterpret_cast<uint32_t*>(take(4ull * I));
   m.ib = reinterpret_cast<uint32_t*>(take(4ull * I));
-  m.irl = reinterpret_cast<uint32_t*>(take(4ull * I));
-  m.nrec = reinterpret_cast<uint32_t*>(take(24ull * I));
-  m.npos = C + I + 2 > 8 * I + 8 ? C + I + 2 : 8 * I + 8;
-  m.pos = reinterpret_cast<int32_t*>(take(4ull * m.npos));
-  m.hkey = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hdef = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hti = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hvt = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hname = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.himp = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hser = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hrl = reinterpret_cast<uint32_t*>(take(4ull * (C + 1)));
-  m.hA = take(C + 1);
-  m.hfl = take(C + 1);
-  m.C = C;
-  uint32_t lg = 0;
-  while ((1u << lg) < C) ++lg;
-  m.shift = 32 - lg;
+  m.irl = reinterpret_cast<uint16_t*>(take(2ull * I));
+  m.direct = direct;
+  if (direct) {
+    m.S = S_or_C; m.C = 0; m.shift = 0; m.hkey = nullptr;
+  } else {
+    m.C = S_or_C; m.S = S_or_C + 1;
+    uint32_t lg = 0;
+    while ((1u << lg) < m.C) ++lg;
+    m.shift = 32 - lg;
+    m.hkey = reinterpret_cast<uint32_t*>(take(4ull * m.S));
+  }
+  const uint32_t S = m.S;
+  m.hdef = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.hti = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.hvt = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.hname = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.himp = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.hser = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.hrl = reinterpret_cast<uint16_t*>(take(2ull * S));
+  m.hA = take(S);
+  m.hfl = take(S);
+  m.hpres = take(S);
+  // work region: the friendly-name arrays live here during name resolution;
+  // the render workspace reuses the same bytes afterwards
+  m.work = p;
+  const size_t used = (size_t)(p - m.base);
+  size_t wb = work_need(S, work_min);
+  if (region_bytes > used + wb) wb = region_bytes - used;
+  m.work_bytes = (uint32_t)wb;
+  m.nH = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.nP = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.nLen = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.ndl = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.pos = reinterpret_cast<int32_t*>(take(4ull * (S + 2)));
 }
 
 // -- warp helpers -------------------------------------------------------------
@@ -184,12 +225,13 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// -- id hash table --------------------------------------------------------------
+// -- id table -------------------------------------------------------------------
 __device__ __forceinline__ uint32_t ht_home(const Mod& m, uint32_t key) {
   return (key * 0x9E3779B1u) >> m.shift;
 }
 
 __device__ inline uint32_t ht_find(const Mod& m, uint32_t key) {
+  if (m.direct) return (key < m.S && m.hpres[key]) ? key : NONE32;
   if (key == EMPTY) return *m.top_present ? m.C : NONE32;   // dedicated slot for 0xFFFFFFFF
   uint32_t s = ht_home(m, key);
   for (uint32_t probe = 0; probe < m.C; ++probe) {
@@ -202,8 +244,14 @@ __device__ inline uint32_t ht_find(const Mod& m, uint32_t key) {
 }
 
 __device__ inline uint32_t ht_insert(const Mod& m, uint32_t key) {
+  if (m.direct) {
+    if (key < m.S) { m.hpres[key] = 1; return key; }
+    *m.overflow = 1;
+    return NONE32;
+  }
   if (key == EMPTY) {
     *m.top_present = 1;
+    m.hpres[m.C] = 1;
     return m.C;
   }
   uint32_t s = ht_home(m, key);
@@ -212,17 +260,19 @@ __device__ inline uint32_t ht_insert(const Mod& m, uint32_t key) {
     if (k == key) return s;
     if (k == EMPTY) {
       uint32_t old = atomicCAS(&m.hkey[s], EMPTY, key);
-      if (old == EMPTY) {
-        uint32_t f = atomicAdd(m.fill, 1u) + 1;
-        if (f * 4 > m.C * 3) *m.overflow = 1;
-        return s;
-      }
+      if (old == EMPTY) { m.hpres[s] = 1; return s; }
       if (old == key) return s;
     }
     s = (s + 1) & (m.C - 1);
   }
   *m.overflow = 1;
   return NONE32;
+}
+
+// key held by a slot (valid when hpres[slot])
+__device__ __forceinline__ uint32_t slot_key(const Mod& m, uint32_t s) {
+  if (m.direct) return s;
+  return s < m.C ? m.hkey[s] : EMPTY;
 }
 
 // -- instruction accessors ------------------------------------------------------
@@ -385,14 +435,45 @@ __device__ inline int32_t load_and_split(Mod& m, const uint8_t* src, uint64_t nb
 
 __device__ inline void init_tables(Mod& m) {
   const uint32_t lane = lane_id();
-  for (uint32_t s = lane; s <= m.C; s += 32) {
-    m.hkey[s] = EMPTY;
+  for (uint32_t s = lane; s < m.S; s += 32) {
+    if (!m.direct) m.hkey[s] = EMPTY;
     m.hdef[s] = NONE32; m.hti[s] = NONE32; m.hvt[s] = NONE32; m.hname[s] = NONE32;
-    m.himp[s] = NONE32; m.hser[s] = NONE32; m.hrl[s] = 0;
-    m.hA[s] = 0; m.hfl[s] = 0;
+    m.himp[s] = NONE32; m.hser[s] = NONE32;
+    m.hA[s] = 0; m.hfl[s] = 0; m.hpres[s] = 0;
   }
   if (lane == 0) { *m.fill = 0; *m.overflow = 0; *m.top_present = 0; }
   __syncwarp();
+}
+
+// move words + offsets from the shared slab to the global slot
+__device__ inline void move_to_global(Mod& m, uint8_t* gslot) {
+  Mod g;
+  layout_head(g, gslot, m.W);
+  for (uint32_t k = lane_id(); k < m.W; k += 32) g.w[k] = m.w[k];
+  for (uint32_t k = lane_id(); k < m.I; k += 32) g.ioff[k] = m.ioff[k];
+  g.I = m.I; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
+  __syncwarp();
+  m = g;
+}
+
+// Lay out the id tables (direct when ids fit below the header bound, hash
+// otherwise), moving to the global slot when the shared slab is too small.
+// Returns false if even the global slot cannot hold the module.
+__device__ inline bool place_tables(Mod& m, bool direct, bool& in_smem, uint8_t* gslot,
+                                    uint64_t gslot_bytes, uint32_t slab_bytes, size_t work_min) {
+  const uint32_t SC = direct ? m.bound : hash_capacity(m.W);
+  const size_t need = tables_need(m, direct, SC, work_min);
+  const size_t greg = gslot_bytes - spill_bytes(m.I);
+  if (in_smem && need > slab_bytes) {
+    if (need > greg) return false;
+    move_to_global(m, gslot);
+    in_smem = false;
+  }
+  if (!in_smem && need > greg) return false;
+  layout_tables(m, direct, SC, in_smem ? slab_bytes : greg, work_min);
+  m.work_shared = in_smem;
+  m.spill = gslot + greg;
+  return true;
 }
 
 // last-writer / first-writer within a chunk for equal keys
@@ -474,6 +555,21 @@ __device__ inline bool prescan(Mod& m, const Tables& T) {
     __syncwarp();
   }
   return __any_sync(FULL, any_name);
+}
+
+// Output placement: a bump allocator over the text arena.  Modules are
+// independent, so each warp reserves its module's bytes with one atomic and
+// never waits on another module (no ordering dependency between tickets).
+// counters: [0] ticket, [1] error count, [2] overflow flag, [4..5] u64 cursor
+__device__ inline uint64_t alloc_text(uint32_t* counters, uint64_t bytes, uint64_t cap, bool& fits) {
+  uint64_t off = 0;
+  if (lane_id() == 0 && bytes) {
+    off = atomicAdd(reinterpret_cast<unsigned long long*>(counters + 4), (unsigned long long)bytes);
+    if (off + bytes > cap) atomicExch(counters + 2, 1u);
+  }
+  off = __shfl_sync(FULL, off, 0);
+  fits = off + bytes <= cap;
+  return off;
 }
 
 // decoupled look-back over module tickets: returns the exclusive prefix of `agg`

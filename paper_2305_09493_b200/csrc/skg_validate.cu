@@ -20,9 +20,8 @@ struct ValidateArgs {
   uint32_t n_mod;
   uint8_t* text;
   uint64_t text_cap;
-  int64_t* text_off;
+  int64_t* text_span;
   int32_t* status;
-  unsigned long long* state;
   uint32_t* ticket;
   ErrRec* errs;
   uint32_t err_cap;
@@ -198,7 +197,7 @@ __device__ inline void shape_diags(S& s, const Shape& sh) {
   }
 }
 
-__global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
+__global__ void __launch_bounds__(128) validate_kernel(ValidateArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t warp_in_block = threadIdx.x >> 5;
@@ -224,7 +223,7 @@ __global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
     const uint32_t W = (nbytes >= 0 && nbytes % 4 == 0) ? (uint32_t)(nbytes / 4) : 0;
     bool in_smem = head_bytes(W) <= a.smem_slab;
     ErrRec* drec = nullptr;
-    if (!in_smem && worst_bytes(W) > a.gslot_bytes) {
+    if (!in_smem && worst_bytes(W, 0) > a.gslot_bytes) {
       status = ST_INTERNAL;
       if (lane == 0 && (drec = es.alloc())) {
         ErrWriter ew{drec};
@@ -236,28 +235,17 @@ __global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
       decode_status = load_and_split(m, src, (uint64_t)nbytes, nullptr, (int32_t)t);
     }
     if (status == ST_OK && decode_status == ST_OK) {
-      uint32_t C = table_capacity(m.I);
-      for (int attempt = 0; attempt < 3; ++attempt) {
-        if (head_bytes(m.W) + tables_bytes(m.I, C) > (in_smem ? a.smem_slab : a.gslot_bytes)) {
-          if (in_smem) {
-            Mod g;
-            layout_head(g, gslot, m.W);
-            for (uint32_t k = lane; k < m.W; k += 32) g.w[k] = m.w[k];
-            for (uint32_t k = lane; k < m.I; k += 32) g.ioff[k] = m.ioff[k];
-            g.I = m.I; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
-            __syncwarp();
-            m = g;
-            in_smem = false;
-          }
-          if (head_bytes(m.W) + tables_bytes(m.I, C) > a.gslot_bytes) { status = ST_INTERNAL; break; }
+      bool direct = m.bound <= 2 * m.W + 64;
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, 0)) {
+          status = ST_INTERNAL;
+          break;
         }
-        layout_tables(m, C);
         init_tables(m);
         prescan(m, T);
         if (*m.overflow) {
-          C = C * 4;
-          while (C < 2 * m.W + 8) C <<= 1;
           __syncwarp();
+          direct = false;
           continue;
         }
         // module shape + effective capabilities (validate.py:101-136)
@@ -366,13 +354,13 @@ __global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
         tmp.len = ew.n;
       }
       total = cs.n + (uint32_t)tmp.len + 1;
-      uint64_t off = lookback(a.state, t, total);
+      bool fits;
+      uint64_t off = alloc_text(a.ticket, total, a.text_cap, fits);
       if (lane == 0) {
-        a.text_off[t] = (int64_t)off;
+        a.text_span[2 * t] = (int64_t)off;
+        a.text_span[2 * t + 1] = (int64_t)total;
         a.status[t] = ST_OK;
-        if (t == a.n_mod - 1) a.text_off[a.n_mod] = (int64_t)(off + total);
-        if (off + total > a.text_cap) atomicExch(a.ticket + 2, 1u);
-        else {
+        if (fits) {
           MemSink ms(a.text + off);
           diag_head(ms, true, code, NONE32);
           ms.putn((const uint8_t*)tmp.msg, (uint32_t)tmp.len);
@@ -383,15 +371,15 @@ __global__ void __launch_bounds__(256) validate_kernel(ValidateArgs a) {
       continue;
     }
     if (status != ST_OK) total = 0;
-    uint64_t off = lookback(a.state, t, total);
+    bool fits;
+    uint64_t off = alloc_text(a.ticket, total, a.text_cap, fits);
     if (lane == 0) {
-      a.text_off[t] = (int64_t)off;
+      a.text_span[2 * t] = (int64_t)off;
+      a.text_span[2 * t + 1] = (int64_t)total;
       a.status[t] = status;
-      if (t == a.n_mod - 1) a.text_off[a.n_mod] = (int64_t)(off + total);
     }
     if (status == ST_OK && total > 0) {
-      if (off + total > a.text_cap) {
-        if (lane == 0) atomicExch(a.ticket + 2, 1u);
+      if (!fits) {
       } else {
         uint8_t* out = a.text + off;
         if (lane == 0) { MemSink ms(out); shape_diags(ms, sh); }

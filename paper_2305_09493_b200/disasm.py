@@ -10,6 +10,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _native
 
 
@@ -65,3 +67,85 @@ def disassemble_module(data: bytes, options=None, sink=None, spec=None, ext=None
                        strict: bool = False):
     tool = Disassembler(spec=spec, ext=ext, options=options, strict=strict)
     return tool.to_text(data) if sink is None else tool.disassemble(data, sink)
+
+
+class DisasmSession:
+    """Host-buffer batch API: packed modules in, packed text out.
+
+    ``run(data, offsets, lengths)`` takes a host byte arena (module starts
+    16-byte aligned) with int64 offsets/lengths, copies it to the device from
+    pinned memory, disassembles every module and copies the used text arena,
+    the per-module (offset, length) spans and statuses back (pinned).  Buffers
+    are reused across calls of the same shape.  Returns (text uint8[],
+    spans int64[n, 2], status int32[n]); module m's text is
+    text[spans[m, 0] : spans[m, 0] + spans[m, 1]].  Failing modules have
+    status != 0 and an empty span; ``errors()`` maps them to exceptions.
+    """
+
+    def __init__(self, options=None, spec=None, ext=None, strict=False):
+        self.opts = option_bits(options, strict)
+        self.spec, self.ext = spec, ext
+        self._key = None
+
+    def _prepare(self, data, offsets, lengths):
+        import torch
+        key = (data.nbytes, len(offsets), int(lengths.max()) if len(lengths) else 0)
+        if key == self._key:
+            return
+        n = len(offsets)
+        self.h_data = torch.empty(data.nbytes, dtype=torch.uint8).pin_memory()
+        self.h_meta = torch.empty(2 * n, dtype=torch.int64).pin_memory()
+        self.d_data = torch.empty(data.nbytes, dtype=torch.uint8, device="cuda")
+        self.d_meta = torch.empty(2 * n, dtype=torch.int64, device="cuda")
+        self.batch = _native.DeviceBatch(self.d_data, self.d_meta[:n], self.d_meta[n:],
+                                         key[2] // 4, int(lengths.sum()))
+        self.plan = _native.DisasmPlan(self.batch, self.opts, self.spec, self.ext,
+                                       text_cap=6 * int(lengths.sum()) + 4096)
+        self.h_span = torch.empty(2 * max(n, 1), dtype=torch.int64).pin_memory()
+        self.h_status = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
+        self.h_counts = torch.empty(8, dtype=torch.int32).pin_memory()
+        self.h_text = torch.empty(0, dtype=torch.uint8).pin_memory()
+        self._key = key
+
+    def stage(self, data, offsets, lengths):
+        """Host arrays -> pinned staging buffers (outside any timed region)."""
+        import numpy as np
+        self._prepare(data, offsets, lengths)
+        n = len(offsets)
+        self.h_data.numpy()[:] = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)
+        self.h_meta.numpy()[:n] = offsets
+        self.h_meta.numpy()[n:] = lengths
+
+    def run_staged(self):
+        """H2D of the staged inputs, kernel, D2H of text + spans + status."""
+        import torch
+        self.d_data.copy_(self.h_data, non_blocking=True)
+        self.d_meta.copy_(self.h_meta, non_blocking=True)
+        self.plan.launch()
+        n = self.batch.n
+        self.h_span.copy_(self.plan.span, non_blocking=True)
+        self.h_status.copy_(self.plan.status, non_blocking=True)
+        self.h_counts.copy_(self.plan.ws[:32].view(torch.int32), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        c = self.h_counts.numpy()
+        used = int(c[4]) & 0xFFFFFFFF | (int(c[5]) & 0xFFFFFFFF) << 32
+        if c[2]:   # arena overflow: grow and rerun
+            self.plan.grow(used)
+            self.plan.launch()
+            self.h_span.copy_(self.plan.span, non_blocking=True)
+        if self.h_text.numel() < used:
+            self.h_text = torch.empty(used, dtype=torch.uint8).pin_memory()
+        self.h_text[:used].copy_(self.plan.text[:used], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return (self.h_text[:used].numpy(), self.h_span[: 2 * n].numpy().reshape(n, 2),
+                self.h_status[:n].numpy())
+
+    def run(self, data, offsets, lengths):
+        self.stage(data, offsets, lengths)
+        return self.run_staged()
+
+    def errors(self):
+        """module index -> exception instance for the last run."""
+        info = self.plan.check()
+        ne = min(info["errors"], self.plan.ecap)
+        return _native.decode_errors(self.plan.errs[: ne * 256].cpu().numpy()) if ne else {}
