@@ -46,7 +46,6 @@ uint64_t gslot_bytes(uint32_t max_words) {
   return (skg::worst_bytes(max_words, skg::RENDER_MIN) + 255) & ~(uint64_t)255;
 }
 
-constexpr uint64_t kTextScratch = 64 * 1024;   // per-warp module text scratch
 
 struct WsLayout {
   uint64_t state, counters, scratch, total, slot, gtext;
@@ -61,8 +60,8 @@ WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   l.counters = 0;
   l.state = 0;
   l.scratch = 256;
-  l.gtext = l.scratch + l.slot * l.n_warps;
-  l.total = l.gtext + kTextScratch * l.n_warps;
+  l.gtext = 0;
+  l.total = l.scratch + l.slot * l.n_warps;
   return l;
 }
 
@@ -156,8 +155,6 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   a.err_cap = err_cap;
   a.gscratch = ws + l.scratch;
   a.gslot_bytes = l.slot;
-  a.gtext = ws + l.gtext;
-  a.gtext_bytes = kTextScratch;
   a.smem_slab = kSlabBytes;
   const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
   static bool attr = false;

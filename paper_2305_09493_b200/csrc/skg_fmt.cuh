@@ -8,6 +8,9 @@
 #ifndef SKG_HD
 #define SKG_HD __host__ __device__
 #endif
+#ifndef SKG_NOINLINE
+#define SKG_NOINLINE __noinline__
+#endif
 
 #include "skg_pow5.cuh"
 
@@ -16,30 +19,29 @@ namespace skg {
 // ---------------------------------------------------------------------------
 // Sinks.  Every renderer is templated on a sink so the size pass and the write
 // pass run the same code (disasm size-then-write).
-struct CountSink {
-  uint32_t n = 0;
-  SKG_HD void put(uint8_t) { ++n; }
-  SKG_HD void putn(const uint8_t*, uint32_t len) { n += len; }
-  SKG_HD void fill(uint8_t, uint32_t k) { n += k; }
-};
-
-struct MemSink {
+// One sink type for both passes keeps a single instantiation of every
+// renderer (code size matters: the kernels are instruction-fetch bound when
+// each visitor/sink pair is inlined separately).  p == nullptr counts only.
+struct Sink {
   uint8_t* p;
   uint32_t n = 0;
-  SKG_HD explicit MemSink(uint8_t* dst) : p(dst) {}
-  SKG_HD void put(uint8_t c) { p[n++] = c; }
+  SKG_HD explicit Sink(uint8_t* dst = nullptr) : p(dst) {}
+  SKG_HD void put(uint8_t c) { if (p) p[n] = c; ++n; }
   SKG_HD void putn(const uint8_t* s, uint32_t len) {
-    for (uint32_t i = 0; i < len; ++i) p[n + i] = s[i];
+    if (p) for (uint32_t i = 0; i < len; ++i) p[n + i] = s[i];
     n += len;
   }
   SKG_HD void fill(uint8_t c, uint32_t k) {
-    for (uint32_t i = 0; i < k; ++i) p[n + i] = c;
+    if (p) for (uint32_t i = 0; i < k; ++i) p[n + i] = c;
     n += k;
   }
 };
+using CountSink = Sink;
+using MemSink = Sink;
 
 template <class S>
-SKG_HD inline void put_cstr(S& s, const char* z) {
+SKG_HD SKG_NOINLINE void put_cstr(S& s, const char* z) {
+#pragma unroll 1
   while (*z) s.put((uint8_t)*z++);
 }
 
@@ -50,10 +52,12 @@ SKG_HD inline uint32_t dec_len_u64(uint64_t v) {
 }
 
 template <class S>
-SKG_HD inline void put_u64(S& s, uint64_t v) {
+SKG_HD SKG_NOINLINE void put_u64(S& s, uint64_t v) {
   char buf[20];
   int n = 0;
+#pragma unroll 1
   do { buf[n++] = (char)('0' + v % 10); v /= 10; } while (v);
+#pragma unroll 1
   while (n) s.put((uint8_t)buf[--n]);
 }
 
@@ -125,7 +129,7 @@ SKG_HD inline bool mult_pow2(uint64_t v, uint32_t p) { return p < 64 && (v & ((1
 
 // Decompose a finite nonzero double into (digits, exponent): value = digits * 10^exp,
 // digits shortest with round-half-even acceptance of the interval ends.
-SKG_HD inline void shortest_decimal(uint64_t bits, uint64_t& out_digits, int32_t& out_exp) {
+SKG_HD SKG_NOINLINE void shortest_decimal(uint64_t bits, uint64_t& out_digits, int32_t& out_exp) {
   const uint64_t ieee_m = bits & ((1ull << 52) - 1);
   const uint32_t ieee_e = (uint32_t)((bits >> 52) & 0x7FF);
   int32_t e2;
@@ -248,7 +252,7 @@ struct FloatParts {
   bool neg;
 };
 
-SKG_HD inline FloatParts repr_parts(uint64_t bits) {
+SKG_HD SKG_NOINLINE FloatParts repr_parts(uint64_t bits) {
   FloatParts p;
   p.neg = bits >> 63;
   const uint32_t e = (uint32_t)((bits >> 52) & 0x7FF);
@@ -262,7 +266,7 @@ SKG_HD inline FloatParts repr_parts(uint64_t bits) {
 }
 
 // length of repr() text (disasm.py:93-94 / float_repr_style 'short')
-SKG_HD inline uint32_t repr_len(const FloatParts& p) {
+SKG_HD SKG_NOINLINE uint32_t repr_len(const FloatParts& p) {
   const uint32_t sgn = p.neg ? 1 : 0;
   if (p.kind != 0) return sgn + 3;                        // nan / inf / 0.0
   const int32_t n = (int32_t)dec_len_u64(p.digits);
@@ -278,7 +282,7 @@ SKG_HD inline uint32_t repr_len(const FloatParts& p) {
 }
 
 template <class S>
-SKG_HD inline void put_repr_parts(S& s, const FloatParts& p) {
+SKG_HD SKG_NOINLINE void put_repr_parts(S& s, const FloatParts& p) {
   if (p.kind == 1) { put_cstr(s, "nan"); return; }
   if (p.neg) s.put('-');
   if (p.kind == 2) { put_cstr(s, "inf"); return; }
@@ -292,6 +296,7 @@ SKG_HD inline void put_repr_parts(S& s, const FloatParts& p) {
     s.put((uint8_t)buf[n - 1]);
     if (n > 1) {
       s.put('.');
+      #pragma unroll 1
       for (int i = n - 2; i >= 0; --i) s.put((uint8_t)buf[i]);
     }
     s.put('e');
@@ -303,17 +308,23 @@ SKG_HD inline void put_repr_parts(S& s, const FloatParts& p) {
   }
   if (decpt <= 0) {
     s.put('0'); s.put('.');
+    #pragma unroll 1
     for (int32_t i = 0; i < -decpt; ++i) s.put('0');
+    #pragma unroll 1
     for (int i = n - 1; i >= 0; --i) s.put((uint8_t)buf[i]);
     return;
   }
   if (decpt < n) {
+    #pragma unroll 1
     for (int i = n - 1; i >= n - decpt; --i) s.put((uint8_t)buf[i]);
     s.put('.');
+    #pragma unroll 1
     for (int i = n - decpt - 1; i >= 0; --i) s.put((uint8_t)buf[i]);
     return;
   }
+  #pragma unroll 1
   for (int i = n - 1; i >= 0; --i) s.put((uint8_t)buf[i]);
+  #pragma unroll 1
   for (int32_t i = n; i < decpt; ++i) s.put('0');
   s.put('.'); s.put('0');
 }
@@ -361,7 +372,7 @@ SKG_HD inline uint64_t f16_to_f64_bits(uint32_t h) {
 enum : uint32_t { U8_OK = 0, U8_START = 1, U8_CONT = 2, U8_END = 3 };
 
 template <class ByteAt>
-SKG_HD inline uint32_t utf8_check(const ByteAt& at, uint32_t len, uint32_t& start, uint32_t& end) {
+SKG_HD SKG_NOINLINE uint32_t utf8_check(const ByteAt& at, uint32_t len, uint32_t& start, uint32_t& end) {
   uint32_t s = 0;
   while (s < len) {
     uint32_t ch = at(s);

@@ -56,6 +56,7 @@ struct Mod {
   uint32_t* ia;
   uint32_t* ib;
   uint16_t* irl;
+  uint32_t* wk;           // per word render code (disassembler)
   // per id "slot": direct mode slot = id (ids < bound, the canonical case);
   // hash mode (any id >= bound seen): open addressing over hkey, slot C holds 0xFFFFFFFF
   bool direct;
@@ -101,6 +102,7 @@ __host__ __device__ inline size_t head_used(uint32_t W, uint32_t I) {
 __host__ __device__ inline size_t inst_bytes(uint32_t I) {
   return align16(2ull * I) + 3 * align16(1ull * I) + 2 * align16(4ull * I) + align16(2ull * I);
 }
+__host__ __device__ inline size_t word_bytes(uint32_t W) { return align16(4ull * W); }
 __host__ __device__ inline size_t slot_bytes(uint32_t S, bool hash) {
   return (hash ? align16(4ull * S) : 0) + 6 * align16(4ull * S) + align16(2ull * S) +
          3 * align16(1ull * S);
@@ -122,7 +124,8 @@ __host__ __device__ inline size_t work_need(uint32_t S, size_t work_min) {
 __host__ __device__ inline size_t worst_bytes(uint32_t W, size_t work_min) {
   uint32_t I = W > 5 ? W - 5 : 0;
   uint32_t S = hash_capacity(W) + 1;
-  return head_bytes(W) + inst_bytes(I) + slot_bytes(S, true) + work_need(S, work_min) + spill_bytes(I);
+  return head_bytes(W) + inst_bytes(I) + word_bytes(W) + slot_bytes(S, true) + work_need(S, work_min) +
+         spill_bytes(I);
 }
 
 __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
@@ -137,7 +140,8 @@ __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
 
 __device__ inline size_t tables_need(const Mod& m, bool direct, uint32_t S_or_C, size_t work_min) {
   const uint32_t S = direct ? S_or_C : S_or_C + 1;
-  return head_used(m.W, m.I) + inst_bytes(m.I) + slot_bytes(S, !direct) + work_need(S, work_min);
+  return head_used(m.W, m.I) + inst_bytes(m.I) + word_bytes(m.W) + slot_bytes(S, !direct) +
+         work_need(S, work_min);
 }
 
 // lay out per-instruction, per-slot and work arrays after the instruction offsets
@@ -153,6 +157,7 @@ __device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_
   m.ia = reinterpret_cast<uint32_t*>(take(4ull * I));
   m.ib = reinterpret_cast<uint32_t*>(take(4ull * I));
   m.irl = reinterpret_cast<uint16_t*>(take(2ull * I));
+  m.wk = reinterpret_cast<uint32_t*>(take(4ull * m.W));
   m.direct = direct;
   if (direct) {
     m.S = S_or_C; m.C = 0; m.shift = 0; m.hkey = nullptr;
@@ -285,7 +290,7 @@ __device__ __forceinline__ const uint32_t* inst_ops(const Mod& m, uint32_t i) { 
 struct Resolver {
   const Mod* m;
   const Tables* T;
-  __device__ Width rt(uint32_t id) const {
+  __device__ __noinline__ Width rt(uint32_t id) const {
     uint32_t s = ht_find(*m, id);
     if (s == NONE32 || m->hti[s] == NONE32) return Width{0, false, false, false};
     uint32_t j = m->hti[s];
@@ -294,11 +299,22 @@ struct Resolver {
     if (T->special(d) == SP_TYPEINT) return Width{ops[1], ops[2] == 1, false, true};
     return Width{ops[1], false, true, true};
   }
-  __device__ Width sel(uint32_t selector) const {
+  __device__ __noinline__ Width sel(uint32_t selector) const {
     uint32_t s = ht_find(*m, selector);
     if (s == NONE32 || m->hvt[s] == NONE32) return Width{0, false, false, false};
     return rt(inst_ops(*m, m->hvt[s])[0]);
   }
+};
+
+struct NullVis {
+  __device__ void id(uint32_t, uint32_t, int, uint32_t) {}
+  __device__ void venum(uint32_t, uint32_t, uint32_t, uint32_t) {}
+  __device__ void benum(uint32_t, uint32_t, bool, uint64_t, uint32_t) {}
+  __device__ void str(const uint32_t*, uint32_t, uint32_t) {}
+  __device__ void typed(const LitVal&, uint32_t, uint32_t) {}
+  __device__ void lit(uint32_t, uint32_t, uint32_t) {}
+  __device__ void comp_begin() {}
+  __device__ void comp_end() {}
 };
 
 // -- error records --------------------------------------------------------------
@@ -324,7 +340,7 @@ struct ErrSink {
 // Compose the str(exc) text of a walk error (ops.py:351-374, codec.py:127-129,
 // ops.py:420-422, CPython UnicodeDecodeError.__str__).
 template <class S>
-__device__ inline void put_walk_error(S& s, const Tables& T, uint32_t idef, const WalkErr& e) {
+__device__ __noinline__ void put_walk_error(S& s, const Tables& T, uint32_t idef, const WalkErr& e) {
   auto opname = [&]() { s.putn(T.str + T.iname_off(idef), T.iname_len(idef)); };
   switch (e.code) {
     case W_EXHAUSTED: opname(); put_cstr(s, ": operand words exhausted mid-instruction"); break;
@@ -359,7 +375,7 @@ __device__ inline int32_t walk_status(uint32_t code) {
 // ---------------------------------------------------------------------------
 // load + boundary.  Returns ST_OK or an error class; on error fills `err`
 // (on lane 0).  Words are loaded into m.w (already laid out via layout_head).
-__device__ inline int32_t load_and_split(Mod& m, const uint8_t* src, uint64_t nbytes, ErrSink* es,
+__device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint64_t nbytes, ErrSink* es,
                                          int32_t module) {
   const uint32_t lane = lane_id();
   ErrRec* err = nullptr;
@@ -433,7 +449,7 @@ __device__ inline int32_t load_and_split(Mod& m, const uint8_t* src, uint64_t nb
   return st;
 }
 
-__device__ inline void init_tables(Mod& m) {
+__device__ __noinline__ void init_tables(Mod& m) {
   const uint32_t lane = lane_id();
   for (uint32_t s = lane; s < m.S; s += 32) {
     if (!m.direct) m.hkey[s] = EMPTY;
@@ -459,7 +475,7 @@ __device__ inline void move_to_global(Mod& m, uint8_t* gslot) {
 // Lay out the id tables (direct when ids fit below the header bound, hash
 // otherwise), moving to the global slot when the shared slab is too small.
 // Returns false if even the global slot cannot hold the module.
-__device__ inline bool place_tables(Mod& m, bool direct, bool& in_smem, uint8_t* gslot,
+__device__ __noinline__ bool place_tables(Mod& m, bool direct, bool& in_smem, uint8_t* gslot,
                                     uint64_t gslot_bytes, uint32_t slab_bytes, size_t work_min) {
   const uint32_t SC = direct ? m.bound : hash_capacity(m.W);
   const size_t need = tables_need(m, direct, SC, work_min);
@@ -489,7 +505,7 @@ __device__ __forceinline__ bool group_first(bool part, uint32_t key) {
 }
 
 // prescan: returns whether any OpName was recorded
-__device__ inline bool prescan(Mod& m, const Tables& T) {
+__device__ __noinline__ bool prescan(Mod& m, const Tables& T) {
   const uint32_t lane = lane_id();
   bool any_name = false;
   for (uint32_t base = 0; base < m.I; base += 32) {

@@ -57,22 +57,13 @@ __device__ inline void put_req_repr(S& s, const Tables& T, uint32_t r) {
   s.putn(T.str + __ldg(rec), __ldg(rec + 1));
 }
 
-struct NullVis {
-  __device__ void id(uint32_t, uint32_t, int) {}
-  __device__ void venum(uint32_t, uint32_t, uint32_t) {}
-  __device__ void benum(uint32_t, uint32_t, bool, uint64_t) {}
-  __device__ void str(const uint32_t*, uint32_t, uint32_t) {}
-  __device__ void typed(const LitVal&) {}
-  __device__ void lit(uint32_t, uint32_t) {}
-  __device__ void comp_begin() {}
-  __device__ void comp_end() {}
-};
+
 
 template <class S>
 struct BoundVis : NullVis {
   S* s;
   uint32_t i, bound;
-  __device__ void id(uint32_t, uint32_t v, int) {
+  __device__ __noinline__ void id(uint32_t, uint32_t v, int, uint32_t) {
     if (v >= bound) {
       diag_head(*s, true, "BoundTooSmall", i);
       s->put('%'); put_u64(*s, v); put_cstr(*s, " is not below the header bound "); put_u64(*s, bound);
@@ -87,23 +78,23 @@ struct ReqVis : NullVis {
   const Tables* T;
   const uint64_t* eff;
   uint32_t i, d;
-  __device__ void line(uint32_t r) {
+  __device__ __noinline__ void line(uint32_t r) {
     diag_head(*s, true, "MissingCapability", i);
     s->putn(T->str + T->iname_off(d), T->iname_len(d));
     put_cstr(*s, " operand requires one of ");
     put_req_repr(*s, *T, r);
     s->put('\n');
   }
-  __device__ void venum(uint32_t, uint32_t, uint32_t e) {
+  __device__ __noinline__ void venum(uint32_t, uint32_t, uint32_t e, uint32_t) {
     if (e == NONE32) return;
     uint32_t r = T->emerged(e);
     if (unsatisfied(*T, r, eff)) line(r);
   }
-  __device__ void benum(uint32_t k, uint32_t mask, bool full, uint64_t comp) {
+  __device__ __noinline__ void benum(uint32_t k, uint32_t mask, bool full, uint64_t comp, uint32_t) {
     if (!full) return;
     uint32_t eo = T->kenum_off(k);
-    for (int j = 0; j < 64; ++j) {
-      if (!((comp >> j) & 1)) continue;
+    for (uint64_t rest = comp; rest; rest &= rest - 1) {
+      const int j = __ffsll((long long)rest) - 1;
       uint32_t r = T->ereq(eo + j);
       if (unsatisfied(*T, r, eff)) line(r);
     }
@@ -112,7 +103,7 @@ struct ReqVis : NullVis {
 
 // all located diagnostics of instruction i; returns the walk status
 template <class S>
-__device__ inline WalkErr inst_diags(S& s, const Mod& m, const Tables& T, uint32_t i,
+__device__ __noinline__ WalkErr inst_diags(S& s, const Mod& m, const Tables& T, uint32_t i,
                                      const uint64_t* eff) {
   const uint32_t d = m.idef[i];
   const uint32_t* ops = inst_ops(m, i);
@@ -183,7 +174,7 @@ struct Shape {
 };
 
 template <class S>
-__device__ inline void shape_diags(S& s, const Shape& sh) {
+__device__ __noinline__ void shape_diags(S& s, const Shape& sh) {
   if (!sh.has_fn) { diag_head(s, true, "MissingFunction", NONE32); put_cstr(s, "module declares no function\n"); }
   if (!sh.has_cap) { diag_head(s, true, "MissingCapability", NONE32); put_cstr(s, "module declares no capability\n"); }
   if (sh.n_mm == 0) { diag_head(s, true, "MissingMemoryModel", NONE32); put_cstr(s, "module has no memory model\n"); }

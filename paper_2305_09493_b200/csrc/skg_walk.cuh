@@ -30,7 +30,7 @@ struct Width {
 
 // Bytes of a NUL-terminated literal starting at ops[pos]; returns false if no
 // NUL byte occurs before ops[n] (codec.py:117-129).
-__device__ inline bool string_span(const uint32_t* ops, uint32_t pos, uint32_t n,
+__device__ __noinline__ bool string_span(const uint32_t* ops, uint32_t pos, uint32_t n,
                                    uint32_t& nbytes, uint32_t& next) {
   for (uint32_t i = pos; i < n; ++i) {
     uint32_t w = ops[i];
@@ -50,7 +50,7 @@ struct WordBytes {
   __device__ uint32_t operator()(uint32_t i) const { return (w[i >> 2] >> ((i & 3) * 8)) & 0xFF; }
 };
 
-__device__ inline uint32_t string_utf8(const uint32_t* ops, uint32_t pos, uint32_t nbytes, WalkErr& err) {
+__device__ __noinline__ uint32_t string_utf8(const uint32_t* ops, uint32_t pos, uint32_t nbytes, WalkErr& err) {
   WordBytes at{ops + pos};
   uint32_t s = 0, e = 0;
   uint32_t r = utf8_check(at, nbytes, s, e);
@@ -66,10 +66,14 @@ struct LitVal {
   bool flt;
   bool neg;           // int only
   bool wide_unsigned; // int: value >= 2^63 unsigned
+  bool sgn;           // governing type (width, signedness)
+  uint32_t width;
 };
 
-__device__ inline bool decode_typed(const uint32_t* raw, uint32_t width, bool sgn, bool flt,
+__device__ __noinline__ bool decode_typed(const uint32_t* raw, uint32_t width, bool sgn, bool flt,
                                     LitVal& out, WalkErr& err) {
+  out.sgn = sgn;
+  out.width = width;
   if (flt) {
     out.flt = true; out.neg = false; out.wide_unsigned = false;
     if (width == 64) { out.bits = (uint64_t)raw[0] | ((uint64_t)raw[1] << 32); return true; }
@@ -101,17 +105,17 @@ __device__ inline bool decode_typed(const uint32_t* raw, uint32_t width, bool sg
 constexpr uint32_t STACK_MARK = 0xFFFFFFFFu;   // composite end marker
 constexpr int WALK_STACK = 48;
 
-// Visitor interface (all __device__):
-//   id(role, value, depth)          role IDR_*
-//   venum(kind, value, enum_index)  enum_index NONE32 if unknown
-//   benum(kind, mask, full)         full: covered by enumerants (components exist)
+// Visitor interface (all __device__; p = operand word index of the event):
+//   id(role, value, depth, p)           role IDR_*
+//   venum(kind, value, enum_index, p)   enum_index NONE32 if unknown
+//   benum(kind, mask, full, comp, p)    full: covered by enumerants (comp = positions)
 //   str(ops, word_pos, nbytes)
-//   typed(LitVal)                   ctx number / OpSwitch literal
-//   lit(sub, value)                 LIT_PLAIN / LIT_EXTINST / LIT_SPECOP / LIT_INTEGER
+//   typed(LitVal, p, nwords)            ctx number / OpSwitch literal
+//   lit(sub, value, p)                  LIT_PLAIN / LIT_EXTINST / LIT_SPECOP / LIT_INTEGER
 //   comp_begin(), comp_end()
 // Resolver: Width rt(uint32_t result_type_id), Width sel(uint32_t selector)
 template <class V, class R>
-__device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uint32_t n,
+__device__ __noinline__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uint32_t n,
                         V& vis, const R& res) {
   WalkErr err;
   uint32_t pos = 0;
@@ -153,13 +157,13 @@ __device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uin
         uint32_t role = T.ksub(k);
         if (depth == 0 && role == IDR_RESULT_TYPE && !have_rt) { have_rt = true; rt = v; }
         note_first(true, v);
-        vis.id(role, v, depth);
+        vis.id(role, v, depth, pos - 1);
       } else if (cat == CAT_VALUEENUM) {
         if (pos >= n) { err.code = W_EXHAUSTED; return false; }
         uint32_t v = ops[pos++];
         uint32_t e = T.venum_lookup(k, v);
         note_first(true, v);
-        vis.venum(k, v, e);
+        vis.venum(k, v, e, pos - 1);
         if (e != NONE32) {
           uint32_t np = T.enparams(e), po = T.eparam_off(e);
           if (sp + (int)np > WALK_STACK) { err.code = W_EXHAUSTED; return false; }
@@ -172,6 +176,7 @@ __device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uin
         uint64_t comp = 0;          // component positions within the kind (file order)
         uint32_t covered = 0;
         if (mask != 0) {
+#pragma unroll 1
           for (uint32_t j = 0; j < ne && j < 64; ++j) {
             uint32_t ev = T.evalue(eo + j);
             if (ev && (mask & ev) == ev && (covered & ev) != ev) { comp |= 1ull << j; covered |= ev; }
@@ -179,10 +184,10 @@ __device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uin
         }
         bool full = mask != 0 && covered == mask;
         note_first(true, mask);
-        vis.benum(k, mask, full, comp);
+        vis.benum(k, mask, full, comp, pos - 1);
         if (full) {
-          for (int j = 63; j >= 0; --j) {
-            if (!((comp >> j) & 1)) continue;
+          for (uint64_t rest = comp; rest; rest &= ~(1ull << (63 - __clzll((long long)rest)))) {
+            const int j = 63 - __clzll((long long)rest);
             uint32_t e = eo + j;
             uint32_t np = T.enparams(e), po = T.eparam_off(e);
             if (sp + (int)np > WALK_STACK) { err.code = W_EXHAUSTED; return false; }
@@ -217,7 +222,7 @@ __device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uin
           LitVal lv;
           if (!decode_typed(raw, wd.width, wd.sgn, wd.flt, lv, err)) return false;
           note_first(!lv.flt && !lv.neg && !(lv.bits >> 32), lv.bits);
-          vis.typed(lv);
+          vis.typed(lv, pos - need, need);
         } else {
           if (sub == LIT_INTEGER && is_switch) {
             Width wd = resolve();
@@ -231,33 +236,49 @@ __device__ WalkErr walk(const Tables& T, uint32_t idef, const uint32_t* ops, uin
               LitVal lv;
               if (!decode_typed(raw, wd.width, wd.sgn, false, lv, err)) return false;
               note_first(!lv.neg && !(lv.bits >> 32), lv.bits);
-              vis.typed(lv);
+              vis.typed(lv, pos - need, need);
               continue;
             }
           }
           if (pos >= n) { err.code = W_EXHAUSTED; return false; }
           uint32_t v = ops[pos++];
           note_first(true, v);
-          vis.lit(sub, v);
+          vis.lit(sub, v, pos - 1);
         }
       }
     }
     return true;
   };
 
+  // slot iteration as a state machine so `one` has a single call site
+  // (decode_operands, ops.py:340-350): '*' repeats its kind to the end, '?' is
+  // skipped when no words remain, LiteralSpecConstantOpInteger is followed by
+  // IdRef operands until the words run out.
   const uint32_t ns = T.inslots(idef), so = T.islot_off(idef);
-  for (uint32_t s = 0; s < ns; ++s) {
-    uint32_t q = T.slot_quant(so + s);
-    uint32_t k = T.slot_kind(so + s);
-    if (q == Q_VAR) {
-      while (pos < n) if (!one(k)) return err;
-      break;
+  uint32_t s = 0, rep_kind = 0;
+  bool repeat = false, stop_after_repeat = false, pending_tail = false;
+#pragma unroll 1
+  for (;;) {
+    uint32_t k;
+    if (repeat) {
+      if (pos >= n) {
+        repeat = false;
+        if (stop_after_repeat) break;
+        continue;
+      }
+      k = rep_kind;
+    } else {
+      if (s >= ns) break;
+      const uint32_t q = T.slot_quant(so + s);
+      k = T.slot_kind(so + s);
+      const bool tail = T.slot_spec_tail(so + s);
+      ++s;
+      if (q == Q_VAR) { repeat = true; stop_after_repeat = true; rep_kind = k; continue; }
+      if (q == Q_OPT && pos >= n) continue;
+      pending_tail = tail;
     }
-    if (q == Q_OPT && pos >= n) continue;
     if (!one(k)) return err;
-    if (T.slot_spec_tail(so + s)) {
-      while (pos < n) if (!one(T.idref)) return err;
-    }
+    if (pending_tail) { pending_tail = false; repeat = true; stop_after_repeat = false; rep_kind = T.idref; }
   }
   if (pos < n) { err.code = W_LEFTOVER; err.a = n - pos; }
   return err;

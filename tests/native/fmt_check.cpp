@@ -3,6 +3,7 @@
 // prints the repr the CUDA code would emit, one per line.
 #define SKG_HD
 #define SKG_TABLE
+#define SKG_NOINLINE
 #include <cstdio>
 #include <cstring>
 #include <string>
