@@ -601,135 +601,259 @@ __device__ __noinline__ void collect_ids(Mod& m) {
   __syncwarp();
 }
 
-// text of one word (count-only when s.p == nullptr)
-__device__ __noinline__ void word_out(Sink& s, const Mod& m, const Tables& T, uint32_t w,
-                                      uint32_t x, uint32_t width, bool hl) {
+// ---------------------------------------------------------------------------
+// Per-word length (arithmetic only) and emission (register-resident pointer).
+__device__ __forceinline__ uint32_t dlen32(uint32_t v) {
+  return v < 10 ? 1 : v < 100 ? 2 : v < 1000 ? 3 : v < 10000 ? 4 : v < 100000 ? 5 :
+         v < 1000000 ? 6 : v < 10000000 ? 7 : v < 100000000 ? 8 : v < 1000000000 ? 9 : 10;
+}
+__device__ __forceinline__ uint8_t* emit_u32(uint8_t* p, uint32_t v) {
+  uint8_t* e = p + dlen32(v);
+  uint8_t* q = e;
+#pragma unroll 1
+  do { *--q = (uint8_t)('0' + v % 10); v /= 10; } while (v);
+  return e;
+}
+__device__ __forceinline__ uint8_t* emit_cstr(uint8_t* p, const char* z) {
+#pragma unroll 1
+  while (*z) *p++ = (uint8_t)*z++;
+  return p;
+}
+__device__ __forceinline__ uint8_t* emit_tab(uint8_t* p, const Tables& T, uint32_t off, uint32_t len) {
+  const uint8_t* src = T.str + off;
+#pragma unroll 1
+  for (uint32_t q = 0; q < len; ++q) p[q] = __ldg(src + q);
+  return p + len;
+}
+
+__device__ __noinline__ uint8_t* emit_ref(uint8_t* p, const Mod& m, uint32_t id) {
+  *p++ = '%';
+  const uint32_t slot = ht_find(m, id);
+  if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
+    const NameView nv = name_of(m, m.hname[slot]);
+    for_sanitized(nv, [&](uint32_t c) { *p++ = (uint8_t)c; });
+    if (m.hser[slot] != NONE32) { *p++ = '_'; p = emit_u32(p, m.hser[slot]); }
+    return p;
+  }
+  return emit_u32(p, id);
+}
+
+// components of a BitEnum mask in file order (ops.py:77-89): total name bytes,
+// count, and whether they cover the mask
+__device__ __forceinline__ bool bit_cover(const Tables& T, uint32_t k, uint32_t v, uint32_t& bytes,
+                                          uint32_t& count) {
+  const uint32_t eo = T.kenum_off(k), ne = T.knenum(k);
+  uint32_t covered = 0;
+  bytes = 0; count = 0;
+#pragma unroll 1
+  for (uint32_t j = 0; j < ne; ++j) {
+    const uint32_t ev = T.evalue(eo + j);
+    if (ev && (v & ev) == ev && (covered & ev) != ev) { covered |= ev; bytes += T.ename_len(eo + j); ++count; }
+  }
+  return covered == v;
+}
+
+__device__ __forceinline__ uint32_t hex_digits(uint32_t v) {
+  uint32_t hd = 1;
+#pragma unroll 1
+  for (uint32_t x = v >> 4; x; x >>= 4) ++hd;
+  return hd;
+}
+
+__device__ __forceinline__ uint64_t typed_float_bits(const Mod& m, uint32_t w, uint32_t v, uint32_t width_t) {
+  if (width_t == 63) return (uint64_t)v | ((uint64_t)m.w[w + 1] << 32);
+  if (width_t == 32) return f32_to_f64_bits(v);
+  return f16_to_f64_bits(v & 0xFFFF);
+}
+
+__device__ __forceinline__ LitVal typed_int(const Mod& m, uint32_t w, uint32_t v, uint32_t width_t, bool sgn) {
+  LitVal lv;
+  WalkErr e;
+  uint32_t raw[2] = {v, width_t == 63 ? m.w[w + 1] : 0};
+  decode_typed(raw, width_t == 63 ? 64 : (width_t == 62 ? 33 : width_t), sgn, false, lv, e);
+  return lv;
+}
+
+// byte length of word w's text (disasm.py:284-377)
+__device__ __noinline__ uint32_t word_len(const Mod& m, const Tables& T, uint32_t w, uint32_t x,
+                                          uint32_t width, bool hl) {
+  const uint32_t v = m.w[w];
+  const uint32_t color = hl ? 9 : 0;
+  uint32_t n = (x & WK_LAST) ? 1 : 0;
+  switch (wk_code(x)) {
+    case C_OPC: {
+      const uint32_t i = wk_pay(x);
+      if (x & WK_BLANK) n += 1;
+      if (m.iflag[i] & IF_HAS_RESULT) {
+        const uint32_t rl = m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i];
+        n += (width ? width : rl) + color + 3;
+      } else if (width) {
+        n += width + 3;
+      }
+      const uint32_t d = m.idef[i];
+      n += color + (d == NONE16 ? 11 + dlen32(v & 0xFFFF) : T.iname_len(d));
+      return n;
+    }
+    case C_NONE: case C_RES: return n;
+    case C_REF: return n + 1 + ref_len(m, v) + color;
+    case C_DEC: case C_DECID: return n + 1 + dlen32(v);
+    case C_VEN: return n + 1 + T.ename_len(wk_pay(x));
+    case C_BEN: {
+      const uint32_t k = wk_pay(x);
+      if (v == 0) { const uint32_t z = T.kzero(k); return n + 1 + (z != NONE32 ? T.ename_len(z) : 1); }
+      uint32_t bytes, cnt;
+      if (!bit_cover(T, k, v, bytes, cnt)) return n + 3 + hex_digits(v);
+      return n + 1 + bytes + cnt - 1;
+    }
+    case C_STR: {
+      const uint32_t pl = wk_pay(x), nb = pl >> 2;
+      n += nb;
+#pragma unroll 1
+      for (uint32_t q = 0; q < nb; ++q) { const uint32_t b = (v >> (8 * q)) & 0xFF; n += (b == '\\' || b == '"'); }
+      if (pl & 1) n += 2 + (hl ? 5 : 0);
+      if (pl & 2) n += 1 + (hl ? 4 : 0);
+      return n;
+    }
+    case C_TYP: {
+      const uint32_t pl = wk_pay(x), width_t = pl >> 2;
+      if (pl & 1) return n + 1 + repr_len(repr_parts(typed_float_bits(m, w, v, width_t)));
+      const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
+      return n + 1 + (lv.neg ? 1 + dec_len_u64((uint64_t)0 - lv.bits) : dec_len_u64(lv.bits));
+    }
+    case C_EXT: {
+      uint32_t off, ln;
+      if (wk_pay(x) && T.ext_name(v, off, ln)) return n + 1 + ln;
+      return n + 1 + dlen32(v);
+    }
+    case C_SPO: {
+      const uint32_t d = T.inst_of(v);
+      return n + 1 + (d != NONE32 ? T.iname_len(d) - 2 : dlen32(v));
+    }
+    case C_UNK: return n + 12;
+    default: return n;
+  }
+}
+
+// emit word w's text at p; `spaces` = destination already holds spaces (skip padding)
+__device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T, uint32_t w, uint32_t x,
+                                       uint32_t width, bool hl, bool spaces) {
   const uint32_t v = m.w[w];
   switch (wk_code(x)) {
     case C_OPC: {
       const uint32_t i = wk_pay(x);
-      if (x & WK_BLANK) s.put('\n');
-      if (m.iflag[i] & IF_HAS_RESULT) {
-        const uint32_t rl = m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i];
-        if (width) s.fill(' ', width - rl);
-        if (hl) put_cstr(s, ANSI_ID);
-        put_ref(s, m, m.ib[i]);
-        if (hl) put_cstr(s, ANSI_RESET);
-        s.put(' '); s.put('='); s.put(' ');
-      } else if (width) {
-        s.fill(' ', width + 3);
+      if (x & WK_BLANK) *p++ = '\n';
+      uint32_t pad = 0;
+      const bool res = m.iflag[i] & IF_HAS_RESULT;
+      const uint32_t rl = res ? (m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i]) : 0;
+      if (res) pad = width ? width - rl : 0;
+      else pad = width ? width + 3 : 0;
+      if (!spaces) {
+#pragma unroll 1
+        for (uint32_t q = 0; q < pad; ++q) p[q] = ' ';
       }
-      if (hl) put_cstr(s, ANSI_OPCODE);
+      p += pad;
+      if (res) {
+        if (hl) p = emit_cstr(p, ANSI_ID);
+        p = emit_ref(p, m, m.ib[i]);
+        if (hl) p = emit_cstr(p, ANSI_RESET);
+        p[0] = ' '; p[1] = '='; p[2] = ' '; p += 3;
+      }
+      if (hl) p = emit_cstr(p, ANSI_OPCODE);
       const uint32_t d = m.idef[i];
-      if (d == NONE16) { put_cstr(s, "OpUnknown("); put_u64(s, v & 0xFFFF); s.put(')'); }
-      else s.putn(T.str + T.iname_off(d), T.iname_len(d));
-      if (hl) put_cstr(s, ANSI_RESET);
+      if (d == NONE16) { p = emit_cstr(p, "OpUnknown("); p = emit_u32(p, v & 0xFFFF); *p++ = ')'; }
+      else p = emit_tab(p, T, T.iname_off(d), T.iname_len(d));
+      if (hl) p = emit_cstr(p, ANSI_RESET);
       break;
     }
-    case C_NONE:
-    case C_RES:
-      break;
+    case C_NONE: case C_RES: break;
     case C_REF:
-      s.put(' ');
-      if (hl) put_cstr(s, ANSI_ID);
-      put_ref(s, m, v);
-      if (hl) put_cstr(s, ANSI_RESET);
+      *p++ = ' ';
+      if (hl) p = emit_cstr(p, ANSI_ID);
+      p = emit_ref(p, m, v);
+      if (hl) p = emit_cstr(p, ANSI_RESET);
       break;
-    case C_DEC:
-    case C_DECID:
-      s.put(' ');
-      put_u64(s, v);
-      break;
-    case C_VEN: {
-      const uint32_t e = wk_pay(x);
-      s.put(' ');
-      s.putn(T.str + T.ename_off(e), T.ename_len(e));
-      break;
-    }
+    case C_DEC: case C_DECID: *p++ = ' '; p = emit_u32(p, v); break;
+    case C_VEN: { const uint32_t e = wk_pay(x); *p++ = ' '; p = emit_tab(p, T, T.ename_off(e), T.ename_len(e)); break; }
     case C_BEN: {
       const uint32_t k = wk_pay(x);
-      s.put(' ');
+      *p++ = ' ';
       if (v == 0) {
         const uint32_t z = T.kzero(k);
-        if (z != NONE32) s.putn(T.str + T.ename_off(z), T.ename_len(z));
-        else s.put('0');
+        if (z != NONE32) p = emit_tab(p, T, T.ename_off(z), T.ename_len(z)); else *p++ = '0';
         break;
       }
-      // components in file order (ops.py:77-89), else 0x%x
+      uint32_t bytes, cnt;
+      if (!bit_cover(T, k, v, bytes, cnt)) {
+        const uint32_t hd = hex_digits(v);
+        *p++ = '0'; *p++ = 'x';
+#pragma unroll 1
+        for (uint32_t q = 0; q < hd; ++q) p[q] = (uint8_t)"0123456789abcdef"[(v >> (4 * (hd - 1 - q))) & 0xF];
+        p += hd;
+        break;
+      }
       const uint32_t eo = T.kenum_off(k), ne = T.knenum(k);
       uint32_t covered = 0;
-#pragma unroll 1
-      for (uint32_t j = 0; j < ne; ++j) {
-        const uint32_t ev = T.evalue(eo + j);
-        if (ev && (v & ev) == ev && (covered & ev) != ev) covered |= ev;
-      }
-      if (covered != v) { put_hex_lower(s, v); break; }
-      covered = 0;
       bool first = true;
 #pragma unroll 1
       for (uint32_t j = 0; j < ne; ++j) {
         const uint32_t ev = T.evalue(eo + j);
         if (ev && (v & ev) == ev && (covered & ev) != ev) {
           covered |= ev;
-          if (!first) s.put('|');
+          if (!first) *p++ = '|';
           first = false;
-          s.putn(T.str + T.ename_off(eo + j), T.ename_len(eo + j));
+          p = emit_tab(p, T, T.ename_off(eo + j), T.ename_len(eo + j));
         }
       }
       break;
     }
     case C_STR: {
       const uint32_t pl = wk_pay(x), nb = pl >> 2;
-      if (pl & 1) { s.put(' '); if (hl) put_cstr(s, ANSI_STRING); s.put('"'); }
+      if (pl & 1) { *p++ = ' '; if (hl) p = emit_cstr(p, ANSI_STRING); *p++ = '"'; }
 #pragma unroll 1
       for (uint32_t q = 0; q < nb; ++q) {
         const uint32_t b = (v >> (8 * q)) & 0xFF;
-        if (b == '\\' || b == '"') s.put('\\');
-        s.put((uint8_t)b);
+        if (b == '\\' || b == '"') *p++ = '\\';
+        *p++ = (uint8_t)b;
       }
-      if (pl & 2) { s.put('"'); if (hl) put_cstr(s, ANSI_RESET); }
+      if (pl & 2) { *p++ = '"'; if (hl) p = emit_cstr(p, ANSI_RESET); }
       break;
     }
     case C_TYP: {
       const uint32_t pl = wk_pay(x), width_t = pl >> 2;
-      const bool flt = pl & 1, sgn = pl & 2;
+      Sink s(p);
       s.put(' ');
-      if (flt) {
-        uint64_t bits;
-        if (width_t == 63) bits = (uint64_t)v | ((uint64_t)m.w[w + 1] << 32);
-        else if (width_t == 32) bits = f32_to_f64_bits(v);
-        else bits = f16_to_f64_bits(v & 0xFFFF);
-        put_repr_double(s, bits);
-      } else {
-        LitVal lv;
-        WalkErr e;
-        uint32_t raw[2] = {v, (width_t == 63) ? m.w[w + 1] : 0};
-        decode_typed(raw, width_t == 63 ? 64 : (width_t == 62 ? 33 : width_t), sgn, false, lv, e);
+      if (pl & 1) put_repr_double(s, typed_float_bits(m, w, v, width_t));
+      else {
+        const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
         if (lv.neg) put_i64(s, (int64_t)lv.bits); else put_u64(s, lv.bits);
       }
+      p += s.n;
       break;
     }
     case C_EXT: {
-      s.put(' ');
+      *p++ = ' ';
       uint32_t off, ln;
-      if (wk_pay(x) && T.ext_name(v, off, ln)) s.putn(T.str + off, ln);
-      else put_u64(s, v);
+      if (wk_pay(x) && T.ext_name(v, off, ln)) p = emit_tab(p, T, off, ln);
+      else p = emit_u32(p, v);
       break;
     }
     case C_SPO: {
-      s.put(' ');
+      *p++ = ' ';
       const uint32_t d = T.inst_of(v);
-      if (d != NONE32) s.putn(T.str + T.iname_off(d) + 2, T.iname_len(d) - 2);
-      else put_u64(s, v);
+      if (d != NONE32) p = emit_tab(p, T, T.iname_off(d) + 2, T.iname_len(d) - 2);
+      else p = emit_u32(p, v);
       break;
     }
-    case C_UNK:
-      s.put(' '); s.put('!'); s.put('0'); s.put('x'); put_hex8_upper(s, v);
+    case C_UNK: {
+      *p++ = ' '; *p++ = '!'; *p++ = '0'; *p++ = 'x';
+#pragma unroll 1
+      for (uint32_t q = 0; q < 8; ++q) p[q] = (uint8_t)"0123456789ABCDEF"[(v >> (28 - 4 * q)) & 0xF];
+      p += 8;
       break;
-    default:
-      break;
+    }
+    default: break;
   }
-  if (x & WK_LAST) s.put('\n');
+  if (x & WK_LAST) *p = '\n';
 }
 
 // result ref of every instruction -> irl/ib/iflag, module width (disasm.py:286-288)
@@ -768,11 +892,7 @@ __device__ __noinline__ void mark_blanks(Mod& m) {
 __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32_t opts, uint32_t width) {
   const bool hl = opts & OPT_HIGHLIGHT;
   uint32_t sum = 0;
-  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) {
-    Sink cs;
-    word_out(cs, m, T, w, m.wk[w], width, hl);
-    sum += cs.n;
-  }
+  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) sum += word_len(m, T, w, m.wk[w], width, hl);
   uint64_t total = warp_sum_u32(sum);
   if (!(opts & OPT_NO_HEADER)) {
     Sink hs;
@@ -782,7 +902,10 @@ __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32
   return total;
 }
 
-// write the module text at `out` (16-byte aligned) through the shared stage
+// write the module text at `out` (16-byte aligned) through the shared stage:
+// per 32-word chunk the stage is pre-filled with spaces (so indentation costs
+// nothing), every lane emits its word at its scanned offset, and the chunk is
+// flushed with 16-byte stores.
 __device__ __noinline__ void text_write(const Mod& m, const Tables& T, uint32_t opts, uint32_t width,
                                         uint8_t* out) {
   const uint32_t lane = lane_id();
@@ -796,26 +919,24 @@ __device__ __noinline__ void text_write(const Mod& m, const Tables& T, uint32_t 
   }
   uint8_t* stage = m.work_shared ? m.work : nullptr;
   const uint32_t cap = m.work_shared ? m.work_bytes : 0;
+  const uint4 sp4 = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
   for (uint32_t base = 5; base < m.W; base += 32) {
     const uint32_t w = base + lane;
     uint32_t x = 0, len = 0;
-    if (w < m.W) {
-      x = m.wk[w];
-      Sink cs;
-      word_out(cs, m, T, w, x, width, hl);
-      len = cs.n;
-    }
+    if (w < m.W) { x = m.wk[w]; len = word_len(m, T, w, x, width, hl); }
     const uint32_t incl = warp_incl_sum(len);
     const uint32_t chunk = __shfl_sync(FULL, incl, 31);
     const uint32_t shift = (uint32_t)(reinterpret_cast<uintptr_t>(out + pos) & 15);
     if (shift + chunk <= cap) {
-      if (len) { Sink ss(stage + shift + incl - len); word_out(ss, m, T, w, x, width, hl); }
+      const uint32_t n16 = (shift + chunk + 15) >> 4;
+      for (uint32_t k = lane; k < n16; k += 32) reinterpret_cast<uint4*>(stage)[k] = sp4;
+      __syncwarp();
+      if (len) word_emit(stage + shift + incl - len, m, T, w, x, width, hl, true);
       __syncwarp();
       flush_stage(out + pos, out + pos + chunk, stage);
       __syncwarp();
     } else if (len) {
-      Sink ss(out + pos + incl - len);
-      word_out(ss, m, T, w, x, width, hl);
+      word_emit(out + pos + incl - len, m, T, w, x, width, hl, false);
     }
     pos += chunk;
   }
