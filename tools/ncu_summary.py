@@ -6,8 +6,9 @@ import sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
-hdr, vals = rows[0], rows[2] if len(rows) > 2 else rows[1]
+hdr, units, vals = rows[0], rows[1], rows[2] if len(rows) > 2 else rows[1]
 d = dict(zip(hdr, vals))
+u = dict(zip(hdr, units))
 
 
 def g(k):
@@ -25,7 +26,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
         "smsp__sass_inst_executed_op_global_ld.sum", "smsp__sass_inst_executed_op_global_st.sum"]
 for k in keys:
-    print(f"{k}: {d.get(k)}")
+    print(f"{k}: {d.get(k)} {u.get(k, '')}")
 st = {k: g(k) for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued")}
 tot = sum(v for v in st.values() if v) or 1
 print("stall reasons (share of samples):")
