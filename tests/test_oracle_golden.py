@@ -36,3 +36,15 @@ def test_oracle_fixpoint_equals_closed_form(rec):
 def test_oracle_validate(rec):
     got = outcome(lambda: [list(d) for d in validate.validate(rec["bytes"])])
     assert same(got, rec["validate"])
+
+
+from golden_io import asm_texts  # noqa: E402
+from oracle import asm as oasm  # noqa: E402
+
+ASM = asm_texts()
+
+
+@pytest.mark.parametrize("rec", ASM, ids=[r["name"] for r in ASM])
+def test_oracle_assemble(rec):
+    got = outcome(lambda: oasm.assemble(rec["text"]).hex())
+    assert same(got, rec["asm"])

@@ -282,11 +282,55 @@ def asm_cases(mods):
         "missing_operand": "OpMemoryModel Physical64\n",
     }
     texts.update({f"crafted:{k}": v for k, v in crafted.items()})
+    texts.update(asm_mutations(texts))
     recs = []
     for name, text in texts.items():
         res = outcome(lambda t=text: sk.assemble_module(t).hex())
         recs.append({"name": name, "text": text, "asm": res})
     return recs
+
+
+JUNK = ["foo", "%", "007", "1e999", "-5", "0x", '"str"', "Inline|Bogus", "99999999999999999999",
+        "-0x1F", "+7", "1_000", "0b101", "0o17", "%undefined_name", "%0", "%4294967295", "1.5",
+        "-1", "nan", "inf", "2.5e-300", "0x1p3", "%٣", "None", "Const|Pure", "|Inline|", "4294967296"]
+
+
+def asm_mutations(texts):
+    rng = random.Random(99)
+    out = {}
+    bases = [(k, v) for k, v in texts.items() if k.endswith(":default")][:25]
+    for name, text in bases:
+        lines = text.split("\n")
+        body = [i for i, ln in enumerate(lines) if ln.strip() and not ln.startswith(";")]
+        for k in range(6):
+            ls = list(lines)
+            i = rng.choice(body)
+            toks = ls[i].split(" ")
+            kind = rng.randrange(7)
+            if kind == 0 and len(toks) > 1:
+                j = rng.randrange(1, len(toks))
+                toks[j] = rng.choice(JUNK)
+            elif kind == 1 and len(toks) > 2:
+                del toks[rng.randrange(1, len(toks))]
+            elif kind == 2:
+                toks.append(rng.choice(JUNK))
+            elif kind == 3:
+                ls.insert(i, ls[rng.choice(body)])
+            elif kind == 4:
+                del ls[i]
+                toks = None
+            elif kind == 5:
+                ls[i], ls[body[-1]] = ls[body[-1]], ls[i]
+                toks = None
+            else:
+                ls.insert(i, rng.choice(["OpNop", "OpFunctionEnd", "%x = OpLabel", "OpReturn",
+                                         "%q = OpTypeInt 12 1", "OpMemoryModel Logical GLSL450",
+                                         '%s = OpString "a\\"b"', "OpCapability Bogus"]))
+                toks = None
+            if toks is not None:
+                ls[i] = " ".join(toks)
+            out[f"mut:{name}:{k}"] = "\n".join(ls)
+    return out
 
 
 def main():
