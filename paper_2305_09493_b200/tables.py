@@ -274,6 +274,7 @@ def pack(spec=None, ext=None) -> PackedTables:
     header[29] = linkage
     header[30], header[31] = ocl_off, ocl_len
     header[32] = 2 + 2 * cap_words   # requirement record stride (u32)
+    _asm_sections(spec, ext, insts, kinds, kind_index, header, put, strings)
     sbuf = bytes(strings.buf) + b"\x00" * (-len(strings.buf) % 4)
     header[12] = put(np.frombuffer(sbuf, dtype=np.uint32) if sbuf else [0])
     header[13] = len(strings.buf)
@@ -289,3 +290,161 @@ def describe(t: PackedTables) -> str:
 
 
 __all__ = ["pack", "PackedTables", "describe", "struct"]
+
+
+# -- assembler sections (asm.py / builder.py / ops.Encoder lookups) ---------------
+# Route codes: bucket index 0..10 (builder._SECTIONS order), or
+ROUTE_SCOPE, ROUTE_VARIABLE, ROUTE_KEYERROR = 11, 12, 13
+SECTIONS = ("capabilities", "extensions", "ext_imports", "memory_model", "entry_points",
+            "execution_modes", "debug_sources", "debug_names", "debug_processed",
+            "annotations", "globals")                                    # builder.py:39-43
+_MODE_BUCKET = {"OpCapability": 0, "OpMemoryModel": 3, "OpEntryPoint": 4,
+                "OpExecutionMode": 5, "OpExecutionModeId": 5}          # builder.py:45-51
+_DEBUG_BUCKET = {"OpName": 7, "OpMemberName": 7, "OpModuleProcessed": 8}   # builder.py:53-61
+TERMINATORS = frozenset({"OpBranch", "OpBranchConditional", "OpSwitch", "OpKill", "OpReturn",
+                         "OpReturnValue", "OpUnreachable", "OpTerminateInvocation",
+                         "OpIgnoreIntersectionKHR", "OpTerminateRayKHR",
+                         "OpEmitMeshTasksEXT"})                       # builder.py:31-35
+AF_TERMINATOR, AF_BLOCK_FORBIDDEN, AF_CTXNUM = 1, 2, 4
+
+
+def fnv1a(raw: bytes) -> int:
+    h = 2166136261
+    for b in raw:
+        h = ((h ^ b) * 16777619) & 0xFFFFFFFF
+    return h
+
+
+def _route(inst) -> int:
+    """builder.ModuleScope._route (builder.py:157-183) as a code."""
+    name, cls = inst.name, inst.class_attr
+    if name == "OpExtInst":
+        return ROUTE_SCOPE
+    if name == "OpUndef":
+        return 10
+    if name in ("OpLine", "OpNoLine"):
+        return 6
+    if name == "OpVariable":
+        return ROUTE_VARIABLE
+    if cls == "Mode-Setting":
+        return _MODE_BUCKET.get(name, ROUTE_KEYERROR)
+    if cls == "Extension":
+        return 1 if name == "OpExtension" else 2
+    if cls == "Debug":
+        return _DEBUG_BUCKET.get(name, 6)
+    if cls == "Annotation":
+        return 9
+    if cls in ("Type-Declaration", "Constant-Creation"):
+        return 10
+    if cls == "@exclude" and name.startswith("OpType"):
+        return 10
+    return ROUTE_SCOPE
+
+
+def _hash_table(items, cap_min):
+    """Open addressing (linear probe): items = [(hash, payload words...)]."""
+    width = 1 + len(items[0][1]) if items else 2
+    cap = 64
+    while cap < 2 * len(items) + 8 or cap < cap_min:
+        cap <<= 1
+    tab = np.zeros((cap, width), dtype=np.uint32)
+    used = np.zeros(cap, dtype=bool)
+    for h, payload in items:
+        s = h & (cap - 1)
+        while used[s]:
+            s = (s + 1) & (cap - 1)
+        used[s] = True
+        tab[s, 0] = h
+        tab[s, 1:] = payload
+    return tab, cap
+
+
+def _unicode_tables():
+    """Python str predicates the assembler relies on, as code-point tables:
+    str.isprintable (repr), str.isspace / int()/float() whitespace, decimal
+    digits (int(), float(), re ``\\d``) and str.isdigit-only digits."""
+    printable = []
+    prev, start = False, 0
+    for c in range(0x110000):
+        p = chr(c).isprintable()
+        if p != prev:
+            if p:
+                start = c
+            else:
+                printable.append((start, c))
+            prev = p
+    if prev:
+        printable.append((start, 0x110000))
+    space = [c for c in range(0x110000) if chr(c).isspace()]
+    dec_starts = [c for c in range(0x110000) if chr(c).isdecimal() and int(chr(c)) == 0]
+    for s0 in dec_starts:
+        assert all(chr(s0 + j).isdecimal() and int(chr(s0 + j)) == j for j in range(10))
+    assert sum(chr(c).isdecimal() for c in range(0x110000)) == 10 * len(dec_starts)
+    digit_only = [c for c in range(0x110000) if chr(c).isdigit() and not chr(c).isdecimal()]
+    return printable, space, dec_starts, digit_only
+
+
+def _asm_sections(spec, ext, insts, kinds, kind_index, header, put, strings):
+    ctx_kind = "LiteralContextDependentNumber"
+    info = []
+    for inst in insts:
+        rslot = next((j for j, s in enumerate(inst.operands) if s.kind == "IdResult"), 0xFF)
+        flags = AF_TERMINATOR if inst.name in TERMINATORS else 0
+        cls = inst.class_attr
+        if cls in ("Mode-Setting", "Annotation", "Type-Declaration", "Constant-Creation") or \
+                inst.name in ("OpExtension", "OpExtInstImport", "OpFunction",
+                              "OpFunctionParameter", "OpFunctionEnd"):
+            flags |= AF_BLOCK_FORBIDDEN
+        if any(s.kind == ctx_kind for s in inst.operands):
+            flags |= AF_CTXNUM
+        c_off, c_len = strings.add(cls or "unclassified")
+        info.append([min(rslot, 0xFF) | (_route(inst) << 8) | (flags << 16), c_off, c_len, 0])
+    header[34] = put(info if info else [0])
+    # opname -> instruction index (exact names, grammar.py:108-112)
+    items = [(fnv1a(i.name.encode()), [j]) for j, i in enumerate(insts)]
+    tab, cap = _hash_table(items, 1024)
+    header[35], header[36] = put(tab), cap
+    # (kind, enumerant name) -> first enumerant index by name (grammar.py:56-63)
+    items, eoff = [], 0
+    for ki, k in enumerate(kinds):
+        seen = set()
+        for j, e in enumerate(k.enumerants or ()):
+            if e.name not in seen and kind_index.get(k.kind) == ki:
+                seen.add(e.name)
+                items.append(((fnv1a(e.name.encode()) ^ (ki * 0x9E3779B1)) & 0xFFFFFFFF,
+                              [eoff + j, ki]))
+        eoff += len(k.enumerants or ())
+    tab, cap = _hash_table(items, 2048)
+    header[37], header[38] = put(tab), cap
+    # extended-instruction name -> number (last definition wins, grammar.py:139-141)
+    by_name = {}
+    for i in (ext.instructions if ext is not None else ()):
+        by_name[i.name] = i.opcode
+    items = []
+    for nm, num in by_name.items():
+        off, ln = strings.add(nm)
+        items.append((fnv1a(nm.encode()), [num, off, ln]))
+    tab, cap = _hash_table(items, 256)
+    header[39], header[40] = put(tab), cap
+    printable, space, dec_starts, digit_only = _unicode_tables_cached()
+    header[41], header[42] = put(np.array(printable, dtype=np.uint32).ravel()), len(printable)
+    header[43], header[44] = put(space), len(space)
+    header[45], header[46] = put(dec_starts), len(dec_starts)
+    header[47], header[48] = put(digit_only), len(digit_only)
+    try:
+        header[49] = spec.kind("StorageClass").enumerant("Function").value
+    except Exception:  # noqa: BLE001 - custom grammar without StorageClass
+        header[49] = NONE32
+    names = [i.name for i in insts]
+    header[50] = names.index("OpLabel") if "OpLabel" in names else NONE32
+    header[51] = names.index("OpFunctionEnd") if "OpFunctionEnd" in names else NONE32
+
+
+_UNI = None
+
+
+def _unicode_tables_cached():
+    global _UNI
+    if _UNI is None:
+        _UNI = _unicode_tables()
+    return _UNI
