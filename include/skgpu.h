@@ -35,6 +35,10 @@ enum {
   SKG_ST_UNICODE = 5,      /* UnicodeDecodeError */
   SKG_ST_KEY = 6,          /* KeyError */
   SKG_ST_VALUE = 7,        /* ValueError */
+  SKG_ST_OVERFLOW = 8,     /* OverflowError (struct.pack of a float literal) */
+  SKG_ST_ASSEMBLY = 9,     /* AssemblyError (message = all diagnostics) */
+  SKG_ST_STRUCTURE = 10,   /* StructureError */
+  SKG_ST_SERIALIZATION = 11, /* SerializationError */
   SKG_ST_INTERNAL = 99     /* scratch/capacity problem: rerun with more workspace */
 };
 
@@ -104,6 +108,27 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
                uint32_t* header, uint32_t* inst_off, const int64_t* inst_base, uint32_t* inst_count,
                uint32_t* words_out, const int64_t* words_base, int32_t* status, skg_error* errors,
                uint32_t err_cap, void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* Batch assembly (text -> binary).
+ * Replaces: Assembler.assemble / assemble_module(text) (reference asm.py:133-180,
+ * 365-368) together with the builder serialization it drives (builder.py:108-242).
+ * Input: UTF-8 text arena `text` (module starts 16-byte aligned, arena padded
+ * to 16 bytes) with int64 per-module offsets/lengths.  Output arena `out`:
+ * module m's result is out[out_span[2m] : out_span[2m] + out_span[2m+1]] -- the
+ * module binary when status[m] == SKG_ST_OK, otherwise the exact str(exc) text
+ * (UTF-8) of the exception class status[m] names.  Bytes are reserved with an
+ * atomic bump allocator (skg_last_counts reports overflow / bytes used, as for
+ * skg_disasm).  `slot_bytes` is the per-warp scratch (skg_asm_slot_hint); a
+ * module that needs more reports SKG_ST_INTERNAL and can be rerun with a
+ * larger slot.  `workspace` must hold skg_asm_workspace_bytes(slot_bytes).
+ * default_version = major << 16 | minor: the Assembler's default_version
+ * (asm.py:128), used when the text has no "; Version:" comment. */
+uint64_t skg_asm_slot_hint(uint64_t max_text_bytes);
+uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes);
+int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
+            uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
+            int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,
+            uint32_t default_version);
 
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,

@@ -1,6 +1,7 @@
-"""B200-native SPIR-V codec path (disassemble / validate / decode) behind the
+"""B200-native SPIR-V codec path (disassemble / assemble / validate / decode) behind the
 ``spirvkit`` (arXiv 2305.09493 reference) API.  See DESIGN.md."""
 
+from .asm import Assembler, assemble_batch, assemble_module
 from .codec import ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module
 from .disasm import Disassembler, DisassemblerOptions, disassemble_batch, disassemble_module
 from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,

@@ -340,3 +340,152 @@ class DisasmPlan:
             self.launch()
             info = self.check()
         return info
+
+
+# -- assembler -----------------------------------------------------------------------
+ST_OVERFLOW, ST_ASSEMBLY, ST_STRUCTURE, ST_SERIALIZATION = 8, 9, 10, 11
+
+
+def _bind_asm(L):
+    if getattr(L, "_asm_bound", False):
+        return L
+    P, U32, U64, I32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+    L.skg_asm_slot_hint.argtypes = [U64]
+    L.skg_asm_slot_hint.restype = U64
+    L.skg_asm_workspace_bytes.argtypes = [U64]
+    L.skg_asm_workspace_bytes.restype = U64
+    L.skg_asm.argtypes = [P, P, P, P, U32, U64, P, U64, P, P, P, U64, P, U32]  # ..., stream, default_version
+    L.skg_asm.restype = I32
+    L._asm_bound = True
+    return L
+
+
+def pack_texts(texts):
+    """list[str] -> (uint8 arena, int64 offsets, int64 lengths); module starts 16-byte aligned."""
+    raws = [t.encode("utf-8", "surrogatepass") if isinstance(t, str) else bytes(t) for t in texts]
+    lengths = np.array([len(r) for r in raws], dtype=np.int64)
+    padded = (lengths + 15) // 16 * 16
+    offsets = np.zeros(len(raws), dtype=np.int64)
+    if len(raws) > 1:
+        offsets[1:] = np.cumsum(padded)[:-1]
+    buf = np.zeros(int(padded.sum()) + 16, dtype=np.uint8)
+    for r, o in zip(raws, offsets):
+        buf[o:o + len(r)] = np.frombuffer(r, dtype=np.uint8)
+    return buf, offsets, lengths
+
+
+class AsmPlan:
+    """Device buffers for repeated skg_asm launches over one resident text batch."""
+
+    def __init__(self, batch: DeviceBatch, spec=None, ext=None, out_cap=None, slot_bytes=None,
+                 default_version=(1, 2)):
+        torch = _torch()
+        L = _bind_asm(lib())
+        self.batch = batch
+        self.th = tables_handle(spec, ext)
+        n = batch.n
+        max_len = int(batch.max_words) * 4 + 16
+        self.slot = int(slot_bytes or L.skg_asm_slot_hint(max_len))
+        self.ws_bytes = int(L.skg_asm_workspace_bytes(self.slot))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        self.cap = int(out_cap or (batch.total_bytes + 64 * n + 4096))
+        self.out = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
+        self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
+        self.status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        maj, mnr = default_version
+        self.dv = ((int(maj) & 0xFFFF) << 16) | (int(mnr) & 0xFFFF)
+
+    def launch(self, stream=None):
+        b = self.batch
+        s = stream if stream is not None else _stream()
+        rc = lib().skg_asm(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n, self.slot,
+                           self.out.data_ptr(), self.cap, self.span.data_ptr(), self.status.data_ptr(),
+                           self.ws.data_ptr(), self.ws_bytes, s, self.dv)
+        _check(rc, "asm")
+
+    def check(self):
+        nerr, over, used = last_counts(self.ws)
+        return {"overflow": over, "bytes": used}
+
+    def grow(self, need):
+        torch = _torch()
+        self.cap = int(need) + 4096
+        self.out = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
+
+    def fit(self):
+        self.launch()
+        info = self.check()
+        if info["overflow"]:
+            self.grow(info["bytes"])
+            self.launch()
+            info = self.check()
+        return info
+
+
+def asm_exception(status, msg: str):
+    if status == ST_ASSEMBLY:
+        lines = msg.split("\n")
+        diags = []
+        for ln in lines[1:]:
+            a, b, rest = ln.split(":", 2)
+            diags.append(_err.AsmDiagnostic(int(a), int(b), rest[1:]))
+        exc = _err.AssemblyError(diags)
+        return exc
+    if status == ST_VALUE:
+        return ValueError(msg)
+    if status == ST_OVERFLOW:
+        return OverflowError(msg)
+    if status == ST_STRUCTURE:
+        return _err.StructureError(msg)
+    if status == ST_SERIALIZATION:
+        return _err.SerializationError(msg)
+    if status == ST_CODEC:
+        return _err.CodecError(msg)
+    return RuntimeError(f"libskgpu internal error: {msg}")
+
+
+def run_asm(texts, spec=None, ext=None, default_version=(1, 2)):
+    """list[str] -> list[bytes | exception instance]."""
+    buf, off, ln = pack_texts(texts)
+    n = len(texts)
+    if n == 0:
+        return []
+    batch = DeviceBatch.from_host(buf, off, ln)
+    batch.max_words = (int(ln.max()) + 3) // 4
+    plan = AsmPlan(batch, spec, ext, default_version=default_version)
+    plan.fit()
+    status = plan.status[:n].cpu().numpy()
+    span = plan.span[: 2 * n].cpu().numpy()
+    out = plan.out.cpu().numpy().tobytes()
+    res = []
+    retry = []
+    for m in range(n):
+        o, k = int(span[2 * m]), int(span[2 * m + 1])
+        data = out[o:o + k]
+        st = int(status[m])
+        if st == ST_OK:
+            res.append(data)
+        elif st == ST_INTERNAL:
+            res.append(None)
+            retry.append(m)
+        else:
+            res.append(asm_exception(st, data.decode("utf-8", "surrogatepass")))
+    for m in retry:   # module larger than the default per-warp scratch: rerun alone, bigger slot
+        slot = plan.slot
+        for _ in range(6):
+            slot *= 4
+            b1, o1, l1 = pack_texts([texts[m]])
+            single = DeviceBatch.from_host(b1, o1, l1)
+            single.max_words = (int(l1.max()) + 3) // 4
+            p1 = AsmPlan(single, spec, ext, slot_bytes=slot, default_version=default_version)
+            p1.fit()
+            st = int(p1.status[0].item())
+            if st == ST_INTERNAL:
+                continue
+            o, k = (int(x) for x in p1.span[:2].cpu().numpy())
+            data = p1.out[o:o + k].cpu().numpy().tobytes()
+            res[m] = data if st == ST_OK else asm_exception(st, data.decode("utf-8", "surrogatepass"))
+            break
+        else:
+            res[m] = RuntimeError("libskgpu internal error: module exceeds the assembler scratch")
+    return res

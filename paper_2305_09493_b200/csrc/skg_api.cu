@@ -14,9 +14,12 @@ struct DecodeArgs;
 #include "skg_disasm.cu"
 #include "skg_validate.cu"
 #include "skg_decode.cu"
+#include "skg_asm.cu"
 
 struct skg_tables {
   skg::Tables t;
+  skg::Uni u;
+  skg::AsmTables a;
   uint32_t* d_blob;
 };
 
@@ -108,6 +111,13 @@ int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** 
   T.ocl_off = h[30]; T.ocl_len = h[31];
   T.req_stride = h[32];
   T.cap_kind = h[33];
+  skg::AsmTables& A = t->a;
+  A.info = b + h[34];
+  A.ophash = b + h[35]; A.ophash_cap = h[36];
+  A.enhash = b + h[37]; A.enhash_cap = h[38];
+  A.exhash = b + h[39]; A.exhash_cap = h[40];
+  A.storage_fn = h[49]; A.op_label = h[50]; A.op_fnend = h[51];
+  t->u = skg::Uni{b + h[41], h[42], b + h[43], h[44], b + h[45], h[46], b + h[47], h[48]};
   *out = t;
   return 0;
 }
@@ -194,6 +204,37 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
     attr = true;
   }
   skg::validate_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, smem, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+uint64_t skg_asm_slot_hint(uint64_t max_text_bytes) {
+  return ((32ull * max_text_bytes + 65536) + 255) & ~255ull;
+}
+
+uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes) {
+  return 256 + (uint64_t)grid_blocks() * kWarpsPerBlock * slot_bytes;
+}
+
+int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
+            uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
+            int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,
+            uint32_t default_version) {
+  if (!t || !workspace) return -1;
+  if (t->a.op_label == 0xFFFFFFFFu || t->a.op_fnend == 0xFFFFFFFFu) return -4;
+  if (workspace_bytes < skg_asm_workspace_bytes(slot_bytes)) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  if (int e = check(cudaMemsetAsync(ws, 0, 256, s))) return e;
+  if (n_mod == 0) return 0;
+  skg::AsmArgs a;
+  a.T = t->t; a.U = t->u; a.A = t->a;
+  a.text = text; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod;
+  a.out = out; a.out_cap = out_cap; a.out_span = out_span; a.status = status;
+  a.counters = reinterpret_cast<uint32_t*>(ws);
+  a.gscratch = ws + 256;
+  a.gslot_bytes = slot_bytes;
+  a.default_version = default_version;
+  skg::asm_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, 0, s>>>(a);
   return check(cudaGetLastError());
 }
 

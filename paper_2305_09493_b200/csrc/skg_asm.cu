@@ -1,0 +1,1835 @@
+// Batch assembler: text -> SPIR-V binary, bit-exact with the reference
+// Assembler.assemble (asm.py:133-180) including the builder's serialization
+// (builder.py:108-242) and the Encoder slot walk (ops.py:104-271).
+//
+// One warp per module (persistent warps take module tickets).  Phases:
+//   A  copy the text into the warp's scratch + str.splitlines() boundaries,
+//      word-parallel (asm.py:137)
+//   B  tokenize_line, lane per line (asm.py:51-90); string escapes are undone
+//      in place; numeric %ids are reserved (asm.py:148-153, builder.py:118-123)
+//   C  leading header comments (asm.py:184-206), lane 0
+//   D  symbolic result names -> ids in document order: a name table keyed by
+//      the token bytes, the k-th new name gets the k-th unreserved positive
+//      integer (select over the reservation bitmap; builder.py:108-116)
+//   E  opname lookup, type-width and value-type scans (asm.py:215-245)
+//   F  encode pass 1 (count), lane per line: Encoder.encode + coerce
+//      (ops.py:120-271, asm.py:286-349) -> words per line + first error
+//   G  the scope state machine (asm.py:249-284, builder.py:140-334), lane 0:
+//      routing, SSA registry, functions/blocks -> placement of every line
+//   H  serialization checks (builder.py:187-242) and layout: 11 section
+//      buckets, then function declarations before definitions
+//   I  encode pass 2 (write) at the final offsets + reference check
+// Failing modules produce str(exc) of the exception the reference raises.
+#include "skg_text.cuh"
+
+namespace skg {
+
+struct AsmTables {
+  const uint32_t* info;       // 4 words / instruction: rslot | route<<8 | flags<<16, class str off, len
+  const uint32_t* ophash; uint32_t ophash_cap;   // (hash, inst)
+  const uint32_t* enhash; uint32_t enhash_cap;   // (hash, enum index, kind)
+  const uint32_t* exhash; uint32_t exhash_cap;   // (hash, number, name off, name len)
+  uint32_t storage_fn, op_label, op_fnend;
+};
+
+constexpr uint32_t ROUTE_SCOPE = 11, ROUTE_VARIABLE = 12, ROUTE_KEYERROR = 13;
+constexpr uint32_t AF_TERMINATOR = 1, AF_BLOCK_FORBIDDEN = 2, AF_CTXNUM = 4;
+constexpr uint32_t MAX_ID = 0xFFFFFFFEu;
+
+struct AsmArgs {
+  Tables T;
+  Uni U;
+  AsmTables A;
+  const uint8_t* text;
+  const int64_t* mod_off;
+  const int64_t* mod_len;
+  uint32_t n_mod;
+  uint8_t* out;
+  uint64_t out_cap;
+  int64_t* out_span;
+  int32_t* status;
+  uint32_t* counters;        // [0] ticket, [2] overflow, [4..5] u64 cursor
+  uint8_t* gscratch;
+  uint64_t gslot_bytes;
+  uint32_t default_version;   // major << 16 | minor
+};
+
+// token: off (text byte offset), lenf = len | TK_STR
+constexpr uint32_t TK_STR = 0x80000000u, TK_LEN = 0x3FFFFFFFu;
+
+// line flags
+enum : uint32_t {
+  LF_TOKERR = 1, LF_RESULT = 2, LF_EMPTY = 4, LF_RESVERR = 8, LF_UNRES = 16, LF_VARFN = 32,
+  LF_RESOLVE_ERR = 64, LF_PLACED = 128, LF_DROP = 256
+};
+
+// error codes (per line; E_* from the encoder, S_* from the state machine)
+enum : uint32_t {
+  E_OK = 0, E_NOINST, E_NEEDS_RESULT, E_NOT_PRODUCE, E_MISSING, E_EXTRA, E_STR_FOR, E_EXPECT_ID,
+  E_INT_INVALID, E_INT_LIMIT, E_FLOAT_INVALID, E_NO_WIDTH, E_NEG, E_NO_ENUM_STR, E_NO_ENUM_INT,
+  E_MASK_RANGE, E_LITSTR_INT, E_NUL, E_SURROGATE, E_WIDTH, E_FWIDTH, E_OVF_E, E_OVF_F, E_FIT,
+  E_NO_EXT, E_NO_SPECOP, E_LIT_RANGE, E_INT_STRLIMIT,
+  S_LABEL_OUTSIDE = 64, S_LABEL_NORESULT, S_LABEL_USED, S_DUP, S_FUNC_BEFORE_END, S_OUTSIDE,
+  S_PARAM_AFTER_BLOCK, S_MM_DUP, S_NEED_BLOCK, S_TERMINATED, S_VAR_FIRST, S_NOT_BLOCK, S_KEYERROR,
+  S_LABEL_RESOLVE, S_VAR_NOTFN
+};
+
+// module-level outcome
+enum : uint32_t {
+  X_NONE = 0, X_VERSION, X_VERSION_LIMIT, X_VERSION_DEFAULT, X_RESERVE, X_OVERFLOW, X_ASSEMBLY, X_STRUCT_END,
+  X_STRUCT_TERM, X_SERIAL, X_WC, X_INTERNAL
+};
+
+struct AsmMod {
+  uint8_t* base;
+  uint8_t* txt;       // module text copy (escapes undone in place)
+  uint32_t T;         // bytes
+  uint32_t L;         // lines
+  uint32_t* ls;       // line start
+  uint32_t* le;       // line end
+  uint32_t* lt0;      // first token
+  uint32_t* lnt;      // token count
+  uint32_t* lfl;      // flags
+  uint32_t* ld;       // instruction index
+  uint32_t* lec;      // error code
+  uint32_t* lnw;      // operand words
+  uint32_t* lrid;     // result / label id
+  uint32_t* lgrp;     // placement group
+  uint32_t* loff;     // offset within group, then absolute word offset
+  uint32_t* lerr;     // 4 words / line: error details
+  uint32_t* tok;      // 2 words / token
+  uint32_t ntb;       // token slots
+  uint32_t* nt;       // name table: 6 words / entry
+  uint32_t ncap;
+  uint32_t* rbm;      // reservation bitmap (RB bits)
+  uint32_t* zpre;     // unreserved ids in [0, 32 w)
+  uint32_t* reg;      // registry bitmap
+  uint32_t* lab;      // label bitmap
+  uint32_t RB;
+  uint32_t* fn;       // functions: 4 words (result id, flags, size, base)
+  uint32_t* blk;      // blocks: 3 words (fn, label, terminated)
+  uint32_t* big;      // big-id lists: [0] count reg, [1] count lab, then pairs
+  uint32_t big_cap;
+  uint32_t* misc;     // 64 words of counters
+};
+
+// misc slots
+enum : uint32_t {
+  MS_BIGMAX_LO = 0, MS_BIGMAX_HI, MS_NPCT, MS_RESV_LINE, MS_NSYM, MS_NFN, MS_NBLK, MS_BUCKET0 = 8,
+  MS_X = 24, MS_XA, MS_XB, MS_XC, MS_NEWCOUNT, MS_GEN, MS_SCHEMA, MS_MAJOR, MS_MINOR, MS_GENSET,
+  MS_HDR_LINE_V, MS_HDR_LINE_G, MS_HDR_LINE_S, MS_TOTAL, MS_NDIAG, MS_OVF_LINE, MS_SER_LINE,
+  MS_WC_LINE, MS_COUNTER, MS_V0 = 48
+};
+
+__device__ __forceinline__ uint32_t lane_id_a() { return threadIdx.x & 31; }
+constexpr unsigned FULLM = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t wincl(uint32_t v) {
+  const uint32_t l = lane_id_a();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(FULLM, v, d);
+    if (l >= (uint32_t)d) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t wsum(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULLM, v, d);
+  return v;
+}
+__device__ __forceinline__ uint32_t wmax(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(FULLM, v, d));
+  return v;
+}
+__device__ __forceinline__ uint32_t wmin(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v = min(v, __shfl_xor_sync(FULLM, v, d));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t fnv(const uint8_t* p, uint32_t n, uint32_t h = 2166136261u) {
+  for (uint32_t i = 0; i < n; ++i) h = (h ^ p[i]) * 16777619u;
+  return h;
+}
+
+__device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) if (a[i] != b[i]) return false;
+  return true;
+}
+
+__device__ __forceinline__ bool bytes_eq_z(const uint8_t* a, uint32_t n, const char* z) {
+  uint32_t i = 0;
+  for (; i < n; ++i) if (!z[i] || (uint8_t)z[i] != a[i]) return false;
+  return z[i] == 0;
+}
+
+struct Tok {
+  const uint8_t* p;
+  uint32_t n;
+  bool str;
+  uint32_t raw;   // raw byte offset of the token start (quote for strings)
+};
+
+__device__ __forceinline__ Tok tok_at(const AsmMod& m, uint32_t t) {
+  const uint32_t off = m.tok[2 * t], lf = m.tok[2 * t + 1];
+  Tok k;
+  k.p = m.txt + off;
+  k.n = lf & TK_LEN;
+  k.str = (lf & TK_STR) != 0;
+  k.raw = off - (k.str ? 1 : 0);
+  return k;
+}
+
+// str.isdigit() of p[0..n) (non-empty)
+__device__ inline bool py_isdigit(const uint8_t* p, uint32_t n, const Uni& U) {
+  if (n == 0) return false;
+  for (uint32_t i = 0; i < n;) {
+    if (p[i] < 0x80) { if (p[i] < '0' || p[i] > '9') return false; ++i; continue; }
+    uint32_t len;
+    const uint32_t c = utf8_cp(p, n, i, len);
+    if (!U.is_digit(c)) return false;
+    i += len;
+  }
+  return true;
+}
+
+// re.match(r"[+-]?(0[xX][0-9a-fA-F]+|\d+)$", text)  (asm.py:31)
+__device__ inline bool int_token(const uint8_t* p, uint32_t n, const Uni& U) {
+  uint32_t i = 0;
+  if (i < n && (p[i] == '+' || p[i] == '-')) ++i;
+  if (i + 2 < n + 0 && p[i] == '0' && (p[i + 1] == 'x' || p[i + 1] == 'X')) {
+    uint32_t j = i + 2;
+    bool hex = j < n;
+    for (uint32_t k = j; k < n; ++k) {
+      const uint8_t c = p[k];
+      if (!((c >= '0' && c <= '9') || (c >= 'a' && c <= 'f') || (c >= 'A' && c <= 'F'))) { hex = false; break; }
+    }
+    if (hex) return true;
+  }
+  if (i >= n) return false;
+  while (i < n) {
+    uint32_t len = 1, c = p[i];
+    if (c >= 0x80) c = utf8_cp(p, n, i, len);
+    if (U.decimal(c) < 0) return false;
+    i += len;
+  }
+  return true;
+}
+
+// Python str.strip() bounds (isspace)
+__device__ inline void py_strip(const uint8_t* p, uint32_t n, const Uni& U, uint32_t& s, uint32_t& e) {
+  s = 0; e = n;
+  while (s < e) {
+    uint32_t len, c = utf8_cp(p, n, s, len);
+    if (!U.is_space(c)) break;
+    s += len;
+  }
+  while (e > s) {
+    uint32_t k = e - 1;
+    while (k > s && (p[k] & 0xC0) == 0x80) --k;
+    uint32_t len, c = utf8_cp(p, n, k, len);
+    if (!U.is_space(c)) break;
+    e = k;
+  }
+}
+
+// -- name table -------------------------------------------------------------------
+// entry: [0] key token (EMPTY), [1] hash, [2] first symbolic line (min), [3] id,
+//        [4] last OpTypeInt/Float line + 1 (max), [5] last value-type line + 1 (max)
+constexpr uint32_t NT_W = 6;
+constexpr uint32_t EMPTYK = 0xFFFFFFFFu;
+
+__device__ inline uint32_t nt_find(const AsmMod& m, const uint8_t* p, uint32_t n) {
+  const uint32_t h = fnv(p, n);
+  uint32_t s = (h * 0x9E3779B1u) & (m.ncap - 1);
+  for (uint32_t probe = 0; probe < m.ncap; ++probe) {
+    const uint32_t* e = m.nt + NT_W * s;
+    const uint32_t k = e[0];
+    if (k == EMPTYK) return NONE32;
+    if (e[1] == h) {
+      const Tok t = tok_at(m, k);
+      if (t.n == n && bytes_eq(t.p, p, n)) return s;
+    }
+    s = (s + 1) & (m.ncap - 1);
+  }
+  return NONE32;
+}
+
+// insert (concurrent-safe); returns the entry slot
+__device__ inline uint32_t nt_insert(const AsmMod& m, uint32_t t) {
+  const Tok me = tok_at(m, t);
+  const uint32_t h = fnv(me.p, me.n);
+  uint32_t s = (h * 0x9E3779B1u) & (m.ncap - 1);
+  for (uint32_t probe = 0; probe < m.ncap; ++probe) {
+    uint32_t* e = m.nt + NT_W * s;
+    uint32_t k = *(volatile uint32_t*)e;
+    if (k == EMPTYK) {
+      // inserting lanes compare bytes, not hashes; lookups run after the insert phase
+      k = atomicCAS(e, EMPTYK, t);
+      if (k == EMPTYK) { e[1] = h; return s; }
+    }
+    const Tok o = tok_at(m, k);
+    if (o.n == me.n && bytes_eq(o.p, me.p, me.n)) return s;
+    s = (s + 1) & (m.ncap - 1);
+  }
+  return NONE32;
+}
+
+// -- id sets ------------------------------------------------------------------------
+__device__ inline bool bit_get(const uint32_t* bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1; }
+__device__ inline void bit_set(uint32_t* bm, uint32_t v) { bm[v >> 5] |= 1u << (v & 31); }
+
+// registry / label sets with a small overflow list for ids >= RB (lane 0 only)
+__device__ inline bool idset_has(const AsmMod& m, const uint32_t* bm, uint32_t which, uint32_t v) {
+  if (v < m.RB) return bit_get(bm, v);
+  const uint32_t n = m.big[which];
+  const uint32_t* lst = m.big + 2 + which * m.big_cap;
+  for (uint32_t i = 0; i < n; ++i) if (lst[i] == v) return true;
+  return false;
+}
+__device__ inline bool idset_add(const AsmMod& m, uint32_t* bm, uint32_t which, uint32_t v) {
+  if (v < m.RB) { bit_set(bm, v); return true; }
+  const uint32_t n = m.big[which];
+  if (n >= m.big_cap) return false;
+  m.big[2 + which * m.big_cap + n] = v;
+  m.big[which] = n + 1;
+  return true;
+}
+
+// k-th (1-based) positive integer that is not reserved
+__device__ inline uint32_t select_unreserved(const AsmMod& m, uint32_t k) {
+  const uint32_t nw = m.RB / 32;
+  uint32_t lo = 0, hi = nw;   // largest w with zpre[w] < k
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (m.zpre[mid] < k) lo = mid; else hi = mid;
+  }
+  const uint32_t r = k - m.zpre[lo];   // r-th zero of word lo
+  uint32_t z = ~m.rbm[lo];
+  for (uint32_t q = 1; q < r; ++q) z &= z - 1;
+  return lo * 32 + (__ffs(z) - 1);
+}
+
+// ============================================================================
+// Phase A: copy + line split.  Line separators of str.splitlines():
+// \n \r \r\n \v \f \x1c \x1d \x1e \x85    .
+__device__ inline uint32_t sep_len_at(const uint8_t* t, uint32_t T, uint32_t i) {
+  const uint8_t b = t[i];
+  if (b == '\n') return (i > 0 && t[i - 1] == '\r') ? 0 : 1;
+  if (b == '\r') return (i + 1 < T && t[i + 1] == '\n') ? 2 : 1;
+  if (b == 0x0B || b == 0x0C || b == 0x1C || b == 0x1D || b == 0x1E) return 1;
+  if (b == 0xC2) return (i + 1 < T && t[i + 1] == 0x85) ? 2 : 0;
+  if (b == 0xE2) return (i + 2 < T && t[i + 1] == 0x80 && (t[i + 2] == 0xA8 || t[i + 2] == 0xA9)) ? 3 : 0;
+  return 0;
+}
+
+__device__ __forceinline__ bool word_maybe_sep(uint32_t w) {
+  // any byte < 0x20 or any of 0xC2 / 0xE2
+  const uint32_t lt = (w - 0x20202020u) & ~w & 0x80808080u;
+  const uint32_t x2 = w ^ 0xC2C2C2C2u, x3 = w ^ 0xE2E2E2E2u;
+  const uint32_t z2 = (x2 - 0x01010101u) & ~x2 & 0x80808080u;
+  const uint32_t z3 = (x3 - 0x01010101u) & ~x3 & 0x80808080u;
+  return (lt | z2 | z3) != 0;
+}
+
+// returns L; fills ls/le (capacity cap)
+__device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint32_t cap) {
+  const uint32_t lane = lane_id_a();
+  const uint32_t T = m.T;
+  // copy (16-byte vectors when aligned; the batch arena pads modules to 16 bytes)
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const uint32_t n16 = (T + 15) / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(m.txt);
+    for (uint32_t k = lane; k < n16; k += 32) d4[k] = __ldg(s4 + k);
+  } else {
+    for (uint32_t k = lane; k < T; k += 32) m.txt[k] = src[k];
+  }
+  __syncwarp();
+  // separators: lanes scan 4-byte words; each lane records its separators in order
+  uint32_t nsep = 0;
+  const uint32_t nw = (T + 3) / 4;
+  for (uint32_t base = 0; base < nw; base += 32) {
+    const uint32_t w = base + lane;
+    uint32_t cnt = 0;
+    uint32_t pos[4], len[4];
+    if (w < nw) {
+      const uint32_t word = reinterpret_cast<const uint32_t*>(m.txt)[w];
+      if (word_maybe_sep(word)) {
+        for (uint32_t b = 0; b < 4; ++b) {
+          const uint32_t i = 4 * w + b;
+          if (i >= T) break;
+          const uint32_t sl = sep_len_at(m.txt, T, i);
+          if (sl) { pos[cnt] = i; len[cnt] = sl; ++cnt; }
+        }
+      }
+    }
+    const uint32_t incl = wincl(cnt);
+    uint32_t k = nsep + incl - cnt;
+    for (uint32_t q = 0; q < cnt; ++q, ++k) {
+      if (k < cap) { m.le[k] = pos[q]; m.ls[k + 1] = pos[q] + len[q]; }
+    }
+    nsep += __shfl_sync(FULLM, incl, 31);
+  }
+  __syncwarp();
+  if (lane == 0) m.ls[0] = 0;
+  // lines: one per separator, plus a final unterminated one if non-empty
+  uint32_t L = nsep;
+  const uint32_t last_start = nsep ? (nsep < cap ? m.ls[nsep] : T) : 0;
+  if (last_start < T) {
+    if (lane == 0 && nsep < cap) m.le[nsep] = T;
+    ++L;
+  }
+  __syncwarp();
+  return L;
+}
+
+// ============================================================================
+// Phase B: tokenize (asm.py:51-90), lane per line.  Token slots: per line
+// ub = 2*len/3 + 2 (a token needs >= 1.5 bytes on average).
+__device__ __forceinline__ uint32_t tok_ub(uint32_t len) { return 2 * len / 3 + 2; }
+
+struct AsmCtx {
+  const Tables& T;
+  const Uni& U;
+  const AsmTables& A;
+};
+
+__device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
+                                           uint32_t& npct) {
+  uint8_t* t = m.txt;
+  const uint32_t s0 = m.ls[li], e0 = m.le[li];
+  uint32_t nt = 0;
+  uint32_t fl = 0;
+  uint32_t i = s0;
+  while (i < e0) {
+    const uint8_t c = t[i];
+    if (c == ' ' || c == '\t' || c == '\r' || c == '\n') { ++i; continue; }
+    if (c == ';') break;
+    const uint32_t start = i;
+    if (c == '"') {
+      ++i;
+      uint32_t w = i;
+      bool esc = false;
+      while (i < e0 && t[i] != '"') {
+        if (t[i] == '\\' && i + 1 < e0) { ++i; esc = true; }
+        if (esc) t[w] = t[i];
+        ++w; ++i;
+      }
+      if (i >= e0) {
+        fl |= LF_TOKERR;
+        m.lerr[4 * li] = start;   // raw position of the quote
+        nt = 0;
+        break;
+      }
+      ++i;
+      m.tok[2 * (tb + nt)] = start + 1;
+      m.tok[2 * (tb + nt) + 1] = (w - start - 1) | TK_STR;
+      ++nt;
+      continue;
+    }
+    while (i < e0) {
+      const uint8_t d = t[i];
+      if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
+      ++i;
+    }
+    m.tok[2 * (tb + nt)] = start;
+    m.tok[2 * (tb + nt) + 1] = i - start;
+    ++nt;
+  }
+  if (!(fl & LF_TOKERR) && nt == 0) fl |= LF_EMPTY;
+  if (!(fl & (LF_TOKERR | LF_EMPTY)) && nt >= 3) {
+    const Tok a = tok_at(m, tb), b = tok_at(m, tb + 1);
+    if (a.n >= 1 && a.p[0] == '%' && b.n == 1 && b.p[0] == '=') fl |= LF_RESULT;
+  }
+  m.lt0[li] = tb;
+  m.lnt[li] = (fl & LF_TOKERR) ? 0 : nt;
+  m.lfl[li] = fl;
+  // reservations: result + non-string operand tokens starting with '%' (asm.py:148-153)
+  uint32_t bad = NONE32;
+  if (!(fl & (LF_TOKERR | LF_EMPTY))) {
+    const uint32_t first_op = (fl & LF_RESULT) ? 3 : 1;
+    for (uint32_t k = 0; k < nt; ++k) {
+      const bool is_res = (fl & LF_RESULT) && k == 0;
+      if (!is_res && k < first_op) continue;
+      const Tok tk = tok_at(m, tb + k);
+      if (!(tk.n >= 1 && tk.p[0] == '%')) continue;
+      if (!is_res && tk.str) continue;
+      ++npct;
+      if (!py_isdigit(tk.p + 1, tk.n - 1, X.U)) continue;
+      const IntVal v = parse_int(tk.p + 1, tk.n - 1, 10, X.U);
+      if (v.status != INT_OK || v.big || v.mag == 0 || v.mag > MAX_ID) { bad = k; break; }
+      const uint32_t id = (uint32_t)v.mag;
+      if (id < m.RB) atomicOr(&m.rbm[id >> 5], 1u << (id & 31));
+      else atomicMax(&m.misc[MS_BIGMAX_LO], id);
+    }
+  }
+  if (bad != NONE32) {
+    m.lfl[li] = fl | LF_RESVERR;
+    m.lerr[4 * li + 1] = tb + bad;
+  }
+}
+
+// ============================================================================
+// literal info (asm.py:351-362): width / signed / floating of the governing type
+struct LitInfo {
+  bool ok;
+  uint32_t wtok;     // token holding the width (int(text, 0))
+  bool sgn, flt;
+  IntVal w;
+};
+
+__device__ inline uint32_t op_tok(const AsmMod& m, uint32_t li, uint32_t k) {
+  // k-th operand token of line li (after result '=' opname), NONE32 if absent
+  const uint32_t first = (m.lfl[li] & LF_RESULT) ? 3 : 1;
+  return first + k < m.lnt[li] ? m.lt0[li] + first + k : NONE32;
+}
+
+__device__ inline LitInfo width_of_entry(const AsmMod& m, const AsmCtx& X, uint32_t ent) {
+  LitInfo r{};
+  r.ok = false;
+  if (ent == NONE32) return r;
+  const uint32_t wl = m.nt[NT_W * ent + 4];
+  if (wl == 0) return r;
+  const uint32_t li = wl - 1;
+  const uint32_t t0 = op_tok(m, li, 0);
+  const Tok w = tok_at(m, t0);
+  const uint32_t opn = m.lt0[li] + 2;   // opname token (result line)
+  const Tok on = tok_at(m, opn);
+  r.ok = true;
+  r.wtok = t0;
+  r.w = parse_int(w.p, w.n, 0, X.U);
+  if (bytes_eq_z(on.p, on.n, "OpTypeInt")) {
+    const Tok s = tok_at(m, op_tok(m, li, 1));
+    const IntVal sv = parse_int(s.p, s.n, 0, X.U);
+    r.sgn = !sv.big && !sv.neg && sv.mag == 1;
+    r.flt = false;
+  } else {
+    r.sgn = false;
+    r.flt = true;
+  }
+  return r;
+}
+
+// ============================================================================
+// The encoder (ops.py:104-271 with the assembler's coerce, asm.py:286-332)
+enum : uint32_t { M_COUNT = 0, M_WRITE = 1, M_RESOLVE = 2 };
+
+struct EncOut {
+  uint32_t nw;
+  uint32_t ecode, etok, eaux, eaux2, eaux3;
+  uint32_t result_id;
+  uint32_t word2;         // third operand word (OpVariable storage class)
+  bool unres;
+  uint32_t bad_ref;       // M_WRITE: first referenced id not in the registry
+};
+
+struct EncCtx {
+  const AsmMod& m;
+  const AsmCtx& X;
+  uint32_t li, d, mode;
+  uint32_t* out;          // M_WRITE: operand words
+  uint32_t ops0, nops;    // operand tokens
+  uint32_t rtok, ridx;    // result token, insertion index (NONE32 = none)
+  uint32_t nitems, pos;
+  EncOut r;
+  LitInfo info;
+  bool is_switch;
+};
+
+__device__ __forceinline__ uint32_t enc_item(const EncCtx& c, uint32_t k) {
+  if (c.ridx == NONE32) return c.ops0 + k;
+  if (k < c.ridx) return c.ops0 + k;
+  if (k == c.ridx) return c.rtok;
+  return c.ops0 + k - 1;
+}
+
+__device__ __forceinline__ void emit_word(EncCtx& c, uint32_t w) {
+  if (c.r.nw == 2) c.r.word2 = w;
+  if (c.out) c.out[c.r.nw] = w;
+  ++c.r.nw;
+}
+
+__device__ inline bool enc_fail(EncCtx& c, uint32_t code, uint32_t tok = 0, uint32_t a = 0, uint32_t b = 0,
+                                uint32_t c3 = 0) {
+  c.r.ecode = code; c.r.etok = tok; c.r.eaux = a; c.r.eaux2 = b; c.r.eaux3 = c3;
+  return false;
+}
+
+// enumerant of kind k by name
+__device__ inline uint32_t enum_by_name(const AsmCtx& X, uint32_t k, const uint8_t* p, uint32_t n) {
+  const uint32_t h = fnv(p, n) ^ (k * 0x9E3779B1u);
+  const uint32_t cap = X.A.enhash_cap;
+  uint32_t s = h & (cap - 1);
+  for (uint32_t probe = 0; probe < cap; ++probe) {
+    const uint32_t* e = X.A.enhash + 3 * s;
+    const uint32_t eh = __ldg(e), ei = __ldg(e + 1), ek = __ldg(e + 2);
+    if (eh == 0 && ei == 0 && ek == 0) return NONE32;
+    if (eh == h && ek == k && X.T.ename_len(ei) == n && bytes_eq(X.T.str + X.T.ename_off(ei), p, n)) return ei;
+    s = (s + 1) & (cap - 1);
+  }
+  return NONE32;
+}
+
+__device__ inline uint32_t inst_by_name(const AsmCtx& X, const uint8_t* p, uint32_t n, const uint8_t* pre = nullptr,
+                                        uint32_t npre = 0) {
+  uint32_t h = 2166136261u;
+  if (pre) h = fnv(pre, npre, h);
+  h = fnv(p, n, h);
+  const uint32_t cap = X.A.ophash_cap;
+  uint32_t s = h & (cap - 1);
+  for (uint32_t probe = 0; probe < cap; ++probe) {
+    const uint32_t* e = X.A.ophash + 2 * s;
+    const uint32_t eh = __ldg(e), ei = __ldg(e + 1);
+    if (eh == 0 && ei == 0) return NONE32;
+    if (eh == h && X.T.iname_len(ei) == n + npre) {
+      const uint8_t* nm = X.T.str + X.T.iname_off(ei);
+      if ((!pre || bytes_eq(nm, pre, npre)) && bytes_eq(nm + npre, p, n)) return ei;
+    }
+    s = (s + 1) & (cap - 1);
+  }
+  return NONE32;
+}
+
+__device__ inline bool ext_by_name(const AsmCtx& X, const uint8_t* p, uint32_t n, uint32_t& num) {
+  const uint32_t h = fnv(p, n);
+  const uint32_t cap = X.A.exhash_cap;
+  uint32_t s = h & (cap - 1);
+  for (uint32_t probe = 0; probe < cap; ++probe) {
+    const uint32_t* e = X.A.exhash + 4 * s;
+    const uint32_t eh = __ldg(e), en = __ldg(e + 1), eo = __ldg(e + 2), el = __ldg(e + 3);
+    if (eh == 0 && en == 0 && eo == 0 && el == 0) return false;
+    if (eh == h && el == n && bytes_eq(X.T.str + eo, p, n)) { num = en; return true; }
+    s = (s + 1) & (cap - 1);
+  }
+  return false;
+}
+
+// id of an %name token for coerce (asm.py:106-120); false on error
+__device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id) {
+  if (!(k.n >= 2 && k.p[0] == '%')) return enc_fail(c, E_EXPECT_ID, t);
+  if (py_isdigit(k.p + 1, k.n - 1, c.X.U)) {
+    const IntVal v = parse_int(k.p + 1, k.n - 1, 10, c.X.U);
+    id = (uint32_t)v.mag;   // validated by the reservation pass
+    return true;
+  }
+  const uint32_t e = nt_find(c.m, k.p, k.n);
+  if (e != NONE32 && c.m.nt[NT_W * e + 3] != 0) { id = c.m.nt[NT_W * e + 3]; return true; }
+  if (c.mode == M_RESOLVE) {
+    const uint32_t s = nt_insert(c.m, t);
+    uint32_t* ent = c.m.nt + NT_W * s;
+    if (ent[3] == 0) {
+      const uint32_t kk = ++c.m.misc[MS_NEWCOUNT];
+      ent[3] = select_unreserved(c.m, kk);
+    }
+    id = ent[3];
+    return true;
+  }
+  c.r.unres = true;
+  id = 0;
+  return true;
+}
+
+// encode_string (codec.py:104-114) of a string token
+__device__ inline bool enc_string(EncCtx& c, uint32_t t, const Tok& k) {
+  // text.encode("utf-8"): surrogates raise UnicodeEncodeError, then embedded NULs
+  bool nul = false;
+  uint32_t cpi = 0;
+  for (uint32_t i = 0; i < k.n;) {
+    const uint8_t b = k.p[i];
+    nul |= b == 0;
+    if (b == 0xED && i + 1 < k.n && k.p[i + 1] >= 0xA0) {
+      uint32_t j = i, cpe = cpi;   // surrogate run [cpi, cpe)
+      while (j + 3 <= k.n && k.p[j] == 0xED && k.p[j + 1] >= 0xA0) { j += 3; ++cpe; }
+      return enc_fail(c, E_SURROGATE, t, cpi, cpe);
+    }
+    i += b < 0x80 ? 1 : b < 0xE0 ? 2 : b < 0xF0 ? 3 : 4;
+    ++cpi;
+  }
+  if (nul) return enc_fail(c, E_NUL, t);
+  const uint32_t nw = k.n / 4 + 1;
+  if (c.out) {
+    for (uint32_t q = 0; q < nw; ++q) {
+      uint32_t w = 0;
+      for (uint32_t b = 0; b < 4; ++b) {
+        const uint32_t i = 4 * q + b;
+        if (i < k.n) w |= (uint32_t)k.p[i] << (8 * b);
+      }
+      emit_word(c, w);
+    }
+  } else {
+    if (c.r.nw <= 2 && c.r.nw + nw > 2) c.r.word2 = 0;
+    c.r.nw += nw;
+  }
+  return true;
+}
+
+// encode_context_dependent_literal, integer flavour (codec.py:132-168)
+__device__ inline bool enc_typed_int(EncCtx& c, uint32_t t, const IntVal& v, const LitInfo& inf) {
+  const IntVal& w = inf.w;
+  if (w.status != INT_OK || w.big || w.neg ||
+      !(w.mag == 8 || w.mag == 16 || w.mag == 32 || w.mag == 64))
+    return enc_fail(c, E_WIDTH, inf.wtok);
+  const uint32_t width = (uint32_t)w.mag;
+  bool fits;
+  if (inf.sgn) {
+    const uint64_t lim = 1ull << (width - 1);
+    fits = !v.big && (v.neg ? v.mag <= lim : v.mag < lim);
+  } else {
+    fits = !v.big && (!v.neg || v.mag == 0) && (width == 64 || v.mag < (1ull << width));
+  }
+  if (!fits) return enc_fail(c, E_FIT, t, inf.sgn ? 1 : 0, width);
+  uint64_t bits = v.neg ? (uint64_t)0 - v.mag : v.mag;
+  if (width == 64) { emit_word(c, (uint32_t)bits); emit_word(c, (uint32_t)(bits >> 32)); return true; }
+  uint32_t b = (uint32_t)bits & (width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1));
+  if (inf.sgn && v.neg && v.mag != 0 && width < 32) b |= 0xFFFFFFFFu << width;
+  emit_word(c, b);
+  return true;
+}
+
+__device__ inline bool enc_typed_float(EncCtx& c, uint32_t t, const Tok& k, const LitInfo& inf) {
+  uint64_t bits;
+  if (parse_float(k.p, k.n, c.X.U, bits) != FLT_OK) return enc_fail(c, E_FLOAT_INVALID, t);
+  const IntVal& w = inf.w;
+  if (w.status != INT_OK || w.big || w.neg ||
+      !(w.mag == 8 || w.mag == 16 || w.mag == 32 || w.mag == 64))
+    return enc_fail(c, E_WIDTH, inf.wtok);
+  if (w.mag == 8) return enc_fail(c, E_FWIDTH, inf.wtok);
+  if (w.mag == 64) { emit_word(c, (uint32_t)bits); emit_word(c, (uint32_t)(bits >> 32)); return true; }
+  uint32_t o;
+  if (w.mag == 32) { if (!pack_f32(bits, o)) return enc_fail(c, E_OVF_F, t); }
+  else if (!pack_f16(bits, o)) return enc_fail(c, E_OVF_E, t);
+  emit_word(c, o);
+  return true;
+}
+
+constexpr int ESTACK = 48;
+constexpr uint32_t KP_PARAM = 0x10000u;   // stack entry flag: take() with the "enumerant parameter" message
+
+// value(kind, item) for one stack entry; pushes follow-ups
+__device__ __noinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st, int& sp) {
+  const Tables& T = c.X.T;
+  const uint32_t k = entry & 0xFFFF;
+  if (c.pos >= c.nitems) return enc_fail(c, E_MISSING, 0, k, (entry & KP_PARAM) ? 1 : 0);
+  const uint32_t t = enc_item(c, c.pos++);
+  const Tok tk = tok_at(c.m, t);
+  uint32_t kk = k;
+  // composite: value(bases[0], tok) then param(b) for the rest
+  while (T.kcat(kk) == CAT_COMPOSITE) {
+    const uint32_t nb = T.knbases(kk), bo = T.kbase_off(kk);
+    if (sp + (int)nb > ESTACK) return enc_fail(c, E_MISSING, 0, kk, 1);
+    for (int j = (int)nb - 1; j >= 1; --j) st[sp++] = (__ldg(T.slot + bo + j) & 0xFFFF) | KP_PARAM;
+    kk = __ldg(T.slot + bo) & 0xFFFF;
+  }
+  const uint32_t cat = T.kcat(kk), sub = T.ksub(kk);
+  if (tk.str && !(cat == CAT_LITERAL && sub == LIT_STRING)) return enc_fail(c, E_STR_FOR, t, kk);
+  if (cat == CAT_ID) {
+    uint32_t id;
+    if (!enc_id(c, t, tk, id)) return false;
+    emit_word(c, id);
+    if (sub == IDR_RESULT) c.r.result_id = id;
+    else if (c.mode == M_WRITE && c.r.bad_ref == NONE32) {
+      if (!idset_has(c.m, c.m.reg, 0, id)) c.r.bad_ref = id;
+    }
+    return true;
+  }
+  if (cat == CAT_VALUEENUM) {
+    uint32_t e;
+    if (int_token(tk.p, tk.n, c.X.U)) {
+      const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+      if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+      if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+      e = (!v.big && !(v.neg && v.mag) && v.mag <= 0xFFFFFFFFull) ? T.venum_lookup(kk, (uint32_t)v.mag) : NONE32;
+      if (e == NONE32) return enc_fail(c, E_NO_ENUM_INT, t, kk);
+    } else {
+      e = enum_by_name(c.X, kk, tk.p, tk.n);
+      if (e == NONE32) return enc_fail(c, E_NO_ENUM_STR, t, kk, 0, tk.n);
+    }
+    emit_word(c, T.evalue(e));
+    const uint32_t np = T.enparams(e), po = T.eparam_off(e);
+    if (sp + (int)np > ESTACK) return enc_fail(c, E_MISSING, 0, kk, 1);
+    for (int j = (int)np - 1; j >= 0; --j) st[sp++] = T.slot_kind(po + j) | KP_PARAM;
+    return true;
+  }
+  if (cat == CAT_BITENUM) {
+    const uint32_t eo = T.kenum_off(kk), ne = T.knenum(kk);
+    uint64_t parts = 0;
+    uint32_t mask = 0;
+    if (int_token(tk.p, tk.n, c.X.U)) {
+      const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+      if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+      if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+      if (v.big || (v.neg && v.mag) || v.mag > 0xFFFFFFFFull) return enc_fail(c, E_MASK_RANGE, t, kk);
+      mask = (uint32_t)v.mag;
+      if (mask) {   // bit_components: all-or-nothing cover in file order (ops.py:77-89)
+        uint32_t covered = 0;
+        uint64_t p = 0;
+        for (uint32_t j = 0; j < ne && j < 64; ++j) {
+          const uint32_t ev = T.evalue(eo + j);
+          if (ev && (mask & ev) == ev && (covered & ev) != ev) { covered |= ev; p |= 1ull << j; }
+        }
+        if (covered == mask) parts = p;
+      }
+    } else {
+      // "A|B" names (ops.py:189-201)
+      uint32_t s = 0;
+      while (s <= tk.n) {
+        uint32_t e = s;
+        while (e < tk.n && tk.p[e] != '|') ++e;
+        uint32_t a, b;
+        py_strip(tk.p + s, e - s, c.X.U, a, b);
+        if (b > a) {
+          const uint32_t en = enum_by_name(c.X, kk, tk.p + s + a, b - a);
+          if (en == NONE32) return enc_fail(c, E_NO_ENUM_STR, t, kk, s + a, b - a);
+          const uint32_t ev = T.evalue(en);
+          if (ev && (mask & ev) != ev) parts |= 1ull << ((en - eo) & 63);
+          mask |= ev;
+        }
+        s = e + 1;
+      }
+    }
+    emit_word(c, mask);
+    // parameters of the parts in file order: push in reverse
+    for (int j = 63; j >= 0; --j) {
+      if (!((parts >> j) & 1)) continue;
+      const uint32_t e = eo + (uint32_t)j;
+      const uint32_t np = T.enparams(e), po = T.eparam_off(e);
+      if (sp + (int)np > ESTACK) return enc_fail(c, E_MISSING, 0, kk, 1);
+      for (int q = (int)np - 1; q >= 0; --q) st[sp++] = T.slot_kind(po + q) | KP_PARAM;
+    }
+    return true;
+  }
+  // literals
+  if (sub == LIT_STRING) {
+    if (tk.str) return enc_string(c, t, tk);
+    const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+    if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+    if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+    if (v.neg && (v.mag || v.big)) return enc_fail(c, E_NEG, t, kk);
+    return enc_fail(c, E_LITSTR_INT, t);
+  }
+  if (sub == LIT_CTXNUM) {
+    if (!c.info.ok) return enc_fail(c, E_NO_WIDTH, t);
+    if (c.info.flt) return enc_typed_float(c, t, tk, c.info);
+    const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+    if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+    if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+    return enc_typed_int(c, t, v, c.info);
+  }
+  if (sub == LIT_INTEGER && c.is_switch && c.info.ok) {
+    const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+    if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+    if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+    return enc_typed_int(c, t, v, c.info);
+  }
+  if ((sub == LIT_EXTINST || sub == LIT_SPECOP) && !int_token(tk.p, tk.n, c.X.U)) {
+    if (sub == LIT_EXTINST) {
+      uint32_t num;
+      if (!ext_by_name(c.X, tk.p, tk.n, num)) return enc_fail(c, E_NO_EXT, t);
+      emit_word(c, num);
+      return true;
+    }
+    const bool has_op = tk.n >= 2 && tk.p[0] == 'O' && tk.p[1] == 'p';
+    const uint32_t d = has_op ? inst_by_name(c.X, tk.p, tk.n)
+                              : inst_by_name(c.X, tk.p, tk.n, (const uint8_t*)"Op", 2);
+    if (d == NONE32) return enc_fail(c, E_NO_SPECOP, t, has_op ? 0 : 1);
+    emit_word(c, __ldg(T.irec(d) + 5));
+    return true;
+  }
+  const IntVal v = parse_int(tk.p, tk.n, 0, c.X.U);
+  if (v.status == INT_INVALID) return enc_fail(c, E_INT_INVALID, t);
+  if (v.status == INT_LIMIT) return enc_fail(c, E_INT_LIMIT, t, v.ndig);
+  const bool negative = v.neg && (v.mag || v.big);
+  if (negative && sub != LIT_EXTINST && sub != LIT_SPECOP) return enc_fail(c, E_NEG, t, kk);
+  if (negative || v.big || v.mag > 0xFFFFFFFFull) return enc_fail(c, E_LIT_RANGE, t, kk);
+  emit_word(c, (uint32_t)v.mag);
+  return true;
+}
+
+// Encoder.encode (ops.py:120-155) over the instruction's slots
+__device__ __noinline__ void encode_line(EncCtx& c) {
+  const Tables& T = c.X.T;
+  c.r.nw = 0; c.r.ecode = E_OK; c.r.result_id = 0; c.r.word2 = NONE32; c.r.unres = false;
+  c.r.bad_ref = NONE32;
+  c.pos = 0;
+  uint32_t st[ESTACK];
+  int sp = 0;
+  const uint32_t ns = T.inslots(c.d), so = T.islot_off(c.d);
+  for (uint32_t s = 0; s < ns; ++s) {
+    const uint32_t q = T.slot_quant(so + s), k = T.slot_kind(so + s);
+    if (q == Q_VAR) {
+      while (c.pos < c.nitems) {
+        st[0] = k; sp = 1;
+        while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
+      }
+      break;
+    }
+    if (q == Q_OPT && c.pos >= c.nitems) continue;
+    st[0] = k; sp = 1;
+    while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
+    if (T.slot_spec_tail(so + s)) {
+      while (c.pos < c.nitems) {
+        st[0] = T.idref; sp = 1;
+        while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
+      }
+    }
+  }
+  if (c.pos < c.nitems) enc_fail(c, E_EXTRA, 0, c.nitems - c.pos);
+}
+
+// set up an encoder context for line li (d known, not OpLabel); false = pre-encode error
+__device__ inline bool enc_setup(EncCtx& c, const AsmMod& m, uint32_t li) {
+  const Tables& T = c.X.T;
+  const uint32_t fl = m.lfl[li];
+  const bool has_res = fl & LF_RESULT;
+  c.rtok = has_res ? m.lt0[li] : NONE32;
+  const uint32_t first = has_res ? 3 : 1;
+  c.ops0 = m.lt0[li] + first;
+  c.nops = m.lnt[li] - first;
+  const uint32_t info = __ldg(c.X.A.info + 4 * c.d);
+  if (T.has_result(c.d)) {
+    if (!has_res) { c.r.ecode = E_NEEDS_RESULT; return false; }
+    const uint32_t rs = info & 0xFF;
+    c.ridx = rs < c.nops ? rs : c.nops;
+    c.nitems = c.nops + 1;
+  } else {
+    if (has_res) { c.r.ecode = E_NOT_PRODUCE; return false; }
+    c.ridx = NONE32;
+    c.nitems = c.nops;
+  }
+  c.is_switch = T.special(c.d) == SP_SWITCH;
+  c.info.ok = false;
+  if (c.is_switch) {
+    if (c.nops > 0) {
+      const Tok sel = tok_at(m, c.ops0);
+      const uint32_t e = nt_find(m, sel.p, sel.n);
+      const uint32_t vl = e != NONE32 ? m.nt[NT_W * e + 5] : 0;
+      if (vl) {
+        const Tok vt = tok_at(m, op_tok(m, vl - 1, 0));
+        c.info = width_of_entry(m, c.X, nt_find(m, vt.p, vt.n));
+      }
+    }
+  } else if (((info >> 16) & AF_CTXNUM) && T.has_rtype(c.d) && c.nops > 0) {
+    const Tok rt = tok_at(m, c.ops0);
+    c.info = width_of_entry(m, c.X, nt_find(m, rt.p, rt.n));
+  }
+  return true;
+}
+
+// ============================================================================
+// Header comments (asm.py:184-206): returns X_NONE or a ValueError outcome.
+// Groups are matched on the stripped line with Unicode \s and \d.
+struct Dec {   // a \d+ group: value mod 2^32, ==1 test, small (< 2^32) value
+  uint32_t mod32;
+  uint32_t ndig;
+  bool fits;       // value < 2^32
+  uint32_t s, e;   // byte range
+};
+
+__device__ inline uint32_t skip_ws(const uint8_t* p, uint32_t n, uint32_t i, const Uni& U) {
+  while (i < n) { uint32_t len, c = utf8_cp(p, n, i, len); if (!U.is_space(c)) break; i += len; }
+  return i;
+}
+__device__ inline bool match_dec(const uint8_t* p, uint32_t n, uint32_t& i, const Uni& U, Dec& d) {
+  d.mod32 = 0; d.ndig = 0; d.fits = true; d.s = i;
+  uint64_t v = 0;
+  while (i < n) {
+    uint32_t len, c = utf8_cp(p, n, i, len);
+    const int x = U.decimal(c);
+    if (x < 0) break;
+    d.mod32 = d.mod32 * 10 + (uint32_t)x;
+    if (d.fits) { v = v * 10 + (uint64_t)x; if (v > 0xFFFFFFFFull) d.fits = false; }
+    ++d.ndig;
+    i += len;
+  }
+  d.e = i;
+  return d.ndig > 0;
+}
+__device__ inline bool match_lit(const uint8_t* p, uint32_t n, uint32_t& i, const char* z) {
+  uint32_t j = i;
+  for (; *z; ++z, ++j) if (j >= n || p[j] != (uint8_t)*z) return false;
+  i = j;
+  return true;
+}
+
+
+// ============================================================================
+// Message formatting (lane 0): str(exc) of the exceptions the reference raises.
+struct FmtCtx {
+  const AsmMod& m;
+  const AsmCtx& X;
+  const uint32_t* knames;   // per kind: (string offset, length)
+  uint32_t* scratch;        // big-integer limbs
+  uint32_t scratch_limbs;
+};
+
+__device__ const char* const STR_LIMIT_MSG =
+    "Exceeds the limit (4300 digits) for integer string conversion; use sys.set_int_max_str_digits() "
+    "to increase the limit";
+
+template <class S>
+__device__ void put_tab(S& s, const Tables& T, uint32_t off, uint32_t len) {
+  for (uint32_t i = 0; i < len; ++i) s.put(__ldg(T.str + off + i));
+}
+template <class S>
+__device__ void put_dname(S& s, const FmtCtx& F, uint32_t d) {
+  put_tab(s, F.X.T, F.X.T.iname_off(d), F.X.T.iname_len(d));
+}
+template <class S>
+__device__ void put_kname(S& s, const FmtCtx& F, uint32_t k) {
+  put_tab(s, F.X.T, __ldg(F.knames + 2 * k), __ldg(F.knames + 2 * k + 1));
+}
+template <class S>
+__device__ void put_id(S& s, uint32_t id) {   // Id.__repr__ inside "%{id}" -> "%%N"
+  s.put('%'); s.put('%'); put_u64(s, id);
+}
+
+// does str(int(text, 0)) succeed (<= 4300 digits)?
+__device__ inline bool int_prints(const FmtCtx& F, const Tok& k, const IntVal& v) {
+  Sink cnt;
+  return put_int_decimal(cnt, k.p, v, F.X.U, F.scratch, F.scratch_limbs / 2);
+}
+template <class S>
+__device__ void put_int_of(S& s, const FmtCtx& F, const Tok& k, const IntVal& v) {
+  put_int_decimal(s, k.p, v, F.X.U, F.scratch, F.scratch_limbs / 2);
+}
+
+template <class S>
+__device__ void put_col(S& s, const FmtCtx& F, uint32_t li, uint32_t raw) {
+  put_u64(s, li + 1);
+  s.put(':');
+  put_u64(s, cp_count(F.m.txt + F.m.ls[li], raw - F.m.ls[li]) + 1);
+  s.put(':'); s.put(' ');
+}
+
+// message of an emit-phase diagnostic of line li
+template <class S>
+__device__ __noinline__ void put_emit_msg(S& s, const FmtCtx& F, uint32_t li) {
+  const AsmMod& m = F.m;
+  const uint32_t code = m.lec[li];
+  const uint32_t* e = m.lerr + 4 * li;
+  const uint32_t d = m.ld[li];
+  const Uni& U = F.X.U;
+  auto tokrepr = [&](uint32_t t, uint32_t limit) { const Tok k = tok_at(m, t); put_py_repr(s, k.p, k.n, U, limit); };
+  switch (code) {
+    case E_NOINST: {
+      put_cstr(s, "no instruction ");
+      tokrepr(m.lt0[li] + ((m.lfl[li] & LF_RESULT) ? 2 : 0), 0);
+      put_cstr(s, " in grammar");
+      break;
+    }
+    case E_NEEDS_RESULT: put_dname(s, F, d); put_cstr(s, " needs a result name"); break;
+    case E_NOT_PRODUCE: put_dname(s, F, d); put_cstr(s, " does not produce a result"); break;
+    case E_MISSING:
+      put_cstr(s, "missing operand: expected "); put_dname(s, F, d);
+      put_cstr(s, e[2] ? " enumerant parameter of kind " : " operand of kind "); put_kname(s, F, e[1]);
+      break;
+    case E_EXTRA: put_dname(s, F, d); put_cstr(s, ": "); put_u64(s, e[1]); put_cstr(s, " unexpected extra operand(s)"); break;
+    case E_STR_FOR: put_cstr(s, "string literal given for a "); put_kname(s, F, e[1]); put_cstr(s, " operand"); break;
+    case E_EXPECT_ID: put_cstr(s, "expected an id like %name, got "); tokrepr(e[0], 0); break;
+    case E_INT_INVALID: put_cstr(s, "invalid literal for int() with base 0: "); tokrepr(e[0], 200); break;
+    case E_INT_LIMIT:
+      put_cstr(s, "Exceeds the limit (4300 digits) for integer string conversion: value has ");
+      put_u64(s, e[1]);
+      put_cstr(s, " digits; use sys.set_int_max_str_digits() to increase the limit");
+      break;
+    case E_FLOAT_INVALID: put_cstr(s, "could not convert string to float: "); tokrepr(e[0], 0); break;
+    case E_NO_WIDTH: put_cstr(s, "cannot resolve the literal width (unknown governing type)"); break;
+    case E_NEG: put_kname(s, F, e[1]); put_cstr(s, " cannot be negative"); break;
+    case E_NO_ENUM_STR: {
+      const Tok k = tok_at(m, e[0]);
+      put_cstr(s, "no enumerant ");
+      put_py_repr(s, k.p + e[2], e[3], U);
+      put_cstr(s, " in operand kind "); put_kname(s, F, e[1]);
+      break;
+    }
+    case E_NO_ENUM_INT: case E_LITSTR_INT: case E_FIT: case E_LIT_RANGE: case E_WIDTH: case E_FWIDTH: {
+      const Tok k = tok_at(m, e[0]);
+      const IntVal v = parse_int(k.p, k.n, 0, U);
+      if (!int_prints(F, k, v)) { put_cstr(s, STR_LIMIT_MSG); break; }
+      if (code == E_NO_ENUM_INT) {
+        put_cstr(s, "no enumerant "); put_int_of(s, F, k, v); put_cstr(s, " in operand kind "); put_kname(s, F, e[1]);
+      } else if (code == E_LITSTR_INT) {
+        put_dname(s, F, d); put_cstr(s, ": literal string expected, got "); put_int_of(s, F, k, v);
+      } else if (code == E_FIT) {
+        put_cstr(s, "value "); put_int_of(s, F, k, v);
+        put_cstr(s, e[1] ? " does not fit a signed " : " does not fit an unsigned "); put_u64(s, e[2]);
+        put_cstr(s, "-bit literal");
+      } else if (code == E_LIT_RANGE) {
+        put_dname(s, F, d); put_cstr(s, ": "); put_kname(s, F, e[1]); put_cstr(s, " value ");
+        put_int_of(s, F, k, v); put_cstr(s, " out of range");
+      } else {
+        put_cstr(s, code == E_WIDTH ? "unsupported literal width " : "unsupported float width ");
+        put_int_of(s, F, k, v);
+      }
+      break;
+    }
+    case E_MASK_RANGE: {
+      const Tok k = tok_at(m, e[0]);
+      const IntVal v = parse_int(k.p, k.n, 0, U);
+      put_dname(s, F, d); put_cstr(s, ": "); put_kname(s, F, e[1]); put_cstr(s, " mask ");
+      put_int_hex(s, k.p, v, U, F.scratch, F.scratch_limbs);
+      put_cstr(s, " out of range");
+      break;
+    }
+    case E_NUL: put_cstr(s, "string literal contains an embedded NUL byte"); break;
+    case E_SURROGATE: {
+      const Tok k = tok_at(m, e[0]);
+      put_cstr(s, "'utf-8' codec can't encode ");
+      if (e[2] - e[1] == 1) {
+        uint32_t cp = 0;   // the surrogate code point at index e[1]
+        for (uint32_t i = 0, q = 0; i < k.n; ++q) {
+          uint32_t len, c = utf8_cp(k.p, k.n, i, len);
+          if (q == e[1]) { cp = c; break; }
+          i += len;
+        }
+        put_cstr(s, "character '\\u");
+        for (int sh = 12; sh >= 0; sh -= 4) s.put((uint8_t)"0123456789abcdef"[(cp >> sh) & 0xF]);
+        put_cstr(s, "' in position "); put_u64(s, e[1]);
+      } else {
+        put_cstr(s, "characters in position "); put_u64(s, e[1]); s.put('-'); put_u64(s, e[2] - 1);
+      }
+      put_cstr(s, ": surrogates not allowed");
+      break;
+    }
+    case E_NO_EXT: put_cstr(s, "no extended instruction "); tokrepr(e[0], 0); break;
+    case E_NO_SPECOP: {
+      const Tok k = tok_at(m, e[0]);
+      put_cstr(s, "no instruction ");
+      put_py_repr_prefixed(s, e[1] ? "Op" : "", k.p, k.n, U);
+      put_cstr(s, " in grammar");
+      break;
+    }
+    case S_LABEL_OUTSIDE: put_cstr(s, "OpLabel outside a function"); break;
+    case S_LABEL_NORESULT: put_cstr(s, "OpLabel needs a result name"); break;
+    case S_LABEL_RESOLVE: put_cstr(s, "expected an id like %name, got "); tokrepr(m.lt0[li], 0); break;
+    case S_LABEL_USED: put_id(s, e[0]); put_cstr(s, " is already used as a block label"); break;
+    case S_DUP: put_id(s, e[0]); put_cstr(s, " is defined by more than one instruction"); break;
+    case S_FUNC_BEFORE_END: put_cstr(s, "OpFunction before the previous OpFunctionEnd"); break;
+    case S_OUTSIDE: put_dname(s, F, d); put_cstr(s, " outside a function"); break;
+    case S_PARAM_AFTER_BLOCK: put_cstr(s, "function parameters must precede all blocks"); break;
+    case S_MM_DUP: put_cstr(s, "module already has a memory model"); break;
+    case S_NEED_BLOCK: put_dname(s, F, d); put_cstr(s, " must appear inside a block"); break;
+    case S_TERMINATED: put_cstr(s, "block already has its terminator"); break;
+    case S_VAR_FIRST: put_cstr(s, "Function-storage OpVariable must open the first block"); break;
+    case S_VAR_NOTFN: put_cstr(s, "only Function-storage OpVariable belongs in a block"); break;
+    case S_NOT_BLOCK: {
+      put_dname(s, F, d); put_cstr(s, " (");
+      const uint32_t* inf = F.X.A.info + 4 * d;
+      put_tab(s, F.X.T, __ldg(inf + 1), __ldg(inf + 2));
+      put_cstr(s, ") is not a block instruction");
+      break;
+    }
+    case S_KEYERROR: {   // str(KeyError(name)) = repr(name)
+      const Tables& T = F.X.T;
+      put_py_repr(s, T.str + T.iname_off(d), T.iname_len(d), U);
+      break;
+    }
+    default: put_cstr(s, "internal: unknown diagnostic"); break;
+  }
+}
+
+// AssemblyError text: "{n} error(s):\n" + "line:col: msg" lines (errors.py:73-94)
+template <class S>
+__device__ __noinline__ void put_assembly_error(S& s, const FmtCtx& F, uint32_t ndiag) {
+  const AsmMod& m = F.m;
+  put_u64(s, ndiag);
+  put_cstr(s, " error(s):");
+  for (uint32_t li = 0; li < m.L; ++li) {          // tokenizer diagnostics
+    if (!(m.lfl[li] & LF_TOKERR)) continue;
+    s.put('\n'); put_col(s, F, li, m.lerr[4 * li]); put_cstr(s, "unterminated string literal");
+  }
+  for (uint32_t li = 0; li < m.L; ++li) {          // result-name diagnostics
+    if (!(m.lfl[li] & LF_RESOLVE_ERR)) continue;
+    s.put('\n'); put_col(s, F, li, tok_at(m, m.lt0[li]).raw);
+    put_cstr(s, "expected an id like %name, got ");
+    const Tok k = tok_at(m, m.lt0[li]);
+    put_py_repr(s, k.p, k.n, F.X.U);
+  }
+  for (uint32_t li = 0; li < m.L; ++li) {          // emit diagnostics
+    if ((m.lfl[li] & (LF_TOKERR | LF_EMPTY)) || m.lec[li] == E_OK) continue;
+    s.put('\n');
+    put_col(s, F, li, tok_at(m, m.lt0[li] + ((m.lfl[li] & LF_RESULT) ? 2 : 0)).raw);
+    put_emit_msg(s, F, li);
+  }
+}
+
+// module-level exception text
+template <class S>
+__device__ __noinline__ void put_module_error(S& s, const FmtCtx& F, uint32_t x, uint32_t ndiag) {
+  const AsmMod& m = F.m;
+  const uint32_t* ms = m.misc;
+  switch (x) {
+    case X_VERSION: {
+      put_cstr(s, "unsupported SPIR-V version ");
+      // normalised decimals of the last Version: groups (byte ranges in misc)
+      for (int g = 0; g < 2; ++g) {
+        if (g) s.put('.');
+        const uint32_t a = ms[MS_V0 + 2 * g], b = ms[MS_V0 + 2 * g + 1];
+        bool lead = true, any = false;
+        for (uint32_t i = a; i < b;) {
+          uint32_t len, c = utf8_cp(m.txt, b, i, len);
+          i += len;
+          const int dv = F.X.U.decimal(c);
+          if (lead && dv == 0) continue;
+          lead = false; any = true;
+          s.put((uint8_t)('0' + dv));
+        }
+        if (!any) s.put('0');
+      }
+      break;
+    }
+    case X_VERSION_DEFAULT:
+      put_cstr(s, "unsupported SPIR-V version "); put_u64(s, ms[MS_V0]); s.put('.'); put_u64(s, ms[MS_V0 + 1]);
+      break;
+    case X_VERSION_LIMIT:
+      put_cstr(s, "Exceeds the limit (4300 digits) for integer string conversion: value has ");
+      put_u64(s, ms[MS_XA]);
+      put_cstr(s, " digits; use sys.set_int_max_str_digits() to increase the limit");
+      break;
+    case X_RESERVE: {
+      const uint32_t li = ms[MS_RESV_LINE];
+      const Tok k = tok_at(m, m.lerr[4 * li + 1]);
+      const IntVal v = parse_int(k.p + 1, k.n - 1, 10, F.X.U);
+      if (v.status == INT_INVALID) {
+        put_cstr(s, "invalid literal for int() with base 10: ");
+        put_py_repr(s, k.p + 1, k.n - 1, F.X.U, 200);
+      } else if (v.status == INT_LIMIT) {
+        put_cstr(s, "Exceeds the limit (4300 digits) for integer string conversion: value has ");
+        put_u64(s, v.ndig);
+        put_cstr(s, " digits; use sys.set_int_max_str_digits() to increase the limit");
+      } else {
+        put_cstr(s, "id ");
+        put_int_decimal(s, k.p + 1, v, F.X.U, F.scratch, F.scratch_limbs / 2);
+        put_cstr(s, " out of range");
+      }
+      break;
+    }
+    case X_OVERFLOW:
+      put_cstr(s, m.lec[ms[MS_OVF_LINE]] == E_OVF_E ? "float too large to pack with e format"
+                                                     : "float too large to pack with f format");
+      break;
+    case X_ASSEMBLY: put_assembly_error(s, F, ndiag); break;
+    case X_STRUCT_END: put_cstr(s, "function "); put_id(s, ms[MS_XA]); put_cstr(s, " has no OpFunctionEnd"); break;
+    case X_STRUCT_TERM:
+      put_cstr(s, "block "); put_id(s, ms[MS_XB]); put_cstr(s, " in function "); put_id(s, ms[MS_XA]);
+      put_cstr(s, " has no terminator");
+      break;
+    case X_SERIAL:
+      put_id(s, ms[MS_XA]); put_cstr(s, " is referenced by "); put_dname(s, F, ms[MS_XB]);
+      put_cstr(s, " but never defined");
+      break;
+    case X_WC:
+      put_cstr(s, "instruction length "); put_u64(s, ms[MS_XA]);
+      put_cstr(s, " words overflows the 16-bit count");
+      break;
+    default: put_cstr(s, "internal: module exceeds the per-warp assembler scratch"); break;
+  }
+}
+
+// ============================================================================
+// Phase C: header comments (lane 0).  Returns X_NONE / X_VERSION_LIMIT and
+// fills major/minor validity, generator and schema (asm.py:184-206).
+__device__ __noinline__ uint32_t scan_header(AsmMod& m, const AsmCtx& X, uint32_t dv) {
+  const Uni& U = X.U;
+  uint32_t* ms = m.misc;
+  bool vset = false;
+  for (uint32_t li = 0; li < m.L; ++li) {
+    const uint8_t* p = m.txt + m.ls[li];
+    const uint32_t n = m.le[li] - m.ls[li];
+    uint32_t a, b;
+    py_strip(p, n, U, a, b);
+    if (b > a && p[a] != ';') break;
+    if (b == a) continue;
+    // the three patterns, anchored at a, must consume up to b
+    for (int key = 0; key < 3; ++key) {
+      uint32_t i = a;
+      if (!match_lit(p, b, i, ";")) break;
+      i = skip_ws(p, b, i, U);
+      const char* kw = key == 0 ? "Version:" : key == 1 ? "Generator:" : "Schema:";
+      if (!match_lit(p, b, i, kw)) continue;
+      i = skip_ws(p, b, i, U);
+      Dec d1, d2;
+      if (!match_dec(p, b, i, U, d1)) continue;
+      if (key == 0) {
+        if (!match_lit(p, b, i, ".")) continue;
+        if (!match_dec(p, b, i, U, d2)) continue;
+      } else if (key == 1) {
+        if (!match_lit(p, b, i, ";")) continue;
+        i = skip_ws(p, b, i, U);
+        if (!match_dec(p, b, i, U, d2)) continue;
+      }
+      i = skip_ws(p, b, i, U);
+      if (i != b) continue;
+      // int() of each group, in order (the 4300-digit limit raises here)
+      if (d1.ndig > PY_MAX_STR_DIGITS) { ms[MS_XA] = d1.ndig; return X_VERSION_LIMIT; }
+      if (key != 2 && d2.ndig > PY_MAX_STR_DIGITS) { ms[MS_XA] = d2.ndig; return X_VERSION_LIMIT; }
+      const uint32_t base = m.ls[li];
+      if (key == 0) {
+        vset = true;
+        ms[MS_MAJOR] = (d1.fits && d1.mod32 == 1) ? 1 : 0;
+        ms[MS_MINOR] = (d2.fits && d2.mod32 <= 6) ? d2.mod32 + 1 : 0;
+        ms[MS_V0] = base + d1.s; ms[MS_V0 + 1] = base + d1.e;
+        ms[MS_V0 + 2] = base + d2.s; ms[MS_V0 + 3] = base + d2.e;
+      } else if (key == 1) {
+        ms[MS_GEN] = ((d1.mod32 & 0xFFFFu) << 16) | d2.mod32;
+        ms[MS_GENSET] = 1;
+      } else {
+        ms[MS_SCHEMA] = d1.mod32;
+      }
+      break;
+    }
+  }
+  if (!vset) {   // Assembler.default_version
+    const uint32_t mj = dv >> 16, mn = dv & 0xFFFF;
+    if (!(mj == 1 && mn <= 6)) { ms[MS_V0] = mj; ms[MS_V0 + 1] = mn; return X_VERSION_DEFAULT; }
+    ms[MS_MAJOR] = 1; ms[MS_MINOR] = mn + 1;
+    return X_NONE;
+  }
+  if (!(ms[MS_MAJOR] == 1 && ms[MS_MINOR] != 0)) return X_VERSION;
+  return X_NONE;
+}
+
+// label id / result id of a result token without encoding (lane-local)
+__device__ inline uint32_t result_id_of(const AsmMod& m, const AsmCtx& X, uint32_t t) {
+  const Tok k = tok_at(m, t);
+  if (k.n < 2) return 0;
+  if (py_isdigit(k.p + 1, k.n - 1, X.U)) return (uint32_t)parse_int(k.p + 1, k.n - 1, 10, X.U).mag;
+  const uint32_t e = nt_find(m, k.p, k.n);
+  return e != NONE32 ? m.nt[NT_W * e + 3] : 0;
+}
+
+// lane 0: re-run the encoder of line li assigning ids to unseen names in order
+__device__ __noinline__ void resolve_line(AsmMod& m, const AsmCtx& X, uint32_t li) {
+  EncCtx c{m, X, li, m.ld[li], M_RESOLVE, nullptr};
+  if (!enc_setup(c, m, li)) return;
+  encode_line(c);
+}
+
+// Phase G (lane 0): the scope state machine of Assembler._emit / builder scopes.
+constexpr uint32_t FN_ENDED = 1, FN_BLOCKS = 2;
+__device__ __noinline__ uint32_t state_machine(AsmMod& m, const AsmCtx& X) {
+  const Tables& T = X.T;
+  int32_t fn = -1, blk = -1;
+  uint32_t nfn = 0, nblk = 0, ndiag = 0;
+  bool mm = false, blk_term = false, blk_nonvar = false;
+  uint32_t* bucket = m.misc + MS_BUCKET0;
+  auto diag = [&](uint32_t li, uint32_t code, uint32_t a = 0) {
+    m.lec[li] = code;
+    m.lerr[4 * li] = a;
+    ++ndiag;
+  };
+  auto place_fn = [&](uint32_t li, uint32_t words) {
+    m.lgrp[li] = 16 + (uint32_t)fn;
+    m.loff[li] = m.fn[4 * fn + 2];
+    m.fn[4 * fn + 2] += words;
+    m.lfl[li] |= LF_PLACED;
+  };
+  for (uint32_t li = 0; li < m.L; ++li) {
+    const uint32_t fl = m.lfl[li];
+    if (fl & (LF_TOKERR | LF_EMPTY)) continue;
+    const uint32_t d = m.ld[li];
+    if (d == NONE32) { ++ndiag; continue; }
+    const uint32_t sp = T.special(d);
+    if (sp == SP_LABEL) {
+      if (fn < 0) { diag(li, S_LABEL_OUTSIDE); continue; }
+      if (!(fl & LF_RESULT)) { diag(li, S_LABEL_NORESULT); continue; }
+      if (fl & LF_RESOLVE_ERR) { diag(li, S_LABEL_RESOLVE); continue; }
+      const uint32_t L = m.lrid[li];
+      if (idset_has(m, m.lab, 1, L)) { diag(li, S_LABEL_USED, L); continue; }
+      if (idset_has(m, m.reg, 0, L)) { diag(li, S_DUP, L); continue; }
+      if (!idset_add(m, m.lab, 1, L) || !idset_add(m, m.reg, 0, L)) return NONE32;
+      blk = (int32_t)nblk++;
+      m.blk[3 * blk] = (uint32_t)fn; m.blk[3 * blk + 1] = L; m.blk[3 * blk + 2] = 0;
+      m.fn[4 * fn + 1] |= FN_BLOCKS;
+      blk_term = false; blk_nonvar = false;
+      m.lnw[li] = 1;
+      place_fn(li, 2);
+      continue;
+    }
+    if (fl & LF_UNRES) resolve_line(m, X, li);
+    if (m.lec[li] != E_OK) { ++ndiag; continue; }
+    const uint32_t info = __ldg(X.A.info + 4 * d);
+    const uint32_t words = 1 + m.lnw[li];
+    const bool has_res = T.has_result(d);
+    const uint32_t rid = m.lrid[li];
+    if (sp == SP_FUNCTION) {
+      if (fn >= 0 && !(m.fn[4 * fn + 1] & FN_ENDED)) { diag(li, S_FUNC_BEFORE_END); continue; }
+      if (idset_has(m, m.reg, 0, rid)) { diag(li, S_DUP, rid); continue; }
+      if (!idset_add(m, m.reg, 0, rid)) return NONE32;
+      fn = (int32_t)nfn++;
+      m.fn[4 * fn] = rid; m.fn[4 * fn + 1] = 0; m.fn[4 * fn + 2] = 0; m.fn[4 * fn + 3] = 0;
+      blk = -1;
+      place_fn(li, words);
+      continue;
+    }
+    if (sp == SP_FUNCTIONPARAM || sp == SP_FUNCTIONEND) {
+      if (fn < 0) { diag(li, S_OUTSIDE); continue; }
+      if (sp == SP_FUNCTIONPARAM) {
+        if (m.fn[4 * fn + 1] & FN_BLOCKS) { diag(li, S_PARAM_AFTER_BLOCK); continue; }
+        if (has_res) {
+          if (idset_has(m, m.reg, 0, rid)) { diag(li, S_DUP, rid); continue; }
+          if (!idset_add(m, m.reg, 0, rid)) return NONE32;
+        }
+        place_fn(li, words);
+        continue;
+      }
+      m.fn[4 * fn + 1] |= FN_ENDED;
+      m.lfl[li] |= LF_DROP;
+      fn = -1; blk = -1;
+      continue;
+    }
+    uint32_t route = (info >> 8) & 0xFF;
+    if (route == ROUTE_VARIABLE) route = (fl & LF_VARFN) ? ROUTE_SCOPE : 10;
+    if (route == ROUTE_KEYERROR) { diag(li, S_KEYERROR); continue; }
+    if (route != ROUTE_SCOPE) {   // ModuleScope.add
+      if (route == 3 && mm) { diag(li, S_MM_DUP); continue; }
+      if (has_res) {
+        if (idset_has(m, m.reg, 0, rid)) { diag(li, S_DUP, rid); continue; }
+        if (!idset_add(m, m.reg, 0, rid)) return NONE32;
+      }
+      if (route == 3) mm = true;
+      m.lgrp[li] = route;
+      m.loff[li] = bucket[route];
+      bucket[route] += words;
+      m.lfl[li] |= LF_PLACED;
+      continue;
+    }
+    // BlockScope.add
+    if (blk < 0) { diag(li, S_NEED_BLOCK); continue; }
+    if (blk_term) { diag(li, S_TERMINATED); continue; }
+    if (sp == SP_VARIABLE) {
+      if (!(fl & LF_VARFN)) { diag(li, S_VAR_NOTFN); continue; }
+      if (blk_nonvar) { diag(li, S_VAR_FIRST); continue; }
+    } else if ((info >> 16) & AF_BLOCK_FORBIDDEN) {
+      diag(li, S_NOT_BLOCK);
+      continue;
+    }
+    if (has_res) {
+      if (idset_has(m, m.reg, 0, rid)) { diag(li, S_DUP, rid); continue; }
+      if (!idset_add(m, m.reg, 0, rid)) return NONE32;
+    }
+    place_fn(li, words);
+    if ((info >> 16) & AF_TERMINATOR) { blk_term = true; m.blk[3 * blk + 2] = 1; }
+    if (sp != SP_VARIABLE) blk_nonvar = true;
+  }
+  m.misc[MS_NFN] = nfn;
+  m.misc[MS_NBLK] = nblk;
+  return ndiag;
+}
+
+// ============================================================================
+// Module driver
+constexpr uint32_t BIG_CAP = 64;
+
+__device__ __forceinline__ uint64_t al16(uint64_t x) { return (x + 15) & ~15ull; }
+
+// reserve output bytes (bump allocator, 16-byte aligned)
+__device__ inline uint64_t asm_alloc(const AsmArgs& a, uint64_t bytes, bool& fits) {
+  uint64_t off = 0;
+  if (lane_id_a() == 0 && bytes) {
+    off = atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 4), (unsigned long long)al16(bytes));
+    if (off + bytes > a.out_cap) atomicExch(a.counters + 2, 1u);
+  }
+  off = __shfl_sync(FULLM, off, 0);
+  fits = off + bytes <= a.out_cap;
+  return off;
+}
+
+// status codes (skgpu.h)
+enum : int32_t { AST_OK = 0, AST_CODEC = 4, AST_VALUE = 7, AST_OVERFLOW = 8, AST_ASSEMBLY = 9,
+                 AST_STRUCTURE = 10, AST_SERIALIZATION = 11, AST_INTERNAL = 99 };
+
+__device__ inline int32_t outcome_status(uint32_t x) {
+  switch (x) {
+    case X_VERSION: case X_VERSION_LIMIT: case X_VERSION_DEFAULT: case X_RESERVE: return AST_VALUE;
+    case X_OVERFLOW: return AST_OVERFLOW;
+    case X_ASSEMBLY: return AST_ASSEMBLY;
+    case X_STRUCT_END: case X_STRUCT_TERM: return AST_STRUCTURE;
+    case X_SERIAL: return AST_SERIALIZATION;
+    case X_WC: return AST_CODEC;
+    default: return AST_INTERNAL;
+  }
+}
+
+__device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const AsmCtx& X, uint32_t t, uint32_t x,
+                                          uint32_t ndiag, uint32_t* fscratch, uint32_t flimbs) {
+  const uint32_t lane = lane_id_a();
+  FmtCtx F{m, X, X.T.blob + __ldg(X.T.blob + 52), fscratch, flimbs};
+  uint32_t n = 0;
+  if (lane == 0) {
+    Sink cnt;
+    if (x == X_INTERNAL) put_cstr(cnt, "internal: module exceeds the per-warp assembler scratch");
+    else put_module_error(cnt, F, x, ndiag);
+    n = cnt.n;
+  }
+  n = __shfl_sync(FULLM, n, 0);
+  bool fits;
+  const uint64_t off = asm_alloc(a, n, fits);
+  if (lane == 0) {
+    if (fits) {
+      Sink w(a.out + off);
+      if (x == X_INTERNAL) put_cstr(w, "internal: module exceeds the per-warp assembler scratch");
+      else put_module_error(w, F, x, ndiag);
+    }
+    a.out_span[2 * t] = (int64_t)off;
+    a.out_span[2 * t + 1] = (int64_t)n;
+    a.status[t] = outcome_status(x);
+  }
+  __syncwarp();
+}
+
+__device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot) {
+  const uint32_t lane = lane_id_a();
+  const int64_t len64 = a.mod_len[t];
+  const uint8_t* src = a.text + a.mod_off[t];
+  AsmMod m{};
+  uint64_t used = 0;
+  auto take = [&](uint64_t bytes) -> uint8_t* { uint8_t* r = slot + used; used += al16(bytes); return r; };
+  uint32_t* fscratch = nullptr;
+  uint32_t flimbs = 0;
+  auto fail_internal = [&]() { finish_error(a, m, X, t, X_INTERNAL, 0, nullptr, 0); };
+  const uint32_t T = (uint32_t)len64;
+  m.T = T;
+  m.misc = reinterpret_cast<uint32_t*>(take(64 * 4));
+  m.txt = take((uint64_t)T + 16);
+  m.ls = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
+  m.le = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
+  if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); return; }
+  for (uint32_t k = lane; k < 64; k += 32) m.misc[k] = 0;
+  __syncwarp();
+  const uint32_t L = split_lines(m, src, T + 1);
+  m.L = L;
+  // per-line arrays
+  m.lt0 = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lnt = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lfl = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.ld = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lec = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lnw = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lrid = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lgrp = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.loff = reinterpret_cast<uint32_t*>(take(4ull * L));
+  m.lerr = reinterpret_cast<uint32_t*>(take(16ull * L));
+  // token slots
+  uint32_t ntb = 0;
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    ntb += li < L ? tok_ub(m.le[li] - m.ls[li]) : 0;
+  }
+  ntb = wsum(ntb);
+  m.ntb = ntb;
+  m.tok = reinterpret_cast<uint32_t*>(take(8ull * ntb));
+  m.RB = ((2 * T / 3 + 2 * L + 64) + 31) & ~31u;
+  m.rbm = reinterpret_cast<uint32_t*>(take(m.RB / 8));
+  m.zpre = reinterpret_cast<uint32_t*>(take(m.RB / 8 + 4));
+  m.reg = reinterpret_cast<uint32_t*>(take(m.RB / 8));
+  m.lab = reinterpret_cast<uint32_t*>(take(m.RB / 8));
+  m.fn = reinterpret_cast<uint32_t*>(take(16ull * L + 16));
+  m.blk = reinterpret_cast<uint32_t*>(take(12ull * L + 16));
+  m.big_cap = BIG_CAP;
+  m.big = reinterpret_cast<uint32_t*>(take(4ull * (2 + 2 * BIG_CAP)));
+  if (used > a.gslot_bytes) { fail_internal(); return; }
+  for (uint32_t k = lane; k < m.RB / 32; k += 32) { m.rbm[k] = 0; m.reg[k] = 0; m.lab[k] = 0; }
+  if (lane < 2) m.big[lane] = 0;
+  __syncwarp();
+  if (lane == 0) m.rbm[0] = 1;   // id 0 is never allocated
+  __syncwarp();
+
+  // -- B: tokenize + reservations ------------------------------------------------
+  uint32_t npct = 0;
+  {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < L; base += 32) {
+      const uint32_t li = base + lane;
+      const uint32_t ub = li < L ? tok_ub(m.le[li] - m.ls[li]) : 0;
+      const uint32_t incl = wincl(ub);
+      if (li < L) {
+        m.lec[li] = E_OK;
+        tokenize_line(m, X, li, carry + incl - ub, npct);
+      }
+      carry += __shfl_sync(FULLM, incl, 31);
+    }
+  }
+  npct = wsum(npct);
+  m.ncap = 64;
+  while (m.ncap < 2 * npct + 16) m.ncap <<= 1;
+  m.nt = reinterpret_cast<uint32_t*>(take(4ull * NT_W * m.ncap));
+  // formatting scratch (lane 0, error paths): big integers of the longest token
+  flimbs = T / 2 + 64;
+  fscratch = reinterpret_cast<uint32_t*>(take(4ull * flimbs));
+  if (used > a.gslot_bytes) { fail_internal(); return; }
+  for (uint32_t k = lane; k < m.ncap; k += 32) {
+    uint32_t* e = m.nt + NT_W * k;
+    e[0] = EMPTYK; e[1] = 0; e[2] = NONE32; e[3] = 0; e[4] = 0; e[5] = 0;
+  }
+  __syncwarp();
+
+  // -- C: header comments; then the first reservation failure --------------------
+  uint32_t x = X_NONE;
+  if (lane == 0) x = scan_header(m, X, a.default_version);
+  x = __shfl_sync(FULLM, x, 0);
+  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); return; }
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    const unsigned bad = __ballot_sync(FULLM, li < L && (m.lfl[li] & LF_RESVERR));
+    if (bad) {
+      if (lane == 0) m.misc[MS_RESV_LINE] = base + __ffs(bad) - 1;
+      __syncwarp();
+      finish_error(a, m, X, t, X_RESERVE, 0, fscratch, flimbs);
+      return;
+    }
+  }
+
+  // -- D: unreserved prefix counts; symbolic result names in document order -------
+  {
+    uint32_t carry = 0;
+    const uint32_t nw = m.RB / 32;
+    for (uint32_t base = 0; base < nw; base += 32) {
+      const uint32_t w = base + lane;
+      const uint32_t z = w < nw ? 32 - __popc(m.rbm[w]) : 0;
+      const uint32_t incl = wincl(z);
+      if (w < nw) m.zpre[w] = carry + incl - z;
+      carry += __shfl_sync(FULLM, incl, 31);
+    }
+  }
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    if (li < L && (m.lfl[li] & LF_RESULT)) {
+      const uint32_t rt = m.lt0[li];
+      const Tok k = tok_at(m, rt);
+      const uint32_t e = nt_insert(m, rt);
+      if (!py_isdigit(k.p + 1, k.n - 1, X.U)) {
+        if (k.n == 1) m.lfl[li] |= LF_RESOLVE_ERR;
+        else if (e != NONE32) atomicMin(&m.nt[NT_W * e + 2], li);
+      }
+    }
+  }
+  __syncwarp();
+  {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < L; base += 32) {
+      const uint32_t li = base + lane;
+      uint32_t e = NONE32;
+      bool first = false;
+      if (li < L && (m.lfl[li] & LF_RESULT) && !(m.lfl[li] & LF_RESOLVE_ERR)) {
+        const Tok k = tok_at(m, m.lt0[li]);
+        if (!py_isdigit(k.p + 1, k.n - 1, X.U)) {
+          e = nt_find(m, k.p, k.n);
+          first = e != NONE32 && m.nt[NT_W * e + 2] == li;
+        }
+      }
+      const unsigned b = __ballot_sync(FULLM, first);
+      if (first) m.nt[NT_W * e + 3] = select_unreserved(m, carry + __popc(b & ((1u << lane) - 1)) + 1);
+      carry += __popc(b);
+    }
+    if (lane == 0) m.misc[MS_NEWCOUNT] = carry;
+  }
+  __syncwarp();
+
+  // -- E: opname lookup, width / value-type scans ---------------------------------
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    if (li >= L) continue;
+    const uint32_t fl = m.lfl[li];
+    if (fl & (LF_TOKERR | LF_EMPTY)) { m.ld[li] = NONE32; continue; }
+    const bool res = fl & LF_RESULT;
+    const Tok on = tok_at(m, m.lt0[li] + (res ? 2 : 0));
+    const uint32_t d = inst_by_name(X, on.p, on.n);
+    m.ld[li] = d;
+    if (!res || m.lnt[li] < 4) continue;
+    const uint32_t e = nt_find(m, tok_at(m, m.lt0[li]).p, tok_at(m, m.lt0[li]).n);
+    if (e == NONE32) continue;
+    const Tok o0 = tok_at(m, m.lt0[li] + 3);
+    const bool ti = bytes_eq_z(on.p, on.n, "OpTypeInt"), tf = bytes_eq_z(on.p, on.n, "OpTypeFloat");
+    if (ti || tf) {
+      bool ok = parse_int(o0.p, o0.n, 0, X.U).status == INT_OK;
+      if (ok && ti) {
+        if (m.lnt[li] < 5) ok = false;
+        else { const Tok o1 = tok_at(m, m.lt0[li] + 4); ok = parse_int(o1.p, o1.n, 0, X.U).status == INT_OK; }
+      }
+      if (ok) atomicMax(&m.nt[NT_W * e + 4], li + 1);
+    }
+    if (d != NONE32 && X.T.has_rtype(d) && o0.n >= 1 && o0.p[0] == '%') atomicMax(&m.nt[NT_W * e + 5], li + 1);
+  }
+  __syncwarp();
+
+  // -- F: encode pass 1 -------------------------------------------------------------
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    if (li >= L) continue;
+    const uint32_t fl = m.lfl[li];
+    m.lnw[li] = 0; m.lrid[li] = 0;
+    if (fl & (LF_TOKERR | LF_EMPTY)) continue;
+    const uint32_t d = m.ld[li];
+    if (d == NONE32) { m.lec[li] = E_NOINST; continue; }
+    if (X.T.special(d) == SP_LABEL) {
+      if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
+      continue;
+    }
+    EncCtx c{m, X, li, d, M_COUNT, nullptr};
+    if (!enc_setup(c, m, li)) { m.lec[li] = c.r.ecode; continue; }
+    encode_line(c);
+    m.lec[li] = c.r.ecode;
+    uint32_t* e = m.lerr + 4 * li;
+    e[0] = c.r.etok; e[1] = c.r.eaux; e[2] = c.r.eaux2; e[3] = c.r.eaux3;
+    m.lnw[li] = c.r.nw;
+    m.lrid[li] = c.r.result_id;
+    uint32_t f2 = fl;
+    if (c.r.unres) f2 |= LF_UNRES;
+    if (X.T.special(d) == SP_VARIABLE && c.r.word2 == X.A.storage_fn) f2 |= LF_VARFN;
+    m.lfl[li] = f2;
+  }
+  __syncwarp();
+  // first OverflowError (escapes the emit loop's except clause)
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    const unsigned b = __ballot_sync(FULLM, li < L && !(m.lfl[li] & (LF_TOKERR | LF_EMPTY)) &&
+                                                (m.lec[li] == E_OVF_E || m.lec[li] == E_OVF_F));
+    if (b) {
+      if (lane == 0) m.misc[MS_OVF_LINE] = base + __ffs(b) - 1;
+      __syncwarp();
+      finish_error(a, m, X, t, X_OVERFLOW, 0, fscratch, flimbs);
+      return;
+    }
+  }
+
+  // -- G: state machine ------------------------------------------------------------
+  uint32_t ndiag = 0;
+  if (lane == 0) {
+    ndiag = state_machine(m, X);
+    if (ndiag != NONE32) {
+      for (uint32_t li = 0; li < L; ++li) {
+        const uint32_t fl = m.lfl[li];
+        ndiag += (fl & LF_TOKERR) ? 1 : 0;
+        ndiag += (fl & LF_RESOLVE_ERR) ? 1 : 0;
+      }
+    }
+  }
+  ndiag = __shfl_sync(FULLM, ndiag, 0);
+  if (ndiag == NONE32) { fail_internal(); return; }
+  if (ndiag) { finish_error(a, m, X, t, X_ASSEMBLY, ndiag, fscratch, flimbs); return; }
+
+  // -- H: structure checks + layout (lane 0) ----------------------------------------
+  if (lane == 0) {
+    const uint32_t nfn = m.misc[MS_NFN], nblk = m.misc[MS_NBLK];
+    uint32_t bi = 0;
+    x = X_NONE;
+    for (uint32_t f = 0; f < nfn && x == X_NONE; ++f) {
+      if (!(m.fn[4 * f + 1] & FN_ENDED)) { x = X_STRUCT_END; m.misc[MS_XA] = m.fn[4 * f]; break; }
+      for (; bi < nblk && m.blk[3 * bi] == f; ++bi) {
+        if (!m.blk[3 * bi + 2]) {
+          x = X_STRUCT_TERM; m.misc[MS_XA] = m.fn[4 * f]; m.misc[MS_XB] = m.blk[3 * bi + 1];
+          break;
+        }
+      }
+    }
+    uint32_t pos = 5;
+    for (uint32_t b = 0; b < 11; ++b) {
+      const uint32_t sz = m.misc[MS_BUCKET0 + b];
+      m.misc[MS_BUCKET0 + b] = pos;
+      pos += sz;
+    }
+    for (int pass = 0; pass < 2; ++pass)
+      for (uint32_t f = 0; f < nfn; ++f) {
+        const bool has_blocks = m.fn[4 * f + 1] & FN_BLOCKS;
+        if (has_blocks != (pass == 1)) continue;
+        m.fn[4 * f + 3] = pos;
+        pos += m.fn[4 * f + 2] + 1;
+      }
+    m.misc[MS_TOTAL] = pos;
+  }
+  x = __shfl_sync(FULLM, x, 0);
+  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); return; }
+  __syncwarp();
+  const uint32_t total = m.misc[MS_TOTAL];
+
+  // -- I: output ---------------------------------------------------------------------
+  bool fits;
+  const uint64_t off = asm_alloc(a, 4ull * total, fits);
+  uint32_t* ow = reinterpret_cast<uint32_t*>(a.out + off);
+  if (fits && lane == 0) {
+    ow[0] = 0x07230203u;
+    ow[1] = (m.misc[MS_MAJOR] << 16) | ((m.misc[MS_MINOR] - 1) << 8);
+    ow[2] = m.misc[MS_GENSET] ? m.misc[MS_GEN] : (32u << 16);
+    ow[4] = m.misc[MS_SCHEMA];
+  }
+  if (lane == 0) {   // bound = max(counter, max reserved) + 1
+    const uint32_t nnew = m.misc[MS_NEWCOUNT];
+    uint32_t mx = nnew ? select_unreserved(m, nnew) : 0;
+    mx = max(mx, m.misc[MS_BIGMAX_LO]);
+    for (int w = (int)m.RB / 32 - 1; w >= 0; --w) {
+      const uint32_t bits = m.rbm[w] & (w == 0 ? ~1u : ~0u);
+      if (bits) { mx = max(mx, (uint32_t)w * 32 + 31 - __clz(bits)); break; }
+    }
+    if (fits) ow[3] = mx + 1;
+  }
+  // function ends
+  {
+    const uint32_t nfn = m.misc[MS_NFN];
+    const uint32_t endw = (1u << 16) | __ldg(X.T.irec(X.A.op_fnend) + 5);
+    for (uint32_t f = lane; f < nfn; f += 32)
+      if (fits) ow[m.fn[4 * f + 3] + m.fn[4 * f + 2]] = endw;
+  }
+  uint32_t ser_off = NONE32, wc_off = NONE32;
+  const uint32_t label_word = (2u << 16) | __ldg(X.T.irec(X.A.op_label) + 5);
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    if (li >= L || !(m.lfl[li] & LF_PLACED)) continue;
+    const uint32_t g = m.lgrp[li];
+    const uint32_t at = m.loff[li] + (g < 16 ? m.misc[MS_BUCKET0 + g] : m.fn[4 * (g - 16) + 3]);
+    m.loff[li] = at;
+    const uint32_t d = m.ld[li];
+    if (X.T.special(d) == SP_LABEL) {
+      if (fits) { ow[at] = label_word; ow[at + 1] = m.lrid[li]; }
+      continue;
+    }
+    if (1 + m.lnw[li] > 0xFFFF) wc_off = min(wc_off, at);
+    EncCtx c{m, X, li, d, M_WRITE, fits ? ow + at + 1 : nullptr};   // M_WRITE also checks references
+    enc_setup(c, m, li);
+    encode_line(c);
+    if (fits) ow[at] = ((1 + c.r.nw) << 16) | __ldg(X.T.irec(d) + 5);
+    m.lerr[4 * li + 3] = c.r.bad_ref;
+    if (c.r.bad_ref != NONE32) ser_off = min(ser_off, at);
+  }
+  ser_off = wmin(ser_off);
+  wc_off = wmin(wc_off);
+  if (ser_off != NONE32 || wc_off != NONE32) {
+    const uint32_t target = ser_off != NONE32 ? ser_off : wc_off;
+    for (uint32_t base = 0; base < L; base += 32) {
+      const uint32_t li = base + lane;
+      const bool hit = li < L && (m.lfl[li] & LF_PLACED) && m.loff[li] == target;
+      if (hit) {
+        if (ser_off != NONE32) { m.misc[MS_XA] = m.lerr[4 * li + 3]; m.misc[MS_XB] = m.ld[li]; }
+        else m.misc[MS_XA] = 1 + m.lnw[li];
+      }
+    }
+    __syncwarp();
+    finish_error(a, m, X, t, ser_off != NONE32 ? X_SERIAL : X_WC, 0, fscratch, flimbs);
+    return;
+  }
+  if (lane == 0) {
+    a.out_span[2 * t] = (int64_t)off;
+    a.out_span[2 * t + 1] = (int64_t)(4ull * total);
+    a.status[t] = AST_OK;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(128) asm_kernel(AsmArgs a) {
+  const uint32_t lane = lane_id_a();
+  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint8_t* slot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
+  const AsmCtx X{a.T, a.U, a.A};
+  while (true) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.counters, 1u);
+    t = __shfl_sync(FULLM, t, 0);
+    if (t >= a.n_mod) break;
+    assemble_module(a, X, t, slot);
+  }
+}
+
+}  // namespace skg

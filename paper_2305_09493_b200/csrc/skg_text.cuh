@@ -107,7 +107,18 @@ struct ReprLimit {
 };
 
 template <class S>
-SKG_HD SKG_NOINLINE void put_py_repr(S& s, const uint8_t* p, uint32_t n, const Uni& U, uint32_t limit = 0) {
+SKG_HD SKG_NOINLINE void put_py_repr_prefixed(S& s, const char* pre, const uint8_t* p, uint32_t n, const Uni& U,
+                                          uint32_t limit = 0);
+
+template <class S>
+SKG_HD inline void put_py_repr(S& s, const uint8_t* p, uint32_t n, const Uni& U, uint32_t limit = 0) {
+  put_py_repr_prefixed(s, "", p, n, U, limit);
+}
+
+// repr(pre + text); `pre` is plain ASCII without quotes or backslashes
+template <class S>
+SKG_HD SKG_NOINLINE void put_py_repr_prefixed(S& s, const char* pre, const uint8_t* p, uint32_t n, const Uni& U,
+                                          uint32_t limit) {
   bool has_sq = false, has_dq = false;
   for (uint32_t i = 0; i < n; ++i) { has_sq |= p[i] == '\''; has_dq |= p[i] == '"'; }
   const uint8_t q = (has_sq && !has_dq) ? '"' : '\'';
@@ -122,6 +133,7 @@ SKG_HD SKG_NOINLINE void put_py_repr(S& s, const uint8_t* p, uint32_t n, const U
     for (int k = digits - 1; k >= 0; --k) emit((uint8_t)"0123456789abcdef"[(v >> (4 * k)) & 0xF]);
   };
   emit(q);
+  for (const char* z = pre; *z; ++z) emit((uint8_t)*z);
   for (uint32_t i = 0; i < n;) {
     if (limit && out >= limit) return;
     uint32_t len;

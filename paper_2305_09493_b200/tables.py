@@ -435,6 +435,11 @@ def _asm_sections(spec, ext, insts, kinds, kind_index, header, put, strings):
         header[49] = spec.kind("StorageClass").enumerant("Function").value
     except Exception:  # noqa: BLE001 - custom grammar without StorageClass
         header[49] = NONE32
+    knames = []
+    for k in kinds:
+        off, ln = strings.add(k.kind)
+        knames += [off, ln]
+    header[52] = put(knames if knames else [0])
     names = [i.name for i in insts]
     header[50] = names.index("OpLabel") if "OpLabel" in names else NONE32
     header[51] = names.index("OpFunctionEnd") if "OpFunctionEnd" in names else NONE32
