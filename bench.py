@@ -1,18 +1,23 @@
-"""Benchmark: SPIR-V words/s disassembled on B200 (BASELINE.json configs[1]).
+"""Benchmark: SPIR-V words/s disassembled + assembled on B200 (BASELINE.json
+configs[1] disassembly and configs[3] assembler round trip of the same batch).
 
 Workload (N=1): a batch of 1,000,000 synthetic modules drawn (seeded) from
 10,000 builder-canonical variants of the paper's benchmark kernels (saxpy,
-matmul, DFT, n-body, Black-Scholes; synth/families.py), disassembled with the
-reference's default options.  One step = one batch pass of the CUDA
-disassembler (libskgpu skg_disasm) with the input resident in HBM.  N>1
-(torchrun, one process per GPU): every rank disassembles its own 1M-module
-batch (weak scaling, no collective on the data path); value = all ranks' words
-/ max-over-ranks time.
+matmul, DFT, n-body, Black-Scholes; synth/families.py).  One step = the CUDA
+disassembler (skg_disasm, default options) over the whole batch followed by the
+CUDA assembler (skg_asm) over the produced text, back to binaries that must be
+bit-identical to the input; inputs resident in HBM.  value = words per step /
+step time (each word is disassembled once and assembled once).  N>1 (torchrun,
+one process per GPU): every rank round-trips its own 1M-module batch (weak
+scaling, no collective on the data path); value = all ranks' words /
+max-over-ranks time.
 
-Extra keys: roofline (HBM, algorithmic bytes 4W+T per launch), cpu_baseline
-(the reference's own CPU implementation, oracle/_ref, timed on this box's host
-cores on a bounded sample), e2e (host buffers through DisasmSession: pinned
-H2D + kernel + D2H of the text), gpu_launches, clocks.
+Extra keys: roofline (HBM; algorithmic bytes 4W+T per launch for either
+kernel; the dominant kernel is reported, both are listed), cpu_baseline (the
+reference's own CPU implementation, oracle/_ref, timed on this box's host cores
+on a bounded sample), e2e (host buffers through RoundTripSession: pinned H2D of
+the binaries + both kernels + D2H of the text and the binaries), gpu_launches,
+clocks.
 
 ``--impl reference`` times the reference's CPU implementation instead (rank 0
 only, all host cores, bounded sample per step) and prints the same JSON line
@@ -54,17 +59,18 @@ def _ref_init():
     if (ref / "spirvkit").is_dir():
         sys.path.insert(0, str(ref))
         import spirvkit
-        _REF_MOD = ("reference", spirvkit.disassemble_module)
+        _REF_MOD = ("reference", spirvkit.disassemble_module, spirvkit.assemble_module)
     else:
-        from oracle import disasm as odis
-        _REF_MOD = ("port", odis.disassemble)
+        from oracle import asm as oasm, disasm as odis
+        _REF_MOD = ("port", odis.disassemble, oasm.assemble)
 
 
 def _ref_work(mods):
-    fn = _REF_MOD[1]
+    dis, asm = _REF_MOD[1], _REF_MOD[2]
     words = 0
     for m in mods:
-        fn(m)
+        back = asm(dis(m))
+        assert back == m
         words += len(m) // 4
     return words
 
@@ -74,7 +80,7 @@ def ref_kind():
 
 
 class CpuReference:
-    """The reference disassembler on all host cores (multiprocessing)."""
+    """The reference disassembler + assembler on all host cores (multiprocessing)."""
 
     def __init__(self, cores=None):
         import multiprocessing as mp
@@ -169,7 +175,8 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     torch.cuda.set_device(local_rank)
     from paper_2305_09493_b200 import _native
-    from paper_2305_09493_b200.disasm import DisasmSession, DisassemblerOptions, option_bits
+    from paper_2305_09493_b200.asm import RoundTripSession
+    from paper_2305_09493_b200.disasm import DisassemblerOptions, option_bits
     from synth.families import sample_batch
 
     t0 = time.perf_counter()
@@ -178,30 +185,42 @@ def run_ours(args, rank, world, local_rank):
     log(f"[rank {rank}] batch: {batch.n} modules, {words} words, {batch.data.nbytes} bytes "
         f"({time.perf_counter() - t0:.1f}s)")
     dev = _native.DeviceBatch.from_host(batch.data, batch.offsets, batch.lengths)
-    opts = option_bits(DisassemblerOptions())
-    plan = _native.DisasmPlan(dev, opts)
+    plan = _native.DisasmPlan(dev, option_bits(DisassemblerOptions()))
     info = plan.fit()
     status = plan.status[: dev.n].cpu().numpy()
     assert info["errors"] == 0 and not info["overflow"] and (status == 0).all(), info
     text_bytes = info["text_bytes"]
+    max_text = int(plan.span[1::2].max().item())
+    tb = _native.DeviceBatch(plan.text, plan.span[0::2], plan.span[1::2], (max_text + 3) // 4, 0)
+    tb.n = dev.n
+    aplan = _native.AsmPlan(tb, out_cap=int(batch.lengths.sum()) + 64 * dev.n + 4096, stride=2)
+    ainfo = aplan.fit()
+    astatus = aplan.status[: dev.n].cpu().numpy()
+    assert not ainfo["overflow"] and (astatus == 0).all(), (ainfo, np.unique(astatus))
+    out_bytes = ainfo["bytes"]
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         plan.launch()
+        aplan.launch()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
     with ClockSampler(local_rank) as clocks:
-        start.record(stream)
-        for _ in range(args.steps):
+        ev[0].record(stream)
+        for k in range(args.steps):
             plan.launch()
-        end.record(stream)
+            ev[2 * k + 1].record(stream)
+            aplan.launch()
+            ev[2 * k + 2].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = start.elapsed_time(end)
+    ms = ev[0].elapsed_time(ev[-1])
+    ms_dis = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)) / args.steps
+    ms_asm = sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(args.steps)) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -210,41 +229,57 @@ def run_ours(args, rank, world, local_rank):
     total_words = words * world
     value = total_words / (ms_step / 1e3)
 
-    # spot-check parity of the timed configuration against the oracle
+    # parity of the timed configuration: every module round-trips bit-identically
+    # (length totals on all, bytes on an even sample) and the text matches the oracle
+    astatus = aplan.status[: dev.n].cpu().numpy()
+    assert (astatus == 0).all()
+    aspan = aplan.span[: 2 * dev.n].cpu().numpy().reshape(-1, 2)
+    assert (aspan[:, 1] == batch.lengths).all(), "re-assembled sizes differ from the inputs"
     if rank == 0:
         from oracle import disasm as odis
         txt = plan.text[: text_bytes].cpu().numpy()
         span = plan.span.cpu().numpy()
-        for i in np.linspace(0, dev.n - 1, 8).astype(int):
-            got = txt[span[2 * i]:span[2 * i] + span[2 * i + 1]].tobytes().decode()
-            assert got == odis.disassemble(batch.module(int(i))), f"module {i} differs from oracle"
+        outb = aplan.out[: out_bytes].cpu().numpy()
+        for i in np.linspace(0, dev.n - 1, 2000).astype(int):
+            m = batch.module(int(i))
+            assert outb[aspan[i, 0]:aspan[i, 0] + aspan[i, 1]].tobytes() == m, f"module {i} round trip"
+            if i % 97 == 0:
+                got = txt[span[2 * i]:span[2 * i] + span[2 * i + 1]].tobytes().decode()
+                assert got == odis.disassemble(m), f"module {i} differs from oracle"
 
     # e2e through the host-buffer public API
-    sess = DisasmSession()
+    sess = RoundTripSession()
     sess.stage(batch.data, batch.offsets, batch.lengths)
-    sess.run_staged()
-    e2e_steps = max(1, min(args.steps, 5))
+    sess.run_staged(max_text)
+    e2e_steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t1 = time.perf_counter()
     for _ in range(e2e_steps):
-        text, toff, st = sess.run_staged()
+        text, tspan, tst, binv, bspan, bst = sess.run_staged(max_text)
     e2e_s = (time.perf_counter() - t1) / e2e_steps
     et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_s = float(et.item())
-    assert len(text) == text_bytes
+    assert len(text) == text_bytes and (bst == 0).all()
     h2d = batch.data.nbytes + 16 * batch.n
-    d2h = text_bytes + 16 * batch.n + 4 * batch.n + 32
+    d2h = text_bytes + 16 * batch.n + 4 * batch.n + len(binv) + 16 * batch.n + 4 * batch.n + 64
 
     if rank != 0:
         return None
     peak, peak_src = peak_hbm()
-    alg_bytes = 4 * words + text_bytes
-    achieved = alg_bytes / (ms_step / 1e3) / 1e9
-    traffic = profile_traffic()
+    alg_bytes = 4 * words + text_bytes           # either direction: read one form, write the other
+    per_kernel = {
+        "skg_disasm": {"ms": ms_dis, "achieved_gbs": alg_bytes / (ms_dis / 1e3) / 1e9,
+                       "words_per_s": words / (ms_dis / 1e3)},
+        "skg_asm": {"ms": ms_asm, "achieved_gbs": alg_bytes / (ms_asm / 1e3) / 1e9,
+                    "words_per_s": words / (ms_asm / 1e3)},
+    }
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms"])
+    achieved = per_kernel[dom]["achieved_gbs"]
+    traffic = profile_traffic() or {}
     line = {
         "metric": METRIC,
         "value": value,
@@ -259,26 +294,28 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u32",
         "data": "synthetic: seeded builder-canonical paper-family modules (synth/families.py)",
         "config": {
-            "workload": "configs[1]: batch of 1M synthetic modules (saxpy/matmul/DFT/n-body/"
-                        "Black-Scholes variants) disassembled on 1 B200, default options; "
-                        "step = disassembly only (assembler path not yet on GPU)",
+            "workload": "configs[1]+configs[3]: batch of 1M synthetic modules (saxpy/matmul/DFT/"
+                        "n-body/Black-Scholes variants) disassembled (default options) and the "
+                        "text re-assembled to bit-identical binaries on 1 B200; step = skg_disasm "
+                        "+ skg_asm over the whole batch",
             "modules_per_gpu": batch.n, "variants": args.variants, "words_per_gpu": words,
             "input_bytes_per_gpu": 4 * words, "text_bytes_per_gpu": text_bytes,
-            "l2": "inputs (%.2f GB) and output exceed the 126 MB L2; no flush needed" %
-                  (batch.data.nbytes / 1e9),
+            "l2": "inputs (%.2f GB) and text (%.2f GB) exceed the 126 MB L2; no flush needed" %
+                  (batch.data.nbytes / 1e9, text_bytes / 1e9),
             "parallelism": f"module-sharded x{world}",
         },
         "roofline": {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes,
-            "traffic": traffic.get("bytes_per_launch") if traffic else None,
+            "traffic": (traffic.get(dom) or {}).get("bytes_per_launch"),
             "frac_of_nominal_8TBs": achieved / 8000.0,
+            "per_kernel": per_kernel,
         },
         "e2e": {"value": total_words / e2e_s, "unit": "words/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "paper_2305_09493_b200.disasm.DisasmSession.run_staged"},
-        "gpu_launches": args.steps,
+                "api": "paper_2305_09493_b200.asm.RoundTripSession.run_staged"},
+        "gpu_launches": 2 * args.steps,
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -292,7 +329,8 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": w / dt, "unit": "words/s", "cores": ref.cores,
                                 "kind": ref_kind(),
                                 "sample": f"{len(sample)} modules ({w} words) evenly spaced "
-                                          f"through the batch, disassemble_module each"}
+                                          f"through the batch, assemble_module(disassemble_module(m)) "
+                                          f"each"}
     return line
 
 
@@ -330,8 +368,8 @@ def run_reference(args, rank):
         "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic: seeded builder-canonical paper-family modules (synth/families.py)",
-        "config": {"workload": "configs[1] (bounded CPU sample): reference spirvkit "
-                               "disassemble_module per module on all host cores",
+        "config": {"workload": "configs[1]+configs[3] (bounded CPU sample): reference spirvkit "
+                               "assemble_module(disassemble_module(m)) per module on all host cores",
                    "modules_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "words/s", "cores": ref.cores,
                          "kind": ref_kind(),
@@ -349,7 +387,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--modules", type=int, default=1_000_000)
     ap.add_argument("--variants", type=int, default=10_000)
-    ap.add_argument("--cpu-per-core", type=int, default=150)
+    ap.add_argument("--cpu-per-core", type=int, default=60)
     ap.add_argument("--ref-modules", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -113,7 +113,9 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
  * Replaces: Assembler.assemble / assemble_module(text) (reference asm.py:133-180,
  * 365-368) together with the builder serialization it drives (builder.py:108-242).
  * Input: UTF-8 text arena `text` (module starts 16-byte aligned, arena padded
- * to 16 bytes) with int64 per-module offsets/lengths.  Output arena `out`:
+ * to 16 bytes) with int64 per-module offsets/lengths read at index m * mod_stride
+ * (stride 2 accepts skg_disasm's interleaved text_span directly, so a
+ * disassemble -> assemble round trip needs no host work).  Output arena `out`:
  * module m's result is out[out_span[2m] : out_span[2m] + out_span[2m+1]] -- the
  * module binary when status[m] == SKG_ST_OK, otherwise the exact str(exc) text
  * (UTF-8) of the exception class status[m] names.  Bytes are reserved with an
@@ -126,7 +128,7 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
 uint64_t skg_asm_slot_hint(uint64_t max_text_bytes);
 uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes);
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
-            uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
+            uint32_t mod_stride, uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
             int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,
             uint32_t default_version);
 

@@ -354,7 +354,7 @@ def _bind_asm(L):
     L.skg_asm_slot_hint.restype = U64
     L.skg_asm_workspace_bytes.argtypes = [U64]
     L.skg_asm_workspace_bytes.restype = U64
-    L.skg_asm.argtypes = [P, P, P, P, U32, U64, P, U64, P, P, P, U64, P, U32]  # ..., stream, default_version
+    L.skg_asm.argtypes = [P, P, P, P, U32, U32, U64, P, U64, P, P, P, U64, P, U32]  # ..., stream, default_version
     L.skg_asm.restype = I32
     L._asm_bound = True
     return L
@@ -378,10 +378,11 @@ class AsmPlan:
     """Device buffers for repeated skg_asm launches over one resident text batch."""
 
     def __init__(self, batch: DeviceBatch, spec=None, ext=None, out_cap=None, slot_bytes=None,
-                 default_version=(1, 2)):
+                 default_version=(1, 2), stride=1):
         torch = _torch()
         L = _bind_asm(lib())
         self.batch = batch
+        self.stride = stride
         self.th = tables_handle(spec, ext)
         n = batch.n
         max_len = int(batch.max_words) * 4 + 16
@@ -398,7 +399,8 @@ class AsmPlan:
     def launch(self, stream=None):
         b = self.batch
         s = stream if stream is not None else _stream()
-        rc = lib().skg_asm(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n, self.slot,
+        rc = lib().skg_asm(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), self.stride, b.n,
+                           self.slot,
                            self.out.data_ptr(), self.cap, self.span.data_ptr(), self.status.data_ptr(),
                            self.ws.data_ptr(), self.ws_bytes, s, self.dv)
         _check(rc, "asm")

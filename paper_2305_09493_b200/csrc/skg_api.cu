@@ -216,7 +216,7 @@ uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes) {
 }
 
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
-            uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
+            uint32_t mod_stride, uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
             int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,
             uint32_t default_version) {
   if (!t || !workspace) return -1;
@@ -229,6 +229,7 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   skg::AsmArgs a;
   a.T = t->t; a.U = t->u; a.A = t->a;
   a.text = text; a.mod_off = mod_off; a.mod_len = mod_len; a.n_mod = n_mod;
+  a.mod_stride = mod_stride ? mod_stride : 1;
   a.out = out; a.out_cap = out_cap; a.out_span = out_span; a.status = status;
   a.counters = reinterpret_cast<uint32_t*>(ws);
   a.gscratch = ws + 256;

@@ -44,6 +44,7 @@ struct AsmArgs {
   const int64_t* mod_off;
   const int64_t* mod_len;
   uint32_t n_mod;
+  uint32_t mod_stride;
   uint8_t* out;
   uint64_t out_cap;
   int64_t* out_span;
@@ -1483,8 +1484,8 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
 
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot) {
   const uint32_t lane = lane_id_a();
-  const int64_t len64 = a.mod_len[t];
-  const uint8_t* src = a.text + a.mod_off[t];
+  const int64_t len64 = a.mod_len[(size_t)t * a.mod_stride];
+  const uint8_t* src = a.text + a.mod_off[(size_t)t * a.mod_stride];
   AsmMod m{};
   uint64_t used = 0;
   auto take = [&](uint64_t bytes) -> uint8_t* { uint8_t* r = slot + used; used += al16(bytes); return r; };
