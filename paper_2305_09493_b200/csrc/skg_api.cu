@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include "../../include/skgpu.h"
 #include "skg_module.cuh"
 
@@ -81,6 +82,12 @@ int check(cudaError_t e) {
 extern "C" {
 
 const char* skg_version(void) { return "skgpu 0.1 (sm_100a)"; }
+
+#ifdef SKG_PHASE_TIMING
+int skg_debug_asm_phases(unsigned long long* out16) {
+  return check(cudaMemcpyFromSymbol(out16, skg::g_asm_phase, 16 * sizeof(unsigned long long)));
+}
+#endif
 
 int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** out) {
   if (!host_blob || n_words < 64 || !out) return -1;
@@ -211,8 +218,16 @@ uint64_t skg_asm_slot_hint(uint64_t max_text_bytes) {
   return ((32ull * max_text_bytes + 65536) + 255) & ~255ull;
 }
 
+// assembler: phase-synchronised CTAs of kAsmWarps warps (one module per warp), 2 per SM
+int asm_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+int kAsmWarps = asm_env("SKG_ASM_WARPS", 32);
+uint32_t asm_blocks() { return (uint32_t)sm_count() * asm_env("SKG_ASM_BLOCKS_PER_SM", 1); }
+
 uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes) {
-  return 256 + (uint64_t)grid_blocks() * kWarpsPerBlock * slot_bytes;
+  return 256 + (uint64_t)asm_blocks() * kAsmWarps * slot_bytes;
 }
 
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
@@ -235,7 +250,7 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.gscratch = ws + 256;
   a.gslot_bytes = slot_bytes;
   a.default_version = default_version;
-  skg::asm_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, 0, s>>>(a);
+  skg::asm_kernel<<<asm_blocks(), 32 * kAsmWarps, 0, s>>>(a);
   return check(cudaGetLastError());
 }
 

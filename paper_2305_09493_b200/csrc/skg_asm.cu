@@ -69,7 +69,7 @@ enum : uint32_t {
   E_OK = 0, E_NOINST, E_NEEDS_RESULT, E_NOT_PRODUCE, E_MISSING, E_EXTRA, E_STR_FOR, E_EXPECT_ID,
   E_INT_INVALID, E_INT_LIMIT, E_FLOAT_INVALID, E_NO_WIDTH, E_NEG, E_NO_ENUM_STR, E_NO_ENUM_INT,
   E_MASK_RANGE, E_LITSTR_INT, E_NUL, E_SURROGATE, E_WIDTH, E_FWIDTH, E_OVF_E, E_OVF_F, E_FIT,
-  E_NO_EXT, E_NO_SPECOP, E_LIT_RANGE, E_INT_STRLIMIT,
+  E_NO_EXT, E_NO_SPECOP, E_LIT_RANGE, E_INT_STRLIMIT, E_INTERNAL,
   S_LABEL_OUTSIDE = 64, S_LABEL_NORESULT, S_LABEL_USED, S_DUP, S_FUNC_BEFORE_END, S_OUTSIDE,
   S_PARAM_AFTER_BLOCK, S_MM_DUP, S_NEED_BLOCK, S_TERMINATED, S_VAR_FIRST, S_NOT_BLOCK, S_KEYERROR,
   S_LABEL_RESOLVE, S_VAR_NOTFN
@@ -99,6 +99,7 @@ struct AsmMod {
   uint32_t* loff;     // offset within group, then absolute word offset
   uint32_t* lerr;     // 4 words / line: error details
   uint32_t* tok;      // 2 words / token
+  uint32_t* tid;      // per token: resolved %id (0 = not an id token / not yet resolved)
   uint32_t ntb;       // token slots
   uint32_t* nt;       // name table: 6 words / entry
   uint32_t ncap;
@@ -112,6 +113,8 @@ struct AsmMod {
   uint32_t* big;      // big-id lists: [0] count reg, [1] count lab, then pairs
   uint32_t big_cap;
   uint32_t* misc;     // 64 words of counters
+  uint8_t* sbase;     // the warp's scratch slot (bump allocated; lane 0 may grow the name table)
+  uint64_t sused, scap;
 };
 
 // misc slots
@@ -119,7 +122,7 @@ enum : uint32_t {
   MS_BIGMAX_LO = 0, MS_BIGMAX_HI, MS_NPCT, MS_RESV_LINE, MS_NSYM, MS_NFN, MS_NBLK, MS_BUCKET0 = 8,
   MS_X = 24, MS_XA, MS_XB, MS_XC, MS_NEWCOUNT, MS_GEN, MS_SCHEMA, MS_MAJOR, MS_MINOR, MS_GENSET,
   MS_HDR_LINE_V, MS_HDR_LINE_G, MS_HDR_LINE_S, MS_TOTAL, MS_NDIAG, MS_OVF_LINE, MS_SER_LINE,
-  MS_WC_LINE, MS_COUNTER, MS_V0 = 48
+  MS_WC_LINE, MS_COUNTER, MS_NTCOUNT, MS_V0 = 48
 };
 
 __device__ __forceinline__ uint32_t lane_id_a() { return threadIdx.x & 31; }
@@ -150,18 +153,22 @@ __device__ __forceinline__ uint32_t wmin(uint32_t v) {
   return v;
 }
 
-__device__ __forceinline__ uint32_t fnv(const uint8_t* p, uint32_t n, uint32_t h = 2166136261u) {
+// one out-of-line copy each: these run at many call sites (instruction-cache footprint)
+__device__ __noinline__ uint32_t fnv(const uint8_t* p, uint32_t n, uint32_t h = 2166136261u) {
+#pragma unroll 1
   for (uint32_t i = 0; i < n; ++i) h = (h ^ p[i]) * 16777619u;
   return h;
 }
 
-__device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, uint32_t n) {
+__device__ __noinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, uint32_t n) {
+#pragma unroll 1
   for (uint32_t i = 0; i < n; ++i) if (a[i] != b[i]) return false;
   return true;
 }
 
-__device__ __forceinline__ bool bytes_eq_z(const uint8_t* a, uint32_t n, const char* z) {
+__device__ __noinline__ bool bytes_eq_z(const uint8_t* a, uint32_t n, const char* z) {
   uint32_t i = 0;
+#pragma unroll 1
   for (; i < n; ++i) if (!z[i] || (uint8_t)z[i] != a[i]) return false;
   return z[i] == 0;
 }
@@ -193,6 +200,20 @@ __device__ inline bool py_isdigit(const uint8_t* p, uint32_t n, const Uni& U) {
     if (!U.is_digit(c)) return false;
     i += len;
   }
+  return true;
+}
+
+// Fast path of body.isdigit() + int(body): 1-9 ASCII digits (no sign, no
+// underscores) -> value; false means "use the general path".
+__device__ __forceinline__ bool ascii_dec9(const uint8_t* p, uint32_t n, uint32_t& v) {
+  if (n == 0 || n > 9) return false;
+  uint32_t x = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t d = (uint32_t)p[i] - '0';
+    if (d > 9) return false;
+    x = x * 10 + d;
+  }
+  v = x;
   return true;
 }
 
@@ -276,6 +297,29 @@ __device__ inline uint32_t nt_insert(const AsmMod& m, uint32_t t) {
     s = (s + 1) & (m.ncap - 1);
   }
   return NONE32;
+}
+
+// lane 0: grow the name table 4x (re-hash) when unresolved operand names fill it
+__device__ __noinline__ bool nt_grow(AsmMod& m) {
+  const uint32_t ncap = m.ncap * 4;
+  const uint64_t bytes = 4ull * NT_W * ncap;
+  if (m.sused + bytes > m.scap) return false;
+  uint32_t* nt = reinterpret_cast<uint32_t*>(m.sbase + m.sused);
+  m.sused += (bytes + 15) & ~15ull;
+  for (uint32_t k = 0; k < ncap; ++k) {
+    uint32_t* e = nt + NT_W * k;
+    e[0] = EMPTYK; e[1] = 0; e[2] = NONE32; e[3] = 0; e[4] = 0; e[5] = 0;
+  }
+  for (uint32_t k = 0; k < m.ncap; ++k) {
+    const uint32_t* o = m.nt + NT_W * k;
+    if (o[0] == EMPTYK) continue;
+    uint32_t sl = (o[1] * 0x9E3779B1u) & (ncap - 1);
+    while (nt[NT_W * sl] != EMPTYK) sl = (sl + 1) & (ncap - 1);
+    for (uint32_t q = 0; q < NT_W; ++q) nt[NT_W * sl + q] = o[q];
+  }
+  m.nt = nt;
+  m.ncap = ncap;
+  return true;
 }
 
 // -- id sets ------------------------------------------------------------------------
@@ -388,9 +432,8 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
 }
 
 // ============================================================================
-// Phase B: tokenize (asm.py:51-90), lane per line.  Token slots: per line
-// ub = 2*len/3 + 2 (a token needs >= 1.5 bytes on average).
-__device__ __forceinline__ uint32_t tok_ub(uint32_t len) { return 2 * len / 3 + 2; }
+// Phase B: tokenize (asm.py:51-90), lane per line: a counting pass sizes the
+// token array exactly, the second pass stores tokens and undoes escapes.
 
 struct AsmCtx {
   const Tables& T;
@@ -398,8 +441,34 @@ struct AsmCtx {
   const AsmTables& A;
 };
 
+// tokens of a line without storing them (same scan as tokenize_line; an
+// unterminated string makes the line token-less)
+__device__ __noinline__ uint32_t count_tokens(const uint8_t* t, uint32_t i, uint32_t e0) {
+  uint32_t nt = 0;
+  while (i < e0) {
+    const uint8_t c = t[i];
+    if (c == ' ' || c == '\t' || c == '\r' || c == '\n') { ++i; continue; }
+    if (c == ';') break;
+    if (c == '"') {
+      ++i;
+      while (i < e0 && t[i] != '"') { if (t[i] == '\\' && i + 1 < e0) ++i; ++i; }
+      if (i >= e0) return 0;
+      ++i;
+      ++nt;
+      continue;
+    }
+    while (i < e0) {
+      const uint8_t d = t[i];
+      if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
+      ++i;
+    }
+    ++nt;
+  }
+  return nt;
+}
+
 __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
-                                           uint32_t& npct) {
+                                           uint32_t cap, uint32_t& npct) {
   uint8_t* t = m.txt;
   const uint32_t s0 = m.ls[li], e0 = m.le[li];
   uint32_t nt = 0;
@@ -426,8 +495,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
         break;
       }
       ++i;
-      m.tok[2 * (tb + nt)] = start + 1;
-      m.tok[2 * (tb + nt) + 1] = (w - start - 1) | TK_STR;
+      if (nt < cap) {
+        m.tok[2 * (tb + nt)] = start + 1;
+        m.tok[2 * (tb + nt) + 1] = (w - start - 1) | TK_STR;
+      }
       ++nt;
       continue;
     }
@@ -436,8 +507,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
       ++i;
     }
-    m.tok[2 * (tb + nt)] = start;
-    m.tok[2 * (tb + nt) + 1] = i - start;
+    if (nt < cap) {   // cap = count_tokens of this line (0 for an unterminated string)
+      m.tok[2 * (tb + nt)] = start;
+      m.tok[2 * (tb + nt) + 1] = i - start;
+    }
     ++nt;
   }
   if (!(fl & LF_TOKERR) && nt == 0) fl |= LF_EMPTY;
@@ -459,10 +532,14 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       if (!(tk.n >= 1 && tk.p[0] == '%')) continue;
       if (!is_res && tk.str) continue;
       ++npct;
-      if (!py_isdigit(tk.p + 1, tk.n - 1, X.U)) continue;
-      const IntVal v = parse_int(tk.p + 1, tk.n - 1, 10, X.U);
-      if (v.status != INT_OK || v.big || v.mag == 0 || v.mag > MAX_ID) { bad = k; break; }
-      const uint32_t id = (uint32_t)v.mag;
+      uint32_t id;
+      if (!ascii_dec9(tk.p + 1, tk.n - 1, id)) {
+        if (!py_isdigit(tk.p + 1, tk.n - 1, X.U)) continue;
+        const IntVal v = parse_int(tk.p + 1, tk.n - 1, 10, X.U);
+        if (v.status != INT_OK || v.big || v.mag == 0 || v.mag > MAX_ID) { bad = k; break; }
+        id = (uint32_t)v.mag;
+      }
+      if (id == 0) { bad = k; break; }
       if (id < m.RB) atomicOr(&m.rbm[id >> 5], 1u << (id & 31));
       else atomicMax(&m.misc[MS_BIGMAX_LO], id);
     }
@@ -610,7 +687,12 @@ __device__ inline bool ext_by_name(const AsmCtx& X, const uint8_t* p, uint32_t n
 
 // id of an %name token for coerce (asm.py:106-120); false on error
 __device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id) {
+  if (c.mode != M_RESOLVE) {   // resolved once per token after the result names are bound
+    const uint32_t cached = c.m.tid[t];
+    if (cached) { id = cached; return true; }
+  }
   if (!(k.n >= 2 && k.p[0] == '%')) return enc_fail(c, E_EXPECT_ID, t);
+  if (ascii_dec9(k.p + 1, k.n - 1, id)) return true;
   if (py_isdigit(k.p + 1, k.n - 1, c.X.U)) {
     const IntVal v = parse_int(k.p + 1, k.n - 1, 10, c.X.U);
     id = (uint32_t)v.mag;   // validated by the reservation pass
@@ -619,6 +701,9 @@ __device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id)
   const uint32_t e = nt_find(c.m, k.p, k.n);
   if (e != NONE32 && c.m.nt[NT_W * e + 3] != 0) { id = c.m.nt[NT_W * e + 3]; return true; }
   if (c.mode == M_RESOLVE) {
+    AsmMod& mm = const_cast<AsmMod&>(c.m);
+    if (2 * (mm.misc[MS_NTCOUNT] + 1) > mm.ncap && !nt_grow(mm)) return enc_fail(c, E_INTERNAL, t);
+    ++mm.misc[MS_NTCOUNT];
     const uint32_t s = nt_insert(c.m, t);
     uint32_t* ent = c.m.nt + NT_W * s;
     if (ent[3] == 0) {
@@ -1295,6 +1380,7 @@ __device__ __noinline__ uint32_t scan_header(AsmMod& m, const AsmCtx& X, uint32_
 
 // label id / result id of a result token without encoding (lane-local)
 __device__ inline uint32_t result_id_of(const AsmMod& m, const AsmCtx& X, uint32_t t) {
+  if (m.tid[t]) return m.tid[t];
   const Tok k = tok_at(m, t);
   if (k.n < 2) return 0;
   if (py_isdigit(k.p + 1, k.n - 1, X.U)) return (uint32_t)parse_int(k.p + 1, k.n - 1, 10, X.U).mag;
@@ -1303,10 +1389,11 @@ __device__ inline uint32_t result_id_of(const AsmMod& m, const AsmCtx& X, uint32
 }
 
 // lane 0: re-run the encoder of line li assigning ids to unseen names in order
-__device__ __noinline__ void resolve_line(AsmMod& m, const AsmCtx& X, uint32_t li) {
+__device__ __noinline__ bool resolve_line(AsmMod& m, const AsmCtx& X, uint32_t li) {
   EncCtx c{m, X, li, m.ld[li], M_RESOLVE, nullptr};
-  if (!enc_setup(c, m, li)) return;
+  if (!enc_setup(c, m, li)) return true;
   encode_line(c);
+  return c.r.ecode != E_INTERNAL;
 }
 
 // Phase G (lane 0): the scope state machine of Assembler._emit / builder scopes.
@@ -1350,7 +1437,7 @@ __device__ __noinline__ uint32_t state_machine(AsmMod& m, const AsmCtx& X) {
       place_fn(li, 2);
       continue;
     }
-    if (fl & LF_UNRES) resolve_line(m, X, li);
+    if ((fl & LF_UNRES) && !resolve_line(m, X, li)) return NONE32;
     if (m.lec[li] != E_OK) { ++ndiag; continue; }
     const uint32_t info = __ldg(X.A.info + 4 * d);
     const uint32_t words = 1 + m.lnw[li];
@@ -1421,6 +1508,180 @@ __device__ __noinline__ uint32_t state_machine(AsmMod& m, const AsmCtx& X) {
   return ndiag;
 }
 
+
+// Warp-parallel form of the state machine for modules without diagnostics
+// (the common case).  Every rule the sequential machine enforces is checked as
+// a per-line predicate over prefix scans (function nesting, block membership,
+// terminators, parameter placement, one memory model, SSA uniqueness via
+// atomic test-and-set on the registry bitmaps); the first violated rule makes
+// it return false, and the caller resets and runs the exact sequential
+// machine, which produces the diagnostics.  On success the placement (group,
+// offset within group) of every line, the bucket sizes and the function
+// records equal the sequential machine's.
+enum : uint32_t { K_SKIP = 0, K_MOD, K_FUNC, K_PARAM, K_END, K_LABEL, K_BLOCK, K_BLOCKVAR };
+
+__device__ __noinline__ bool state_fast(AsmMod& m, const AsmCtx& X) {
+  const Tables& T = X.T;
+  const uint32_t lane = lane_id_a();
+  const uint32_t below = (1u << lane) - 1;
+  uint32_t nF = 0, nE = 0, nMM = 0;          // running counts
+  uint32_t last_struct_kind = K_SKIP;         // kind of the previous structural line
+  uint32_t last_struct_term = 0;
+  uint32_t last_func_line = NONE32, last_label_line = NONE32;
+  uint32_t bucket_run[11];
+  for (int b = 0; b < 11; ++b) bucket_run[b] = 0;
+  uint32_t P = 0;                             // words of function-group lines so far
+  bool ok = true;
+  for (uint32_t base = 0; base < m.L && ok; base += 32) {
+    const uint32_t li = base + lane;
+    uint32_t kind = K_SKIP, words = 0, route = 0, term = 0, rid = 0;
+    bool has_res = false, bad = false;
+    if (li < m.L) {
+      const uint32_t fl = m.lfl[li];
+      if (!(fl & (LF_TOKERR | LF_EMPTY))) {
+        const uint32_t d = m.ld[li];
+        if (d == NONE32 || m.lec[li] != E_OK || (fl & (LF_UNRES | LF_RESOLVE_ERR))) bad = true;
+        else {
+          const uint32_t sp = T.special(d), info = __ldg(X.A.info + 4 * d);
+          rid = m.lrid[li];
+          has_res = T.has_result(d);
+          words = 1 + m.lnw[li];
+          if (sp == SP_LABEL) { kind = K_LABEL; words = 2; has_res = (fl & LF_RESULT) != 0; bad |= !has_res; }
+          else if (sp == SP_FUNCTION) kind = K_FUNC;
+          else if (sp == SP_FUNCTIONPARAM) kind = K_PARAM;
+          else if (sp == SP_FUNCTIONEND) { kind = K_END; words = 0; }
+          else {
+            route = (info >> 8) & 0xFF;
+            if (route == ROUTE_VARIABLE) route = (fl & LF_VARFN) ? ROUTE_SCOPE : 10;
+            if (route == ROUTE_KEYERROR) bad = true;
+            else if (route != ROUTE_SCOPE) kind = K_MOD;
+            else {
+              kind = sp == SP_VARIABLE ? K_BLOCKVAR : K_BLOCK;
+              if (kind == K_BLOCK && ((info >> 16) & AF_BLOCK_FORBIDDEN)) bad = true;
+              term = ((info >> 16) & AF_TERMINATOR) ? 1 : 0;
+            }
+          }
+        }
+      }
+    }
+    // function nesting: F = OpFunction lines <= li, E = OpFunctionEnd lines < li
+    const unsigned bF = __ballot_sync(FULLM, kind == K_FUNC), bE = __ballot_sync(FULLM, kind == K_END);
+    const uint32_t F = nF + __popc(bF & (below | (1u << lane))), E = nE + __popc(bE & below);
+    const bool inside = F > E;
+    if (kind == K_FUNC && F - 1 != E) bad = true;                       // previous function not ended
+    if ((kind == K_PARAM || kind == K_END || kind == K_LABEL || kind == K_BLOCK || kind == K_BLOCKVAR) && !inside)
+      bad = true;
+    // previous structural line (function-scope lines) and its kind
+    const bool structural = kind == K_FUNC || kind == K_PARAM || kind == K_END || kind == K_LABEL ||
+                            kind == K_BLOCK || kind == K_BLOCKVAR;
+    const unsigned bS = __ballot_sync(FULLM, structural);
+    const unsigned prevS = bS & below;
+    const uint32_t my_kind_term = kind | (term << 8);
+    uint32_t pk = last_struct_kind, pt = last_struct_term;
+    {
+      const int src = prevS ? 31 - __clz(prevS) : 0;
+      const uint32_t v = __shfl_sync(FULLM, my_kind_term, src);
+      if (prevS) { pk = v & 0xFF; pt = v >> 8; }
+    }
+    const bool open_block = pk == K_LABEL || pk == K_BLOCK || pk == K_BLOCKVAR;
+    if ((kind == K_LABEL || kind == K_END) && open_block && !(pk == K_BLOCK && pt)) bad = true;  // unterminated block
+    if (kind == K_BLOCK && (!open_block || (pk == K_BLOCK && pt))) bad = true;
+    if (kind == K_BLOCKVAR && !(pk == K_LABEL || pk == K_BLOCKVAR)) bad = true;
+    // parameters precede all blocks of their function
+    const unsigned bL = __ballot_sync(FULLM, kind == K_LABEL), bFn = bF;
+    uint32_t lastL = last_label_line, lastF = last_func_line;
+    {
+      const unsigned pl = bL & below, pf = bFn & (below | (1u << lane));
+      if (pl) lastL = base + 31 - __clz(pl);
+      if (pf) lastF = base + 31 - __clz(pf);
+    }
+    if (kind == K_PARAM && lastL != NONE32 && lastF != NONE32 && lastL > lastF) bad = true;
+    // one memory model
+    const unsigned bMM = __ballot_sync(FULLM, kind == K_MOD && route == 3);
+    if (kind == K_MOD && route == 3 && nMM + __popc(bMM & below) > 0) bad = true;
+    // SSA registry / labels: atomic test-and-set (any collision -> exact path)
+    if (!bad && has_res && kind != K_SKIP) {
+      if (rid >= m.RB || rid == 0) bad = true;
+      else {
+        const uint32_t bit = 1u << (rid & 31);
+        if (atomicOr(&m.reg[rid >> 5], bit) & bit) bad = true;
+        if (kind == K_LABEL && (atomicOr(&m.lab[rid >> 5], bit) & bit)) bad = true;
+      }
+    }
+    if (__any_sync(FULLM, bad)) { ok = false; break; }
+    // placement: buckets
+    uint32_t off = 0;
+#pragma unroll
+    for (int b = 0; b < 11; ++b) {
+      const uint32_t v = (kind == K_MOD && route == (uint32_t)b) ? words : 0;
+      const uint32_t incl = wincl(v);
+      if (v) off = bucket_run[b] + incl - v;
+      bucket_run[b] += __shfl_sync(FULLM, incl, 31);
+    }
+    // placement: function lines, offset from the function's first line
+    const bool fline = kind == K_FUNC || kind == K_PARAM || kind == K_LABEL || kind == K_BLOCK || kind == K_BLOCKVAR;
+    const uint32_t fv = fline ? words : 0;
+    const uint32_t fincl = wincl(fv);
+    const uint32_t Pexcl = P + fincl - fv;
+    const uint32_t f = F - 1;
+    if (kind == K_FUNC) { m.fn[4 * f] = rid; m.fn[4 * f + 1] = 0; m.fn[4 * f + 3] = Pexcl; }
+    __syncwarp();
+    if (kind == K_LABEL) m.fn[4 * f + 1] |= FN_BLOCKS;   // same value from every lane: benign
+    __syncwarp();
+    if (fline) off = Pexcl - m.fn[4 * f + 3];
+    if (kind == K_END) { m.fn[4 * f + 2] = Pexcl - m.fn[4 * f + 3]; m.fn[4 * f + 1] |= FN_ENDED; }
+    if (kind == K_MOD) { m.lgrp[li] = route; m.loff[li] = off; m.lfl[li] |= LF_PLACED; }
+    else if (fline) { m.lgrp[li] = 16 + f; m.loff[li] = off; m.lfl[li] |= LF_PLACED; }
+    else if (kind == K_END) m.lfl[li] |= LF_DROP;
+    if (kind == K_LABEL) m.lnw[li] = 1;
+    P += __shfl_sync(FULLM, fincl, 31);
+    nF += __popc(bF); nE += __popc(bE); nMM += __popc(bMM);
+    if (bS) {
+      const uint32_t v = __shfl_sync(FULLM, my_kind_term, 31 - __clz(bS));
+      last_struct_kind = v & 0xFF; last_struct_term = v >> 8;
+    }
+    if (bL) last_label_line = base + 31 - __clz(bL);
+    if (bF) last_func_line = base + 31 - __clz(bF);
+    __syncwarp();
+  }
+  if (ok && nF != nE) ok = false;                 // a function without OpFunctionEnd
+  if (!ok) return false;
+  if (lane == 0) {
+    for (int b = 0; b < 11; ++b) m.misc[MS_BUCKET0 + b] = bucket_run[b];
+    m.misc[MS_NFN] = nF;
+    m.misc[MS_NBLK] = 0;                          // every block was checked terminated above
+  }
+  __syncwarp();
+  return true;
+}
+
+// reset what state_fast may have touched before the exact machine runs
+__device__ __noinline__ void state_reset(AsmMod& m) {
+  const uint32_t lane = lane_id_a();
+  for (uint32_t k = lane; k < m.RB / 32; k += 32) { m.reg[k] = 0; m.lab[k] = 0; }
+  for (uint32_t li = lane; li < m.L; li += 32) m.lfl[li] &= ~(LF_PLACED | LF_DROP);
+  if (lane < 11) m.misc[MS_BUCKET0 + lane] = 0;
+  if (lane < 2) m.big[lane] = 0;
+  __syncwarp();
+}
+
+// ============================================================================
+// Optional per-phase cycle counters (build with -DSKG_PHASE_TIMING; profiling only)
+#ifdef SKG_PHASE_TIMING
+__device__ unsigned long long g_asm_phase[16];
+#define PHASE_MARK(k)                                                   \
+  do {                                                                  \
+    __syncwarp();                                                       \
+    const long long now_ = clock64();                                   \
+    if (lane_id_a() == 0) atomicAdd(&g_asm_phase[k], (unsigned long long)(now_ - ph_t0_)); \
+    ph_t0_ = now_;                                                      \
+  } while (0)
+#define PHASE_START() long long ph_t0_ = clock64()
+#else
+#define PHASE_MARK(k) do {} while (0)
+#define PHASE_START() do {} while (0)
+#endif
+
 // ============================================================================
 // Module driver
 constexpr uint32_t BIG_CAP = 64;
@@ -1482,10 +1743,19 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
   __syncwarp();
 }
 
+// All warps of the CTA run this together, one module per warp, with a CTA
+// barrier between phases: every warp of an SM then executes the same phase's
+// code at the same time, which keeps the instruction working set to one phase
+// (the per-warp independent schedule thrashed the instruction cache).  A warp
+// whose module is finished (error exit) or absent (t >= n_mod) idles through
+// the remaining phases.
+#define CTA_SYNC() __syncthreads()
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot) {
   const uint32_t lane = lane_id_a();
-  const int64_t len64 = a.mod_len[(size_t)t * a.mod_stride];
-  const uint8_t* src = a.text + a.mod_off[(size_t)t * a.mod_stride];
+  PHASE_START();
+  bool done = t >= a.n_mod;
+  const int64_t len64 = done ? 0 : a.mod_len[(size_t)t * a.mod_stride];
+  const uint8_t* src = done ? a.text : a.text + a.mod_off[(size_t)t * a.mod_stride];
   AsmMod m{};
   uint64_t used = 0;
   auto take = [&](uint64_t bytes) -> uint8_t* { uint8_t* r = slot + used; used += al16(bytes); return r; };
@@ -1493,16 +1763,26 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   uint32_t flimbs = 0;
   auto fail_internal = [&]() { finish_error(a, m, X, t, X_INTERNAL, 0, nullptr, 0); };
   const uint32_t T = (uint32_t)len64;
+  uint32_t L = 0, npct = 0, x = X_NONE, ndiag = 0, total = 0;
+  bool fits = false;
+  uint64_t off = 0;
+  uint32_t* ow = nullptr;
+  if (done) goto end_a;
   m.T = T;
   m.misc = reinterpret_cast<uint32_t*>(take(64 * 4));
   m.txt = take((uint64_t)T + 16);
   m.ls = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
   m.le = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
-  if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); return; }
+  if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); done = true; goto end_a; }
   for (uint32_t k = lane; k < 64; k += 32) m.misc[k] = 0;
   __syncwarp();
-  const uint32_t L = split_lines(m, src, T + 1);
+  L = split_lines(m, src, T + 1);
   m.L = L;
+end_a:
+  PHASE_MARK(0);
+  CTA_SYNC();
+  if (done) goto end_b;
+  {
   // per-line arrays
   m.lt0 = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lnt = reinterpret_cast<uint32_t*>(take(4ull * L));
@@ -1514,16 +1794,19 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   m.lgrp = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.loff = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lerr = reinterpret_cast<uint32_t*>(take(16ull * L));
-  // token slots
+  // exact token counts (first pass of the tokenizer): per-line bases in lt0
   uint32_t ntb = 0;
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;
-    ntb += li < L ? tok_ub(m.le[li] - m.ls[li]) : 0;
+    const uint32_t c = li < L ? count_tokens(m.txt, m.ls[li], m.le[li]) : 0;
+    const uint32_t incl = wincl(c);
+    if (li < L) m.lt0[li] = ntb + incl - c;
+    ntb += __shfl_sync(FULLM, incl, 31);
   }
-  ntb = wsum(ntb);
   m.ntb = ntb;
-  m.tok = reinterpret_cast<uint32_t*>(take(8ull * ntb));
-  m.RB = ((2 * T / 3 + 2 * L + 64) + 31) & ~31u;
+  m.tok = reinterpret_cast<uint32_t*>(take(8ull * ntb + 8));
+  m.tid = reinterpret_cast<uint32_t*>(take(4ull * ntb + 4));
+  m.RB = (ntb + 64 + 31) & ~31u;   // ids to select among: <= tokens + reserved
   m.rbm = reinterpret_cast<uint32_t*>(take(m.RB / 8));
   m.zpre = reinterpret_cast<uint32_t*>(take(m.RB / 8 + 4));
   m.reg = reinterpret_cast<uint32_t*>(take(m.RB / 8));
@@ -1532,47 +1815,51 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   m.blk = reinterpret_cast<uint32_t*>(take(12ull * L + 16));
   m.big_cap = BIG_CAP;
   m.big = reinterpret_cast<uint32_t*>(take(4ull * (2 + 2 * BIG_CAP)));
-  if (used > a.gslot_bytes) { fail_internal(); return; }
+  if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_b; }
   for (uint32_t k = lane; k < m.RB / 32; k += 32) { m.rbm[k] = 0; m.reg[k] = 0; m.lab[k] = 0; }
   if (lane < 2) m.big[lane] = 0;
   __syncwarp();
   if (lane == 0) m.rbm[0] = 1;   // id 0 is never allocated
   __syncwarp();
 
+  PHASE_MARK(1);
   // -- B: tokenize + reservations ------------------------------------------------
-  uint32_t npct = 0;
-  {
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < L; base += 32) {
-      const uint32_t li = base + lane;
-      const uint32_t ub = li < L ? tok_ub(m.le[li] - m.ls[li]) : 0;
-      const uint32_t incl = wincl(ub);
-      if (li < L) {
-        m.lec[li] = E_OK;
-        tokenize_line(m, X, li, carry + incl - ub, npct);
-      }
-      carry += __shfl_sync(FULLM, incl, 31);
+  uint32_t nres = 0;
+  for (uint32_t base = 0; base < L; base += 32) {
+    const uint32_t li = base + lane;
+    if (li < L) {
+      m.lec[li] = E_OK;
+      const uint32_t cap = (li + 1 < L ? m.lt0[li + 1] : ntb) - m.lt0[li];
+      tokenize_line(m, X, li, m.lt0[li], cap, npct);
+      nres += (m.lfl[li] & LF_RESULT) ? 1 : 0;
     }
   }
   npct = wsum(npct);
-  m.ncap = 64;
-  while (m.ncap < 2 * npct + 16) m.ncap <<= 1;
+  nres = wsum(nres);
+  m.ncap = 64;   // result names (+ unresolved operand names: lane 0 grows the table)
+  while (m.ncap < 2 * nres + 32) m.ncap <<= 1;
+  if (lane == 0) m.misc[MS_NTCOUNT] = nres;
   m.nt = reinterpret_cast<uint32_t*>(take(4ull * NT_W * m.ncap));
   // formatting scratch (lane 0, error paths): big integers of the longest token
   flimbs = T / 2 + 64;
   fscratch = reinterpret_cast<uint32_t*>(take(4ull * flimbs));
-  if (used > a.gslot_bytes) { fail_internal(); return; }
+  m.sbase = slot; m.sused = used; m.scap = a.gslot_bytes;
+  if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_b; }
   for (uint32_t k = lane; k < m.ncap; k += 32) {
     uint32_t* e = m.nt + NT_W * k;
     e[0] = EMPTYK; e[1] = 0; e[2] = NONE32; e[3] = 0; e[4] = 0; e[5] = 0;
   }
   __syncwarp();
 
+  }
+end_b:
+  PHASE_MARK(2);
+  CTA_SYNC();
+  if (done) goto end_c;
   // -- C: header comments; then the first reservation failure --------------------
-  uint32_t x = X_NONE;
   if (lane == 0) x = scan_header(m, X, a.default_version);
   x = __shfl_sync(FULLM, x, 0);
-  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); return; }
+  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); done = true; goto end_c; }
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;
     const unsigned bad = __ballot_sync(FULLM, li < L && (m.lfl[li] & LF_RESVERR));
@@ -1580,10 +1867,14 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
       if (lane == 0) m.misc[MS_RESV_LINE] = base + __ffs(bad) - 1;
       __syncwarp();
       finish_error(a, m, X, t, X_RESERVE, 0, fscratch, flimbs);
-      return;
+      done = true;
+      goto end_c;
     }
   }
-
+end_c:
+  PHASE_MARK(3);
+  CTA_SYNC();
+  if (done) goto end_d;
   // -- D: unreserved prefix counts; symbolic result names in document order -------
   {
     uint32_t carry = 0;
@@ -1629,7 +1920,28 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
     if (lane == 0) m.misc[MS_NEWCOUNT] = carry;
   }
   __syncwarp();
-
+  // every %name token resolved once, token-parallel (load-balanced across lanes)
+  for (uint32_t k = lane; k < m.ntb; k += 32) {
+    const Tok tk = tok_at(m, k);
+    uint32_t id = 0;
+    if (tk.n >= 2 && tk.p[0] == '%') {
+      if (!ascii_dec9(tk.p + 1, tk.n - 1, id)) {
+        id = 0;
+        if (py_isdigit(tk.p + 1, tk.n - 1, X.U)) {
+          const IntVal v = parse_int(tk.p + 1, tk.n - 1, 10, X.U);
+          if (v.status == INT_OK && !v.big && v.mag && v.mag <= MAX_ID) id = (uint32_t)v.mag;
+        } else {
+          const uint32_t e = nt_find(m, tk.p, tk.n);
+          if (e != NONE32) id = m.nt[NT_W * e + 3];
+        }
+      }
+    }
+    m.tid[k] = id;
+  }
+end_d:
+  PHASE_MARK(4);
+  CTA_SYNC();
+  if (done) goto end_e;
   // -- E: opname lookup, width / value-type scans ---------------------------------
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;
@@ -1655,8 +1967,10 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
     }
     if (d != NONE32 && X.T.has_rtype(d) && o0.n >= 1 && o0.p[0] == '%') atomicMax(&m.nt[NT_W * e + 5], li + 1);
   }
-  __syncwarp();
-
+end_e:
+  PHASE_MARK(5);
+  CTA_SYNC();
+  if (done) goto end_f;
   // -- F: encode pass 1 -------------------------------------------------------------
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;
@@ -1693,26 +2007,35 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
       if (lane == 0) m.misc[MS_OVF_LINE] = base + __ffs(b) - 1;
       __syncwarp();
       finish_error(a, m, X, t, X_OVERFLOW, 0, fscratch, flimbs);
-      return;
+      done = true;
+      goto end_f;
     }
   }
-
+end_f:
+  PHASE_MARK(6);
+  CTA_SYNC();
+  if (done) goto end_g;
   // -- G: state machine ------------------------------------------------------------
-  uint32_t ndiag = 0;
-  if (lane == 0) {
-    ndiag = state_machine(m, X);
-    if (ndiag != NONE32) {
-      for (uint32_t li = 0; li < L; ++li) {
-        const uint32_t fl = m.lfl[li];
-        ndiag += (fl & LF_TOKERR) ? 1 : 0;
-        ndiag += (fl & LF_RESOLVE_ERR) ? 1 : 0;
-      }
+  if (state_fast(m, X)) {
+    ndiag = 0;
+  } else {
+    state_reset(m);
+    if (lane == 0) ndiag = state_machine(m, X);
+  }
+  if (lane == 0 && ndiag != NONE32) {
+    for (uint32_t li = 0; li < L; ++li) {
+      const uint32_t fl = m.lfl[li];
+      ndiag += (fl & LF_TOKERR) ? 1 : 0;
+      ndiag += (fl & LF_RESOLVE_ERR) ? 1 : 0;
     }
   }
   ndiag = __shfl_sync(FULLM, ndiag, 0);
-  if (ndiag == NONE32) { fail_internal(); return; }
-  if (ndiag) { finish_error(a, m, X, t, X_ASSEMBLY, ndiag, fscratch, flimbs); return; }
-
+  if (ndiag == NONE32) { fail_internal(); done = true; goto end_g; }
+  if (ndiag) { finish_error(a, m, X, t, X_ASSEMBLY, ndiag, fscratch, flimbs); done = true; goto end_g; }
+end_g:
+  PHASE_MARK(7);
+  CTA_SYNC();
+  if (done) goto end_h;
   // -- H: structure checks + layout (lane 0) ----------------------------------------
   if (lane == 0) {
     const uint32_t nfn = m.misc[MS_NFN], nblk = m.misc[MS_NBLK];
@@ -1743,14 +2066,17 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
     m.misc[MS_TOTAL] = pos;
   }
   x = __shfl_sync(FULLM, x, 0);
-  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); return; }
+  if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); done = true; goto end_h; }
   __syncwarp();
-  const uint32_t total = m.misc[MS_TOTAL];
-
+  total = m.misc[MS_TOTAL];
+end_h:
+  PHASE_MARK(8);
+  CTA_SYNC();
+  if (done) goto end_i;
+  {
   // -- I: output ---------------------------------------------------------------------
-  bool fits;
-  const uint64_t off = asm_alloc(a, 4ull * total, fits);
-  uint32_t* ow = reinterpret_cast<uint32_t*>(a.out + off);
+  off = asm_alloc(a, 4ull * total, fits);
+  ow = reinterpret_cast<uint32_t*>(a.out + off);
   if (fits && lane == 0) {
     ow[0] = 0x07230203u;
     ow[1] = (m.misc[MS_MAJOR] << 16) | ((m.misc[MS_MINOR] - 1) << 8);
@@ -1809,27 +2135,33 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
     }
     __syncwarp();
     finish_error(a, m, X, t, ser_off != NONE32 ? X_SERIAL : X_WC, 0, fscratch, flimbs);
-    return;
+    done = true;
+    goto end_i;
+  }
   }
   if (lane == 0) {
     a.out_span[2 * t] = (int64_t)off;
     a.out_span[2 * t + 1] = (int64_t)(4ull * total);
     a.status[t] = AST_OK;
   }
-  __syncwarp();
+end_i:
+  PHASE_MARK(9);
+  CTA_SYNC();
 }
 
-__global__ void __launch_bounds__(128) asm_kernel(AsmArgs a) {
-  const uint32_t lane = lane_id_a();
-  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(1024) asm_kernel(AsmArgs a) {
+  __shared__ uint32_t s_base;
+  const uint32_t warps = blockDim.x >> 5;
+  const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5);
   uint8_t* slot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
   const AsmCtx X{a.T, a.U, a.A};
   while (true) {
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(a.counters, 1u);
-    t = __shfl_sync(FULLM, t, 0);
-    if (t >= a.n_mod) break;
-    assemble_module(a, X, t, slot);
+    if (threadIdx.x == 0) s_base = atomicAdd(a.counters, warps);
+    __syncthreads();
+    const uint32_t base = s_base;
+    __syncthreads();
+    if (base >= a.n_mod) break;
+    assemble_module(a, X, base + (threadIdx.x >> 5), slot);
   }
 }
 

@@ -38,14 +38,29 @@ struct Uni {
   const uint32_t* dec; uint32_t n_dec;               // starts of 10-digit runs, sorted
   const uint32_t* digit; uint32_t n_digit;           // isdigit() but not isdecimal(), sorted
 
+  // ASCII answers inline; the table searches are out of line (one copy of code)
   SKG_HD bool is_space(uint32_t c) const {
     if (c < 0x80) return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1C && c <= 0x1F);
+    return is_space_slow(c);
+  }
+  SKG_HD int decimal(uint32_t c) const {   // decimal value 0..9 or -1 (str.isdecimal)
+    if (c < 0x80) return (c >= '0' && c <= '9') ? (int)(c - '0') : -1;
+    return decimal_slow(c);
+  }
+  SKG_HD bool is_digit(uint32_t c) const {
+    if (c < 0x80) return c >= '0' && c <= '9';
+    return is_digit_slow(c);
+  }
+  SKG_HD bool is_printable(uint32_t c) const {
+    if (c >= 0x20 && c < 0x7F) return true;
+    if (c < 0xA0) return false;
+    return is_printable_slow(c);
+  }
+  SKG_HD SKG_NOINLINE bool is_space_slow(uint32_t c) const {
     for (uint32_t i = 0; i < n_space; ++i) if (ldg32(space + i) == c) return true;
     return false;
   }
-  // decimal value 0..9 or -1 (str.isdecimal)
-  SKG_HD int decimal(uint32_t c) const {
-    if (c < 0x80) return (c >= '0' && c <= '9') ? (int)(c - '0') : -1;
+  SKG_HD SKG_NOINLINE int decimal_slow(uint32_t c) const {
     uint32_t lo = 0, hi = n_dec;
     while (lo < hi) {
       uint32_t mid = (lo + hi) >> 1;
@@ -55,9 +70,8 @@ struct Uni {
     uint32_t s = ldg32(dec + lo - 1);
     return c - s < 10 ? (int)(c - s) : -1;
   }
-  SKG_HD bool is_digit(uint32_t c) const {
-    if (decimal(c) >= 0) return true;
-    if (c < 0x80) return false;
+  SKG_HD SKG_NOINLINE bool is_digit_slow(uint32_t c) const {
+    if (decimal_slow(c) >= 0) return true;
     uint32_t lo = 0, hi = n_digit;
     while (lo < hi) {
       uint32_t mid = (lo + hi) >> 1;
@@ -67,9 +81,7 @@ struct Uni {
     }
     return false;
   }
-  SKG_HD bool is_printable(uint32_t c) const {
-    if (c >= 0x20 && c < 0x7F) return true;
-    if (c < 0xA0) return false;
+  SKG_HD SKG_NOINLINE bool is_printable_slow(uint32_t c) const {
     uint32_t lo = 0, hi = n_printable;
     while (lo < hi) {
       uint32_t mid = (lo + hi) >> 1;
@@ -79,8 +91,16 @@ struct Uni {
   }
 };
 
+SKG_HD SKG_NOINLINE uint32_t utf8_cp_multi(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len);
+
 // One code point of (valid, surrogatepass) UTF-8 at p[i]; sets its byte length.
 SKG_HD inline uint32_t utf8_cp(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len) {
+  const uint32_t c = p[i];
+  if (c < 0x80) { len = 1; return c; }
+  return utf8_cp_multi(p, n, i, len);
+}
+
+SKG_HD SKG_NOINLINE uint32_t utf8_cp_multi(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len) {
   uint32_t c = p[i];
   if (c < 0x80 || i + 1 >= n) { len = 1; return c; }
   if (c < 0xE0) { len = 2; return ((c & 0x1F) << 6) | (p[i + 1] & 0x3F); }
@@ -173,8 +193,12 @@ struct IntVal {
 // The interpreter's view of a character in int()/float(): ASCII as is, other
 // white space -> ' ', other decimal digits -> '0'..'9', anything else -> '?'
 // (_PyUnicode_TransformDecimalAndSpaceToASCII).
+SKG_HD SKG_NOINLINE uint32_t xform_multi(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len, const Uni& U);
 SKG_HD inline uint32_t xform(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len, const Uni& U) {
   if (p[i] < 0x80) { len = 1; return p[i] ? p[i] : '?'; }   // embedded NUL: invalid in both parsers
+  return xform_multi(p, n, i, len, U);
+}
+SKG_HD SKG_NOINLINE uint32_t xform_multi(const uint8_t* p, uint32_t n, uint32_t i, uint32_t& len, const Uni& U) {
   const uint32_t c = utf8_cp(p, n, i, len);
   if (U.is_space(c)) return ' ';
   const int d = U.decimal(c);

@@ -17,7 +17,7 @@ def main():
     ap.add_argument("--modules", type=int, default=50000)
     ap.add_argument("--variants", type=int, default=2000)
     ap.add_argument("--launches", type=int, default=4)
-    ap.add_argument("--kind", default="disasm", choices=["disasm", "validate"])
+    ap.add_argument("--kind", default="disasm", choices=["disasm", "validate", "asm"])
     ap.add_argument("--opts", type=int, default=2)
     args = ap.parse_args()
     import torch
@@ -25,8 +25,15 @@ def main():
     from synth.families import sample_batch
     b = sample_batch(args.modules, args.variants, 20261017)
     dev = _native.DeviceBatch.from_host(b.data, b.offsets, b.lengths)
-    plan = _native.DisasmPlan(dev, args.opts, kind=args.kind)
+    plan = _native.DisasmPlan(dev, args.opts, kind="disasm" if args.kind == "asm" else args.kind)
     plan.fit()
+    if args.kind == "asm":   # assemble the disassembled text (stride-2 spans)
+        mx = int(plan.span[1::2].max().item())
+        tb = _native.DeviceBatch(plan.text, plan.span[0::2], plan.span[1::2], (mx + 3) // 4, 0)
+        tb.n = dev.n
+        plan = _native.AsmPlan(tb, out_cap=int(b.lengths.sum()) + 64 * dev.n + 4096, stride=2)
+        plan.fit()
+        assert (plan.status[: dev.n] == 0).all().item()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for _ in range(args.launches):
