@@ -56,7 +56,7 @@ struct AsmArgs {
 };
 
 // token: off (text byte offset), lenf = len | TK_STR
-constexpr uint32_t TK_STR = 0x80000000u, TK_LEN = 0x3FFFFFFFu;
+constexpr uint32_t TK_STR = 0x80000000u, TK_ESC = 0x40000000u, TK_LEN = 0x3FFFFFFFu;
 
 // line flags
 enum : uint32_t {
@@ -83,7 +83,8 @@ enum : uint32_t {
 
 struct AsmMod {
   uint8_t* base;
-  uint8_t* txt;       // module text copy (escapes undone in place)
+  const uint8_t* txt; // the module text (input arena, read in place)
+  uint8_t* esc;       // unescaped string tokens, at the same offsets as in txt
   uint32_t T;         // bytes
   uint32_t L;         // lines
   uint32_t* ls;       // line start
@@ -100,6 +101,9 @@ struct AsmMod {
   uint32_t* lerr;     // 4 words / line: error details
   uint32_t* tok;      // 2 words / token
   uint32_t* tid;      // per token: resolved %id (0 = not an id token / not yet resolved)
+  uint32_t* lwo;      // per line: offset of its encoded words in sw
+  uint32_t* sw;       // encode pass 1 output words (line order)
+  uint32_t* swr;      // bit per sw word: a referenced id (checked against the registry)
   uint32_t ntb;       // token slots
   uint32_t* nt;       // name table: 6 words / entry
   uint32_t ncap;
@@ -183,7 +187,7 @@ struct Tok {
 __device__ __forceinline__ Tok tok_at(const AsmMod& m, uint32_t t) {
   const uint32_t off = m.tok[2 * t], lf = m.tok[2 * t + 1];
   Tok k;
-  k.p = m.txt + off;
+  k.p = ((lf & TK_ESC) ? m.esc : m.txt) + off;
   k.n = lf & TK_LEN;
   k.str = (lf & TK_STR) != 0;
   k.raw = off - (k.str ? 1 : 0);
@@ -379,20 +383,11 @@ __device__ __forceinline__ bool word_maybe_sep(uint32_t w) {
   return (lt | z2 | z3) != 0;
 }
 
-// returns L; fills ls/le (capacity cap)
+// returns L; fills ls/le (capacity cap).  The text is read in place (it is
+// consumed line by line from L1/L2 by the later phases; no scratch copy).
 __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint32_t cap) {
   const uint32_t lane = lane_id_a();
   const uint32_t T = m.T;
-  // copy (16-byte vectors when aligned; the batch arena pads modules to 16 bytes)
-  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    const uint32_t n16 = (T + 15) / 16;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(m.txt);
-    for (uint32_t k = lane; k < n16; k += 32) d4[k] = __ldg(s4 + k);
-  } else {
-    for (uint32_t k = lane; k < T; k += 32) m.txt[k] = src[k];
-  }
-  __syncwarp();
   // separators: lanes scan 4-byte words; each lane records its separators in order
   uint32_t nsep = 0;
   const uint32_t nw = (T + 3) / 4;
@@ -401,7 +396,13 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
     uint32_t cnt = 0;
     uint32_t pos[4], len[4];
     if (w < nw) {
-      const uint32_t word = reinterpret_cast<const uint32_t*>(m.txt)[w];
+      uint32_t word;
+      if ((reinterpret_cast<uintptr_t>(m.txt) & 3) == 0) {
+        word = __ldg(reinterpret_cast<const uint32_t*>(m.txt) + w);
+      } else {
+        word = 0;
+        for (uint32_t b = 0; b < 4 && 4 * w + b < T; ++b) word |= (uint32_t)m.txt[4 * w + b] << (8 * b);
+      }
       if (word_maybe_sep(word)) {
         for (uint32_t b = 0; b < 4; ++b) {
           const uint32_t i = 4 * w + b;
@@ -469,7 +470,7 @@ __device__ __noinline__ uint32_t count_tokens(const uint8_t* t, uint32_t i, uint
 
 __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
                                            uint32_t cap, uint32_t& npct) {
-  uint8_t* t = m.txt;
+  const uint8_t* t = m.txt;
   const uint32_t s0 = m.ls[li], e0 = m.le[li];
   uint32_t nt = 0;
   uint32_t fl = 0;
@@ -484,8 +485,14 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       uint32_t w = i;
       bool esc = false;
       while (i < e0 && t[i] != '"') {
-        if (t[i] == '\\' && i + 1 < e0) { ++i; esc = true; }
-        if (esc) t[w] = t[i];
+        if (t[i] == '\\' && i + 1 < e0) {
+          if (!esc) {   // first escape: the unescaped copy starts with the bytes so far
+            for (uint32_t q = start + 1; q < w; ++q) m.esc[q] = t[q];
+            esc = true;
+          }
+          ++i;
+        }
+        if (esc) m.esc[w] = t[i];
         ++w; ++i;
       }
       if (i >= e0) {
@@ -497,7 +504,7 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       ++i;
       if (nt < cap) {
         m.tok[2 * (tb + nt)] = start + 1;
-        m.tok[2 * (tb + nt) + 1] = (w - start - 1) | TK_STR;
+        m.tok[2 * (tb + nt) + 1] = (w - start - 1) | TK_STR | (esc ? TK_ESC : 0);
       }
       ++nt;
       continue;
@@ -615,7 +622,23 @@ struct EncCtx {
   EncOut r;
   LitInfo info;
   bool is_switch;
+  uint32_t* rbits;        // pass 1: bit per scratch word, set for referenced ids
+  uint32_t rbase;         // bit index of operand word 0
+  const uint32_t* tok;    // register copies of the module arrays the walk reads
+  const uint8_t* txt;
+  const uint8_t* esc;
+  const uint32_t* tid;
 };
+
+__device__ __forceinline__ Tok tok_of(const EncCtx& c, uint32_t t) {
+  const uint32_t off = c.tok[2 * t], lf = c.tok[2 * t + 1];
+  Tok k;
+  k.p = ((lf & TK_ESC) ? c.esc : c.txt) + off;
+  k.n = lf & TK_LEN;
+  k.str = (lf & TK_STR) != 0;
+  k.raw = off - (k.str ? 1 : 0);
+  return k;
+}
 
 __device__ __forceinline__ uint32_t enc_item(const EncCtx& c, uint32_t k) {
   if (c.ridx == NONE32) return c.ops0 + k;
@@ -688,7 +711,7 @@ __device__ inline bool ext_by_name(const AsmCtx& X, const uint8_t* p, uint32_t n
 // id of an %name token for coerce (asm.py:106-120); false on error
 __device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id) {
   if (c.mode != M_RESOLVE) {   // resolved once per token after the result names are bound
-    const uint32_t cached = c.m.tid[t];
+    const uint32_t cached = c.tid[t];
     if (cached) { id = cached; return true; }
   }
   if (!(k.n >= 2 && k.p[0] == '%')) return enc_fail(c, E_EXPECT_ID, t);
@@ -795,12 +818,12 @@ constexpr int ESTACK = 48;
 constexpr uint32_t KP_PARAM = 0x10000u;   // stack entry flag: take() with the "enumerant parameter" message
 
 // value(kind, item) for one stack entry; pushes follow-ups
-__device__ __noinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st, int& sp) {
+__device__ __forceinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st, int& sp) {
   const Tables& T = c.X.T;
   const uint32_t k = entry & 0xFFFF;
   if (c.pos >= c.nitems) return enc_fail(c, E_MISSING, 0, k, (entry & KP_PARAM) ? 1 : 0);
   const uint32_t t = enc_item(c, c.pos++);
-  const Tok tk = tok_at(c.m, t);
+  const Tok tk = tok_of(c, t);
   uint32_t kk = k;
   // composite: value(bases[0], tok) then param(b) for the rest
   while (T.kcat(kk) == CAT_COMPOSITE) {
@@ -814,11 +837,14 @@ __device__ __noinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st, in
   if (cat == CAT_ID) {
     uint32_t id;
     if (!enc_id(c, t, tk, id)) return false;
-    emit_word(c, id);
     if (sub == IDR_RESULT) c.r.result_id = id;
-    else if (c.mode == M_WRITE && c.r.bad_ref == NONE32) {
+    else if (c.rbits) {
+      const uint32_t b = c.rbase + c.r.nw;
+      atomicOr(&c.rbits[b >> 5], 1u << (b & 31));
+    } else if (c.mode == M_WRITE && c.r.bad_ref == NONE32) {
       if (!idset_has(c.m, c.m.reg, 0, id)) c.r.bad_ref = id;
     }
+    emit_word(c, id);
     return true;
   }
   if (cat == CAT_VALUEENUM) {
@@ -934,8 +960,13 @@ __device__ __noinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st, in
   return true;
 }
 
-// Encoder.encode (ops.py:120-155) over the instruction's slots
-__device__ __noinline__ void encode_line(EncCtx& c) {
+// Encoder.encode (ops.py:120-155) over the instruction's slots.  The context
+// is copied into registers for the walk (the caller's copy lives in local
+// memory) and enc_one is inlined at a single call site: the slot sequence
+// ('*' repeats to the end, '?' skipped when no tokens remain, the
+// SpecConstantOp IdRef tail) is generated by a small state machine.
+__device__ __noinline__ void encode_line(EncCtx& cin) {
+  EncCtx c = cin;
   const Tables& T = c.X.T;
   c.r.nw = 0; c.r.ecode = E_OK; c.r.result_id = 0; c.r.word2 = NONE32; c.r.unres = false;
   c.r.bad_ref = NONE32;
@@ -943,31 +974,41 @@ __device__ __noinline__ void encode_line(EncCtx& c) {
   uint32_t st[ESTACK];
   int sp = 0;
   const uint32_t ns = T.inslots(c.d), so = T.islot_off(c.d);
-  for (uint32_t s = 0; s < ns; ++s) {
-    const uint32_t q = T.slot_quant(so + s), k = T.slot_kind(so + s);
-    if (q == Q_VAR) {
-      while (c.pos < c.nitems) {
-        st[0] = k; sp = 1;
-        while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
+  uint32_t s = 0, repk = 0;
+  bool rep = false, stop_after = false, pending_tail = false;
+#pragma unroll 1
+  for (;;) {
+    if (sp == 0) {
+      if (pending_tail) { pending_tail = false; rep = true; stop_after = false; repk = T.idref; }
+      if (rep) {
+        if (c.pos >= c.nitems) {
+          if (stop_after) break;
+          rep = false;
+          continue;
+        }
+        st[sp++] = repk;
+      } else {
+        if (s >= ns) break;
+        const uint32_t q = T.slot_quant(so + s), k = T.slot_kind(so + s);
+        const bool tail = T.slot_spec_tail(so + s);
+        ++s;
+        if (q == Q_VAR) { rep = true; stop_after = true; repk = k; continue; }
+        if (q == Q_OPT && c.pos >= c.nitems) continue;
+        st[sp++] = k;
+        pending_tail = tail;
       }
-      break;
     }
-    if (q == Q_OPT && c.pos >= c.nitems) continue;
-    st[0] = k; sp = 1;
-    while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
-    if (T.slot_spec_tail(so + s)) {
-      while (c.pos < c.nitems) {
-        st[0] = T.idref; sp = 1;
-        while (sp > 0) { const uint32_t e = st[--sp]; if (!enc_one(c, e, st, sp)) return; }
-      }
-    }
+    const uint32_t e = st[--sp];
+    if (!enc_one(c, e, st, sp)) { cin.r = c.r; return; }
   }
   if (c.pos < c.nitems) enc_fail(c, E_EXTRA, 0, c.nitems - c.pos);
+  cin.r = c.r;
 }
 
 // set up an encoder context for line li (d known, not OpLabel); false = pre-encode error
 __device__ inline bool enc_setup(EncCtx& c, const AsmMod& m, uint32_t li) {
   const Tables& T = c.X.T;
+  c.tok = m.tok; c.txt = m.txt; c.esc = m.esc; c.tid = m.tid;
   const uint32_t fl = m.lfl[li];
   const bool has_res = fl & LF_RESULT;
   c.rtok = has_res ? m.lt0[li] : NONE32;
@@ -1770,7 +1811,8 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   if (done) goto end_a;
   m.T = T;
   m.misc = reinterpret_cast<uint32_t*>(take(64 * 4));
-  m.txt = take((uint64_t)T + 16);
+  m.txt = src;
+  m.esc = take((uint64_t)T + 16);   // touched only by strings with escapes
   m.ls = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
   m.le = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
   if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); done = true; goto end_a; }
@@ -1972,6 +2014,30 @@ end_e:
   CTA_SYNC();
   if (done) goto end_f;
   // -- F: encode pass 1 -------------------------------------------------------------
+  {   // words of a line are bounded by 2 per token (4 string bytes per word)
+    uint32_t carry = 0;
+    m.lwo = reinterpret_cast<uint32_t*>(take(4ull * L + 4));
+    for (uint32_t base = 0; base < L; base += 32) {
+      const uint32_t li = base + lane;
+      uint32_t ub = 0;
+      if (li < L) {
+        ub = 1;
+        for (uint32_t k = 0; k < m.lnt[li]; ++k) {
+          const uint32_t lf = m.tok[2 * (m.lt0[li] + k) + 1];
+          ub += (lf & TK_STR) ? (lf & TK_LEN) / 4 + 1 : 2;
+        }
+      }
+      const uint32_t incl = wincl(ub);
+      if (li < L) m.lwo[li] = carry + incl - ub;
+      carry += __shfl_sync(FULLM, incl, 31);
+    }
+    m.sw = reinterpret_cast<uint32_t*>(take(4ull * carry + 4));
+    m.swr = reinterpret_cast<uint32_t*>(take(carry / 8 + 8));
+    if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_f; }
+    m.sused = used;
+    for (uint32_t k = lane; k <= carry / 32; k += 32) m.swr[k] = 0;
+    __syncwarp();
+  }
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;
     if (li >= L) continue;
@@ -1984,12 +2050,16 @@ end_e:
       if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
       continue;
     }
-    EncCtx c{m, X, li, d, M_COUNT, nullptr};
+    EncCtx c{m, X, li, d, M_COUNT, m.sw + m.lwo[li] + 1};
+    c.rbits = m.swr;
+    c.rbase = m.lwo[li] + 1;
     if (!enc_setup(c, m, li)) { m.lec[li] = c.r.ecode; continue; }
     encode_line(c);
     m.lec[li] = c.r.ecode;
-    uint32_t* e = m.lerr + 4 * li;
-    e[0] = c.r.etok; e[1] = c.r.eaux; e[2] = c.r.eaux2; e[3] = c.r.eaux3;
+    if (c.r.ecode != E_OK) {
+      uint32_t* e = m.lerr + 4 * li;
+      e[0] = c.r.etok; e[1] = c.r.eaux; e[2] = c.r.eaux2; e[3] = c.r.eaux3;
+    }
     m.lnw[li] = c.r.nw;
     m.lrid[li] = c.r.result_id;
     uint32_t f2 = fl;
@@ -2114,12 +2184,24 @@ end_h:
       continue;
     }
     if (1 + m.lnw[li] > 0xFFFF) wc_off = min(wc_off, at);
-    EncCtx c{m, X, li, d, M_WRITE, fits ? ow + at + 1 : nullptr};   // M_WRITE also checks references
-    enc_setup(c, m, li);
-    encode_line(c);
-    if (fits) ow[at] = ((1 + c.r.nw) << 16) | __ldg(X.T.irec(d) + 5);
-    m.lerr[4 * li + 3] = c.r.bad_ref;
-    if (c.r.bad_ref != NONE32) ser_off = min(ser_off, at);
+    uint32_t bad_ref = NONE32;
+    if (m.lfl[li] & LF_UNRES) {   // ids of names first seen in the state machine: re-encode
+      EncCtx c{m, X, li, d, M_WRITE, fits ? ow + at + 1 : nullptr};   // M_WRITE also checks references
+      enc_setup(c, m, li);
+      encode_line(c);
+      bad_ref = c.r.bad_ref;
+    } else {                      // copy pass-1 words; check the referenced ids
+      const uint32_t w0 = m.lwo[li] + 1, nw = m.lnw[li];
+      for (uint32_t k = 0; k < nw; ++k) {
+        const uint32_t w = m.sw[w0 + k];
+        if (fits) ow[at + 1 + k] = w;
+        const uint32_t b = w0 + k;
+        if (bad_ref == NONE32 && ((m.swr[b >> 5] >> (b & 31)) & 1) && !idset_has(m, m.reg, 0, w)) bad_ref = w;
+      }
+    }
+    if (fits) ow[at] = ((1 + m.lnw[li]) << 16) | __ldg(X.T.irec(d) + 5);
+    m.lerr[4 * li + 3] = bad_ref;
+    if (bad_ref != NONE32) ser_off = min(ser_off, at);
   }
   ser_off = wmin(ser_off);
   wc_off = wmin(wc_off);
