@@ -122,11 +122,11 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
  * atomic bump allocator (skg_last_counts reports overflow / bytes used, as for
  * skg_disasm).  `slot_bytes` is the per-warp scratch (skg_asm_slot_hint); a
  * module that needs more reports SKG_ST_INTERNAL and can be rerun with a
- * larger slot.  `workspace` must hold skg_asm_workspace_bytes(slot_bytes).
+ * larger slot.  `workspace` must hold skg_asm_workspace_bytes(slot_bytes, n_mod).
  * default_version = major << 16 | minor: the Assembler's default_version
  * (asm.py:128), used when the text has no "; Version:" comment. */
 uint64_t skg_asm_slot_hint(uint64_t max_text_bytes);
-uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes);
+uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes, uint32_t n_mod);
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
             uint32_t mod_stride, uint32_t n_mod, uint64_t slot_bytes, uint8_t* out, uint64_t out_cap, int64_t* out_span,
             int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,

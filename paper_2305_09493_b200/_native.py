@@ -352,7 +352,7 @@ def _bind_asm(L):
     P, U32, U64, I32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
     L.skg_asm_slot_hint.argtypes = [U64]
     L.skg_asm_slot_hint.restype = U64
-    L.skg_asm_workspace_bytes.argtypes = [U64]
+    L.skg_asm_workspace_bytes.argtypes = [U64, U32]
     L.skg_asm_workspace_bytes.restype = U64
     L.skg_asm.argtypes = [P, P, P, P, U32, U32, U64, P, U64, P, P, P, U64, P, U32]  # ..., stream, default_version
     L.skg_asm.restype = I32
@@ -387,7 +387,7 @@ class AsmPlan:
         n = batch.n
         max_len = int(batch.max_words) * 4 + 16
         self.slot = int(slot_bytes or L.skg_asm_slot_hint(max_len))
-        self.ws_bytes = int(L.skg_asm_workspace_bytes(self.slot))
+        self.ws_bytes = int(L.skg_asm_workspace_bytes(self.slot, max(n, 1)))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.cap = int(out_cap or (batch.total_bytes + 64 * n + 4096))
         self.out = torch.empty(self.cap, dtype=torch.uint8, device="cuda")

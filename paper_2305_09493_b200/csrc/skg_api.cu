@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include "../../include/skgpu.h"
 #include "skg_module.cuh"
+#include "skg_sched.cuh"
 
 namespace skg {
 struct DisasmArgs;
@@ -52,18 +53,49 @@ uint64_t gslot_bytes(uint32_t max_words) {
 
 
 struct WsLayout {
-  uint64_t state, counters, scratch, total, slot, gtext;
+  uint64_t state, counters, sched, scratch, total, slot, gtext;
   uint32_t n_warps;
 };
+
+// scheduling region: hist[1024], cursor[1024], perm[n]
+uint64_t sched_bytes(uint32_t n_mod) { return (8192 + 4ull * n_mod + 255) & ~255ull; }
+
+// module processing order (largest first) into sched + 8192
+int launch_sched(const int64_t* len, uint32_t stride, uint32_t n, uint8_t* sched, cudaStream_t s) {
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sched);
+  uint32_t* cursor = hist + skg::SCHED_BUCKETS;
+  uint32_t* perm = cursor + skg::SCHED_BUCKETS;
+  if (cudaError_t e = cudaMemsetAsync(hist, 0, 4 * skg::SCHED_BUCKETS, s)) return (int)e;
+  uint32_t blocks = (n + 4095) / 4096;
+  if (blocks > (uint32_t)sm_count() * 2) blocks = (uint32_t)sm_count() * 2;
+  if (blocks == 0) blocks = 1;
+  skg::sched_hist<<<blocks, 1024, 0, s>>>(len, stride, n, hist);
+  skg::sched_scan<<<1, skg::SCHED_BUCKETS, 0, s>>>(hist, cursor);
+  skg::sched_scatter<<<blocks, 1024, 0, s>>>(len, stride, n, cursor, perm);
+  return (int)cudaGetLastError();
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// disassembler: phase-synchronised CTAs of kDisWarps warps (one module per warp),
+// one CTA per SM, kDisSlab bytes of shared memory per warp
+int kDisWarps = env_int("SKG_DIS_WARPS", 32);
+uint32_t kDisSlab = (uint32_t)env_int("SKG_DIS_SLAB", 6912);
+uint32_t dis_blocks() { return (uint32_t)sm_count() * env_int("SKG_DIS_BLOCKS_PER_SM", 1); }
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
   (void)n_mod;
   l.n_warps = grid_blocks() * kWarpsPerBlock;
+  if (dis_blocks() * kDisWarps > l.n_warps) l.n_warps = dis_blocks() * kDisWarps;
   l.slot = gslot_bytes(max_words);
   l.counters = 0;
   l.state = 0;
-  l.scratch = 256;
+  l.sched = 256;
+  l.scratch = l.sched + sched_bytes(n_mod);
   l.gtext = 0;
   l.total = l.scratch + l.slot * l.n_warps;
   return l;
@@ -84,6 +116,9 @@ extern "C" {
 const char* skg_version(void) { return "skgpu 0.1 (sm_100a)"; }
 
 #ifdef SKG_PHASE_TIMING
+int skg_debug_disasm_phases(unsigned long long* out16) {
+  return check(cudaMemcpyFromSymbol(out16, skg::g_dis_phase, 16 * sizeof(unsigned long long)));
+}
 int skg_debug_asm_phases(unsigned long long* out16) {
   return check(cudaMemcpyFromSymbol(out16, skg::g_asm_phase, 16 * sizeof(unsigned long long)));
 }
@@ -172,14 +207,16 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   a.err_cap = err_cap;
   a.gscratch = ws + l.scratch;
   a.gslot_bytes = l.slot;
-  a.smem_slab = kSlabBytes;
-  const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
+  a.smem_slab = kDisSlab;
+  if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
+  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
+  const size_t smem = (size_t)kDisSlab * kDisWarps;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  skg::disasm_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, smem, s>>>(a);
+  skg::disasm_kernel<<<dis_blocks(), 32 * kDisWarps, smem, s>>>(a);
   return check(cudaGetLastError());
 }
 
@@ -219,15 +256,11 @@ uint64_t skg_asm_slot_hint(uint64_t max_text_bytes) {
 }
 
 // assembler: phase-synchronised CTAs of kAsmWarps warps (one module per warp), 2 per SM
-int asm_env(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-int kAsmWarps = asm_env("SKG_ASM_WARPS", 32);
-uint32_t asm_blocks() { return (uint32_t)sm_count() * asm_env("SKG_ASM_BLOCKS_PER_SM", 1); }
+int kAsmWarps = env_int("SKG_ASM_WARPS", 32);
+uint32_t asm_blocks() { return (uint32_t)sm_count() * env_int("SKG_ASM_BLOCKS_PER_SM", 1); }
 
-uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes) {
-  return 256 + (uint64_t)asm_blocks() * kAsmWarps * slot_bytes;
+uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes, uint32_t n_mod) {
+  return 256 + sched_bytes(n_mod) + (uint64_t)asm_blocks() * kAsmWarps * slot_bytes;
 }
 
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
@@ -236,7 +269,7 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
             uint32_t default_version) {
   if (!t || !workspace) return -1;
   if (t->a.op_label == 0xFFFFFFFFu || t->a.op_fnend == 0xFFFFFFFFu) return -4;
-  if (workspace_bytes < skg_asm_workspace_bytes(slot_bytes)) return -3;
+  if (workspace_bytes < skg_asm_workspace_bytes(slot_bytes, n_mod)) return -3;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)workspace;
   if (int e = check(cudaMemsetAsync(ws, 0, 256, s))) return e;
@@ -247,7 +280,9 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.mod_stride = mod_stride ? mod_stride : 1;
   a.out = out; a.out_cap = out_cap; a.out_span = out_span; a.status = status;
   a.counters = reinterpret_cast<uint32_t*>(ws);
-  a.gscratch = ws + 256;
+  if (int e = check((cudaError_t)launch_sched(mod_len, a.mod_stride, n_mod, ws + 256, s))) return e;
+  a.order = reinterpret_cast<const uint32_t*>(ws + 256 + 8192);
+  a.gscratch = ws + 256 + sched_bytes(n_mod);
   a.gslot_bytes = slot_bytes;
   a.default_version = default_version;
   skg::asm_kernel<<<asm_blocks(), 32 * kAsmWarps, 0, s>>>(a);

@@ -53,6 +53,7 @@ struct AsmArgs {
   uint8_t* gscratch;
   uint64_t gslot_bytes;
   uint32_t default_version;   // major << 16 | minor
+  const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
 };
 
 // token: off (text byte offset), lenf = len | TK_STR
@@ -2243,7 +2244,8 @@ __global__ void __launch_bounds__(1024) asm_kernel(AsmArgs a) {
     const uint32_t base = s_base;
     __syncthreads();
     if (base >= a.n_mod) break;
-    assemble_module(a, X, base + (threadIdx.x >> 5), slot);
+    const uint32_t tk = base + (threadIdx.x >> 5);
+    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot);
   }
 }
 

@@ -43,6 +43,7 @@ struct DisasmArgs {
   uint8_t* gscratch;          // per-warp global slots
   uint64_t gslot_bytes;
   uint32_t smem_slab;         // bytes per warp in dynamic shared memory
+  const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
 };
 
 // -- sanitized friendly names (disasm.py:82-86) --------------------------------
@@ -983,29 +984,44 @@ __device__ __noinline__ void report_internal(ErrSink& es, int32_t t, const char*
   }
 }
 
-__global__ void __launch_bounds__(128) disasm_kernel(DisasmArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t lane = lane_id();
-  const uint32_t warp_in_block = threadIdx.x >> 5;
-  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
-  uint8_t* slab = smem + (size_t)warp_in_block * a.smem_slab;
-  uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
-  const Tables& T = a.T;
-  ErrSink es{a.errs, a.ticket + 1, a.err_cap};
+// ============================================================================
+// Optional per-phase cycle counters (build with -DSKG_PHASE_TIMING; profiling only)
+#ifdef SKG_PHASE_TIMING
+__device__ unsigned long long g_dis_phase[16];
+#define DPHASE_MARK(k)                                                  \
+  do {                                                                  \
+    __syncwarp();                                                       \
+    const long long now_ = clock64();                                   \
+    if (lane_id() == 0) atomicAdd(&g_dis_phase[k], (unsigned long long)(now_ - ph_t0_)); \
+    ph_t0_ = now_;                                                      \
+  } while (0)
+#define DPHASE_START() long long ph_t0_ = clock64()
+#else
+#define DPHASE_MARK(k) do {} while (0)
+#define DPHASE_START() do {} while (0)
+#endif
 
-  while (true) {
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1u);
-    t = __shfl_sync(FULL, t, 0);
-    if (t >= a.n_mod) break;
+// One module per warp; all warps of the CTA run the same phase at the same
+// time (CTA barrier between phases), so the instruction working set of the SM
+// is one phase rather than the whole program.
+__device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
+                                        ErrSink& es) {
+  const uint32_t lane = lane_id();
+  const Tables& T = a.T;
+  DPHASE_START();
+  const bool live = ticket < a.n_mod;
+  const uint32_t t = live ? a.order[ticket] : 0;
+  int32_t status = live ? ST_OK : ST_INTERNAL;
+  uint64_t total = 0;
+  uint32_t width = 0;
+  Mod m;
+  bool in_smem = false, direct = false, names_mode = false;
+  // -- P0: load + boundary (A1, A2)
+  if (live) {
     const int64_t nbytes = a.mod_len[t];
     const uint8_t* src = a.data + a.mod_off[t];
-    int32_t status = ST_OK;
-    uint64_t total = 0;
-    uint32_t width = 0;
-    Mod m;
     const uint32_t W = (nbytes >= 0 && nbytes % 4 == 0) ? (uint32_t)(nbytes / 4) : 0;
-    bool in_smem = head_bytes(W) <= a.smem_slab;
+    in_smem = head_bytes(W) <= a.smem_slab;
     if (!in_smem && worst_bytes(W, RENDER_MIN) > a.gslot_bytes) {
       status = ST_INTERNAL;
       report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
@@ -1013,69 +1029,100 @@ __global__ void __launch_bounds__(128) disasm_kernel(DisasmArgs a) {
       layout_head(m, in_smem ? slab : gslot, W);
       status = load_and_split(m, src, (uint64_t)nbytes, &es, (int32_t)t);
     }
-    if (status == ST_OK) {
-      bool direct = m.bound <= 2 * m.W + 64;
-      for (int attempt = 0; attempt < 2; ++attempt) {
-        if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, RENDER_MIN)) {
-          status = ST_INTERNAL;
-          report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
-          break;
-        }
+  }
+  DPHASE_MARK(0);
+  __syncthreads();
+  // -- P1: id tables + prescan (A15)
+  bool any_name = false;
+  if (status == ST_OK) {
+    direct = m.bound <= 2 * m.W + 64;
+    if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, RENDER_MIN)) {
+      status = ST_INTERNAL;
+      report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
+    } else {
+      init_tables(m);
+      any_name = prescan(m, T);
+    }
+  }
+  DPHASE_MARK(1);
+  __syncthreads();
+  // -- P2: classify (A8-A12) + referenced ids; an id at/above the bound redoes
+  //    P1+P2 with the hash table (rare: non-canonical modules)
+  if (status == ST_OK) {
+    names_mode = (a.opts & OPT_INLINE) && any_name;
+    classify(m, T);
+    if (names_mode) collect_ids(m);
+    if (*m.overflow && direct) {
+      __syncwarp();
+      direct = false;
+      if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, RENDER_MIN)) {
+        status = ST_INTERNAL;
+        report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
+      } else {
         init_tables(m);
-        const bool any_name = prescan(m, T);
-        const bool names_mode = (a.opts & OPT_INLINE) && any_name;
+        any_name = prescan(m, T);
+        names_mode = (a.opts & OPT_INLINE) && any_name;
         classify(m, T);
         if (names_mode) collect_ids(m);
-        if (*m.overflow) {   // an id at/above the bound: redo with the hash table
-          __syncwarp();
-          direct = false;
-          continue;
-        }
-        // --- exceptions, in the reference's evaluation order ---
-        uint32_t bad = first_where(m, [&](uint32_t i) { return (m.iflag[i] & IF_PRESCAN_UTF8) != 0; });
-        if (bad != NONE32) {
-          status = ST_UNICODE;
-          if (lane == 0) report_prescan_error(m, T, bad, es.alloc(), (int32_t)t);
-          break;
-        }
-        if (names_mode) {
-          bad = first_where(m, [&](uint32_t i) {
-            uint32_t e = m.ierr[i]; return m.idef[i] != NONE16 && e != W_OK && !werr_is_codec(e); });
-          if (bad != NONE32) {
-            if (lane == 0) report_inst_error(m, T, bad, es.alloc(), (int32_t)t, status);
-            status = __shfl_sync(FULL, status, 0);
-            break;
-          }
-        }
-        bad = first_where(m, [&](uint32_t i) {
-          return (m.idef[i] == NONE16 && (a.opts & OPT_STRICT)) || (m.idef[i] != NONE16 && m.ierr[i] != W_OK);
-        });
-        if (bad != NONE32) {
-          if (lane == 0) {
-            ErrRec* erec = es.alloc();
-            if (m.idef[bad] == NONE16) {
-              status = ST_CODEC;
-              if (erec) {
-                ErrWriter ew{erec};
-                put_cstr(ew, "unknown opcode "); put_u64(ew, inst_opcode(m, bad));
-                erec->module = (int32_t)t; erec->cls = ST_CODEC; erec->len = ew.n;
-              }
-            } else {
-              report_inst_error(m, T, bad, erec, (int32_t)t, status);
-            }
-          }
-          status = __shfl_sync(FULL, status, 0);
-          break;
-        }
-        if (names_mode) resolve_names(m, T);
-        width = result_refs(m, T);
-        if (a.opts & OPT_NO_INDENT) width = 0;
-        if (a.opts & OPT_GROUP) { compute_sections(m, T); mark_blanks(m); }
-        total = text_size(m, T, a.opts, width);
-        break;
       }
     }
-    // reserve the module's bytes (16-byte aligned starts) and write the text
+  }
+  DPHASE_MARK(2);
+  __syncthreads();
+  // -- P3: exceptions, in the reference's evaluation order
+  if (status == ST_OK) {
+    uint32_t bad = first_where(m, [&](uint32_t i) { return (m.iflag[i] & IF_PRESCAN_UTF8) != 0; });
+    if (bad != NONE32) {
+      status = ST_UNICODE;
+      if (lane == 0) report_prescan_error(m, T, bad, es.alloc(), (int32_t)t);
+    }
+    if (status == ST_OK && names_mode) {
+      bad = first_where(m, [&](uint32_t i) {
+        uint32_t e = m.ierr[i]; return m.idef[i] != NONE16 && e != W_OK && !werr_is_codec(e); });
+      if (bad != NONE32) {
+        if (lane == 0) report_inst_error(m, T, bad, es.alloc(), (int32_t)t, status);
+        status = __shfl_sync(FULL, status, 0);
+      }
+    }
+    if (status == ST_OK) {
+      bad = first_where(m, [&](uint32_t i) {
+        return (m.idef[i] == NONE16 && (a.opts & OPT_STRICT)) || (m.idef[i] != NONE16 && m.ierr[i] != W_OK);
+      });
+      if (bad != NONE32) {
+        if (lane == 0) {
+          ErrRec* erec = es.alloc();
+          if (m.idef[bad] == NONE16) {
+            status = ST_CODEC;
+            if (erec) {
+              ErrWriter ew{erec};
+              put_cstr(ew, "unknown opcode "); put_u64(ew, inst_opcode(m, bad));
+              erec->module = (int32_t)t; erec->cls = ST_CODEC; erec->len = ew.n;
+            }
+          } else {
+            report_inst_error(m, T, bad, erec, (int32_t)t, status);
+          }
+        }
+        status = __shfl_sync(FULL, status, 0);
+      }
+    }
+  }
+  DPHASE_MARK(3);
+  __syncthreads();
+  // -- P4: friendly names (A16)
+  if (status == ST_OK && names_mode) resolve_names(m, T);
+  DPHASE_MARK(4);
+  __syncthreads();
+  // -- P5: result refs, width, sections, text size (A17-A19)
+  if (status == ST_OK) {
+    width = result_refs(m, T);
+    if (a.opts & OPT_NO_INDENT) width = 0;
+    if (a.opts & OPT_GROUP) { compute_sections(m, T); mark_blanks(m); }
+    total = text_size(m, T, a.opts, width);
+  }
+  DPHASE_MARK(5);
+  __syncthreads();
+  // -- P6: reserve the module's bytes (16-byte aligned starts) and write the text
+  if (live) {
     if (status != ST_OK) total = 0;
     bool fits;
     uint64_t off = alloc_text(a.ticket, (total + 15) & ~15ull, a.text_cap, fits);
@@ -1085,7 +1132,27 @@ __global__ void __launch_bounds__(128) disasm_kernel(DisasmArgs a) {
       a.status[t] = status;
     }
     if (status == ST_OK && total > 0 && fits) text_write(m, T, a.opts, width, a.text + off);
-    __syncwarp();
+  }
+  DPHASE_MARK(6);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) disasm_kernel(DisasmArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_base;
+  const uint32_t warps = blockDim.x >> 5;
+  const uint32_t warp_in_block = threadIdx.x >> 5;
+  const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
+  uint8_t* slab = smem + (size_t)warp_in_block * a.smem_slab;
+  uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
+  ErrSink es{a.errs, a.ticket + 1, a.err_cap};
+  while (true) {
+    if (threadIdx.x == 0) s_base = atomicAdd(a.ticket, warps);
+    __syncthreads();
+    const uint32_t base = s_base;
+    __syncthreads();
+    if (base >= a.n_mod) break;
+    disasm_one(a, base + warp_in_block, slab, gslot, es);
   }
 }
 

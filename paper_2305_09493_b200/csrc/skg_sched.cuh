@@ -1,0 +1,78 @@
+// Module scheduling order: a device counting sort of module indices by size,
+// largest first.  The phase-synchronised kernels hand consecutive tickets to
+// the warps of one CTA, and a CTA waits at every phase barrier for its slowest
+// module; sorting by size makes the modules of one CTA similar in size (and
+// puts the largest first, so the tail of the grid is filled by small ones).
+// Only the processing order changes: outputs are addressed by module index.
+#pragma once
+#include <cstdint>
+
+namespace skg {
+
+constexpr uint32_t SCHED_BUCKETS = 1024;
+constexpr uint32_t SCHED_SHIFT = 6;        // 64-byte size classes
+
+__device__ __forceinline__ uint32_t sched_bucket(int64_t len) {
+  const uint64_t c = len <= 0 ? 0 : ((uint64_t)len >> SCHED_SHIFT);
+  return SCHED_BUCKETS - 1 - (uint32_t)(c < SCHED_BUCKETS - 1 ? c : SCHED_BUCKETS - 1);
+}
+
+// hist[b] += number of modules in bucket b
+__global__ void __launch_bounds__(1024) sched_hist(const int64_t* len, uint32_t stride, uint32_t n,
+                                                   uint32_t* hist) {
+  __shared__ uint32_t h[SCHED_BUCKETS];
+  for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[sched_bucket(len[(size_t)i * stride])], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+// cursor = exclusive scan of hist (one CTA of SCHED_BUCKETS threads)
+__global__ void __launch_bounds__(1024) sched_scan(const uint32_t* hist, uint32_t* cursor) {
+  __shared__ uint32_t wsum[32];
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t v = hist[t];
+  uint32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, d);
+      if (lane >= (uint32_t)d) s += y;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  cursor[t] = x - v + (warp ? wsum[warp - 1] : 0);
+}
+
+// perm[cursor[b]++] = i; each CTA owns a contiguous chunk of module indices
+__global__ void __launch_bounds__(1024) sched_scatter(const int64_t* len, uint32_t stride, uint32_t n,
+                                                      uint32_t* cursor, uint32_t* perm) {
+  __shared__ uint32_t h[SCHED_BUCKETS];
+  const uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[sched_bucket(len[(size_t)i * stride])], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x)
+    if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);
+  __syncthreads();
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint32_t b = sched_bucket(len[(size_t)i * stride]);
+    perm[atomicAdd(&h[b], 1u)] = i;
+  }
+}
+
+}  // namespace skg
