@@ -83,7 +83,10 @@ int env_int(const char* name, int dflt) {
 // disassembler: phase-synchronised CTAs of kDisWarps warps (one module per warp),
 // one CTA per SM, kDisSlab bytes of shared memory per warp
 int kDisWarps = env_int("SKG_DIS_WARPS", 32);
-uint32_t kDisSlab = (uint32_t)env_int("SKG_DIS_SLAB", 6912);
+uint32_t kDisStage = (uint32_t)env_int("SKG_DIS_STAGE", 1024);
+// module slab in shared memory (default 0: all module scratch in the per-warp
+// global slot -- measured faster, the L1 that the carve-out leaves caches it)
+uint32_t kDisSlab = (uint32_t)env_int("SKG_DIS_SLAB", 0);
 uint32_t dis_blocks() { return (uint32_t)sm_count() * env_int("SKG_DIS_BLOCKS_PER_SM", 1); }
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
@@ -210,7 +213,8 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   a.smem_slab = kDisSlab;
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
-  const size_t smem = (size_t)kDisSlab * kDisWarps;
+  a.stage_bytes = kDisStage;
+  const size_t smem = (size_t)(kDisSlab + kDisStage) * kDisWarps;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -24,7 +24,7 @@ __device__ const char* const ANSI_STRING = "\x1b[32m";
 __device__ const char* const ANSI_COMMENT = "\x1b[90m";
 __device__ const char* const ANSI_RESET = "\x1b[0m";
 
-constexpr uint32_t RENDER_MIN = 2048;   // minimum work region (text stage)
+constexpr uint32_t RENDER_MIN = 0;      // the text stage is separate shared memory
 
 struct DisasmArgs {
   Tables T;
@@ -42,7 +42,8 @@ struct DisasmArgs {
   uint32_t err_cap;
   uint8_t* gscratch;          // per-warp global slots
   uint64_t gslot_bytes;
-  uint32_t smem_slab;         // bytes per warp in dynamic shared memory
+  uint32_t smem_slab;         // bytes per warp in dynamic shared memory (module scratch)
+  uint32_t stage_bytes;       // bytes per warp of text stage (dynamic shared memory, first)
   const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
 };
 
@@ -85,33 +86,21 @@ __device__ inline void for_sanitized(const NameView& nv, F&& f) {
   }
 }
 
-// -- ref rendering -------------------------------------------------------------
-template <class S>
-__device__ __noinline__ void put_ref(S& s, const Mod& m, uint32_t id) {
-  s.put('%');
-  uint32_t slot = ht_find(m, id);
-  if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
-    NameView nv = name_of(m, m.hname[slot]);
-    for_sanitized(nv, [&](uint32_t c) { s.put((uint8_t)c); });
-    if (m.hser[slot] != NONE32) { s.put('_'); put_u64(s, m.hser[slot]); }
-    return;
-  }
-  put_u64(s, id);
+// -- ref lengths ----------------------------------------------------------------
+// friendly ids render as '%' + sanitized base (narena) + ['_' + serial]
+__device__ __forceinline__ uint32_t dlen32(uint32_t v) {
+  return v < 10 ? 1 : v < 100 ? 2 : v < 1000 ? 3 : v < 10000 ? 4 : v < 100000 ? 5 :
+         v < 1000000 ? 6 : v < 10000000 ? 7 : v < 100000000 ? 8 : v < 1000000000 ? 9 : 10;
 }
 
-
-__device__ __noinline__ uint32_t ref_len(const Mod& m, uint32_t id) {
-  uint32_t slot = ht_find(m, id);
+__device__ __forceinline__ uint32_t ref_len(const Mod& m, uint32_t id) {
+  const uint32_t slot = ht_find(m, id);
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
-    if (m.hrl[slot] != 0xFFFF) return m.hrl[slot];
-    uint32_t n = 1;
-    for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t) { ++n; });
-    if (m.hser[slot] != NONE32) n += 1 + dec_len_u64(m.hser[slot]);
-    return n;
+    const uint32_t ser = m.hser[slot];
+    return 1 + m.nLen[slot] + (ser != NONE32 ? 1 + dlen32(ser) : 0);
   }
-  return 1 + dec_len_u64(id);
+  return 1 + dlen32(id);
 }
-
 
 __device__ __noinline__ bool is_opencl_std(const Mod& m, const Tables& T, uint32_t set_id) {
   uint32_t s = ht_find(m, set_id);
@@ -360,45 +349,92 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     }
   }
   __syncwarp();
-  if (lane == 0) {
-    auto child_of = [&](uint32_t g, uint32_t s) -> uint32_t {
-      #pragma unroll 1
-      for (uint32_t q = 0; q < nd; ++q)
-        if (m.ib[q] == g && m.ia[q] == s) return q;
-      return NONE32;
-    };
+  // child entries (parent group, suffix value, child leader), compacted into the
+  // spill area so the sequential pass finds a child with one ballot per 32
+  uint32_t nc = 0;
+  uint32_t* clist = reinterpret_cast<uint32_t*>(m.spill);
+  #pragma unroll 1
+  for (uint32_t base = 0; base < nd; base += 32) {
+    const uint32_t k = base + lane;
+    const bool isc = k < nd && m.ib[k] != NONE32;
+    const unsigned b = __ballot_sync(FULL, isc);
+    if (isc) {
+      const uint32_t at = nc + __popc(b & ((1u << lane) - 1));
+      clist[3 * at] = m.ib[k]; clist[3 * at + 1] = m.ia[k]; clist[3 * at + 2] = k;
+    }
+    nc += __popc(b);
+  }
+  __syncwarp();
+  const uint32_t c_g = lane < nc ? clist[3 * lane] : NONE32;
+  const uint32_t c_n = lane < nc ? clist[3 * lane + 1] : 0;
+  const uint32_t c_k = lane < nc ? clist[3 * lane + 2] : 0;
+  auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
+    unsigned b = __ballot_sync(FULL, c_g == g && c_n == sv);
+    if (b) return __shfl_sync(FULL, c_k, __ffs(b) - 1);
     #pragma unroll 1
-    for (uint32_t k = 0; k < nd; ++k) {
-      const uint32_t g = (uint32_t)m.pos[k];
-      const uint32_t gs = m.ndl[g];
-      if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
+    for (uint32_t base = 32; base < nc; base += 32) {   // more than 32 child groups
+      const uint32_t q = base + lane;
+      b = __ballot_sync(FULL, q < nc && clist[3 * q] == g && clist[3 * q + 1] == sv);
+      if (b) return clist[3 * (base + __ffs(b) - 1) + 2];
+    }
+    return NONE32;
+  };
+  // the sequential pass in D order, run by the whole warp (uniform control flow;
+  // lane 0 writes); 32 idents' (leader, leader slot, slot) preloaded per round
+  #pragma unroll 1
+  for (uint32_t base = 0; base < nd; base += 32) {
+    const uint32_t kk = base + lane;
+    const uint32_t my_g = kk < nd ? (uint32_t)m.pos[kk] : 0;
+    const uint32_t my_gs = kk < nd ? m.ndl[my_g] : 0;
+    const uint32_t my_s = kk < nd ? m.ndl[kk] : 0;
+    const uint32_t cnt = min(32u, nd - base);
+    #pragma unroll 1
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint32_t k = base + j;
+      const uint32_t g = __shfl_sync(FULL, my_g, j);
+      const uint32_t gs = __shfl_sync(FULL, my_gs, j);
+      const uint32_t ks = __shfl_sync(FULL, my_s, j);
+      if (g == k && lane == 0) m.nP[gs] = 0;            // group counter (nP no longer needed)
+      __syncwarp();
       uint32_t serial = NONE32;
-      if (!(m.hfl[gs] & HF_TB)) {
-        m.hfl[gs] |= HF_TB;
+      const uint8_t fl = m.hfl[gs];
+      if (!(fl & HF_TB)) {
+        if (lane == 0) m.hfl[gs] = fl | HF_TB;
       } else {
         uint32_t sv = m.nP[gs];
-        if (m.hfl[gs] & HF_HASCHILD) {
+        if (fl & HF_HASCHILD) {
           uint32_t c;
           #pragma unroll 1
           while ((c = child_of(g, sv)) != NONE32 && (m.hfl[m.ndl[c]] & HF_TB)) ++sv;
-          if (c != NONE32) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
+          if (c != NONE32 && lane == 0) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
         }
         serial = sv;
-        m.nP[gs] = sv + 1;
+        if (lane == 0) m.nP[gs] = sv + 1;
       }
-      m.hser[m.ndl[k]] = serial;
+      if (lane == 0) m.hser[ks] = serial;
+      __syncwarp();
     }
   }
   __syncwarp();
-  // 5. friendly = named definition that keeps its number; cache its ref length
+  // 5. friendly = named definition that keeps its number; its sanitized base
+  //    name goes into the module's name arena once (refs copy it from there)
+  uint32_t acarry = 0;
   #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    uint32_t slot = m.ndl[k];
-    if (m.hfl[slot] & HF_KEPT) {
+  for (uint32_t base = 0; base < nd; base += 32) {
+    const uint32_t k = base + lane;
+    const uint32_t slot = k < nd ? m.ndl[k] : 0;
+    const bool kept = k < nd && (m.hfl[slot] & HF_KEPT);
+    const uint32_t len = kept ? m.nLen[slot] : 0;
+    const uint32_t incl = warp_incl_sum(len);
+    if (kept) {
       m.hfl[slot] |= HF_FRIENDLY;
-      uint32_t rl = 1 + cand_len(m, slot, m.hser[slot]);
-      m.hrl[slot] = (uint16_t)(rl > 0xFFFF ? 0xFFFF : rl);
+      const uint32_t off = acarry + incl - len;
+      m.hnoff[slot] = off;
+      uint8_t* dst = m.narena + off;
+      uint32_t q = 0;
+      for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t c) { dst[q++] = (uint8_t)c; });
     }
+    acarry += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
 }
@@ -473,26 +509,7 @@ __device__ inline void flush_stage(uint8_t* g0, uint8_t* g1, const uint8_t* stag
   const uint4* s4 = reinterpret_cast<const uint4*>(src + (m0 - a0));
   uint4* d4 = reinterpret_cast<uint4*>(m0);
   #pragma unroll 1
-  for (uint32_t k = lane; k < nb; k += 32) d4[k] = s4[k];
-}
-
-
-// one text line (with its optional preceding blank line) into sink-space at `lo`
-template <class S>
-__device__ __noinline__ void write_line(S& ms, const Mod& m, const Tables& T, uint32_t i, uint32_t width,
-                                  bool hl) {
-  if (m.iflag[i] & IF_HAS_RESULT) {
-    uint32_t rl = m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i];
-    if (width) ms.fill(' ', width - rl);
-    if (hl) put_cstr(ms, ANSI_ID);
-    put_ref(ms, m, m.ib[i]);
-    if (hl) put_cstr(ms, ANSI_RESET);
-    put_cstr(ms, " = ");
-  } else if (width) {
-    ms.fill(' ', width + 3);
-  }
-  render_body(ms, m, T, i, hl, (m.iflag[i] & IF_EXT_KNOWN) != 0);
-  ms.put('\n');
+  for (uint32_t k = lane; k < nb; k += 32) __stcs(d4 + k, s4[k]);   // streaming: keep L2 for scratch
 }
 
 
@@ -604,10 +621,6 @@ __device__ __noinline__ void collect_ids(Mod& m) {
 
 // ---------------------------------------------------------------------------
 // Per-word length (arithmetic only) and emission (register-resident pointer).
-__device__ __forceinline__ uint32_t dlen32(uint32_t v) {
-  return v < 10 ? 1 : v < 100 ? 2 : v < 1000 ? 3 : v < 10000 ? 4 : v < 100000 ? 5 :
-         v < 1000000 ? 6 : v < 10000000 ? 7 : v < 100000000 ? 8 : v < 1000000000 ? 9 : 10;
-}
 __device__ __forceinline__ uint8_t* emit_u32(uint8_t* p, uint32_t v) {
   uint8_t* e = p + dlen32(v);
   uint8_t* q = e;
@@ -631,9 +644,13 @@ __device__ __noinline__ uint8_t* emit_ref(uint8_t* p, const Mod& m, uint32_t id)
   *p++ = '%';
   const uint32_t slot = ht_find(m, id);
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
-    const NameView nv = name_of(m, m.hname[slot]);
-    for_sanitized(nv, [&](uint32_t c) { *p++ = (uint8_t)c; });
-    if (m.hser[slot] != NONE32) { *p++ = '_'; p = emit_u32(p, m.hser[slot]); }
+    const uint8_t* src = m.narena + m.hnoff[slot];
+    const uint32_t n = m.nLen[slot];
+#pragma unroll 1
+    for (uint32_t q = 0; q < n; ++q) p[q] = src[q];
+    p += n;
+    const uint32_t ser = m.hser[slot];
+    if (ser != NONE32) { *p++ = '_'; p = emit_u32(p, ser); }
     return p;
   }
   return emit_u32(p, id);
@@ -893,7 +910,11 @@ __device__ __noinline__ void mark_blanks(Mod& m) {
 __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32_t opts, uint32_t width) {
   const bool hl = opts & OPT_HIGHLIGHT;
   uint32_t sum = 0;
-  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) sum += word_len(m, T, w, m.wk[w], width, hl);
+  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) {
+    const uint32_t l = word_len(m, T, w, m.wk[w], width, hl);
+    m.wl[w] = (uint16_t)(l > 0xFFFF ? 0xFFFF : l);   // 0xFFFF: recompute (huge names only)
+    sum += l;
+  }
   uint64_t total = warp_sum_u32(sum);
   if (!(opts & OPT_NO_HEADER)) {
     Sink hs;
@@ -903,43 +924,54 @@ __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32
   return total;
 }
 
-// write the module text at `out` (16-byte aligned) through the shared stage:
-// per 32-word chunk the stage is pre-filled with spaces (so indentation costs
-// nothing), every lane emits its word at its scanned offset, and the chunk is
-// flushed with 16-byte stores.
+// Write the module text at `out` (16-byte aligned) through the warp's shared
+// stage.  Each window takes the longest run of the next 32 words whose text
+// fits the stage: the stage is pre-filled with spaces (indentation costs
+// nothing), every lane emits its word at its scanned offset (lengths from the
+// size pass), and the window is flushed with 16-byte stores.  A word too long
+// for the stage on its own is written straight to global memory.
 __device__ __noinline__ void text_write(const Mod& m, const Tables& T, uint32_t opts, uint32_t width,
-                                        uint8_t* out) {
+                                        uint8_t* out, uint8_t* stage, uint32_t cap) {
   const uint32_t lane = lane_id();
   const bool hl = opts & OPT_HIGHLIGHT;
   uint64_t pos = 0;
-  if (!(opts & OPT_NO_HEADER)) {
-    Sink hs;
-    put_header(hs, m, hl);
-    if (lane == 0) { Sink ms(out); put_header(ms, m, hl); }
-    pos = hs.n;
-  }
-  uint8_t* stage = m.work_shared ? m.work : nullptr;
-  const uint32_t cap = m.work_shared ? m.work_bytes : 0;
   const uint4 sp4 = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
-  for (uint32_t base = 5; base < m.W; base += 32) {
-    const uint32_t w = base + lane;
+  if (!(opts & OPT_NO_HEADER)) {
+    if (lane == 0) { Sink ms(stage); put_header(ms, m, hl); pos = ms.n; }
+    pos = __shfl_sync(FULL, pos, 0);
+    __syncwarp();
+    flush_stage(out, out + pos, stage);
+    __syncwarp();
+  }
+  uint32_t w0 = 5;
+  while (w0 < m.W) {
+    const uint32_t w = w0 + lane;
     uint32_t x = 0, len = 0;
-    if (w < m.W) { x = m.wk[w]; len = word_len(m, T, w, x, width, hl); }
-    const uint32_t incl = warp_incl_sum(len);
-    const uint32_t chunk = __shfl_sync(FULL, incl, 31);
-    const uint32_t shift = (uint32_t)(reinterpret_cast<uintptr_t>(out + pos) & 15);
-    if (shift + chunk <= cap) {
-      const uint32_t n16 = (shift + chunk + 15) >> 4;
-      for (uint32_t k = lane; k < n16; k += 32) reinterpret_cast<uint4*>(stage)[k] = sp4;
-      __syncwarp();
-      if (len) word_emit(stage + shift + incl - len, m, T, w, x, width, hl, true);
-      __syncwarp();
-      flush_stage(out + pos, out + pos + chunk, stage);
-      __syncwarp();
-    } else if (len) {
-      word_emit(out + pos + incl - len, m, T, w, x, width, hl, false);
+    if (w < m.W) {
+      x = m.wk[w];
+      len = m.wl[w];
+      if (len == 0xFFFF) len = word_len(m, T, w, x, width, hl);
     }
+    const uint32_t incl = warp_incl_sum(len);
+    const uint32_t shift = (uint32_t)(reinterpret_cast<uintptr_t>(out + pos) & 15);
+    const uint32_t take = __popc(__ballot_sync(FULL, w < m.W && shift + incl <= cap));
+    if (take == 0) {   // one word longer than the stage
+      if (lane == 0) word_emit(out + pos, m, T, w, x, width, hl, false);
+      __syncwarp();
+      pos += __shfl_sync(FULL, len, 0);
+      w0 += 1;
+      continue;
+    }
+    const uint32_t chunk = __shfl_sync(FULL, incl, take - 1);
+    const uint32_t n16 = (shift + chunk + 15) >> 4;
+    for (uint32_t k = lane; k < n16; k += 32) reinterpret_cast<uint4*>(stage)[k] = sp4;
+    __syncwarp();
+    if (lane < take && len) word_emit(stage + shift + incl - len, m, T, w, x, width, hl, true);
+    __syncwarp();
+    flush_stage(out + pos, out + pos + chunk, stage);
+    __syncwarp();
     pos += chunk;
+    w0 += take;
   }
 }
 
@@ -1005,7 +1037,7 @@ __device__ unsigned long long g_dis_phase[16];
 // time (CTA barrier between phases), so the instruction working set of the SM
 // is one phase rather than the whole program.
 __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
-                                        ErrSink& es) {
+                                        uint8_t* stage, ErrSink& es) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   DPHASE_START();
@@ -1131,7 +1163,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
       a.text_span[2 * t + 1] = (int64_t)total;
       a.status[t] = status;
     }
-    if (status == ST_OK && total > 0 && fits) text_write(m, T, a.opts, width, a.text + off);
+    if (status == ST_OK && total > 0 && fits) text_write(m, T, a.opts, width, a.text + off, stage, a.stage_bytes);
   }
   DPHASE_MARK(6);
   __syncthreads();
@@ -1143,7 +1175,8 @@ __global__ void __launch_bounds__(1024) disasm_kernel(DisasmArgs a) {
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
-  uint8_t* slab = smem + (size_t)warp_in_block * a.smem_slab;
+  uint8_t* stage = smem + (size_t)warp_in_block * a.stage_bytes;
+  uint8_t* slab = smem + (size_t)warps * a.stage_bytes + (size_t)warp_in_block * a.smem_slab;
   uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
   ErrSink es{a.errs, a.ticket + 1, a.err_cap};
   while (true) {
@@ -1152,7 +1185,7 @@ __global__ void __launch_bounds__(1024) disasm_kernel(DisasmArgs a) {
     const uint32_t base = s_base;
     __syncthreads();
     if (base >= a.n_mod) break;
-    disasm_one(a, base + warp_in_block, slab, gslot, es);
+    disasm_one(a, base + warp_in_block, slab, gslot, stage, es);
   }
 }
 

@@ -57,6 +57,7 @@ struct Mod {
   uint32_t* ib;
   uint16_t* irl;
   uint32_t* wk;           // per word render code (disassembler)
+  uint16_t* wl;           // per word text length (disassembler size pass)
   // per id "slot": direct mode slot = id (ids < bound, the canonical case);
   // hash mode (any id >= bound seen): open addressing over hkey, slot C holds 0xFFFFFFFF
   bool direct;
@@ -73,6 +74,9 @@ struct Mod {
   uint32_t* nP;
   uint32_t* nLen;
   uint32_t* ndl;          // named definitions in D order (slots)
+  uint32_t* hnoff;        // friendly: offset of the sanitized base name in narena
+  uint8_t* narena;        // sanitized base names of friendly ids (disassembler)
+  uint32_t arena_need;    // bound on narena bytes: sum over OpName of 4 * string words + 1
   int32_t* pos;           // closed-form demotion scan, S + 2 entries
   uint16_t* hrl;          // friendly ref length
   uint8_t* hA;            // referenced by a decodable instruction
@@ -102,13 +106,13 @@ __host__ __device__ inline size_t head_used(uint32_t W, uint32_t I) {
 __host__ __device__ inline size_t inst_bytes(uint32_t I) {
   return align16(2ull * I) + 3 * align16(1ull * I) + 2 * align16(4ull * I) + align16(2ull * I);
 }
-__host__ __device__ inline size_t word_bytes(uint32_t W) { return align16(4ull * W); }
+__host__ __device__ inline size_t word_bytes(uint32_t W) { return align16(4ull * W) + align16(2ull * W); }
 __host__ __device__ inline size_t slot_bytes(uint32_t S, bool hash) {
   return (hash ? align16(4ull * S) : 0) + 6 * align16(4ull * S) + align16(2ull * S) +
          3 * align16(1ull * S);
 }
 __host__ __device__ inline size_t names_bytes(uint32_t S) {
-  return 4 * align16(4ull * S) + align16(4ull * (S + 2));
+  return 5 * align16(4ull * S) + align16(4ull * (S + 2));
 }
 __host__ __device__ inline size_t spill_bytes(uint32_t I) { return 32ull * I + 64; }
 __host__ __device__ inline uint32_t hash_capacity(uint32_t W) {
@@ -116,16 +120,16 @@ __host__ __device__ inline uint32_t hash_capacity(uint32_t W) {
   while (C < 2 * W + 8) C <<= 1;
   return C;
 }
-__host__ __device__ inline size_t work_need(uint32_t S, size_t work_min) {
-  size_t nb = names_bytes(S);
+__host__ __device__ inline size_t work_need(uint32_t S, size_t work_min, size_t arena) {
+  size_t nb = names_bytes(S) + align16(arena);
   return nb > work_min ? nb : work_min;
 }
 // worst case for a module of W words: hash mode in the global slot
 __host__ __device__ inline size_t worst_bytes(uint32_t W, size_t work_min) {
   uint32_t I = W > 5 ? W - 5 : 0;
   uint32_t S = hash_capacity(W) + 1;
-  return head_bytes(W) + inst_bytes(I) + word_bytes(W) + slot_bytes(S, true) + work_need(S, work_min) +
-         spill_bytes(I);
+  return head_bytes(W) + inst_bytes(I) + word_bytes(W) + slot_bytes(S, true) +
+         work_need(S, work_min, 5ull * W) + spill_bytes(I);
 }
 
 __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
@@ -141,7 +145,7 @@ __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
 __device__ inline size_t tables_need(const Mod& m, bool direct, uint32_t S_or_C, size_t work_min) {
   const uint32_t S = direct ? S_or_C : S_or_C + 1;
   return head_used(m.W, m.I) + inst_bytes(m.I) + word_bytes(m.W) + slot_bytes(S, !direct) +
-         work_need(S, work_min);
+         work_need(S, work_min, m.arena_need);
 }
 
 // lay out per-instruction, per-slot and work arrays after the instruction offsets
@@ -158,6 +162,7 @@ __device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_
   m.ib = reinterpret_cast<uint32_t*>(take(4ull * I));
   m.irl = reinterpret_cast<uint16_t*>(take(2ull * I));
   m.wk = reinterpret_cast<uint32_t*>(take(4ull * m.W));
+  m.wl = reinterpret_cast<uint16_t*>(take(2ull * m.W));
   m.direct = direct;
   if (direct) {
     m.S = S_or_C; m.C = 0; m.shift = 0; m.hkey = nullptr;
@@ -183,7 +188,7 @@ __device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_
   // the render workspace reuses the same bytes afterwards
   m.work = p;
   const size_t used = (size_t)(p - m.base);
-  size_t wb = work_need(S, work_min);
+  size_t wb = work_need(S, work_min, m.arena_need);
   if (region_bytes > used + wb) wb = region_bytes - used;
   m.work_bytes = (uint32_t)wb;
   m.nH = reinterpret_cast<uint32_t*>(take(4ull * S));
@@ -191,6 +196,8 @@ __device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_
   m.nLen = reinterpret_cast<uint32_t*>(take(4ull * S));
   m.ndl = reinterpret_cast<uint32_t*>(take(4ull * S));
   m.pos = reinterpret_cast<int32_t*>(take(4ull * (S + 2)));
+  m.hnoff = reinterpret_cast<uint32_t*>(take(4ull * S));
+  m.narena = take(m.arena_need);
 }
 
 // -- warp helpers -------------------------------------------------------------
@@ -395,7 +402,7 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(m.w);
     const uint32_t n4 = W / 4;
-    for (uint32_t k = lane; k < n4; k += 32) d4[k] = __ldg(s4 + k);
+    for (uint32_t k = lane; k < n4; k += 32) d4[k] = __ldcs(s4 + k);   // read once: evict first
     for (uint32_t k = n4 * 4 + lane; k < W; k += 32) m.w[k] = __ldg(reinterpret_cast<const uint32_t*>(src) + k);
   } else {
     for (uint32_t k = lane; k < W; k += 32) {
@@ -425,13 +432,15 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
   m.schema = m.w[4];
   // instruction-boundary walk (pointer chase: pos += wc)
   int32_t st = ST_OK;
-  uint32_t I = 0, bad = 0;
+  uint32_t I = 0, bad = 0, arena = 0;
   if (lane == 0) {
     uint32_t p = 5;
     while (p < W) {
-      uint32_t wc = m.w[p] >> 16;
+      const uint32_t x = m.w[p];
+      const uint32_t wc = x >> 16;
       if (wc == 0) { st = ST_CORRUPT; bad = p; break; }
       if (p + wc > W) { st = ST_TRUNCATED; bad = p; break; }
+      if ((x & 0xFFFF) == 5 && wc > 2) arena += 4 * (wc - 2) + 1;   // OpName: sanitized name bound
       m.ioff[I++] = p;
       p += wc;
     }
@@ -445,6 +454,7 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
   }
   st = __shfl_sync(FULL, st, 0);
   m.I = __shfl_sync(FULL, I, 0);
+  m.arena_need = __shfl_sync(FULL, arena, 0);
   __syncwarp();
   return st;
 }
@@ -467,7 +477,7 @@ __device__ inline void move_to_global(Mod& m, uint8_t* gslot) {
   layout_head(g, gslot, m.W);
   for (uint32_t k = lane_id(); k < m.W; k += 32) g.w[k] = m.w[k];
   for (uint32_t k = lane_id(); k < m.I; k += 32) g.ioff[k] = m.ioff[k];
-  g.I = m.I; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
+  g.I = m.I; g.arena_need = m.arena_need; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
   __syncwarp();
   m = g;
 }
