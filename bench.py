@@ -16,7 +16,8 @@ Extra keys: roofline (HBM; algorithmic bytes 4W+T per launch for either
 kernel; the dominant kernel is reported, both are listed), cpu_baseline (the
 reference's own CPU implementation, oracle/_ref, timed on this box's host cores
 on a bounded sample), e2e (host buffers through RoundTripSession: pinned H2D of
-the binaries + both kernels + D2H of the text and the binaries), gpu_launches,
+the binaries + both kernels + D2H of the text and the binaries, pipelined over
+8 module chunks on three streams), gpu_launches,
 clocks.
 
 ``--impl reference`` times the reference's CPU implementation instead (rank 0
@@ -315,7 +316,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": total_words / e2e_s, "unit": "words/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "paper_2305_09493_b200.asm.RoundTripSession.run_staged"},
-        "gpu_launches": 2 * args.steps,
+        # per step: skg_disasm + skg_asm, each = 3 scheduling kernels (size sort) + the main kernel
+        "gpu_launches": 8 * args.steps,
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -292,14 +292,17 @@ class DisasmPlan:
     """
 
     def __init__(self, batch: DeviceBatch, opts: int, spec=None, ext=None, text_cap=None,
-                 kind: str = "disasm"):
+                 kind: str = "disasm", ws=None):
         torch = _torch()
         self.kind = kind
         self.batch, self.opts = batch, opts
         self.th = tables_handle(spec, ext)
         n = batch.n
         self.ws_bytes = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        if ws is not None and ws.numel() >= self.ws_bytes:   # shared by plans launched in order
+            self.ws = ws
+        else:
+            self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.cap = text_cap if text_cap is not None else 6 * batch.total_bytes + 4096
         self.text = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
         self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
@@ -378,7 +381,7 @@ class AsmPlan:
     """Device buffers for repeated skg_asm launches over one resident text batch."""
 
     def __init__(self, batch: DeviceBatch, spec=None, ext=None, out_cap=None, slot_bytes=None,
-                 default_version=(1, 2), stride=1):
+                 default_version=(1, 2), stride=1, ws=None):
         torch = _torch()
         L = _bind_asm(lib())
         self.batch = batch
@@ -388,7 +391,10 @@ class AsmPlan:
         max_len = int(batch.max_words) * 4 + 16
         self.slot = int(slot_bytes or L.skg_asm_slot_hint(max_len))
         self.ws_bytes = int(L.skg_asm_workspace_bytes(self.slot, max(n, 1)))
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
+        if ws is not None and ws.numel() >= self.ws_bytes:   # shared by plans launched in order
+            self.ws = ws
+        else:
+            self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.cap = int(out_cap or (batch.total_bytes + 64 * n + 4096))
         self.out = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
         self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")

@@ -2232,7 +2232,11 @@ end_i:
   CTA_SYNC();
 }
 
-__global__ void __launch_bounds__(1024) asm_kernel(AsmArgs a) {
+#ifndef SKG_ASM_MAXT
+#define SKG_ASM_MAXT 1024
+#define SKG_ASM_MINB 1
+#endif
+__global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs a) {
   __shared__ uint32_t s_base;
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5);

@@ -1169,7 +1169,11 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) disasm_kernel(DisasmArgs a) {
+#ifndef SKG_DIS_MAXT
+#define SKG_DIS_MAXT 1024
+#define SKG_DIS_MINB 1
+#endif
+__global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(DisasmArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_base;
   const uint32_t warps = blockDim.x >> 5;

@@ -181,3 +181,26 @@ def test_asm_edge_cases_vs_oracle(sk):
         if not same(_outcome(g), want):
             bad.append((t[:200], _outcome(g), want))
     assert not bad, bad
+
+
+def test_roundtrip_session_pipelined(sk):
+    """RoundTripSession: chunked 3-stream pipeline; text == oracle, binaries == inputs."""
+    import numpy as np
+    from oracle import disasm as odis
+    from paper_2305_09493_b200.asm import RoundTripSession
+    from synth.families import sample_batch
+    b = sample_batch(3000, 300, 7)
+    for chunks in (1, 5):
+        sess = RoundTripSession(chunks=chunks)
+        sess.stage(b.data, b.offsets, b.lengths)
+        for _ in range(2):
+            text, tspan, tst, binv, bspan, bst = sess.run_staged()
+            assert (tst == 0).all() and (bst == 0).all()
+            assert (bspan[:, 1] == b.lengths).all()
+            for i in range(0, b.n, 37):
+                m = b.module(i)
+                assert binv[bspan[i, 0]:bspan[i, 0] + bspan[i, 1]].tobytes() == m
+                t = text[tspan[i, 0]:tspan[i, 0] + tspan[i, 1]].tobytes().decode()
+                if i % 111 == 0:
+                    assert t == odis.disassemble(m)
+        assert int(np.sum(tspan[:, 1])) <= len(text)
