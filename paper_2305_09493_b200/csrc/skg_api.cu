@@ -87,7 +87,17 @@ uint32_t kDisStage = (uint32_t)env_int("SKG_DIS_STAGE", 1024);
 // module slab in shared memory (default 0: all module scratch in the per-warp
 // global slot -- measured faster, the L1 that the carve-out leaves caches it)
 uint32_t kDisSlab = (uint32_t)env_int("SKG_DIS_SLAB", 0);
-uint32_t dis_blocks() { return (uint32_t)sm_count() * env_int("SKG_DIS_BLOCKS_PER_SM", 1); }
+uint32_t dis_blocks() {
+  const int g = env_int("SKG_DIS_GRID", 0);   // experiments: explicit grid
+  return g > 0 ? (uint32_t)g : (uint32_t)sm_count() * env_int("SKG_DIS_BLOCKS_PER_SM", 1);
+}
+
+// warps per named-barrier group: a divisor of the CTA's warps, at most 15 groups
+uint32_t group_warps(int warps, int want) {
+  int g = want < 1 ? 1 : (want > warps ? warps : want);
+  while (warps % g || warps / g > 15) ++g;
+  return (uint32_t)g;
+}
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
@@ -214,6 +224,7 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   a.stage_bytes = kDisStage;
+  a.group_warps = group_warps(kDisWarps, env_int("SKG_DIS_GROUP", kDisWarps));
   const size_t smem = (size_t)(kDisSlab + kDisStage) * kDisWarps;
   static bool attr = false;
   if (!attr) {
@@ -261,7 +272,10 @@ uint64_t skg_asm_slot_hint(uint64_t max_text_bytes) {
 
 // assembler: phase-synchronised CTAs of kAsmWarps warps (one module per warp), 2 per SM
 int kAsmWarps = env_int("SKG_ASM_WARPS", 32);
-uint32_t asm_blocks() { return (uint32_t)sm_count() * env_int("SKG_ASM_BLOCKS_PER_SM", 1); }
+uint32_t asm_blocks() {
+  const int g = env_int("SKG_ASM_GRID", 0);   // experiments: explicit grid
+  return g > 0 ? (uint32_t)g : (uint32_t)sm_count() * env_int("SKG_ASM_BLOCKS_PER_SM", 1);
+}
 
 uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes, uint32_t n_mod) {
   return 256 + sched_bytes(n_mod) + (uint64_t)asm_blocks() * kAsmWarps * slot_bytes;
@@ -289,6 +303,7 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.gscratch = ws + 256 + sched_bytes(n_mod);
   a.gslot_bytes = slot_bytes;
   a.default_version = default_version;
+  a.group_warps = group_warps(kAsmWarps, env_int("SKG_ASM_GROUP", kAsmWarps));
   skg::asm_kernel<<<asm_blocks(), 32 * kAsmWarps, 0, s>>>(a);
   return check(cudaGetLastError());
 }

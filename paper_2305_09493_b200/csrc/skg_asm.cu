@@ -54,6 +54,7 @@ struct AsmArgs {
   uint64_t gslot_bytes;
   uint32_t default_version;   // major << 16 | minor
   const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
+  uint32_t group_warps;       // warps per phase-barrier group (divides the CTA's warps)
 };
 
 // token: off (text byte offset), lenf = len | TK_STR
@@ -159,15 +160,29 @@ __device__ __forceinline__ uint32_t wmin(uint32_t v) {
 }
 
 // one out-of-line copy each: these run at many call sites (instruction-cache footprint)
+// byte loops unrolled by 4 so the four loads are in flight together (latency bound)
 __device__ __noinline__ uint32_t fnv(const uint8_t* p, uint32_t n, uint32_t h = 2166136261u) {
+  uint32_t i = 0;
 #pragma unroll 1
-  for (uint32_t i = 0; i < n; ++i) h = (h ^ p[i]) * 16777619u;
+  for (; i + 4 <= n; i += 4) {
+    const uint32_t b0 = p[i], b1 = p[i + 1], b2 = p[i + 2], b3 = p[i + 3];
+    h = (h ^ b0) * 16777619u; h = (h ^ b1) * 16777619u; h = (h ^ b2) * 16777619u; h = (h ^ b3) * 16777619u;
+  }
+#pragma unroll 1
+  for (; i < n; ++i) h = (h ^ p[i]) * 16777619u;
   return h;
 }
 
 __device__ __noinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, uint32_t n) {
+  uint32_t i = 0;
 #pragma unroll 1
-  for (uint32_t i = 0; i < n; ++i) if (a[i] != b[i]) return false;
+  for (; i + 4 <= n; i += 4) {
+    const uint32_t x = a[i] | (a[i + 1] << 8) | (a[i + 2] << 16) | ((uint32_t)a[i + 3] << 24);
+    const uint32_t y = b[i] | (b[i + 1] << 8) | (b[i + 2] << 16) | ((uint32_t)b[i + 3] << 24);
+    if (x != y) return false;
+  }
+#pragma unroll 1
+  for (; i < n; ++i) if (a[i] != b[i]) return false;
   return true;
 }
 
@@ -384,44 +399,71 @@ __device__ __forceinline__ bool word_maybe_sep(uint32_t w) {
   return (lt | z2 | z3) != 0;
 }
 
-// returns L; fills ls/le (capacity cap).  The text is read in place (it is
-// consumed line by line from L1/L2 by the later phases; no scratch copy).
-__device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint32_t cap) {
+// A byte that may precede a token start (tokenizer whitespace, any line
+// separator's last byte, text start): every byte < 0x21, 0x85, 0xA8, 0xA9.
+__device__ __forceinline__ bool may_precede_token(uint32_t b) {
+  return b < 0x21 || b == 0x85 || b == 0xA8 || b == 0xA9;
+}
+
+// returns L; fills ls/le (capacity cap) and lt0 = per-line token-slot bases.
+// Slot bound: a line's tokens each start at a "candidate" byte of the line --
+// a non-whitespace byte after a may_precede_token byte (or at the text start),
+// or after/at a '"' (every '"' is one more candidate) -- so the number of
+// candidates in [ls, le) bounds the line's tokens (tokenize_line zero-fills the
+// unused slots).  Separator bytes are never candidates, so the candidate count
+// up to a line start equals the count up to the preceding separator.  The
+// text is read in place (the later phases read it line by line from L1/L2).
+__device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint32_t cap, uint32_t* lt0,
+                                             uint32_t& ncand) {
   const uint32_t lane = lane_id_a();
   const uint32_t T = m.T;
-  // separators: lanes scan 4-byte words; each lane records its separators in order
-  uint32_t nsep = 0;
+  uint32_t nsep = 0, ccarry = 0, prev_last = 0;   // prev_last: byte before this chunk (0 = text start)
   const uint32_t nw = (T + 3) / 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(m.txt) & 3) == 0;
   for (uint32_t base = 0; base < nw; base += 32) {
     const uint32_t w = base + lane;
     uint32_t cnt = 0;
-    uint32_t pos[4], len[4];
+    uint32_t pos[4], len[4], cb[4];
+    uint32_t word = 0;
     if (w < nw) {
-      uint32_t word;
-      if ((reinterpret_cast<uintptr_t>(m.txt) & 3) == 0) {
+      if (aligned) {
         word = __ldg(reinterpret_cast<const uint32_t*>(m.txt) + w);
       } else {
-        word = 0;
         for (uint32_t b = 0; b < 4 && 4 * w + b < T; ++b) word |= (uint32_t)m.txt[4 * w + b] << (8 * b);
       }
-      if (word_maybe_sep(word)) {
-        for (uint32_t b = 0; b < 4; ++b) {
-          const uint32_t i = 4 * w + b;
-          if (i >= T) break;
-          const uint32_t sl = sep_len_at(m.txt, T, i);
-          if (sl) { pos[cnt] = i; len[cnt] = sl; ++cnt; }
-        }
+    }
+    // previous byte of every byte of the word
+    uint32_t pw = __shfl_up_sync(FULLM, word, 1);
+    if (lane == 0) pw = prev_last << 24;
+    const bool sepw = w < nw && word_maybe_sep(word);
+    uint32_t nc = 0;
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t i = 4 * w + b;
+      const uint32_t c = (word >> (8 * b)) & 0xFF;
+      const uint32_t pb = b ? ((word >> (8 * (b - 1))) & 0xFF) : (pw >> 24);
+      uint32_t sl = 0;
+      if (sepw && i < T) {
+        sl = sep_len_at(m.txt, T, i);
+        if (sl) { pos[cnt] = i; len[cnt] = sl; cb[cnt] = nc; ++cnt; }
       }
+      const bool ws = c == ' ' || c == '\t' || c == '\r' || c == '\n';
+      if (i < T && !sl && ((!ws && (i == 0 || may_precede_token(pb))) || c == '"')) ++nc;
+      if (c == '"' && i < T && !sl && !ws && (i == 0 || may_precede_token(pb))) ++nc;   // counted twice: fine
     }
     const uint32_t incl = wincl(cnt);
+    const uint32_t cincl = wincl(nc);
+    const uint32_t c0 = ccarry + cincl - nc;
     uint32_t k = nsep + incl - cnt;
     for (uint32_t q = 0; q < cnt; ++q, ++k) {
-      if (k < cap) { m.le[k] = pos[q]; m.ls[k + 1] = pos[q] + len[q]; }
+      if (k < cap) { m.le[k] = pos[q]; m.ls[k + 1] = pos[q] + len[q]; lt0[k + 1] = c0 + cb[q]; }
     }
     nsep += __shfl_sync(FULLM, incl, 31);
+    ccarry += __shfl_sync(FULLM, cincl, 31);
+    prev_last = __shfl_sync(FULLM, word >> 24, 31);
   }
   __syncwarp();
-  if (lane == 0) m.ls[0] = 0;
+  if (lane == 0) { m.ls[0] = 0; lt0[0] = 0; }
   // lines: one per separator, plus a final unterminated one if non-empty
   uint32_t L = nsep;
   const uint32_t last_start = nsep ? (nsep < cap ? m.ls[nsep] : T) : 0;
@@ -429,45 +471,20 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
     if (lane == 0 && nsep < cap) m.le[nsep] = T;
     ++L;
   }
+  ncand = ccarry;
   __syncwarp();
   return L;
 }
 
 // ============================================================================
-// Phase B: tokenize (asm.py:51-90), lane per line: a counting pass sizes the
-// token array exactly, the second pass stores tokens and undoes escapes.
+// Phase B: tokenize (asm.py:51-90), lane per line, into the line's token
+// slots (bound from split_lines); strings are unescaped into m.esc.
 
 struct AsmCtx {
   const Tables& T;
   const Uni& U;
   const AsmTables& A;
 };
-
-// tokens of a line without storing them (same scan as tokenize_line; an
-// unterminated string makes the line token-less)
-__device__ __noinline__ uint32_t count_tokens(const uint8_t* t, uint32_t i, uint32_t e0) {
-  uint32_t nt = 0;
-  while (i < e0) {
-    const uint8_t c = t[i];
-    if (c == ' ' || c == '\t' || c == '\r' || c == '\n') { ++i; continue; }
-    if (c == ';') break;
-    if (c == '"') {
-      ++i;
-      while (i < e0 && t[i] != '"') { if (t[i] == '\\' && i + 1 < e0) ++i; ++i; }
-      if (i >= e0) return 0;
-      ++i;
-      ++nt;
-      continue;
-    }
-    while (i < e0) {
-      const uint8_t d = t[i];
-      if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
-      ++i;
-    }
-    ++nt;
-  }
-  return nt;
-}
 
 __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
                                            uint32_t cap, uint32_t& npct) {
@@ -476,6 +493,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
   uint32_t nt = 0;
   uint32_t fl = 0;
   uint32_t i = s0;
+  // indentation: whole aligned 4-byte words of spaces at a time
+  while (i < e0 && (reinterpret_cast<uintptr_t>(t + i) & 3) && t[i] == ' ') ++i;
+  while (i + 4 <= e0 && (reinterpret_cast<uintptr_t>(t + i) & 3) == 0 &&
+         *reinterpret_cast<const uint32_t*>(t + i) == 0x20202020u) i += 4;
   while (i < e0) {
     const uint8_t c = t[i];
     if (c == ' ' || c == '\t' || c == '\r' || c == '\n') { ++i; continue; }
@@ -515,12 +536,13 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
       ++i;
     }
-    if (nt < cap) {   // cap = count_tokens of this line (0 for an unterminated string)
+    if (nt < cap) {   // cap = candidate bound of this line (split_lines)
       m.tok[2 * (tb + nt)] = start;
       m.tok[2 * (tb + nt) + 1] = i - start;
     }
     ++nt;
   }
+  for (uint32_t q = min(nt, cap); q < cap; ++q) { m.tok[2 * (tb + q)] = 0; m.tok[2 * (tb + q) + 1] = 0; }
   if (!(fl & LF_TOKERR) && nt == 0) fl |= LF_EMPTY;
   if (!(fl & (LF_TOKERR | LF_EMPTY)) && nt >= 3) {
     const Tok a = tok_at(m, tb), b = tok_at(m, tb + 1);
@@ -1791,8 +1813,9 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
 // (the per-warp independent schedule thrashed the instruction cache).  A warp
 // whose module is finished (error exit) or absent (t >= n_mod) idles through
 // the remaining phases.
-#define CTA_SYNC() __syncthreads()
-__device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot) {
+#define CTA_SYNC() group_sync(gid, gw)
+__device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot,
+                                             uint32_t gid, uint32_t gw) {
   const uint32_t lane = lane_id_a();
   PHASE_START();
   bool done = t >= a.n_mod;
@@ -1805,7 +1828,7 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   uint32_t flimbs = 0;
   auto fail_internal = [&]() { finish_error(a, m, X, t, X_INTERNAL, 0, nullptr, 0); };
   const uint32_t T = (uint32_t)len64;
-  uint32_t L = 0, npct = 0, x = X_NONE, ndiag = 0, total = 0;
+  uint32_t L = 0, npct = 0, x = X_NONE, ndiag = 0, total = 0, ntb0 = 0;
   bool fits = false;
   uint64_t off = 0;
   uint32_t* ow = nullptr;
@@ -1816,18 +1839,18 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   m.esc = take((uint64_t)T + 16);   // touched only by strings with escapes
   m.ls = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
   m.le = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
+  m.lt0 = reinterpret_cast<uint32_t*>(take(4ull * (T + 2)));
   if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); done = true; goto end_a; }
   for (uint32_t k = lane; k < 64; k += 32) m.misc[k] = 0;
   __syncwarp();
-  L = split_lines(m, src, T + 1);
+  L = split_lines(m, src, T + 1, m.lt0, ntb0);
   m.L = L;
 end_a:
   PHASE_MARK(0);
   CTA_SYNC();
   if (done) goto end_b;
   {
-  // per-line arrays
-  m.lt0 = reinterpret_cast<uint32_t*>(take(4ull * L));
+  // per-line arrays (lt0: token-slot bases from split_lines)
   m.lnt = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lfl = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.ld = reinterpret_cast<uint32_t*>(take(4ull * L));
@@ -1837,15 +1860,7 @@ end_a:
   m.lgrp = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.loff = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lerr = reinterpret_cast<uint32_t*>(take(16ull * L));
-  // exact token counts (first pass of the tokenizer): per-line bases in lt0
-  uint32_t ntb = 0;
-  for (uint32_t base = 0; base < L; base += 32) {
-    const uint32_t li = base + lane;
-    const uint32_t c = li < L ? count_tokens(m.txt, m.ls[li], m.le[li]) : 0;
-    const uint32_t incl = wincl(c);
-    if (li < L) m.lt0[li] = ntb + incl - c;
-    ntb += __shfl_sync(FULLM, incl, 31);
-  }
+  const uint32_t ntb = ntb0;   // token slots: candidate bound (split_lines)
   m.ntb = ntb;
   m.tok = reinterpret_cast<uint32_t*>(take(8ull * ntb + 8));
   m.tid = reinterpret_cast<uint32_t*>(take(4ull * ntb + 4));
@@ -2237,19 +2252,22 @@ end_i:
 #define SKG_ASM_MINB 1
 #endif
 __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs a) {
-  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_base[16];
   const uint32_t warps = blockDim.x >> 5;
-  const uint32_t gwarp = blockIdx.x * warps + (threadIdx.x >> 5);
+  const uint32_t warp_in_block = threadIdx.x >> 5;
+  const uint32_t gw = a.group_warps;                 // warps per barrier group
+  const uint32_t gid = warp_in_block / gw, gwarp_in = warp_in_block % gw;
+  const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
   uint8_t* slot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
   const AsmCtx X{a.T, a.U, a.A};
   while (true) {
-    if (threadIdx.x == 0) s_base = atomicAdd(a.counters, warps);
-    __syncthreads();
-    const uint32_t base = s_base;
-    __syncthreads();
+    if (gwarp_in == 0 && (threadIdx.x & 31) == 0) s_base[gid] = atomicAdd(a.counters, gw);
+    group_sync(gid, gw);
+    const uint32_t base = s_base[gid];
+    group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    const uint32_t tk = base + (threadIdx.x >> 5);
-    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot);
+    const uint32_t tk = base + gwarp_in;
+    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw);
   }
 }
 

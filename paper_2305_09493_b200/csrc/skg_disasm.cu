@@ -45,6 +45,7 @@ struct DisasmArgs {
   uint32_t smem_slab;         // bytes per warp in dynamic shared memory (module scratch)
   uint32_t stage_bytes;       // bytes per warp of text stage (dynamic shared memory, first)
   const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
+  uint32_t group_warps;       // warps per phase-barrier group (divides the CTA's warps)
 };
 
 // -- sanitized friendly names (disasm.py:82-86) --------------------------------
@@ -78,11 +79,18 @@ __device__ inline void for_sanitized(const NameView& nv, F&& f) {
   }
   bool prefix = first == 0xFFFFFFFF || (first >= '0' && first <= '9');
   if (prefix) f('_');
+  // one word load per 4 bytes
   #pragma unroll 1
-  for (uint32_t i = 0; i < nv.nbytes; ++i) {
-    uint32_t c = byte_at(nv.w, i);
-    if ((c & 0xC0) == 0x80) continue;
-    f(is_word_char(c) ? c : '_');
+  for (uint32_t i = 0; i < nv.nbytes; i += 4) {
+    const uint32_t x = nv.w[i >> 2];
+    const uint32_t nb = min(4u, nv.nbytes - i);
+    #pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+      if (q < nb) {
+        const uint32_t c = (x >> (8 * q)) & 0xFF;
+        if ((c & 0xC0) != 0x80) f(is_word_char(c) ? c : '_');
+      }
+    }
   }
 }
 
@@ -635,8 +643,14 @@ __device__ __forceinline__ uint8_t* emit_cstr(uint8_t* p, const char* z) {
 }
 __device__ __forceinline__ uint8_t* emit_tab(uint8_t* p, const Tables& T, uint32_t off, uint32_t len) {
   const uint8_t* src = T.str + off;
+  uint32_t q = 0;
 #pragma unroll 1
-  for (uint32_t q = 0; q < len; ++q) p[q] = __ldg(src + q);
+  for (; q + 4 <= len; q += 4) {
+    const uint8_t c0 = __ldg(src + q), c1 = __ldg(src + q + 1), c2 = __ldg(src + q + 2), c3 = __ldg(src + q + 3);
+    p[q] = c0; p[q + 1] = c1; p[q + 2] = c2; p[q + 3] = c3;
+  }
+#pragma unroll 1
+  for (; q < len; ++q) p[q] = __ldg(src + q);
   return p + len;
 }
 
@@ -646,8 +660,14 @@ __device__ __noinline__ uint8_t* emit_ref(uint8_t* p, const Mod& m, uint32_t id)
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
     const uint8_t* src = m.narena + m.hnoff[slot];
     const uint32_t n = m.nLen[slot];
+    uint32_t q = 0;
 #pragma unroll 1
-    for (uint32_t q = 0; q < n; ++q) p[q] = src[q];
+    for (; q + 4 <= n; q += 4) {
+      const uint8_t c0 = src[q], c1 = src[q + 1], c2 = src[q + 2], c3 = src[q + 3];
+      p[q] = c0; p[q + 1] = c1; p[q + 2] = c2; p[q + 3] = c3;
+    }
+#pragma unroll 1
+    for (; q < n; ++q) p[q] = src[q];
     p += n;
     const uint32_t ser = m.hser[slot];
     if (ser != NONE32) { *p++ = '_'; p = emit_u32(p, ser); }
@@ -1037,7 +1057,7 @@ __device__ unsigned long long g_dis_phase[16];
 // time (CTA barrier between phases), so the instruction working set of the SM
 // is one phase rather than the whole program.
 __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
-                                        uint8_t* stage, ErrSink& es) {
+                                        uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   DPHASE_START();
@@ -1063,7 +1083,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     }
   }
   DPHASE_MARK(0);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P1: id tables + prescan (A15)
   bool any_name = false;
   if (status == ST_OK) {
@@ -1077,7 +1097,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     }
   }
   DPHASE_MARK(1);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P2: classify (A8-A12) + referenced ids; an id at/above the bound redoes
   //    P1+P2 with the hash table (rare: non-canonical modules)
   if (status == ST_OK) {
@@ -1100,7 +1120,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     }
   }
   DPHASE_MARK(2);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P3: exceptions, in the reference's evaluation order
   if (status == ST_OK) {
     uint32_t bad = first_where(m, [&](uint32_t i) { return (m.iflag[i] & IF_PRESCAN_UTF8) != 0; });
@@ -1139,11 +1159,11 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     }
   }
   DPHASE_MARK(3);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P4: friendly names (A16)
   if (status == ST_OK && names_mode) resolve_names(m, T);
   DPHASE_MARK(4);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P5: result refs, width, sections, text size (A17-A19)
   if (status == ST_OK) {
     width = result_refs(m, T);
@@ -1152,7 +1172,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     total = text_size(m, T, a.opts, width);
   }
   DPHASE_MARK(5);
-  __syncthreads();
+  group_sync(gid, gw);
   // -- P6: reserve the module's bytes (16-byte aligned starts) and write the text
   if (live) {
     if (status != ST_OK) total = 0;
@@ -1166,7 +1186,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     if (status == ST_OK && total > 0 && fits) text_write(m, T, a.opts, width, a.text + off, stage, a.stage_bytes);
   }
   DPHASE_MARK(6);
-  __syncthreads();
+  group_sync(gid, gw);
 }
 
 #ifndef SKG_DIS_MAXT
@@ -1175,21 +1195,23 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
 #endif
 __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(DisasmArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_base[16];
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
+  const uint32_t gw = a.group_warps;                 // warps per barrier group
+  const uint32_t gid = warp_in_block / gw, gwarp_in = warp_in_block % gw;
   const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
   uint8_t* stage = smem + (size_t)warp_in_block * a.stage_bytes;
   uint8_t* slab = smem + (size_t)warps * a.stage_bytes + (size_t)warp_in_block * a.smem_slab;
   uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
   ErrSink es{a.errs, a.ticket + 1, a.err_cap};
   while (true) {
-    if (threadIdx.x == 0) s_base = atomicAdd(a.ticket, warps);
-    __syncthreads();
-    const uint32_t base = s_base;
-    __syncthreads();
+    if (gwarp_in == 0 && lane_id() == 0) s_base[gid] = atomicAdd(a.ticket, gw);
+    group_sync(gid, gw);
+    const uint32_t base = s_base[gid];
+    group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    disasm_one(a, base + warp_in_block, slab, gslot, stage, es);
+    disasm_one(a, base + gwarp_in, slab, gslot, stage, es, gid, gw);
   }
 }
 

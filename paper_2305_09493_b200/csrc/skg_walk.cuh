@@ -51,6 +51,15 @@ struct WordBytes {
 };
 
 __device__ __noinline__ uint32_t string_utf8(const uint32_t* ops, uint32_t pos, uint32_t nbytes, WalkErr& err) {
+  {   // ASCII fast path, a word at a time
+    uint32_t i = 0;
+    const uint32_t nw = nbytes >> 2;
+    while (i < nw && !(ops[pos + i] & 0x80808080u)) ++i;
+    if (i == nw) {
+      const uint32_t tail = nbytes & 3;
+      if (!tail || !(ops[pos + nw] & 0x80808080u & ((1u << (8 * tail)) - 1))) return U8_OK;
+    }
+  }
   WordBytes at{ops + pos};
   uint32_t s = 0, e = 0;
   uint32_t r = utf8_check(at, nbytes, s, e);
