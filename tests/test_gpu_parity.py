@@ -141,3 +141,28 @@ def test_batch_with_mixed_errors_and_sizes(sk):
         if m not in cache:
             cache[m] = outcome(lambda: odis.disassemble(m))
         assert same(_as_outcome(g), cache[m])
+
+
+def test_sharded_disasm_world1_gpu(sk):
+    """run_sharded + the GPU DisasmSession step (gloo group of one, real kernel)."""
+    import socket
+    import numpy as np
+    import torch.distributed as dist
+    from oracle import disasm as odis
+    from paper_2305_09493_b200.shard import disasm_shard_fn, run_sharded
+    from synth.families import sample_batch
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        b = sample_batch(300, 100, 9)
+        m0, m1, arena, spans, status, base, totals = run_sharded(disasm_shard_fn(), b.data, b.offsets,
+                                                                 b.lengths)
+        assert (m0, m1, base, totals) == (0, b.n, 0, [len(arena)])
+        assert (status == 0).all()
+        for i in range(0, b.n, 7):
+            got = np.asarray(arena)[spans[i, 0]:spans[i, 0] + spans[i, 1]].tobytes().decode()
+            assert got == odis.disassemble(b.module(i))
+    finally:
+        dist.destroy_process_group()
