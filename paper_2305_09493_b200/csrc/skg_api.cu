@@ -99,11 +99,25 @@ uint32_t group_warps(int warps, int want) {
   return (uint32_t)g;
 }
 
+// Launch geometry: the persistent grid, shrunk for batches with fewer modules
+// than resident warps (a single huge module gets one warp and one scratch slot).
+struct Geom { uint32_t blocks, warps; };
+Geom fit_geom(uint32_t blocks, uint32_t warps, uint32_t n_mod, bool shrink_warps) {
+  if ((uint64_t)blocks * warps > n_mod) {
+    blocks = n_mod ? (n_mod + warps - 1) / warps : 1;
+    if (blocks == 1 && shrink_warps) warps = n_mod ? (n_mod < warps ? n_mod : warps) : 1;
+  }
+  return {blocks, warps};
+}
+Geom dis_geom(uint32_t n_mod) { return fit_geom(dis_blocks(), (uint32_t)kDisWarps, n_mod, true); }
+Geom val_geom(uint32_t n_mod) { return fit_geom(grid_blocks(), (uint32_t)kWarpsPerBlock, n_mod, false); }
+
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
   (void)n_mod;
-  l.n_warps = grid_blocks() * kWarpsPerBlock;
-  if (dis_blocks() * kDisWarps > l.n_warps) l.n_warps = dis_blocks() * kDisWarps;
+  const Geom gv = val_geom(n_mod), gd = dis_geom(n_mod);
+  l.n_warps = gv.blocks * gv.warps;
+  if (gd.blocks * gd.warps > l.n_warps) l.n_warps = gd.blocks * gd.warps;
   l.slot = gslot_bytes(max_words);
   l.counters = 0;
   l.state = 0;
@@ -224,14 +238,16 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   a.stage_bytes = kDisStage;
-  a.group_warps = group_warps(kDisWarps, env_int("SKG_DIS_GROUP", kDisWarps));
-  const size_t smem = (size_t)(kDisSlab + kDisStage) * kDisWarps;
+  const Geom g = dis_geom(n_mod);
+  a.group_warps = group_warps((int)g.warps, env_int("SKG_DIS_GROUP", (int)g.warps));
+  const size_t smem_max = (size_t)(kDisSlab + kDisStage) * kDisWarps;
+  const size_t smem = (size_t)(kDisSlab + kDisStage) * g.warps;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     attr = true;
   }
-  skg::disasm_kernel<<<dis_blocks(), 32 * kDisWarps, smem, s>>>(a);
+  skg::disasm_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
   return check(cudaGetLastError());
 }
 
@@ -262,7 +278,7 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
     cudaFuncSetAttribute(skg::validate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  skg::validate_kernel<<<grid_blocks(), 32 * kWarpsPerBlock, smem, s>>>(a);
+  skg::validate_kernel<<<val_geom(n_mod).blocks, 32 * kWarpsPerBlock, smem, s>>>(a);
   return check(cudaGetLastError());
 }
 
@@ -277,8 +293,11 @@ uint32_t asm_blocks() {
   return g > 0 ? (uint32_t)g : (uint32_t)sm_count() * env_int("SKG_ASM_BLOCKS_PER_SM", 1);
 }
 
+Geom asm_geom(uint32_t n_mod) { return fit_geom(asm_blocks(), (uint32_t)kAsmWarps, n_mod, true); }
+
 uint64_t skg_asm_workspace_bytes(uint64_t slot_bytes, uint32_t n_mod) {
-  return 256 + sched_bytes(n_mod) + (uint64_t)asm_blocks() * kAsmWarps * slot_bytes;
+  const Geom g = asm_geom(n_mod);
+  return 256 + sched_bytes(n_mod) + (uint64_t)g.blocks * g.warps * slot_bytes;
 }
 
 int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, const int64_t* mod_len,
@@ -303,8 +322,9 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.gscratch = ws + 256 + sched_bytes(n_mod);
   a.gslot_bytes = slot_bytes;
   a.default_version = default_version;
-  a.group_warps = group_warps(kAsmWarps, env_int("SKG_ASM_GROUP", kAsmWarps));
-  skg::asm_kernel<<<asm_blocks(), 32 * kAsmWarps, 0, s>>>(a);
+  const Geom g = asm_geom(n_mod);
+  a.group_warps = group_warps((int)g.warps, env_int("SKG_ASM_GROUP", (int)g.warps));
+  skg::asm_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
 }
 

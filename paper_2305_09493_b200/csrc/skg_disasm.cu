@@ -306,14 +306,53 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     m.ia[k] = n;
   }
   __syncwarp();
-  // leader = first ident (D order) with the same sanitized base
+  // leader = first ident (D order) with the same sanitized base.  A hash table
+  // (in the spill area: capacity C = pow2 >= 2 nd, 8 C <= 32 nd bytes) keeps the
+  // smallest ident index per base hash; a candidate is verified by comparing the
+  // strings, and only a hash collision falls back to the ordered linear scan.
+  uint32_t C = 4;                     // 8 C < 32 nd <= spill_bytes(I)
+  while (C < 2 * nd) C <<= 1;
+  uint32_t* htab = reinterpret_cast<uint32_t*>(m.spill);
+  #pragma unroll 1
+  for (uint32_t e = lane; e < C; e += 32) { __stcg(htab + 2 * e, EMPTY); __stcg(htab + 2 * e + 1, EMPTY); }
+  __threadfence_block();
+  __syncwarp();
+  auto hkey = [](uint32_t h) { return h == EMPTY ? EMPTY - 1 : h; };
   #pragma unroll 1
   for (uint32_t k = lane; k < nd; k += 32) {
-    uint32_t slot = m.ndl[k], h = m.nH[slot], lead = k;
+    const uint32_t key = hkey(m.nH[m.ndl[k]]);
+    uint32_t e = (key * 0x9E3779B1u) & (C - 1);
     #pragma unroll 1
-    for (uint32_t q = 0; q < k; ++q) {
-      uint32_t o = m.ndl[q];
-      if (m.nH[o] == h && cand_eq(m, slot, NONE32, o, NONE32)) { lead = q; break; }
+    while (true) {
+      const uint32_t old = atomicCAS(&htab[2 * e], EMPTY, key);
+      if (old == EMPTY || old == key) { atomicMin(&htab[2 * e + 1], k); break; }
+      e = (e + 1) & (C - 1);
+    }
+  }
+  __threadfence_block();
+  __syncwarp();
+  auto hmin = [&](uint32_t h) -> uint32_t {   // smallest ident index with this base hash
+    const uint32_t key = hkey(h);
+    uint32_t e = (key * 0x9E3779B1u) & (C - 1);
+    #pragma unroll 1
+    while (true) {   // L2 reads: the table was filled with atomics (not in L1)
+      const uint32_t kk = __ldcg(htab + 2 * e);
+      if (kk == key) return __ldcg(htab + 2 * e + 1);
+      if (kk == EMPTY) return NONE32;
+      e = (e + 1) & (C - 1);
+    }
+  };
+  #pragma unroll 1
+  for (uint32_t k = lane; k < nd; k += 32) {
+    const uint32_t slot = m.ndl[k], h = m.nH[slot];
+    uint32_t lead = hmin(h);
+    if (lead != k && !(lead < k && cand_eq(m, slot, NONE32, m.ndl[lead], NONE32))) {
+      lead = k;   // hash collision with another base: exact ordered scan
+      #pragma unroll 1
+      for (uint32_t q = 0; q < k; ++q) {
+        const uint32_t o = m.ndl[q];
+        if (m.nH[o] == h && cand_eq(m, slot, NONE32, o, NONE32)) { lead = q; break; }
+      }
     }
     m.pos[k] = (int32_t)lead;
   }
@@ -325,8 +364,14 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     uint32_t slot = m.ndl[k];
     if (m.pos[k] == (int32_t)k && (m.hfl[slot] & HF_SUFFIX)) {
       const uint32_t ph = m.nP[slot], n = m.ia[k];
+      // the parent (if any) is the leader of base hash ph: try the hash table's
+      // smallest index first, then the exact scan
+      const uint32_t hq = hmin(ph);
       #pragma unroll 1
-      for (uint32_t q = 0; q < nd && parent == NONE32; ++q) {
+      for (uint32_t it = 0; it <= nd && parent == NONE32; ++it) {
+        const uint32_t q = it == 0 ? hq : it - 1;
+        if (q == NONE32 || (it > 0 && q == hq)) continue;
+        if (it == 1 && hq == NONE32) break;   // no base with that hash: no parent
         uint32_t o = m.ndl[q];
         if (m.pos[q] != (int32_t)q || m.nH[o] != ph) continue;
         if (m.nLen[o] + 1 + dec_len_u64(n) != m.nLen[slot]) continue;
@@ -373,54 +418,35 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     nc += __popc(b);
   }
   __syncwarp();
-  const uint32_t c_g = lane < nc ? clist[3 * lane] : NONE32;
-  const uint32_t c_n = lane < nc ? clist[3 * lane + 1] : 0;
-  const uint32_t c_k = lane < nc ? clist[3 * lane + 2] : 0;
-  auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
-    unsigned b = __ballot_sync(FULL, c_g == g && c_n == sv);
-    if (b) return __shfl_sync(FULL, c_k, __ffs(b) - 1);
+  // the sequential pass in D order (lane 0); child lookups scan the compact list
+  if (lane == 0) {
+    auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
+      #pragma unroll 1
+      for (uint32_t q = 0; q < nc; ++q)
+        if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
+      return NONE32;
+    };
     #pragma unroll 1
-    for (uint32_t base = 32; base < nc; base += 32) {   // more than 32 child groups
-      const uint32_t q = base + lane;
-      b = __ballot_sync(FULL, q < nc && clist[3 * q] == g && clist[3 * q + 1] == sv);
-      if (b) return clist[3 * (base + __ffs(b) - 1) + 2];
-    }
-    return NONE32;
-  };
-  // the sequential pass in D order, run by the whole warp (uniform control flow;
-  // lane 0 writes); 32 idents' (leader, leader slot, slot) preloaded per round
-  #pragma unroll 1
-  for (uint32_t base = 0; base < nd; base += 32) {
-    const uint32_t kk = base + lane;
-    const uint32_t my_g = kk < nd ? (uint32_t)m.pos[kk] : 0;
-    const uint32_t my_gs = kk < nd ? m.ndl[my_g] : 0;
-    const uint32_t my_s = kk < nd ? m.ndl[kk] : 0;
-    const uint32_t cnt = min(32u, nd - base);
-    #pragma unroll 1
-    for (uint32_t j = 0; j < cnt; ++j) {
-      const uint32_t k = base + j;
-      const uint32_t g = __shfl_sync(FULL, my_g, j);
-      const uint32_t gs = __shfl_sync(FULL, my_gs, j);
-      const uint32_t ks = __shfl_sync(FULL, my_s, j);
-      if (g == k && lane == 0) m.nP[gs] = 0;            // group counter (nP no longer needed)
-      __syncwarp();
+    for (uint32_t k = 0; k < nd; ++k) {
+      const uint32_t g = (uint32_t)m.pos[k];
+      const uint32_t gs = m.ndl[g];
+      if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
       uint32_t serial = NONE32;
       const uint8_t fl = m.hfl[gs];
       if (!(fl & HF_TB)) {
-        if (lane == 0) m.hfl[gs] = fl | HF_TB;
+        m.hfl[gs] = fl | HF_TB;
       } else {
         uint32_t sv = m.nP[gs];
         if (fl & HF_HASCHILD) {
           uint32_t c;
           #pragma unroll 1
           while ((c = child_of(g, sv)) != NONE32 && (m.hfl[m.ndl[c]] & HF_TB)) ++sv;
-          if (c != NONE32 && lane == 0) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
+          if (c != NONE32) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
         }
         serial = sv;
-        if (lane == 0) m.nP[gs] = sv + 1;
+        m.nP[gs] = sv + 1;
       }
-      if (lane == 0) m.hser[ks] = serial;
-      __syncwarp();
+      m.hser[m.ndl[k]] = serial;
     }
   }
   __syncwarp();

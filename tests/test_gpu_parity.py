@@ -166,3 +166,19 @@ def test_sharded_disasm_world1_gpu(sk):
             assert got == odis.disassemble(b.module(i))
     finally:
         dist.destroy_process_group()
+
+
+def test_huge_single_module_vs_oracle(sk):
+    """Config-3 shape (one large module, dense OpName, long OpString, ids > 2^16)
+    at a size the oracle finishes in seconds: disassembly (default options and
+    numeric refs) and validation identical."""
+    from oracle import disasm as odis, validate as oval
+    from synth.huge import build_huge
+    m = build_huge(400, chain=200, seed=3)          # ~740k words, ids up to ~81k
+    assert len(m) // 4 > 500_000
+    got = sk.disassemble_batch([m])[0]
+    assert got == odis.disassemble(m)
+    opts = sk.DisassemblerOptions(inline_names=False)
+    assert sk.disassemble_batch([m], opts)[0] == odis.disassemble(m, opts)
+    d = sk.validate_batch([m])[0]
+    assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(m)]

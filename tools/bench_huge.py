@@ -1,0 +1,43 @@
+"""Config 3: disassembly + validation of ONE large module (synth/huge.py) on
+cuda:0, inputs resident in HBM; prints words/s for each kernel.
+
+usage: python tools/bench_huge.py <n_functions> [chain]   (~1840 words per function)
+"""
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    n_fn = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
+    chain = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    import numpy as np
+    import torch
+    from paper_2305_09493_b200 import _native
+    from synth.huge import build_huge
+    t0 = time.time()
+    m = build_huge(n_fn, chain)
+    W = len(m) // 4
+    print(f"module: {W} words, {len(m) / 1e6:.1f} MB (built in {time.time() - t0:.1f}s)", flush=True)
+    data = np.frombuffer(m + b"\0" * 16, dtype=np.uint8)
+    dev = _native.DeviceBatch.from_host(data, np.array([0], np.int64), np.array([len(m)], np.int64))
+    for kind in ("disasm", "validate"):
+        plan = _native.DisasmPlan(dev, 2, kind=kind, text_cap=24 * len(m) + 4096)
+        t1 = time.time()
+        info = plan.fit()
+        st = int(plan.status[0].item())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.launch()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(f"{kind}: status {st} out {info['text_bytes']} B  {ms:.1f} ms  {W / ms / 1e3:.2f} Mwords/s "
+              f"(fit {time.time() - t1:.1f}s)", flush=True)
+
+
+if __name__ == "__main__":
+    main()
