@@ -399,20 +399,23 @@ __device__ __forceinline__ bool word_maybe_sep(uint32_t w) {
   return (lt | z2 | z3) != 0;
 }
 
-// A byte that may precede a token start (tokenizer whitespace, any line
-// separator's last byte, text start): every byte < 0x21, 0x85, 0xA8, 0xA9.
-__device__ __forceinline__ bool may_precede_token(uint32_t b) {
-  return b < 0x21 || b == 0x85 || b == 0xA8 || b == 0xA9;
+// SWAR byte masks (0x80 in every byte of w that matches; exact, no carries)
+__device__ __forceinline__ uint32_t eq_bytes(uint32_t w, uint32_t c) {
+  const uint32_t t = w ^ (c * 0x01010101u);
+  return ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t lt21_bytes(uint32_t w) {   // byte < 0x21
+  return ~(((w & 0x7F7F7F7Fu) + 0x5F5F5F5Fu) | w) & 0x80808080u;
 }
 
 // returns L; fills ls/le (capacity cap) and lt0 = per-line token-slot bases.
-// Slot bound: a line's tokens each start at a "candidate" byte of the line --
-// a non-whitespace byte after a may_precede_token byte (or at the text start),
-// or after/at a '"' (every '"' is one more candidate) -- so the number of
-// candidates in [ls, le) bounds the line's tokens (tokenize_line zero-fills the
-// unused slots).  Separator bytes are never candidates, so the candidate count
-// up to a line start equals the count up to the preceding separator.  The
-// text is read in place (the later phases read it line by line from L1/L2).
+// Slot bound: every token of a line starts at a "candidate" byte -- a byte
+// other than ' ' whose previous byte is < 0x21 or >= 0x80 (tokenizer
+// whitespace, any line separator's last byte, text start), or the byte after
+// a '"' -- so counting those bytes plus one per '"' over-approximates the
+// tokens.  lt0[k+1] = candidates before line k's separator; line k's slots are
+// lt0[k+1] - lt0[k] (tokenize_line zero-fills the unused ones).  The text is
+// read in place (the later phases read it line by line from L1/L2).
 __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint32_t cap, uint32_t* lt0,
                                              uint32_t& ncand) {
   const uint32_t lane = lane_id_a();
@@ -432,24 +435,23 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
         for (uint32_t b = 0; b < 4 && 4 * w + b < T; ++b) word |= (uint32_t)m.txt[4 * w + b] << (8 * b);
       }
     }
-    // previous byte of every byte of the word
     uint32_t pw = __shfl_up_sync(FULLM, word, 1);
     if (lane == 0) pw = prev_last << 24;
-    const bool sepw = w < nw && word_maybe_sep(word);
-    uint32_t nc = 0;
-#pragma unroll
-    for (uint32_t b = 0; b < 4; ++b) {
-      const uint32_t i = 4 * w + b;
-      const uint32_t c = (word >> (8 * b)) & 0xFF;
-      const uint32_t pb = b ? ((word >> (8 * (b - 1))) & 0xFF) : (pw >> 24);
-      uint32_t sl = 0;
-      if (sepw && i < T) {
-        sl = sep_len_at(m.txt, T, i);
-        if (sl) { pos[cnt] = i; len[cnt] = sl; cb[cnt] = nc; ++cnt; }
+    const uint32_t prev = (word << 8) | (pw >> 24);          // previous byte of every byte
+    const uint32_t valid = w >= nw ? 0u : (4 * w + 4 <= T ? 0x80808080u : (0x80808080u >> (8 * (4 * w + 4 - T))));
+    const uint32_t cm = ~eq_bytes(word, ' ') & (lt21_bytes(prev) | (prev & 0x80808080u)) & valid;
+    const uint32_t qm = eq_bytes(word, '"') & valid;
+    const uint32_t nc = __popc(cm) + __popc(qm);
+    if (w < nw && word_maybe_sep(word)) {
+      for (uint32_t b = 0; b < 4; ++b) {
+        const uint32_t i = 4 * w + b;
+        if (i >= T) break;
+        const uint32_t sl = sep_len_at(m.txt, T, i);
+        if (sl) {
+          const uint32_t below = b ? (0xFFFFFFFFu >> (32 - 8 * b)) : 0u;
+          pos[cnt] = i; len[cnt] = sl; cb[cnt] = __popc(cm & below) + __popc(qm & below); ++cnt;
+        }
       }
-      const bool ws = c == ' ' || c == '\t' || c == '\r' || c == '\n';
-      if (i < T && !sl && ((!ws && (i == 0 || may_precede_token(pb))) || c == '"')) ++nc;
-      if (c == '"' && i < T && !sl && !ws && (i == 0 || may_precede_token(pb))) ++nc;   // counted twice: fine
     }
     const uint32_t incl = wincl(cnt);
     const uint32_t cincl = wincl(nc);
@@ -531,10 +533,21 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       ++nt;
       continue;
     }
+    // bare token: up to 4 bytes per (aligned word) load
     while (i < e0) {
-      const uint8_t d = t[i];
-      if (d == ' ' || d == '\t' || d == '\r' || d == '\n' || d == ';' || d == '"') break;
-      ++i;
+      const uintptr_t ad = reinterpret_cast<uintptr_t>(t + i);
+      const uint32_t sh = (uint32_t)(ad & 3);
+      const uint32_t x = *reinterpret_cast<const uint32_t*>(ad - sh) >> (8 * sh);
+      const uint32_t nb = min(4u - sh, e0 - i);
+      uint32_t k = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t d = (x >> (8 * q)) & 0xFF;
+        const bool delim = d < 64 && ((0x0800000500002600ull >> d) & 1);   // \t \n \r ' ' '"' ';'
+        if (k == q && q < nb && !delim) ++k;
+      }
+      i += k;
+      if (k < nb) break;
     }
     if (nt < cap) {   // cap = candidate bound of this line (split_lines)
       m.tok[2 * (tb + nt)] = start;
@@ -1814,6 +1827,37 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
 // whose module is finished (error exit) or absent (t >= n_mod) idles through
 // the remaining phases.
 #define CTA_SYNC() group_sync(gid, gw)
+// Line order grouped by instruction (counting sort over a hash of the
+// instruction index; order within a bucket is arbitrary): perm[0..L).
+constexpr uint32_t OPG_BUCKETS = 64;
+template <class K>
+__device__ __forceinline__ void group_lines(AsmMod& m, uint32_t* perm, K&& key) {
+  const uint32_t lane = lane_id_a();
+  const uint32_t L = m.L;
+  uint32_t* cnt = perm + L;
+  uint32_t* cur = cnt + OPG_BUCKETS;
+  for (uint32_t b = lane; b < OPG_BUCKETS; b += 32) cnt[b] = 0;
+  __syncwarp();
+  for (uint32_t li = lane; li < L; li += 32) atomicAdd(&cnt[key(li)], 1u);
+  __syncwarp();
+  const uint32_t c0 = __ldcg(cnt + lane), c1 = __ldcg(cnt + 32 + lane);
+  const uint32_t i0 = wincl(c0);
+  const uint32_t t0 = __shfl_sync(FULLM, i0, 31);
+  const uint32_t i1 = wincl(c1);
+  cur[lane] = i0 - c0;
+  cur[32 + lane] = t0 + i1 - c1;
+  __syncwarp();
+  for (uint32_t li = lane; li < L; li += 32) perm[atomicAdd(&cur[key(li)], 1u)] = li;
+  __syncwarp();
+}
+
+__device__ __noinline__ void group_lines_by_opcode(AsmMod& m, uint32_t* perm) {
+  group_lines(m, perm, [&](uint32_t li) -> uint32_t {
+    const uint32_t d = (m.lfl[li] & (LF_TOKERR | LF_EMPTY)) ? 0xFFFFu : m.ld[li];
+    return (d * 0x9E3779B1u) >> 26;
+  });
+}
+
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot,
                                              uint32_t gid, uint32_t gw) {
   const uint32_t lane = lane_id_a();
@@ -1829,6 +1873,7 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   auto fail_internal = [&]() { finish_error(a, m, X, t, X_INTERNAL, 0, nullptr, 0); };
   const uint32_t T = (uint32_t)len64;
   uint32_t L = 0, npct = 0, x = X_NONE, ndiag = 0, total = 0, ntb0 = 0;
+  uint32_t* lperm = nullptr;
   bool fits = false;
   uint64_t off = 0;
   uint32_t* ow = nullptr;
@@ -1860,6 +1905,7 @@ end_a:
   m.lgrp = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.loff = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lerr = reinterpret_cast<uint32_t*>(take(16ull * L));
+  lperm = reinterpret_cast<uint32_t*>(take(4ull * L + 4 * 2 * OPG_BUCKETS));
   const uint32_t ntb = ntb0;   // token slots: candidate bound (split_lines)
   m.ntb = ntb;
   m.tok = reinterpret_cast<uint32_t*>(take(8ull * ntb + 8));
@@ -2052,11 +2098,13 @@ end_e:
     if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_f; }
     m.sused = used;
     for (uint32_t k = lane; k <= carry / 32; k += 32) m.swr[k] = 0;
-    __syncwarp();
+    group_lines_by_opcode(m, lperm);
   }
+  // lanes take lines grouped by instruction (one code path per group instead of
+  // the union of 32 different encoders); results are stored per line
   for (uint32_t base = 0; base < L; base += 32) {
-    const uint32_t li = base + lane;
-    if (li >= L) continue;
+    if (base + lane >= L) continue;
+    const uint32_t li = lperm[base + lane];
     const uint32_t fl = m.lfl[li];
     m.lnw[li] = 0; m.lrid[li] = 0;
     if (fl & (LF_TOKERR | LF_EMPTY)) continue;
