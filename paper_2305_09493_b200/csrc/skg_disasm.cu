@@ -497,6 +497,13 @@ __device__ __noinline__ void compute_sections(Mod& m, const Tables& T) {
   __syncwarp();
 }
 
+// length of put_header's text, arithmetically
+__device__ __forceinline__ uint32_t header_len(const Mod& m, bool hl) {
+  return 9 + (11 + dlen32(m.major) + 1 + dlen32(m.minor) + 1) +
+         (13 + dlen32(m.gen >> 16) + 2 + dlen32(m.gen & 0xFFFF) + 1) + (9 + dlen32(m.bound) + 1) +
+         (10 + dlen32(m.schema) + 1) + (hl ? 5 * 9 : 0);
+}
+
 template <class S>
 __device__ __noinline__ void put_header(S& s, const Mod& m, bool hl) {
   auto line = [&](auto&& body) {
@@ -712,7 +719,10 @@ __device__ __forceinline__ bool bit_cover(const Tables& T, uint32_t k, uint32_t 
 #pragma unroll 1
   for (uint32_t j = 0; j < ne; ++j) {
     const uint32_t ev = T.evalue(eo + j);
-    if (ev && (v & ev) == ev && (covered & ev) != ev) { covered |= ev; bytes += T.ename_len(eo + j); ++count; }
+    if (ev && (v & ev) == ev && (covered & ev) != ev) {
+      covered |= ev; bytes += T.ename_len(eo + j); ++count;
+      if (covered == v) break;   // later enumerants can only be skipped
+    }
   }
   return covered == v;
 }
@@ -861,6 +871,7 @@ __device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T
 #pragma unroll 1
       for (uint32_t j = 0; j < ne; ++j) {
         const uint32_t ev = T.evalue(eo + j);
+        if (covered == v) break;
         if (ev && (v & ev) == ev && (covered & ev) != ev) {
           covered |= ev;
           if (!first) *p++ = '|';
@@ -962,11 +973,7 @@ __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32
     sum += l;
   }
   uint64_t total = warp_sum_u32(sum);
-  if (!(opts & OPT_NO_HEADER)) {
-    Sink hs;
-    put_header(hs, m, hl);
-    total += hs.n;
-  }
+  if (!(opts & OPT_NO_HEADER)) total += header_len(m, hl);
   return total;
 }
 

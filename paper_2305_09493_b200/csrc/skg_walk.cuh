@@ -188,7 +188,10 @@ __device__ __noinline__ WalkErr walk(const Tables& T, uint32_t idef, const uint3
 #pragma unroll 1
           for (uint32_t j = 0; j < ne && j < 64; ++j) {
             uint32_t ev = T.evalue(eo + j);
-            if (ev && (mask & ev) == ev && (covered & ev) != ev) { comp |= 1ull << j; covered |= ev; }
+            if (ev && (mask & ev) == ev && (covered & ev) != ev) {
+              comp |= 1ull << j; covered |= ev;
+              if (covered == mask) break;   // later enumerants can only be skipped
+            }
           }
         }
         bool full = mask != 0 && covered == mask;
