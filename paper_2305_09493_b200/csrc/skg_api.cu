@@ -27,8 +27,6 @@ struct skg_tables {
 
 namespace {
 
-constexpr int kWarpsPerBlock = 4;
-constexpr uint32_t kSlabBytes = 18 * 1024;
 
 int g_sms = 0;
 
@@ -40,11 +38,6 @@ int sm_count() {
     if (g_sms <= 0) g_sms = 148;
   }
   return g_sms;
-}
-
-uint32_t grid_blocks() {
-  // persistent grid: 3 blocks of 4 warps per SM (16 KB shared slab per warp)
-  return (uint32_t)sm_count() * 3;
 }
 
 uint64_t gslot_bytes(uint32_t max_words) {
@@ -110,7 +103,7 @@ Geom fit_geom(uint32_t blocks, uint32_t warps, uint32_t n_mod, bool shrink_warps
   return {blocks, warps};
 }
 Geom dis_geom(uint32_t n_mod) { return fit_geom(dis_blocks(), (uint32_t)kDisWarps, n_mod, true); }
-Geom val_geom(uint32_t n_mod) { return fit_geom(grid_blocks(), (uint32_t)kWarpsPerBlock, n_mod, false); }
+Geom val_geom(uint32_t n_mod) { return fit_geom(dis_blocks(), (uint32_t)kDisWarps, n_mod, true); }
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
@@ -271,14 +264,12 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   a.err_cap = err_cap;
   a.gscratch = ws + l.scratch;
   a.gslot_bytes = l.slot;
-  a.smem_slab = kSlabBytes;
-  const size_t smem = (size_t)kSlabBytes * kWarpsPerBlock;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(skg::validate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  skg::validate_kernel<<<val_geom(n_mod).blocks, 32 * kWarpsPerBlock, smem, s>>>(a);
+  a.smem_slab = 0;
+  if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
+  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
+  const Geom g = val_geom(n_mod);
+  a.group_warps = group_warps((int)g.warps, env_int("SKG_VAL_GROUP", (int)g.warps));
+  skg::validate_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
 }
 

@@ -28,6 +28,8 @@ struct ValidateArgs {
   uint8_t* gscratch;
   uint64_t gslot_bytes;
   uint32_t smem_slab;
+  const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
+  uint32_t group_warps;       // warps per phase-barrier group
 };
 
 constexpr int MAX_CAPW = 6;
@@ -188,179 +190,173 @@ __device__ __noinline__ void shape_diags(S& s, const Shape& sh) {
   }
 }
 
-__global__ void __launch_bounds__(128) validate_kernel(ValidateArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// One module per warp; the CTA's warps run each phase together (CTA barrier
+// between phases), like disasm_kernel.  Scratch in the per-warp global slot.
+__device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket, uint8_t* gslot, ErrSink& es,
+                                          uint32_t gid, uint32_t gw) {
   const uint32_t lane = lane_id();
-  const uint32_t warp_in_block = threadIdx.x >> 5;
-  const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
-  uint8_t* slab = smem + (size_t)warp_in_block * a.smem_slab;
-  uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
   const Tables& T = a.T;
-  ErrSink es{a.errs, a.ticket + 1, a.err_cap};
-
-  while (true) {
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1u);
-    t = __shfl_sync(FULL, t, 0);
-    if (t >= a.n_mod) break;
-    const int64_t nbytes = a.mod_len[t];
+  const bool live = ticket < a.n_mod;
+  const uint32_t t = live ? a.order[ticket] : 0;
+  int32_t status = live ? ST_OK : ST_INTERNAL;
+  int32_t decode_status = ST_OK;
+  uint64_t total = 0;
+  Mod m;
+  Shape sh{};
+  uint64_t eff[MAX_CAPW] = {0, 0, 0, 0, 0, 0};
+  int64_t nbytes = 0;
+  // -- V0: load + boundary
+  if (live) {
+    nbytes = a.mod_len[t];
     const uint8_t* src = a.data + a.mod_off[t];
-    int32_t status = ST_OK;
-    uint64_t total = 0;
-    Mod m;
-    Shape sh{};
-    uint64_t eff[MAX_CAPW] = {0, 0, 0, 0, 0, 0};
-    int32_t decode_status = ST_OK;
     const uint32_t W = (nbytes >= 0 && nbytes % 4 == 0) ? (uint32_t)(nbytes / 4) : 0;
-    bool in_smem = head_bytes(W) <= a.smem_slab;
-    ErrRec* drec = nullptr;
-    if (!in_smem && worst_bytes(W, 0) > a.gslot_bytes) {
+    if (worst_bytes(W, 0) > a.gslot_bytes) {
       status = ST_INTERNAL;
+      ErrRec* drec = nullptr;
       if (lane == 0 && (drec = es.alloc())) {
         ErrWriter ew{drec};
         put_cstr(ew, "internal: module exceeds the per-warp scratch slot");
         drec->module = (int32_t)t; drec->cls = ST_INTERNAL; drec->len = ew.n;
       }
     } else {
-      layout_head(m, in_smem ? slab : gslot, W);
+      layout_head(m, gslot, W);
       decode_status = load_and_split(m, src, (uint64_t)nbytes, nullptr, (int32_t)t);
     }
-    if (status == ST_OK && decode_status == ST_OK) {
-      bool direct = m.bound <= 2 * m.W + 64;
-      for (int attempt = 0; attempt < 2; ++attempt) {
-        if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, 0)) {
-          status = ST_INTERNAL;
-          break;
+  }
+  group_sync(gid, gw);
+  // -- V1: id tables + prescan (hash tables when an id is at/above the bound)
+  const bool go = status == ST_OK && decode_status == ST_OK;
+  if (go) {
+    bool in_smem = false;
+    bool direct = m.bound <= 2 * m.W + 64;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, 0, 0)) { status = ST_INTERNAL; break; }
+      init_tables(m);
+      prescan(m, T);
+      if (*m.overflow && direct) { __syncwarp(); direct = false; continue; }
+      break;
+    }
+  }
+  group_sync(gid, gw);
+  // -- V2: module shape + effective capabilities (validate.py:101-136), sizes,
+  //        escaping exceptions, offsets
+  if (go && status == ST_OK) {
+    bool fn = false, cap = false, ep = false;
+    uint32_t mm = 0;
+    for (uint32_t base = 0; base < m.I; base += 32) {
+      uint32_t i = base + lane;
+      if (i >= m.I || m.idef[i] == NONE16) continue;
+      uint32_t sp = T.special(m.idef[i]);
+      fn |= sp == SP_FUNCTION;
+      ep |= sp == SP_ENTRYPOINT;
+      mm += sp == SP_MEMORYMODEL;
+      if (sp == SP_CAPABILITY) {
+        cap = true;
+        if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
+          uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
+          uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
+          if (cn != NONE32)
+            for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k) eff[k] |= __ldg(T.closure + cn * T.cap_words + k);
         }
-        init_tables(m);
-        prescan(m, T);
-        if (*m.overflow) {
-          __syncwarp();
-          direct = false;
-          continue;
-        }
-        // module shape + effective capabilities (validate.py:101-136)
-        bool fn = false, cap = false, ep = false;
-        uint32_t mm = 0;
-        for (uint32_t base = 0; base < m.I; base += 32) {
-          uint32_t i = base + lane;
-          if (i >= m.I || m.idef[i] == NONE16) continue;
-          uint32_t sp = T.special(m.idef[i]);
-          fn |= sp == SP_FUNCTION;
-          ep |= sp == SP_ENTRYPOINT;
-          mm += sp == SP_MEMORYMODEL;
-          if (sp == SP_CAPABILITY) {
-            cap = true;
-            if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
-              uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
-              uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
-              if (cn != NONE32)
-                for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k) eff[k] |= __ldg(T.closure + cn * T.cap_words + k);
-            }
-          }
-        }
-        sh.has_fn = __any_sync(FULL, fn);
-        sh.has_cap = __any_sync(FULL, cap);
-        sh.has_ep = __any_sync(FULL, ep);
-        sh.n_mm = warp_sum_u32(mm);
-        for (int k = 0; k < MAX_CAPW; ++k) {
-#pragma unroll
-          for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
-        }
-        sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
-        // sizes + escaping exceptions
-        for (uint32_t base = 0; base < m.I; base += 32) {
-          uint32_t i = base + lane;
-          if (i < m.I) {
-            CountSink cs;
-            WalkErr e = inst_diags(cs, m, T, i, eff);
-            m.ierr[i] = (uint8_t)e.code;
-            m.ia[i] = cs.n;
-          }
-        }
-        __syncwarp();
-        uint32_t bad = NONE32;
-        for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
-          uint32_t i = base + lane;
-          unsigned b = __ballot_sync(FULL, i < m.I && m.ierr[i] != W_OK && !werr_is_codec(m.ierr[i]));
-          if (b) bad = base + __ffs(b) - 1;
-        }
-        if (bad != NONE32) {
-          if (lane == 0) {
-            ErrRec* rec = es.alloc();
-            CountSink cs;
-            WalkErr e = inst_diags(cs, m, T, bad, eff);
-            status = walk_status(e.code);
-            if (rec) {
-              ErrWriter ew{rec};
-              put_walk_error(ew, T, m.idef[bad], e);
-              rec->module = (int32_t)t; rec->cls = status; rec->len = ew.n;
-              rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
-            }
-          }
-          status = __shfl_sync(FULL, status, 0);
-          break;
-        }
-        CountSink hs;
-        shape_diags(hs, sh);
-        uint64_t run = hs.n;
-        for (uint32_t base = 0; base < m.I; base += 32) {
-          uint32_t i = base + lane;
-          uint32_t len = i < m.I ? m.ia[i] : 0;
-          uint32_t incl = warp_incl_sum(len);
-          if (i < m.I) m.ia[i] = (uint32_t)(run + incl - len);
-          run += __shfl_sync(FULL, incl, 31);
-        }
-        __syncwarp();
-        total = run;
-        break;
       }
     }
-    // the decode error of the module is its only diagnostic line
-    if (status == ST_OK && decode_status != ST_OK) {
-      const char* code = decode_status == ST_NOTSPIRV ? "NotSpirv"
-                         : decode_status == ST_TRUNCATED ? "TruncatedStream" : "CorruptStream";
-      CountSink cs;
-      diag_head(cs, true, code, NONE32);
-      ErrRec tmp;
-      // recompute the message into a local record
-      {
-        ErrWriter ew{&tmp};
-        // identical text to load_and_split's
-        if (nbytes % 4 != 0 || nbytes < 20) {
-          put_u64(ew, (uint64_t)nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
-        } else if (decode_status == ST_NOTSPIRV) {
-          put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, m.w[0]); put_cstr(ew, " is not SPIR-V");
-        } else {
-          // re-walk to find the failing position
-          uint32_t p = 5;
-          while (p < m.W) {
-            uint32_t wc = m.w[p] >> 16;
-            if (wc == 0 || p + wc > m.W) break;
-            p += wc;
-          }
-          put_cstr(ew, "instruction at word "); put_u64(ew, p);
-          put_cstr(ew, decode_status == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
-        }
-        tmp.len = ew.n;
+    sh.has_fn = __any_sync(FULL, fn);
+    sh.has_cap = __any_sync(FULL, cap);
+    sh.has_ep = __any_sync(FULL, ep);
+    sh.n_mm = warp_sum_u32(mm);
+    for (int k = 0; k < MAX_CAPW; ++k) {
+#pragma unroll
+      for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
+    }
+    sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
+    for (uint32_t base = 0; base < m.I; base += 32) {
+      uint32_t i = base + lane;
+      if (i < m.I) {
+        CountSink cs;
+        WalkErr e = inst_diags(cs, m, T, i, eff);
+        m.ierr[i] = (uint8_t)e.code;
+        m.ia[i] = cs.n;
       }
-      total = cs.n + (uint32_t)tmp.len + 1;
-      bool fits;
-      uint64_t off = alloc_text(a.ticket, total, a.text_cap, fits);
+    }
+    __syncwarp();
+    uint32_t bad = NONE32;
+    for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
+      uint32_t i = base + lane;
+      unsigned b = __ballot_sync(FULL, i < m.I && m.ierr[i] != W_OK && !werr_is_codec(m.ierr[i]));
+      if (b) bad = base + __ffs(b) - 1;
+    }
+    if (bad != NONE32) {
       if (lane == 0) {
-        a.text_span[2 * t] = (int64_t)off;
-        a.text_span[2 * t + 1] = (int64_t)total;
-        a.status[t] = ST_OK;
-        if (fits) {
-          MemSink ms(a.text + off);
-          diag_head(ms, true, code, NONE32);
-          ms.putn((const uint8_t*)tmp.msg, (uint32_t)tmp.len);
-          ms.put('\n');
+        ErrRec* rec = es.alloc();
+        CountSink cs;
+        WalkErr e = inst_diags(cs, m, T, bad, eff);
+        status = walk_status(e.code);
+        if (rec) {
+          ErrWriter ew{rec};
+          put_walk_error(ew, T, m.idef[bad], e);
+          rec->module = (int32_t)t; rec->cls = status; rec->len = ew.n;
+          rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
         }
+      }
+      status = __shfl_sync(FULL, status, 0);
+    } else {
+      CountSink hs;
+      shape_diags(hs, sh);
+      uint64_t run = hs.n;
+      for (uint32_t base = 0; base < m.I; base += 32) {
+        uint32_t i = base + lane;
+        uint32_t len = i < m.I ? m.ia[i] : 0;
+        uint32_t incl = warp_incl_sum(len);
+        if (i < m.I) m.ia[i] = (uint32_t)(run + incl - len);
+        run += __shfl_sync(FULL, incl, 31);
       }
       __syncwarp();
-      continue;
+      total = run;
     }
+  }
+  group_sync(gid, gw);
+  // -- V3: output
+  if (live && status == ST_OK && decode_status != ST_OK) {
+    // the decode error of the module is its only diagnostic line
+    const char* code = decode_status == ST_NOTSPIRV ? "NotSpirv"
+                       : decode_status == ST_TRUNCATED ? "TruncatedStream" : "CorruptStream";
+    CountSink cs;
+    diag_head(cs, true, code, NONE32);
+    ErrRec tmp;
+    {
+      ErrWriter ew{&tmp};
+      // identical text to load_and_split's
+      if (nbytes % 4 != 0 || nbytes < 20) {
+        put_u64(ew, (uint64_t)nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
+      } else if (decode_status == ST_NOTSPIRV) {
+        put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, m.w[0]); put_cstr(ew, " is not SPIR-V");
+      } else {
+        uint32_t p = 5;   // re-walk to the failing position
+        while (p < m.W) {
+          uint32_t wc = m.w[p] >> 16;
+          if (wc == 0 || p + wc > m.W) break;
+          p += wc;
+        }
+        put_cstr(ew, "instruction at word "); put_u64(ew, p);
+        put_cstr(ew, decode_status == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
+      }
+      tmp.len = ew.n;
+    }
+    total = cs.n + (uint32_t)tmp.len + 1;
+    bool fits;
+    uint64_t off = alloc_text(a.ticket, total, a.text_cap, fits);
+    if (lane == 0) {
+      a.text_span[2 * t] = (int64_t)off;
+      a.text_span[2 * t + 1] = (int64_t)total;
+      a.status[t] = ST_OK;
+      if (fits) {
+        MemSink ms(a.text + off);
+        diag_head(ms, true, code, NONE32);
+        ms.putn((const uint8_t*)tmp.msg, (uint32_t)tmp.len);
+        ms.put('\n');
+      }
+    }
+  } else if (live) {
     if (status != ST_OK) total = 0;
     bool fits;
     uint64_t off = alloc_text(a.ticket, total, a.text_cap, fits);
@@ -369,20 +365,40 @@ __global__ void __launch_bounds__(128) validate_kernel(ValidateArgs a) {
       a.text_span[2 * t + 1] = (int64_t)total;
       a.status[t] = status;
     }
-    if (status == ST_OK && total > 0) {
-      if (!fits) {
-      } else {
-        uint8_t* out = a.text + off;
-        if (lane == 0) { MemSink ms(out); shape_diags(ms, sh); }
-        for (uint32_t base = 0; base < m.I; base += 32) {
-          uint32_t i = base + lane;
-          if (i >= m.I) continue;
-          MemSink ms(out + m.ia[i]);
-          inst_diags(ms, m, T, i, eff);
-        }
+    if (status == ST_OK && total > 0 && fits) {
+      uint8_t* out = a.text + off;
+      if (lane == 0) { MemSink ms(out); shape_diags(ms, sh); }
+      for (uint32_t base = 0; base < m.I; base += 32) {
+        uint32_t i = base + lane;
+        if (i >= m.I) continue;
+        MemSink ms(out + m.ia[i]);
+        inst_diags(ms, m, T, i, eff);
       }
     }
-    __syncwarp();
+  }
+  __syncwarp();
+  group_sync(gid, gw);
+}
+
+#ifndef SKG_VAL_MAXT
+#define SKG_VAL_MAXT 1024
+#endif
+__global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) {
+  __shared__ uint32_t s_base[16];
+  const uint32_t warps = blockDim.x >> 5;
+  const uint32_t warp_in_block = threadIdx.x >> 5;
+  const uint32_t gw = a.group_warps;
+  const uint32_t gid = warp_in_block / gw, gwarp_in = warp_in_block % gw;
+  const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
+  uint8_t* gslot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
+  ErrSink es{a.errs, a.ticket + 1, a.err_cap};
+  while (true) {
+    if (gwarp_in == 0 && lane_id() == 0) s_base[gid] = atomicAdd(a.ticket, gw);
+    group_sync(gid, gw);
+    const uint32_t base = s_base[gid];
+    group_sync(gid, gw);
+    if (base >= a.n_mod) break;
+    validate_one(a, base + gwarp_in, gslot, es, gid, gw);
   }
 }
 
