@@ -533,21 +533,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       ++nt;
       continue;
     }
-    // bare token: up to 4 bytes per (aligned word) load
     while (i < e0) {
-      const uintptr_t ad = reinterpret_cast<uintptr_t>(t + i);
-      const uint32_t sh = (uint32_t)(ad & 3);
-      const uint32_t x = *reinterpret_cast<const uint32_t*>(ad - sh) >> (8 * sh);
-      const uint32_t nb = min(4u - sh, e0 - i);
-      uint32_t k = 0;
-#pragma unroll
-      for (uint32_t q = 0; q < 4; ++q) {
-        const uint32_t d = (x >> (8 * q)) & 0xFF;
-        const bool delim = d < 64 && ((0x0800000500002600ull >> d) & 1);   // \t \n \r ' ' '"' ';'
-        if (k == q && q < nb && !delim) ++k;
-      }
-      i += k;
-      if (k < nb) break;
+      const uint32_t d = t[i];
+      if (d < 64 && ((0x0800000500002600ull >> d) & 1)) break;   // \t \n \r ' ' '"' ';'
+      ++i;
     }
     if (nt < cap) {   // cap = candidate bound of this line (split_lines)
       m.tok[2 * (tb + nt)] = start;
