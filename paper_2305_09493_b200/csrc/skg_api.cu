@@ -240,6 +240,12 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
     cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     attr = true;
   }
+  static bool carve = false;
+  if (!carve) {   // smallest shared-memory carveout that fits: the rest is L1 for the scratch
+    const int pct = env_int("SKG_CARVEOUT", -2);
+    if (pct != -2) cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    carve = true;
+  }
   skg::disasm_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
   return check(cudaGetLastError());
 }
@@ -269,6 +275,12 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   const Geom g = val_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_VAL_GROUP", (int)g.warps));
+  static bool carve = false;
+  if (!carve) {
+    const int pct = env_int("SKG_CARVEOUT", -2);
+    if (pct != -2) cudaFuncSetAttribute(skg::validate_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    carve = true;
+  }
   skg::validate_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
 }
@@ -315,6 +327,12 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.default_version = default_version;
   const Geom g = asm_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_ASM_GROUP", (int)g.warps));
+  static bool carve = false;
+  if (!carve) {
+    const int pct = env_int("SKG_CARVEOUT", -2);
+    if (pct != -2) cudaFuncSetAttribute(skg::asm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    carve = true;
+  }
   skg::asm_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
 }

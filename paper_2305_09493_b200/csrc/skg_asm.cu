@@ -2253,8 +2253,7 @@ end_h:
       }
     }
     if (fits) ow[at] = ((1 + m.lnw[li]) << 16) | __ldg(X.T.irec(d) + 5);
-    m.lerr[4 * li + 3] = bad_ref;
-    if (bad_ref != NONE32) ser_off = min(ser_off, at);
+    if (bad_ref != NONE32) { m.lerr[4 * li + 3] = bad_ref; ser_off = min(ser_off, at); }
   }
   ser_off = wmin(ser_off);
   wc_off = wmin(wc_off);
