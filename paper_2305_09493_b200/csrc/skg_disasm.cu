@@ -101,13 +101,30 @@ __device__ __forceinline__ uint32_t dlen32(uint32_t v) {
          v < 1000000 ? 6 : v < 10000000 ? 7 : v < 100000000 ? 8 : v < 1000000000 ? 9 : 10;
 }
 
-__device__ __forceinline__ uint32_t ref_len(const Mod& m, uint32_t id) {
+// per-slot ref text lengths for direct-mode modules (P5, before any length is needed)
+__device__ __noinline__ void fill_ref_lengths(Mod& m);
+
+__device__ __forceinline__ uint32_t ref_len_slow(const Mod& m, uint32_t id) {
   const uint32_t slot = ht_find(m, id);
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
     const uint32_t ser = m.hser[slot];
     return 1 + m.nLen[slot] + (ser != NONE32 ? 1 + dlen32(ser) : 0);
   }
   return 1 + dlen32(id);
+}
+
+__device__ __forceinline__ uint32_t ref_len(const Mod& m, uint32_t id) {
+  if (m.direct && id < m.S) { const uint32_t r = m.hrl[id]; if (r != 0xFFFF) return r; }
+  return ref_len_slow(m, id);
+}
+
+__device__ __noinline__ void fill_ref_lengths(Mod& m) {
+  if (!m.direct) return;
+  for (uint32_t s = lane_id(); s < m.S; s += 32) {
+    const uint32_t r = ref_len_slow(m, s);
+    m.hrl[s] = (uint16_t)(r > 0xFFFE ? 0xFFFF : r);
+  }
+  __syncwarp();
 }
 
 __device__ __noinline__ bool is_opencl_std(const Mod& m, const Tables& T, uint32_t set_id) {
@@ -689,7 +706,8 @@ __device__ __forceinline__ uint8_t* emit_tab(uint8_t* p, const Tables& T, uint32
 
 __device__ __noinline__ uint8_t* emit_ref(uint8_t* p, const Mod& m, uint32_t id) {
   *p++ = '%';
-  const uint32_t slot = ht_find(m, id);
+  // direct mode: a slot that is not present has hfl == 0 (init_tables)
+  const uint32_t slot = m.direct ? (id < m.S ? id : NONE32) : ht_find(m, id);
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
     const uint8_t* src = m.narena + m.hnoff[slot];
     const uint32_t n = m.nLen[slot];
@@ -933,6 +951,7 @@ __device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T
 
 // result ref of every instruction -> irl/ib/iflag, module width (disasm.py:286-288)
 __device__ __noinline__ uint32_t result_refs(Mod& m, const Tables& T) {
+  fill_ref_lengths(m);
   uint32_t width = 0;
   for (uint32_t base = 0; base < m.I; base += 32) {
     uint32_t i = base + lane_id();
