@@ -397,8 +397,12 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
     return ST_TRUNCATED;
   }
   const uint32_t W = (uint32_t)(nbytes / 4);
-  // 16-byte vector loads (module starts are 16-byte aligned in a batch)
-  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+  // little-endian, word-aligned input (the batch case): read the words in place
+  // (the input arena is read-only for the kernel; no scratch copy)
+  if ((reinterpret_cast<uintptr_t>(src) & 3) == 0 &&
+      __ldg(reinterpret_cast<const uint32_t*>(src)) == MAGIC) {
+    m.w = const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(src));
+  } else if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {   // 16-byte vector loads
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(m.w);
     const uint32_t n4 = W / 4;
