@@ -218,6 +218,24 @@ SKG_HD inline int digit_value(uint32_t c) {
 SKG_HD SKG_NOINLINE IntVal parse_int(const uint8_t* p, uint32_t n, uint32_t base, const Uni& U) {
   IntVal r{};
   r.status = INT_INVALID;
+  if ((base == 0 || base == 10) && n >= 1 && n <= 19) {   // fast path: [+-]?[1-9][0-9]* | [+-]?0
+    const uint32_t s0 = (p[0] == '-' || p[0] == '+') ? 1u : 0u;
+    const uint32_t nd = n - s0;
+    if (nd >= 1 && nd <= 18 && (p[s0] != '0' || nd == 1)) {
+      uint64_t v = 0;
+      uint32_t i = s0;
+      for (; i < n; ++i) {
+        const uint32_t d = (uint32_t)p[i] - '0';
+        if (d > 9) break;
+        v = v * 10 + d;
+      }
+      if (i == n) {
+        r.status = INT_OK; r.neg = p[0] == '-'; r.big = false; r.mag = v; r.base = 10;
+        r.ndig = nd; r.ds = s0; r.de = n;
+        return r;
+      }
+    }
+  }
   uint32_t i = 0, len = 1, c = 0;
   auto peek = [&](uint32_t at, uint32_t& l) -> uint32_t { return at < n ? xform(p, n, at, l, U) : 0u; };
   c = peek(i, len);
