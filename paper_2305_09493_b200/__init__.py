@@ -3,7 +3,8 @@
 
 from .asm import Assembler, assemble_batch, assemble_module
 from .codec import ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module
-from .disasm import Disassembler, DisassemblerOptions, disassemble_batch, disassemble_module
+from .disasm import (Disassembler, DisassemblerOptions, disassemble_batch, disassemble_module,
+                     format_instruction)
 from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,
                      GenerationError, GrammarError, GrammarParseError, GrammarSchemaError,
                      IdExhaustedError, NotFoundError, NotSpirvError, ScopeError,

@@ -45,6 +45,33 @@ def disassemble_batch(modules, options=None, spec=None, ext=None, strict=False):
             for r in _native.fetch_texts(res, batch.n)]
 
 
+def format_instruction(spec, inst, context=None, ext=None) -> str:
+    """One raw instruction as one plain-text line (reference disasm.py:380-389)
+    with the default, empty RenderContext: no friendly names, no type map, no
+    extended-instruction sets.  Rendered by skg_disasm on a one-instruction
+    module (no header, no indentation, numeric ids), which sees exactly that
+    empty context; decode errors raise the reference's exceptions."""
+    from . import grammar as _grammar
+    if context is not None:
+        raise NotImplementedError("format_instruction: only the default (empty) RenderContext "
+                                  "is supported by the GPU path")
+    spec = spec if spec is not None else _grammar.load_pinned()
+    spec.instruction(inst.opcode)          # NotFoundError outside the grammar, as the reference
+    ops = [int(w) & 0xFFFFFFFF for w in inst.operands]
+    if len(ops) + 1 > 0xFFFF:
+        raise ValueError("format_instruction: more than 65534 operand words")
+    bound = max(ops, default=0) + 1
+    words = [0x07230203, 0x00010200, 0, bound & 0xFFFFFFFF, 0,
+             ((len(ops) + 1) << 16) | (int(inst.opcode) & 0xFFFF), *ops]
+    import struct
+    module = struct.pack(f"<{len(words)}I", *words)
+    opts = DisassemblerOptions(inline_names=False, no_indent=True, no_header=True)
+    out = disassemble_batch([module], opts, spec, ext)[0]
+    if isinstance(out, BaseException):
+        raise out
+    return out[:-1] if out.endswith("\n") else out
+
+
 class Disassembler:
     def __init__(self, spec=None, ext=None, options=None, strict=False):
         self.spec, self.ext = spec, ext

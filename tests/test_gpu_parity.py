@@ -182,3 +182,16 @@ def test_huge_single_module_vs_oracle(sk):
     assert sk.disassemble_batch([m], opts)[0] == odis.disassemble(m, opts)
     d = sk.validate_batch([m])[0]
     assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(m)]
+
+
+def test_format_instruction_known_answers(sk):
+    """reference tests/test_disasm.py:23-41 known answers through the GPU path."""
+    from paper_2305_09493_b200 import CorruptStreamError, NotFoundError, RawInstruction, load_pinned
+    spec = load_pinned()
+    assert sk.format_instruction(spec, RawInstruction(17, (6,))) == "OpCapability Kernel"
+    assert sk.format_instruction(spec, RawInstruction(0, ())) == "OpNop"
+    assert sk.format_instruction(spec, RawInstruction(54, (1, 2, 3, 3))) == "%2 = OpFunction %1 Inline|DontInline %3"
+    with pytest.raises(CorruptStreamError):
+        sk.format_instruction(spec, RawInstruction(17, (6, 7)))
+    with pytest.raises(NotFoundError):
+        sk.format_instruction(spec, RawInstruction(65520, ()))
