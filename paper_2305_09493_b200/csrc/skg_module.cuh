@@ -602,38 +602,4 @@ __device__ inline uint64_t alloc_text(uint32_t* counters, uint64_t bytes, uint64
   return off;
 }
 
-// decoupled look-back over module tickets: returns the exclusive prefix of `agg`
-// (state: bit 62 = aggregate ready, bit 63 = inclusive ready, low 62 bits value)
-__device__ inline uint64_t lookback(unsigned long long* state, uint32_t ticket, uint64_t agg) {
-  constexpr uint64_t FA = 1ull << 62, FP = 1ull << 63, VM = FA - 1;
-  const uint32_t lane = lane_id();
-  if (ticket == 0) {
-    if (lane == 0) atomicExch(state, FP | agg);
-    return 0;
-  }
-  if (lane == 0) atomicExch(state + ticket, FA | agg);
-  uint64_t excl = 0;
-  int64_t j = (int64_t)ticket - 1;
-  while (true) {
-    int64_t idx = j - (int64_t)lane;
-    uint64_t v = idx >= 0 ? *((volatile unsigned long long*)(state + idx)) : FP;
-    bool ready = (v & (FA | FP)) != 0;
-    bool incl = (v & FP) != 0;
-    unsigned not_ready = __ballot_sync(FULL, !ready);
-    unsigned incl_mask = __ballot_sync(FULL, incl);
-    // lanes up to (and including) the first inclusive one are usable if all ready
-    int first_incl = incl_mask ? __ffs(incl_mask) - 1 : 32;
-    unsigned usable = first_incl == 32 ? FULL : ((first_incl == 31) ? FULL : ((1u << (first_incl + 1)) - 1));
-    if (not_ready & usable) continue;   // spin until the window is ready
-    uint64_t part = (lane <= (uint32_t)first_incl && idx >= 0) ? (v & VM) : 0;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(FULL, part, d);
-    excl += part;
-    if (first_incl < 32) break;
-    j -= 32;
-  }
-  if (lane == 0) atomicExch(state + ticket, FP | (excl + agg));
-  return excl;
-}
-
 }  // namespace skg

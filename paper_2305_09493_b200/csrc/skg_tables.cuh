@@ -16,38 +16,6 @@ __device__ __forceinline__ void group_sync(uint32_t group, uint32_t warps) {
   asm volatile("bar.sync %0, %1;" :: "r"(1 + group), "r"(32 * warps) : "memory");
 }
 
-// Sequential byte reader over global memory: keeps the current aligned
-// 16-byte block in registers, so a byte loop issues one 16-byte load per 16
-// bytes instead of one dependent load per byte (the kernels are latency
-// bound).  Reads whole aligned blocks, i.e. up to 15 bytes around the string:
-// callers only read inside 16-byte padded arenas / the table blob.
-struct Rd16 {
-  const uint4* b;
-  uint32_t off;
-  mutable uint32_t cur;
-  mutable uint4 v;
-  __device__ __forceinline__ explicit Rd16(const uint8_t* p)
-      : b(reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15)),
-        off((uint32_t)(reinterpret_cast<uintptr_t>(p) & 15)), cur(0xFFFFFFFFu) {}
-  __device__ __forceinline__ uint32_t word(uint32_t j) const {   // j = aligned word index from b
-    const uint32_t blk = j >> 2;
-    if (blk != cur) { v = b[blk]; cur = blk; }
-    const uint32_t q = j & 3;
-    return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
-  }
-  __device__ __forceinline__ uint32_t operator()(uint32_t i) const {
-    const uint32_t j = i + off;
-    return (word(j >> 2) >> ((j & 3) * 8)) & 0xFF;
-  }
-  // 4 bytes starting at byte i (little-endian), any alignment
-  __device__ __forceinline__ uint32_t u32(uint32_t i) const {
-    const uint32_t j = i + off;
-    const uint32_t lo = word(j >> 2);
-    if ((j & 3) == 0) return lo;
-    const uint32_t hi = word((j >> 2) + 1);
-    return __funnelshift_r(lo, hi, (j & 3) * 8);
-  }
-};
 
 // instruction special codes (tables.py SPECIAL)
 enum : uint32_t {
