@@ -751,7 +751,7 @@ __device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id)
   if (e != NONE32 && c.m.nt[NT_W * e + 3] != 0) { id = c.m.nt[NT_W * e + 3]; return true; }
   if (c.mode == M_RESOLVE) {
     AsmMod& mm = const_cast<AsmMod&>(c.m);
-    if (2 * (mm.misc[MS_NTCOUNT] + 1) > mm.ncap && !nt_grow(mm)) return enc_fail(c, E_INTERNAL, t);
+    if (4 * (mm.misc[MS_NTCOUNT] + 1) > 3 * mm.ncap && !nt_grow(mm)) return enc_fail(c, E_INTERNAL, t);
     ++mm.misc[MS_NTCOUNT];
     const uint32_t s = nt_insert(c.m, t);
     uint32_t* ent = c.m.nt + NT_W * s;
@@ -1930,8 +1930,8 @@ end_a:
   }
   npct = wsum(npct);
   nres = wsum(nres);
-  m.ncap = 64;   // result names (+ unresolved operand names: lane 0 grows the table)
-  while (m.ncap < 2 * nres + 32) m.ncap <<= 1;
+  m.ncap = 32;   // result names at load <= 2/3 (+ unresolved operand names: lane 0 grows the table)
+  while (2 * m.ncap < 3 * nres + 48) m.ncap <<= 1;
   if (lane == 0) m.misc[MS_NTCOUNT] = nres;
   m.nt = reinterpret_cast<uint32_t*>(take(4ull * NT_W * m.ncap));
   // formatting scratch (lane 0, error paths): big integers of the longest token
