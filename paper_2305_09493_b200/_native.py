@@ -233,6 +233,38 @@ def make_exception(status, msg, a=0, b=0, c=0, d=0):
     return RuntimeError(f"libskgpu internal error: {msg}")
 
 
+# Workspace budget of one launch: the per-warp scratch slot is sized for the
+# largest module, so a batch mixing a few very large modules with many small
+# ones runs the large ones in launches of their own (one warp each).
+WS_BUDGET = 8 << 30
+
+
+def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
+    """disasm / validate of a device batch -> list of (text bytes | exception)."""
+    torch = _torch()
+    n = batch.n
+    if n == 0:
+        return []
+    run = (lambda b: run_disasm(b, opts, spec, ext)) if kind == "disasm" else (lambda b: run_validate(b, spec))
+    need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
+    if n == 1 or need <= WS_BUDGET:
+        return fetch_texts(run(batch), n)
+    lens = batch.len.cpu().numpy()
+    words = lens // 4
+    per_word = max(need // max(int(batch.max_words), 1), 1)        # workspace bytes per max-word
+    w_small = max(int(WS_BUDGET // per_word), 1)
+    out = [None] * n
+    small = np.nonzero(words <= w_small)[0]
+    groups = [small] if len(small) else []
+    groups += [np.array([i]) for i in np.nonzero(words > w_small)[0]]
+    for idx in groups:
+        ti = torch.from_numpy(idx.astype(np.int64)).to(batch.off.device)
+        sub = DeviceBatch(batch.data, batch.off[ti], batch.len[ti], int(words[idx].max()), int(lens[idx].sum()))
+        for k, r in zip(idx, fetch_texts(run(sub), len(idx))):
+            out[int(k)] = r
+    return out
+
+
 def fetch_texts(res: TextResult, n: int):
     """Host copies: list of (text bytes | exception) per module."""
     span = res.span.cpu().numpy()
@@ -460,7 +492,13 @@ def run_asm(texts, spec=None, ext=None, default_version=(1, 2)):
         return []
     batch = DeviceBatch.from_host(buf, off, ln)
     batch.max_words = (int(ln.max()) + 3) // 4
-    plan = AsmPlan(batch, spec, ext, default_version=default_version)
+    # per-warp slot for the largest text, capped by the workspace budget; modules
+    # that need more report ST_INTERNAL and are rerun alone with larger slots below
+    L = _bind_asm(lib())
+    hint = int(L.skg_asm_slot_hint(int(batch.max_words) * 4 + 16))
+    n_warps = int(L.skg_asm_workspace_bytes(1, n)) - int(L.skg_asm_workspace_bytes(0, n))   # slots
+    per_warp_cap = max(1 << 20, WS_BUDGET // max(n_warps, 1))
+    plan = AsmPlan(batch, spec, ext, slot_bytes=min(hint, per_warp_cap), default_version=default_version)
     plan.fit()
     status = plan.status[:n].cpu().numpy()
     span = plan.span[: 2 * n].cpu().numpy()

@@ -40,9 +40,8 @@ def disassemble_batch(modules, options=None, spec=None, ext=None, strict=False):
     """list[bytes] -> list[str | Exception] (exception instances, not raised)."""
     batch = modules if isinstance(modules, _native.DeviceBatch) else \
         _native.DeviceBatch.from_modules([bytes(m) for m in modules])
-    res = _native.run_disasm(batch, option_bits(options, strict), spec, ext)
     return [r if isinstance(r, BaseException) else r.decode("utf-8")
-            for r in _native.fetch_texts(res, batch.n)]
+            for r in _native.run_texts("disasm", batch, option_bits(options, strict), spec, ext)]
 
 
 def format_instruction(spec, inst, context=None, ext=None) -> str:

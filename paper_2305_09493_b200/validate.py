@@ -46,9 +46,8 @@ def validate_batch(modules, spec=None):
     """list[bytes] -> list[list[Diagnostic] | Exception]."""
     batch = modules if isinstance(modules, _native.DeviceBatch) else \
         _native.DeviceBatch.from_modules([_as_bytes(m) for m in modules])
-    res = _native.run_validate(batch, spec)
     return [r if isinstance(r, BaseException) else _parse(r.decode("utf-8"))
-            for r in _native.fetch_texts(res, batch.n)]
+            for r in _native.run_texts("validate", batch, 0, spec)]
 
 
 def validate_module(module, spec=None):

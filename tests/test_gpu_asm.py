@@ -204,3 +204,25 @@ def test_roundtrip_session_pipelined(sk):
                 if i % 111 == 0:
                     assert t == odis.disassemble(m)
         assert int(np.sum(tspan[:, 1])) <= len(text)
+
+
+def test_asm_mixed_batch_with_large_text(sk, monkeypatch):
+    """Small texts plus one large one: the per-warp slot is capped by the workspace
+    budget and the large module is re-run alone with a larger slot."""
+    from oracle import disasm as odis
+    from paper_2305_09493_b200 import _native
+    from synth.families import FAMILIES, build_module
+    from synth.huge import build_huge
+    monkeypatch.setattr(_native, "WS_BUDGET", 256 << 20)
+    mods = [build_module(f, s) for f in FAMILIES for s in range(2)]
+    mods.insert(3, build_huge(60, chain=150, seed=2))
+    texts = [odis.disassemble(m) for m in mods]
+    got = sk.assemble_batch(texts)
+    for t, m, g in zip(texts, mods, got):
+        if g != m:   # the huge module is not builder-canonical: compare with the oracle assembler
+            from oracle import asm as oasm
+            try:
+                want = oasm.assemble(t)
+            except Exception as exc:   # noqa: BLE001
+                want = exc
+            assert (type(g), str(g)) == (type(want), str(want)) if isinstance(want, Exception) else g == want

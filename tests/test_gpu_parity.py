@@ -195,3 +195,21 @@ def test_format_instruction_known_answers(sk):
         sk.format_instruction(spec, RawInstruction(17, (6, 7)))
     with pytest.raises(NotFoundError):
         sk.format_instruction(spec, RawInstruction(65520, ()))
+
+
+def test_mixed_batch_with_large_module(sk, monkeypatch):
+    """A batch mixing small modules with one large one (separate launch when the
+    shared per-warp slot would exceed the workspace budget)."""
+    from oracle import disasm as odis
+    from paper_2305_09493_b200 import _native
+    from synth.families import FAMILIES, build_module
+    from synth.huge import build_huge
+    monkeypatch.setattr(_native, "WS_BUDGET", 64 << 20)
+    mods = [build_module(f, s) for f in FAMILIES for s in range(3)]
+    big = build_huge(40, chain=100, seed=5)
+    mods.insert(4, big)
+    got = sk.disassemble_batch(mods)
+    for m, g in zip(mods, got):
+        assert g == odis.disassemble(m)
+    val = sk.validate_batch(mods)
+    assert all(isinstance(v, list) for v in val)
