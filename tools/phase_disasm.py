@@ -23,8 +23,17 @@ def build():
 
 
 def batch(n):
+    import numpy as np
     from paper_2305_09493_b200 import _native
     from synth.families import sample_batch
+    if n < 0:   # one config-3 module of -n functions (synth/huge.py)
+        from synth.huge import build_huge
+        m = build_huge(-n)
+
+        class B:
+            words = len(m) // 4
+        data = np.frombuffer(m + b"\0" * 16, dtype=np.uint8)
+        return B, _native.DeviceBatch.from_host(data, np.array([0], np.int64), np.array([len(m)], np.int64))
     b = sample_batch(n, min(n, 2000), 20261017)
     return b, _native.DeviceBatch.from_host(b.data, b.offsets, b.lengths)
 
@@ -52,7 +61,7 @@ def main():
         L.skg_debug_disasm_phases(arr)
         tot = sum(arr) or 1
         for k, name in enumerate(PH):
-            print(f"{name:20s} {100 * arr[k] / tot:6.2f}%  {arr[k] / n:12.0f} warp-cycles/module")
+            print(f"{name:20s} {100 * arr[k] / tot:6.2f}%  {arr[k] / abs(n):12.0f} warp-cycles/module")
         return
     for _ in range(3):
         plan.launch()
