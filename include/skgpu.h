@@ -132,6 +132,23 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
             int32_t* status, void* workspace, uint64_t workspace_bytes, void* stream,
             uint32_t default_version);
 
+/* decode_module for ONE large module (config-3 sizes), parallel over 4096-word
+ * tiles of the stream: speculative per-tile boundary walks, a sequential link
+ * pass that only walks until the true chain merges with a tile's speculative
+ * chain, then per-tile count / scan / write (skg_bigdecode.cuh).
+ * Replaces: codec.decode_module (reference codec.py:199-231) like skg_decode,
+ * for one module of nbytes bytes at `data` (device).  max_opcode (the grammar's
+ * largest opcode, 0 = no filter) only steers the speculation, never the result.
+ * header[5] = major, minor,
+ * generator, bound, schema; words_out[nbytes/4] = byte-order-normalised words;
+ * inst_off[*inst_count] = instruction start offsets; *status = SKG_ST_*, and on
+ * failure *error holds the exact message.  `workspace` must hold
+ * skg_decode_large_workspace_bytes(nbytes / 4). */
+uint64_t skg_decode_large_workspace_bytes(uint64_t n_words);
+int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, uint32_t* header,
+                     uint32_t* inst_off, uint32_t* inst_count, uint32_t* words_out, int32_t* status,
+                     skg_error* error, void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,
  * and the text bytes the batch needs (allocator cursor). */

@@ -54,8 +54,12 @@ def lib():
     L.skg_validate.argtypes = [P, P, P, P, U32, U32, P, U64, P, P, P, U32, P, U64, P]
     L.skg_decode.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, U32, P, U64, P]
     L.skg_last_counts.argtypes = [P, ctypes.POINTER(U32), ctypes.POINTER(U32), ctypes.POINTER(U64), P]
+    L.skg_decode_large_workspace_bytes.argtypes = [U64]
+    L.skg_decode_large_workspace_bytes.restype = U64
+    L.skg_decode_large.argtypes = [P, U64, U32, P, P, P, P, P, P, P, U64, P]
     L.skg_version.restype = ctypes.c_char_p
-    for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts):
+    for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
+              L.skg_decode_large):
         f.restype = I32
     _lib = L
     return L
@@ -281,6 +285,9 @@ def fetch_texts(res: TextResult, n: int):
     return out
 
 
+LARGE_DECODE_WORDS = 1 << 16   # modules this size and up take the tiled boundary pass
+
+
 def run_decode(data: bytes):
     """Single-module boundary pass -> (header tuple, words array, [(start, wc)]) or raises."""
     torch = _torch()
@@ -290,6 +297,8 @@ def run_decode(data: bytes):
     dev = torch.device("cuda")
     pad = bytes(data) + b"\x00" * (-n % 16 + 16)
     d = torch.frombuffer(bytearray(pad), dtype=torch.uint8).to(dev)
+    if W >= LARGE_DECODE_WORDS:
+        return _run_decode_large(d, n)
     meta = torch.tensor([0, n, 0], dtype=torch.int64, device=dev)   # off, len, base
     header = torch.zeros(5, dtype=torch.int32, device=dev)
     inst_off = torch.zeros(max(W, 1), dtype=torch.int32, device=dev)
@@ -309,6 +318,32 @@ def run_decode(data: bytes):
     k = int(cnt.item())
     return tuple(int(x) for x in h), words.cpu().numpy().view(np.uint32)[:W], \
         inst_off.cpu().numpy().view(np.uint32)[:k]
+
+
+def _run_decode_large(d, n: int):
+    """skg_decode_large: one large module already on the device (tiled boundary pass)."""
+    torch = _torch()
+    L = lib()
+    W = n // 4
+    dev = d.device
+    header = torch.zeros(5, dtype=torch.int32, device=dev)
+    inst_off = torch.zeros(max(W, 1), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    words = torch.zeros(max(W, 1), dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    errs = torch.zeros(256, dtype=torch.uint8, device=dev)
+    ws_bytes = int(L.skg_decode_large_workspace_bytes(W))
+    ws = _ws.get(ws_bytes)
+    from . import grammar as _grammar
+    max_op = max((i.opcode for i in _grammar.load_pinned().instructions), default=0)
+    _check(L.skg_decode_large(d.data_ptr(), n, max_op, header.data_ptr(), inst_off.data_ptr(), cnt.data_ptr(),
+                              words.data_ptr(), status.data_ptr(), errs.data_ptr(), ws.data_ptr(), ws_bytes,
+                              _stream()), "decode_large")
+    if int(status.item()) != ST_OK:
+        raise decode_errors(errs.cpu().numpy())[0]
+    k = int(cnt.item())
+    return tuple(int(x) for x in header.cpu().numpy().view(np.uint32)), \
+        words.cpu().numpy().view(np.uint32)[:W], inst_off.cpu().numpy().view(np.uint32)[:k]
 
 
 __all__ = ["lib", "DeviceBatch", "run_disasm", "run_validate", "run_decode", "fetch_texts",

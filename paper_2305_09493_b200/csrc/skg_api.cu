@@ -6,6 +6,7 @@
 #include "../../include/skgpu.h"
 #include "skg_module.cuh"
 #include "skg_sched.cuh"
+#include "skg_bigdecode.cuh"
 
 namespace skg {
 struct DisasmArgs;
@@ -335,6 +336,45 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
     carve = true;
   }
   skg::asm_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+uint64_t skg_decode_large_workspace_bytes(uint64_t n_words) {
+  const uint64_t nt = (n_words + skg::BD_TILE - 1) / skg::BD_TILE;
+  return 256 + nt * skg::BD_TILE + 3 * 4 * skg::BD_K * nt + 3 * 4 * nt + 256;
+}
+
+int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, uint32_t* header,
+                     uint32_t* inst_off, uint32_t* inst_count, uint32_t* words_out, int32_t* status,
+                     skg_error* error, void* workspace, uint64_t workspace_bytes, void* stream) {
+  const uint64_t W64 = nbytes / 4;
+  if (!workspace || !data || W64 > 0xFFFFFFF0ull) return -1;
+  if (workspace_bytes < skg_decode_large_workspace_bytes(W64)) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  skg::BigDecode b;
+  b.src = data; b.nbytes = nbytes; b.W = (uint32_t)W64; b.words = words_out; b.inst_off = inst_off;
+  b.ntiles = (uint32_t)((W64 + skg::BD_TILE - 1) / skg::BD_TILE);
+  uint8_t* ws = (uint8_t*)workspace;
+  b.result = reinterpret_cast<uint32_t*>(ws);
+  b.max_opcode = max_opcode ? max_opcode : 0xFFFFu;
+  b.chain = ws + 256;
+  uint32_t* q = reinterpret_cast<uint32_t*>(ws + 256 + (uint64_t)b.ntiles * skg::BD_TILE);
+  b.spec_exit = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.spec_err = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.spec_errc = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.entry = q; q += b.ntiles;
+  b.count = q; q += b.ntiles;
+  const uint32_t tb = 128, tg = (b.ntiles + tb - 1) / tb;
+  skg::big_prologue<<<1, 32, 0, s>>>(b);
+  if (b.W >= 5) {
+    skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
+    skg::tile_spec<<<tg, tb, 0, s>>>(b);
+    skg::tile_link<<<1, 32, 0, s>>>(b);
+    skg::tile_count<<<tg, tb, 0, s>>>(b);
+    skg::tile_scan<<<1, 1024, 0, s>>>(b);
+    skg::tile_write<<<tg, tb, 0, s>>>(b);
+  }
+  skg::big_epilogue<<<1, 32, 0, s>>>(b, header, inst_count, status, reinterpret_cast<skg::ErrRec*>(error));
   return check(cudaGetLastError());
 }
 

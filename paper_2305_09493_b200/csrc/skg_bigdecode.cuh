@@ -1,0 +1,234 @@
+// Instruction-boundary pass for ONE large module (decode_module on config-3
+// sizes; reference codec.py:199-231), parallel over tiles of the word stream.
+//
+// The boundary chain p -> p + (w[p] >> 16) is a linked list, not a prefix sum,
+// so it is split speculatively (hard part 1):
+//   1. big_copy      byte-order-normalised words, grid-stride
+//   2. tile_spec     per tile (thread per tile): walk the chains from the tile's
+//                    first BD_K plausible starts (word count >= 1, opcode <= the
+//                    grammar's largest) to the tile end, marking the positions
+//                    each visits (a later chain stops where it joins an earlier
+//                    one) -> per chain the exit X and the first error on it
+//   3. tile_link     one thread, tiles in order: from the true entry e_t walk the
+//                    exact rule until the walk lands on a marked position (from
+//                    there that speculative chain IS the true chain: entry of
+//                    the next tile = its X, and its recorded error is the true
+//                    first error) or leaves the tile.  Typically a few steps per
+//                    tile; a tile whose speculation never merges is walked in full.
+//   4. tile_count    per tile: instructions on the true chain in the tile
+//   5. tile_scan     exclusive scan of the counts (one CTA)
+//   6. tile_write    per tile: the instruction offsets
+// Errors are the first wc == 0 / overrun on the true chain, with the word
+// position and message the reference raises.
+#pragma once
+#include <cstdint>
+
+namespace skg {
+
+constexpr uint32_t BD_TILE = 4096;          // words per tile
+constexpr uint32_t BD_K = 4;                // speculative chains per tile
+constexpr uint32_t BD_SCAN = 64;            // words searched for plausible starts
+constexpr uint32_t BD_NONE = 0xFFFFFFFFu;
+
+struct BigDecode {
+  const uint8_t* src;
+  uint32_t W;
+  uint32_t* words;           // W normalised words
+  uint32_t ntiles;
+  uint8_t* chain;            // ntiles * BD_TILE: 1 + speculative chain visiting the word, or 0
+  uint32_t* spec_exit;       // per tile and chain: first chain position >= tile end (BD_NONE: error)
+  uint32_t* spec_err;        // per tile and chain: first error position on the chain (BD_NONE: none)
+  uint32_t* spec_errc;       // per tile and chain: ST_CORRUPT / ST_TRUNCATED
+  uint32_t max_opcode;       // plausibility filter for speculative starts (0xFFFF: none)
+  uint32_t* entry;           // per tile: first true-chain position in the tile (BD_NONE: none)
+  uint32_t* count;           // per tile: instructions, then exclusive offsets
+  uint32_t* result;          // [0] status, [1] error position, [2] instruction count, [3] byte swap
+  uint32_t* inst_off;
+  uint64_t nbytes;
+};
+
+// length and magic checks (codec.py:199-216); result[0] gates every later kernel
+__global__ void big_prologue(BigDecode b) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t st = ST_OK, swap = 0;
+  if (b.nbytes % 4 != 0 || b.nbytes < 20) {
+    st = ST_TRUNCATED;
+  } else {
+    const uint8_t* p = b.src;
+    const uint32_t w0 = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+    if (w0 != MAGIC) {
+      if (__byte_perm(w0, 0, 0x0123) == MAGIC) swap = 1; else { st = ST_NOTSPIRV; b.result[1] = w0; }
+    }
+  }
+  b.result[0] = st;
+  b.result[2] = 0;
+  b.result[3] = swap;
+}
+
+__global__ void big_copy(BigDecode b) {
+  if (b.result[0] != ST_OK) return;
+  const bool swap = b.result[3] != 0;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(b.src);
+  const bool aligned = (reinterpret_cast<uintptr_t>(b.src) & 3) == 0;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < b.W; k += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v;
+    if (aligned) {
+      v = __ldcs(s + k);
+    } else {
+      const uint8_t* p = b.src + 4 * k;
+      v = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+    }
+    b.words[k] = swap ? __byte_perm(v, 0, 0x0123) : v;
+  }
+}
+
+__global__ void tile_spec(BigDecode b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= b.ntiles || b.result[0] != ST_OK) return;
+  const uint32_t lo = t * BD_TILE, hi = min(lo + BD_TILE, b.W);
+  uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;
+  uint4* cm4 = reinterpret_cast<uint4*>(cm);
+  for (uint32_t k = 0; k < BD_TILE / 16; ++k) cm4[k] = make_uint4(0, 0, 0, 0);
+  uint32_t* ex = b.spec_exit + (uint64_t)t * BD_K;
+  uint32_t* er = b.spec_err + (uint64_t)t * BD_K;
+  uint32_t* ec = b.spec_errc + (uint64_t)t * BD_K;
+  uint32_t s = t == 0 ? 5 : lo;   // tile 0: the true chain itself
+  for (uint32_t k = 0; k < BD_K; ++k) {
+    ex[k] = BD_NONE; er[k] = BD_NONE; ec[k] = 0;
+    if (t != 0 || k != 0) {       // next plausible start
+      while (s < hi && s < lo + BD_SCAN) {
+        const uint32_t x = b.words[s];
+        if ((x >> 16) != 0 && (x & 0xFFFF) <= b.max_opcode && cm[s - lo] == 0) break;
+        ++s;
+      }
+      if (s >= hi || s >= lo + BD_SCAN) break;
+    }
+    uint32_t p = s;
+    ++s;
+    while (p < hi) {
+      const uint32_t c = cm[p - lo];
+      if (c) { ex[k] = ex[c - 1]; er[k] = er[c - 1]; ec[k] = ec[c - 1]; break; }   // joins chain c-1
+      cm[p - lo] = (uint8_t)(k + 1);
+      const uint32_t wc = b.words[p] >> 16;
+      if (wc == 0) { er[k] = p; ec[k] = ST_CORRUPT; break; }
+      if ((uint64_t)p + wc > b.W) { er[k] = p; ec[k] = ST_TRUNCATED; break; }
+      p += wc;
+    }
+    if (p >= hi) ex[k] = p;
+    if (t == 0) break;
+  }
+}
+
+__global__ void tile_link(BigDecode b) {
+  if (blockIdx.x != 0 || threadIdx.x != 0 || b.result[0] != ST_OK) return;
+  uint32_t e = 5, status = ST_OK, errpos = 0;
+  for (uint32_t t = 0; t < b.ntiles; ++t) {
+    const uint32_t lo = t * BD_TILE, hi = min(lo + BD_TILE, b.W);
+    if (status != ST_OK || e >= hi) { b.entry[t] = BD_NONE; continue; }
+    b.entry[t] = e;
+    const uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;
+    uint32_t p = e, c = 0;
+    while (p < hi) {
+      if ((c = cm[p - lo]) != 0) break;
+      const uint32_t wc = b.words[p] >> 16;
+      if (wc == 0) { status = ST_CORRUPT; errpos = p; break; }
+      if ((uint64_t)p + wc > b.W) { status = ST_TRUNCATED; errpos = p; break; }
+      p += wc;
+    }
+    if (status != ST_OK) continue;
+    if (c) {   // on speculative chain c - 1 from here on
+      const uint64_t q = (uint64_t)t * BD_K + (c - 1);
+      if (b.spec_err[q] != BD_NONE) { status = b.spec_errc[q]; errpos = b.spec_err[q]; continue; }
+      e = b.spec_exit[q];
+    } else {
+      e = p;
+    }
+  }
+  b.result[0] = status;
+  b.result[1] = errpos;
+}
+
+__global__ void tile_count(BigDecode b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= b.ntiles) return;
+  uint32_t c = 0;
+  if (b.result[0] == ST_OK && b.entry[t] != BD_NONE) {
+    const uint32_t hi = min(t * BD_TILE + BD_TILE, b.W);
+    for (uint32_t p = b.entry[t]; p < hi; p += b.words[p] >> 16) ++c;
+  }
+  b.count[t] = c;
+}
+
+// exclusive scan of count[0..ntiles) in place; total into result[2] (one CTA of 1024)
+__global__ void __launch_bounds__(1024) tile_scan(BigDecode b) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < b.ntiles; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < b.ntiles ? b.count[i] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if (lane >= (uint32_t)d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t s = wsum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, d);
+        if (lane >= (uint32_t)d) s += y;
+      }
+      wsum[lane] = s;
+    }
+    __syncthreads();
+    const uint32_t c0 = carry;
+    if (i < b.ntiles) b.count[i] = c0 + x - v + (warp ? wsum[warp - 1] : 0);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c0 + wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) b.result[2] = carry;
+}
+
+__global__ void tile_write(BigDecode b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= b.ntiles || b.result[0] != ST_OK || b.entry[t] == BD_NONE) return;
+  const uint32_t hi = min(t * BD_TILE + BD_TILE, b.W);
+  uint32_t k = b.count[t];
+  for (uint32_t p = b.entry[t]; p < hi; p += b.words[p] >> 16) b.inst_off[k++] = p;
+}
+
+// header, count, status and the exact error text (codec.py:82-89, 199-231)
+__global__ void big_epilogue(BigDecode b, uint32_t* header, uint32_t* inst_count, int32_t* status, ErrRec* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t st = b.result[0];
+  *status = (int32_t)st;
+  *inst_count = st == ST_OK ? b.result[2] : 0;
+  if (st == ST_OK) {
+    header[0] = (b.words[1] >> 16) & 0xFF;
+    header[1] = (b.words[1] >> 8) & 0xFF;
+    header[2] = b.words[2];
+    header[3] = b.words[3];
+    header[4] = b.words[4];
+    return;
+  }
+  if (!err) return;
+  ErrWriter ew{err};
+  if (st == ST_TRUNCATED && (b.nbytes % 4 != 0 || b.nbytes < 20)) {
+    put_u64(ew, b.nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
+  } else if (st == ST_NOTSPIRV) {
+    put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, b.result[1]); put_cstr(ew, " is not SPIR-V");
+  } else {
+    put_cstr(ew, "instruction at word "); put_u64(ew, b.result[1]);
+    put_cstr(ew, st == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
+  }
+  err->module = 0; err->cls = (int32_t)st; err->len = ew.n;
+}
+
+}  // namespace skg

@@ -213,3 +213,38 @@ def test_mixed_batch_with_large_module(sk, monkeypatch):
         assert g == odis.disassemble(m)
     val = sk.validate_batch(mods)
     assert all(isinstance(v, list) for v in val)
+
+
+def test_decode_large_module_tiled(sk):
+    """decode_module on large modules takes the tiled boundary pass (skg_decode_large):
+    same instructions as the oracle, LE and BE, and the exact first error."""
+    import struct
+    from oracle import core
+    from synth.huge import build_huge
+    m = build_huge(300, chain=200, seed=4)          # ~560k words, long OpStrings
+    assert len(m) // 4 >= 1 << 16
+    from dataclasses import astuple
+    h, insts = sk.decode_module(m)
+    oh, oinsts = core.decode_module(m)
+    assert astuple(h) == tuple(oh)
+    assert [(i.opcode, tuple(i.operands)) for i in insts] == [(op, tuple(o)) for op, o in oinsts]
+    words = list(struct.unpack(f"<{len(m) // 4}I", m))
+    be = struct.pack(f">{len(words)}I", *words)
+    h2, insts2 = sk.decode_module(be)
+    assert astuple(h2) == astuple(h) and insts2 == insts
+    # errors: word count 0 deep inside, and an overrun at the end
+    starts = []
+    p = 5
+    while p < len(words):
+        starts.append(p)
+        p += words[p] >> 16
+    bad = list(words)
+    bad[starts[len(starts) * 2 // 3]] &= 0xFFFF
+    over = list(words)
+    over[starts[-1]] = (5 << 16) | (over[starts[-1]] & 0xFFFF)
+    for data in (struct.pack(f"<{len(bad)}I", *bad), struct.pack(f"<{len(over)}I", *over)):
+        with pytest.raises(Exception) as e1:
+            sk.decode_module(data)
+        with pytest.raises(Exception) as e2:
+            core.decode_module(data)
+        assert (type(e1.value).__name__, str(e1.value)) == (type(e2.value).__name__, str(e2.value))

@@ -24,6 +24,25 @@ def main():
     print(f"module: {W} words, {len(m) / 1e6:.1f} MB (built in {time.time() - t0:.1f}s)", flush=True)
     data = np.frombuffer(m + b"\0" * 16, dtype=np.uint8)
     dev = _native.DeviceBatch.from_host(data, np.array([0], np.int64), np.array([len(m)], np.int64))
+    from paper_2305_09493_b200 import decode_module
+    for rep in range(2):   # decode_module end to end (host bytes in, host objects out; 2nd run timed)
+        t2 = time.time()
+        h, insts = decode_module(m)
+        if rep:
+            print(f"decode_module (tiled boundary pass, incl. H2D/D2H + Python objects): "
+                  f"{len(insts)} instructions {time.time() - t2:.2f} s", flush=True)
+    from paper_2305_09493_b200 import _native as nat
+    dd = torch.frombuffer(bytearray(m + b"\0" * 16), dtype=torch.uint8).cuda()
+    nat._run_decode_large(dd, len(m))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nat._run_decode_large(dd, len(m))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(f"decode (skg_decode_large, device + result copies): {ms:.1f} ms {W / ms / 1e3:.1f} Mwords/s",
+          flush=True)
     for kind in ("disasm", "validate"):
         plan = _native.DisasmPlan(dev, 2, kind=kind, text_cap=24 * len(m) + 4096)
         t1 = time.time()
