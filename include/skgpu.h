@@ -149,6 +149,23 @@ int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, 
                      uint32_t* inst_off, uint32_t* inst_count, uint32_t* words_out, int32_t* status,
                      skg_error* error, void* workspace, uint64_t workspace_bytes, void* stream);
 
+/* validate_module for ONE large module (config 3) over the whole GPU: the tiled
+ * boundary pass, then one grid-stride kernel per phase (first/last-wins id maps
+ * by atomics on the instruction index, per-instruction diagnostic sizes, a
+ * device-wide scan, the write; skg_big.cuh).  Host-synchronous.
+ * Replaces: validate.validate_module (reference validate.py:73-94) for one
+ * module of nbytes bytes at `data` (device).  Returns 0: text[0:*text_bytes]
+ * holds the diagnostics_text lines and *status = SKG_ST_OK; 1: an exception
+ * escapes (*status, *error); 3: *text_bytes > text_cap (call again with a
+ * larger arena); 10 + s: the module does not decode (status s, *error = the
+ * message: the validator's only diagnostic); 2: ids at/above the header bound
+ * (use skg_validate).  `workspace` must hold skg_large_workspace_bytes(nbytes
+ * / 4, bound) for the module's header bound. */
+uint64_t skg_large_workspace_bytes(uint64_t n_words, uint32_t bound);
+int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint8_t* text,
+                       uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
+                       void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,
  * and the text bytes the batch needs (allocator cursor). */

@@ -57,6 +57,10 @@ def lib():
     L.skg_decode_large_workspace_bytes.argtypes = [U64]
     L.skg_decode_large_workspace_bytes.restype = U64
     L.skg_decode_large.argtypes = [P, U64, U32, P, P, P, P, P, P, P, U64, P]
+    L.skg_large_workspace_bytes.argtypes = [U64, U32]
+    L.skg_large_workspace_bytes.restype = U64
+    L.skg_validate_large.argtypes = [P, P, U64, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
+    L.skg_validate_large.restype = I32
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
               L.skg_decode_large):
@@ -251,10 +255,28 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
         return []
     run = (lambda b: run_disasm(b, opts, spec, ext)) if kind == "disasm" else (lambda b: run_validate(b, spec))
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
-    if n == 1 or need <= WS_BUDGET:
+    if (n == 1 or need <= WS_BUDGET) and not (kind == "validate" and batch.max_words >= LARGE_MODULE_WORDS):
         return fetch_texts(run(batch), n)
     lens = batch.len.cpu().numpy()
     words = lens // 4
+    if kind == "validate":   # single large modules: the whole GPU on one module
+        out = [None] * n
+        rest = []
+        for i in range(n):
+            r = _validate_large(batch, i, int(lens[i]), spec) if words[i] >= LARGE_MODULE_WORDS else None
+            if r is None:
+                rest.append(i)
+            else:
+                out[i] = r
+        if not rest:
+            return out
+        if len(rest) < n:
+            idx = np.array(rest)
+            ti = torch.from_numpy(idx.astype(np.int64)).to(batch.off.device)
+            sub = DeviceBatch(batch.data, batch.off[ti], batch.len[ti], int(words[idx].max()), int(lens[idx].sum()))
+            for k, r in zip(rest, run_texts(kind, sub, opts, spec, ext)):
+                out[k] = r
+            return out
     per_word = max(need // max(int(batch.max_words), 1), 1)        # workspace bytes per max-word
     w_small = max(int(WS_BUDGET // per_word), 1)
     out = [None] * n
@@ -267,6 +289,47 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
         for k, r in zip(idx, fetch_texts(run(sub), len(idx))):
             out[int(k)] = r
     return out
+
+
+LARGE_MODULE_WORDS = 1 << 20   # validate: modules this size and up run grid-wide (skg_validate_large)
+_DECODE_CODES = {ST_NOTSPIRV: "NotSpirv", ST_TRUNCATED: "TruncatedStream", ST_CORRUPT: "CorruptStream"}
+
+
+def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec):
+    """skg_validate_large on module i of a device batch -> text bytes | exception | None (= not handled)."""
+    torch = _torch()
+    L = lib()
+    data = batch.data.data_ptr() + int(batch.off[i].item())
+    W = nbytes // 4
+    head = batch.data[int(batch.off[i].item()):int(batch.off[i].item()) + 20].cpu().numpy().tobytes()
+    bound = 0
+    if len(head) == 20:
+        w = np.frombuffer(head, dtype="<u4")
+        bound = int(w[3]) if w[0] == 0x07230203 else int(np.frombuffer(head, dtype=">u4")[3])
+    ws_bytes = int(L.skg_large_workspace_bytes(W, min(bound, 2 * W + 64)))
+    ws = _ws.get(ws_bytes)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    errs = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    cap = 1 << 20
+    for _ in range(3):
+        text = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        need = ctypes.c_uint64(0)
+        rc = L.skg_validate_large(tables_handle(spec, None), data, nbytes, text.data_ptr(), cap, ctypes.byref(need),
+                                  status.data_ptr(), errs.data_ptr(), ws.data_ptr(), ws_bytes, _stream())
+        if rc == 3:
+            cap = int(need.value) + 16
+            continue
+        break
+    if rc == 2:
+        return None
+    _check(rc if rc < 0 else 0, "validate_large")
+    if rc == 0:
+        return text[: int(need.value)].cpu().numpy().tobytes()
+    exc = decode_errors(errs.cpu().numpy())[0]
+    if rc == 1:
+        return exc
+    code = _DECODE_CODES.get(rc - 10, "CorruptStream")   # the decode error is the only diagnostic
+    return f"error {code} module {exc}\n".encode()
 
 
 def fetch_texts(res: TextResult, n: int):

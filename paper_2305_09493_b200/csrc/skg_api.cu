@@ -7,6 +7,7 @@
 #include "skg_module.cuh"
 #include "skg_sched.cuh"
 #include "skg_bigdecode.cuh"
+#include "skg_big.cuh"
 
 namespace skg {
 struct DisasmArgs;
@@ -376,6 +377,138 @@ int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, 
   }
   skg::big_epilogue<<<1, 32, 0, s>>>(b, header, inst_count, status, reinterpret_cast<skg::ErrRec*>(error));
   return check(cudaGetLastError());
+}
+
+// -- one large module over the whole GPU (skg_big.cuh) ----------------------------
+namespace {
+struct LargeWs {
+  uint32_t* ctl;
+  uint8_t* dec;
+  skg::Mod* mod;
+  uint8_t* slot;
+  uint32_t* sums;
+  uint64_t total;
+};
+uint64_t al256(uint64_t x) { return (x + 255) & ~255ull; }
+LargeWs large_ws(uint8_t* ws, uint64_t W, uint32_t bound) {
+  LargeWs l;
+  uint64_t o = 0;
+  l.ctl = reinterpret_cast<uint32_t*>(ws + o); o += 256;
+  l.dec = ws + o; o += al256(skg_decode_large_workspace_bytes(W));
+  l.mod = reinterpret_cast<skg::Mod*>(ws + o); o += al256(sizeof(skg::Mod));
+  l.slot = ws + o; o += al256(skg::big_slot_bytes((uint32_t)W, bound));
+  l.sums = reinterpret_cast<uint32_t*>(ws + o); o += al256(4 * (W / skg::BS_BLOCK + 2));
+  l.total = o;
+  return l;
+}
+
+// tiled boundary pass into the module scratch + layout; returns the decode status
+// (host-synchronous) or -1 on a CUDA error
+int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const LargeWs& l, skg::ErrRec* derr,
+                cudaStream_t s) {
+  skg::BigDecode b;
+  const uint64_t W = nbytes / 4;
+  b.src = data; b.nbytes = nbytes; b.W = (uint32_t)W;
+  b.words = reinterpret_cast<uint32_t*>(l.slot + 64);
+  b.inst_off = reinterpret_cast<uint32_t*>(l.slot + 64 + skg::align16(4 * W));
+  b.ntiles = (uint32_t)((W + skg::BD_TILE - 1) / skg::BD_TILE);
+  b.result = l.ctl;
+  b.max_opcode = max_opcode ? max_opcode : 0xFFFFu;
+  b.chain = l.dec + 256;
+  uint32_t* q = reinterpret_cast<uint32_t*>(l.dec + 256 + (uint64_t)b.ntiles * skg::BD_TILE);
+  b.spec_exit = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.spec_err = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.spec_errc = q; q += (uint64_t)b.ntiles * skg::BD_K;
+  b.entry = q; q += b.ntiles;
+  b.count = q; q += b.ntiles;
+  const uint32_t tb = 128, tg = (b.ntiles + tb - 1) / tb;
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(l.dec);          // scratch for the epilogue outputs
+  skg::big_prologue<<<1, 32, 0, s>>>(b);
+  if (b.W >= 5) {
+    skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
+    skg::tile_spec<<<tg, tb, 0, s>>>(b);
+    skg::tile_link<<<1, 32, 0, s>>>(b);
+    skg::tile_count<<<tg, tb, 0, s>>>(b);
+    skg::tile_scan<<<1, 1024, 0, s>>>(b);
+    skg::tile_write<<<tg, tb, 0, s>>>(b);
+  }
+  skg::big_epilogue<<<1, 32, 0, s>>>(b, hdr, hdr + 8, reinterpret_cast<int32_t*>(hdr + 9), derr);
+  uint32_t st = 0;
+  if (check(cudaMemcpyAsync(&st, l.ctl, 4, cudaMemcpyDeviceToHost, s)) || check(cudaStreamSynchronize(s))) return -1;
+  if (st != 0) return (int)st;
+  skg::big_setup<<<1, 1, 0, s>>>(l.mod, l.slot, (uint32_t)W, l.ctl);
+  return check(cudaGetLastError()) ? -1 : 0;
+}
+
+// device-wide exclusive scan of n uint32 in place; total into ctl[BC_TOTAL + 2..3]
+void large_scan(uint32_t* a, uint32_t n, const LargeWs& l, cudaStream_t s) {
+  const uint32_t nb = (n + skg::BS_BLOCK - 1) / skg::BS_BLOCK;
+  if (nb) skg::scan_blocks<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
+  skg::scan_top<<<1, skg::BS_BLOCK, 0, s>>>(l.sums, nb, l.ctl + skg::BC_TOTAL + 2);
+  if (nb) skg::scan_apply<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
+}
+
+uint32_t grid_for(uint64_t n) {
+  const uint64_t b = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)sm_count() * 8;
+  return (uint32_t)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+}  // namespace
+
+uint64_t skg_large_workspace_bytes(uint64_t n_words, uint32_t bound) {
+  return large_ws(nullptr, n_words, bound).total;
+}
+
+int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint8_t* text,
+                       uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
+                       void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (!t || !workspace || !data || !text_bytes || nbytes / 4 > 0xFFFFFFF0ull) return -1;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t W = nbytes / 4;
+  // the header bound sizes the direct id tables
+  uint32_t hdr[5] = {0, 0, 0, 0, 0};
+  if (W >= 5 && check(cudaMemcpyAsync(hdr, data, 20, cudaMemcpyDeviceToHost, s))) return -1;
+  if (check(cudaStreamSynchronize(s))) return -1;
+  uint32_t bound = hdr[3];
+  if (hdr[0] == 0x03022307u) bound = __builtin_bswap32(bound);
+  if ((uint64_t)bound > 2 * W + 64) return 2;                      // not direct: use skg_validate
+  const LargeWs l = large_ws((uint8_t*)workspace, W, bound);
+  if (workspace_bytes < l.total) return -3;
+  *text_bytes = 0;
+  const int dst = large_front(data, nbytes, t->t.max_opcode, l, reinterpret_cast<skg::ErrRec*>(error), s);
+  if (dst < 0) return -1;
+  if (dst > 0) return 10 + dst;                                    // decode error: caller formats it
+  skg::big_init_tables<<<grid_for(bound), 256, 0, s>>>(l.mod);
+  uint32_t I = 0;
+  if (check(cudaMemcpyAsync(&I, l.ctl + skg::BC_COUNT, 4, cudaMemcpyDeviceToHost, s))) return -1;
+  skg::big_prescan<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl);
+  skg::big_fix_tables<<<grid_for(bound), 256, 0, s>>>(l.mod);
+  skg::big_val_shape<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl);
+  skg::big_val_sizes<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl);
+  uint32_t ctl[64];
+  if (check(cudaMemcpyAsync(ctl, l.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, s)) || check(cudaStreamSynchronize(s)))
+    return -1;
+  if (ctl[skg::BC_OVER]) return 2;                                 // an id at/above the bound
+  if (ctl[skg::BC_BAD] != 0xFFFFFFFFu) {                           // an exception escapes
+    skg::big_val_error<<<1, 32, 0, s>>>(l.mod, t->t, l.ctl, reinterpret_cast<skg::ErrRec*>(error), status);
+    return check(cudaStreamSynchronize(s)) ? -1 : 1;
+  }
+  // per-instruction offsets: ia (I entries) lives in the module scratch
+  skg::Mod m;
+  if (check(cudaMemcpyAsync(&m, l.mod, sizeof(m), cudaMemcpyDeviceToHost, s))) return -1;
+  if (check(cudaStreamSynchronize(s))) return -1;
+  large_scan(m.ia, I, l, s);
+  uint32_t tot[4];
+  if (check(cudaMemcpyAsync(tot, l.ctl + skg::BC_TOTAL, 16, cudaMemcpyDeviceToHost, s)) ||
+      check(cudaStreamSynchronize(s)))
+    return -1;
+  const uint64_t total = (uint64_t)tot[0] + tot[2];
+  *text_bytes = total;
+  if (total > text_cap) return 3;                                  // grow the arena and call again
+  skg::big_val_write<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl, text);
+  const int32_t ok = 0;
+  if (check(cudaMemcpyAsync(status, &ok, 4, cudaMemcpyHostToDevice, s))) return -1;
+  return check(cudaStreamSynchronize(s)) ? -1 : 0;
 }
 
 int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_len, uint32_t n_mod,

@@ -403,3 +403,95 @@ __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) 
 }
 
 }  // namespace skg
+
+// ---------------------------------------------------------------------------
+// One large module over the whole GPU (skg_big.cuh): shape + effective
+// capabilities, per-instruction diagnostic sizes, scan, write.
+namespace skg {
+
+__global__ void big_val_shape(const Mod* mp, Tables T, uint32_t* ctl) {
+  const Mod m = *mp;
+  unsigned long long* eff = reinterpret_cast<unsigned long long*>(ctl + BC_EFF);
+  uint32_t fl = 0, mm = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m.I; i += gridDim.x * blockDim.x) {
+    if (m.idef[i] == NONE16) continue;
+    const uint32_t sp = T.special(m.idef[i]);
+    fl |= sp == SP_FUNCTION ? BF_FN : 0;
+    fl |= sp == SP_ENTRYPOINT ? BF_EP : 0;
+    mm += sp == SP_MEMORYMODEL;
+    if (sp == SP_CAPABILITY) {
+      fl |= BF_CAP;
+      if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
+        const uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
+        const uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
+        if (cn != NONE32)
+          for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k)
+            atomicOr(eff + k, (unsigned long long)__ldg(T.closure + cn * T.cap_words + k));
+      }
+    }
+  }
+  if (fl) atomicOr(&ctl[BC_FLAGS], fl);
+  if (mm) atomicAdd(&ctl[BC_NMM], mm);
+}
+
+__device__ inline Shape big_shape(const Tables& T, const uint32_t* ctl, uint64_t* eff) {
+  const unsigned long long* e = reinterpret_cast<const unsigned long long*>(ctl + BC_EFF);
+  for (int k = 0; k < MAX_CAPW; ++k) eff[k] = e[k];
+  Shape sh;
+  sh.has_fn = ctl[BC_FLAGS] & BF_FN;
+  sh.has_cap = ctl[BC_FLAGS] & BF_CAP;
+  sh.has_ep = ctl[BC_FLAGS] & BF_EP;
+  sh.n_mm = ctl[BC_NMM];
+  sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
+  return sh;
+}
+
+__global__ void big_val_sizes(const Mod* mp, Tables T, uint32_t* ctl) {
+  const Mod m = *mp;
+  uint64_t eff[MAX_CAPW];
+  const Shape sh = big_shape(T, ctl, eff);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    CountSink hs;
+    shape_diags(hs, sh);
+    ctl[BC_TOTAL] = hs.n;
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m.I; i += gridDim.x * blockDim.x) {
+    CountSink cs;
+    const WalkErr e = inst_diags(cs, m, T, i, eff);
+    m.ia[i] = cs.n;
+    m.ierr[i] = (uint8_t)e.code;
+    if (e.code != W_OK && !werr_is_codec(e.code)) atomicMin(&ctl[BC_BAD], i);
+  }
+}
+
+// the exception of the first instruction whose walk escapes (validate.py:88-94)
+__global__ void big_val_error(const Mod* mp, Tables T, const uint32_t* ctl, ErrRec* rec, int32_t* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const Mod m = *mp;
+  uint64_t eff[MAX_CAPW];
+  big_shape(T, ctl, eff);
+  const uint32_t bad = ctl[BC_BAD];
+  CountSink cs;
+  const WalkErr e = inst_diags(cs, m, T, bad, eff);
+  *status = walk_status(e.code);
+  if (rec) {
+    ErrWriter ew{rec};
+    put_walk_error(ew, T, m.idef[bad], e);
+    rec->module = 0; rec->cls = *status; rec->len = ew.n;
+    rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
+  }
+}
+
+__global__ void big_val_write(const Mod* mp, Tables T, const uint32_t* ctl, uint8_t* out) {
+  const Mod m = *mp;
+  uint64_t eff[MAX_CAPW];
+  const Shape sh = big_shape(T, ctl, eff);
+  if (blockIdx.x == 0 && threadIdx.x == 0) { MemSink ms(out); shape_diags(ms, sh); }
+  const uint32_t head = ctl[BC_TOTAL];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m.I; i += gridDim.x * blockDim.x) {
+    MemSink ms(out + head + m.ia[i]);
+    inst_diags(ms, m, T, i, eff);
+  }
+}
+
+}  // namespace skg

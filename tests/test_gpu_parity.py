@@ -248,3 +248,35 @@ def test_decode_large_module_tiled(sk):
         with pytest.raises(Exception) as e2:
             core.decode_module(data)
         assert (type(e1.value).__name__, str(e1.value)) == (type(e2.value).__name__, str(e2.value))
+
+
+def test_validate_large_module_grid_wide(sk, monkeypatch):
+    """validate on one large module runs grid-wide (skg_validate_large): same diagnostics
+    as the batch path / oracle, including decode errors and instruction diagnostics."""
+    import struct
+    from oracle import validate as oval
+    from paper_2305_09493_b200 import _native
+    from synth.huge import build_huge
+    monkeypatch.setattr(_native, "LARGE_MODULE_WORDS", 1 << 14)
+    m = build_huge(60, chain=100, seed=6)
+    words = list(struct.unpack(f"<{len(m) // 4}I", m))
+    cases = [m]
+    # an unknown opcode (warning), a bound violation and a duplicate result id
+    w2 = list(words)
+    p = 5
+    starts = []
+    while p < len(w2):
+        starts.append(p)
+        p += w2[p] >> 16
+    k = starts[len(starts) // 2]
+    w2[k] = (w2[k] & 0xFFFF0000) | 0x7FF0
+    w2[3] = 50
+    cases.append(struct.pack(f"<{len(w2)}I", *w2))
+    w3 = list(words)
+    w3[starts[-5]] = 0
+    cases.append(struct.pack(f"<{len(w3)}I", *w3))           # word count 0: decode error
+    cases.append(struct.pack(f">{len(words)}I", *words))     # big-endian
+    got = sk.validate_batch(cases)
+    for c, g in zip(cases, got):
+        want = [tuple(x) for x in oval.validate(c)]
+        assert [(x.severity, x.code, x.location, x.message) for x in g] == want

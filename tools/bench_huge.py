@@ -43,6 +43,15 @@ def main():
     ms = e0.elapsed_time(e1)
     print(f"decode (skg_decode_large, device + result copies): {ms:.1f} ms {W / ms / 1e3:.1f} Mwords/s",
           flush=True)
+    for rep in range(2):   # validate, whole GPU on the one module (skg_validate_large), device-resident
+        torch.cuda.synchronize()
+        t3 = time.time()
+        r = nat._validate_large(dev, 0, len(m), None)
+        torch.cuda.synchronize()
+        if rep:
+            print(f"validate (skg_validate_large, grid-wide, incl. host syncs): {time.time() - t3:.3f} s "
+                  f"{W / (time.time() - t3) / 1e6:.1f} Mwords/s -> {len(r) if isinstance(r, bytes) else r}",
+                  flush=True)
     for kind in ("disasm", "validate"):
         plan = _native.DisasmPlan(dev, 2, kind=kind, text_cap=24 * len(m) + 4096)
         t1 = time.time()
