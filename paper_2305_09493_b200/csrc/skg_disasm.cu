@@ -208,44 +208,214 @@ __device__ __noinline__ bool cand_eq(const Mod& m, uint32_t s1, uint32_t r1, uin
   return true;
 }
 
+// ---- friendly names, per-item steps (shared by the warp driver resolve_names
+// and the grid-wide driver of one large module) -------------------------------
+constexpr uint8_t HF_TB = 32, HF_HASCHILD = 64;
+
+// step 1 (slot s): named definition / pinned (P0 = referenced ids that are not
+// named definitions); returns whether s is P0
+__device__ __forceinline__ bool nm_slot_flags(Mod& m, uint32_t s) {
+  uint8_t f = 0;
+  if (m.hpres[s]) {
+    const bool named_d = m.hname[s] != NONE32 && m.hdef[s] != NONE32;
+    if (named_d) f |= HF_NAMED_D;
+    if (m.hA[s] && !named_d) f |= HF_P0;
+  }
+  m.hfl[s] = f;
+  return f & HF_P0;
+}
+
+// step 2 (instruction i): first definition of its result id: in C (= D without
+// P0) and / or a named definition
+__device__ __forceinline__ void nm_def_pred(const Mod& m, const Tables& T, uint32_t i, bool& isC, bool& isN,
+                                            uint32_t& slot) {
+  isC = isN = false;
+  slot = NONE32;
+  const uint32_t d = m.idef[i];
+  if (d == NONE16 || !T.has_result(d)) return;
+  const uint32_t idx = T.has_rtype(d) ? 1 : 0;
+  if (idx >= inst_nops(m, i)) return;
+  slot = ht_find(m, inst_ops(m, i)[idx]);
+  if (slot != NONE32 && m.hdef[slot] == i) {
+    isC = !(m.hfl[slot] & HF_P0);
+    isN = (m.hfl[slot] & HF_NAMED_D) != 0;
+  }
+}
+
+__device__ __forceinline__ uint32_t nm_def_key(const Mod& m, const Tables& T, uint32_t i) {
+  return inst_ops(m, i)[T.has_rtype(m.idef[i]) ? 1 : 0];
+}
+
+// step 4 (named definition k): sanitized-name hash / prefix hash / length and
+// the numeric value of a canonical "_<n>" suffix
+__device__ __forceinline__ void nm_info(Mod& m, uint32_t k) {
+  const uint32_t slot = m.ndl[k];
+  uint32_t h, len, ph;
+  bool suffix;
+  NameView nv = name_of(m, m.hname[slot]);
+  name_info(nv, h, len, ph, suffix);
+  m.nH[slot] = h; m.nP[slot] = ph; m.nLen[slot] = len;
+  uint32_t n = NONE32;
+  if (suffix) {   // numeric value of the canonical suffix (ignored if >= 2^32)
+    uint64_t v = 0;
+    uint32_t idx = 0, start = 0;
+    for_sanitized(nv, [&](uint32_t c) { if (c == '_') start = idx + 1; ++idx; });
+    idx = 0;
+    for_sanitized(nv, [&](uint32_t c) { if (idx >= start && v <= 0xFFFFFFFFull) v = v * 10 + (c - '0'); ++idx; });
+    if (v < 0xFFFFFFFFull) { n = (uint32_t)v; m.hfl[slot] |= HF_SUFFIX; }
+  }
+  m.ia[k] = n;
+}
+
+// base-hash table (key, smallest ident index), open addressing, in the spill area
+__device__ __forceinline__ uint32_t nm_hkey(uint32_t h) { return h == EMPTY ? EMPTY - 1 : h; }
+
+__device__ __forceinline__ void nm_hinsert(uint32_t* htab, uint32_t C, uint32_t h, uint32_t k) {
+  const uint32_t key = nm_hkey(h);
+  uint32_t e = (key * 0x9E3779B1u) & (C - 1);
+  #pragma unroll 1
+  while (true) {
+    const uint32_t old = atomicCAS(&htab[2 * e], EMPTY, key);
+    if (old == EMPTY || old == key) { atomicMin(&htab[2 * e + 1], k); return; }
+    e = (e + 1) & (C - 1);
+  }
+}
+
+__device__ __forceinline__ uint32_t nm_hmin(const uint32_t* htab, uint32_t C, uint32_t h) {
+  const uint32_t key = nm_hkey(h);
+  uint32_t e = (key * 0x9E3779B1u) & (C - 1);
+  #pragma unroll 1
+  while (true) {   // L2 reads: the table was filled with atomics (not in L1)
+    const uint32_t kk = __ldcg(htab + 2 * e);
+    if (kk == key) return __ldcg(htab + 2 * e + 1);
+    if (kk == EMPTY) return NONE32;
+    e = (e + 1) & (C - 1);
+  }
+}
+
+// leader of ident k = first ident (D order) with the same sanitized base
+__device__ __noinline__ uint32_t nm_leader(const Mod& m, const uint32_t* htab, uint32_t C, uint32_t k) {
+  const uint32_t slot = m.ndl[k], h = m.nH[slot];
+  uint32_t lead = nm_hmin(htab, C, h);
+  if (lead != k && !(lead < k && cand_eq(m, slot, NONE32, m.ndl[lead], NONE32))) {
+    lead = k;   // hash collision with another base: exact ordered scan
+    #pragma unroll 1
+    for (uint32_t q = 0; q < k; ++q) {
+      const uint32_t o = m.ndl[q];
+      if (m.nH[o] == h && cand_eq(m, slot, NONE32, o, NONE32)) { lead = q; break; }
+    }
+  }
+  return lead;
+}
+
+// parent group of leader k whose base reads "<base of the parent>_<n>", or NONE32
+__device__ __noinline__ uint32_t nm_parent(const Mod& m, const uint32_t* htab, uint32_t C, uint32_t nd,
+                                           uint32_t k) {
+  uint32_t parent = NONE32;
+  const uint32_t slot = m.ndl[k];
+  if (m.pos[k] != (int32_t)k || !(m.hfl[slot] & HF_SUFFIX)) return NONE32;
+  const uint32_t ph = m.nP[slot], n = m.ia[k];
+  // the parent (if any) is the leader of base hash ph: try the hash table's
+  // smallest index first, then the exact scan
+  const uint32_t hq = nm_hmin(htab, C, ph);
+  #pragma unroll 1
+  for (uint32_t it = 0; it <= nd && parent == NONE32; ++it) {
+    const uint32_t q = it == 0 ? hq : it - 1;
+    if (q == NONE32 || (it > 0 && q == hq)) continue;
+    if (it == 1 && hq == NONE32) break;   // no base with that hash: no parent
+    const uint32_t o = m.ndl[q];
+    if (m.pos[q] != (int32_t)q || m.nH[o] != ph) continue;
+    if (m.nLen[o] + 1 + dec_len_u64(n) != m.nLen[slot]) continue;
+    // compare the first nLen[o] characters
+    bool eq = true;
+    const uint32_t L = m.nLen[o];
+    uint32_t ba[32], bb[32];
+    #pragma unroll 1
+    for (uint32_t from = 0; from < L && eq; from += 32) {
+      uint32_t na = 0, nb = 0, ia = 0, ib = 0;
+      for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t c) { if (ia >= from && ia < L && na < 32) ba[na++] = c; ++ia; });
+      for_sanitized(name_of(m, m.hname[o]), [&](uint32_t c) { if (ib >= from && nb < 32) bb[nb++] = c; ++ib; });
+      #pragma unroll 1
+      for (uint32_t z = 0; z < na; ++z) if (ba[z] != bb[z]) { eq = false; break; }
+    }
+    if (eq) parent = q;
+  }
+  return parent;
+}
+
+__device__ __forceinline__ void nm_mark_parent(Mod& m, uint32_t k) {
+  if (m.ib[k] == NONE32) return;
+  uint8_t* f = &m.hfl[m.ndl[m.ib[k]]];
+  atomicOr(reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(f) & ~(uintptr_t)3),
+           (unsigned)HF_HASCHILD << (8 * (reinterpret_cast<uintptr_t>(f) & 3)));
+}
+
+// uniquify in D order (disasm.py:173-185), one thread: the k-th ident gets the
+// first of base, base_0, base_1, ... not taken yet.  Exact reformulation: group
+// idents by sanitized base; a candidate base_s can only collide with the *base*
+// of another group that reads "base_<s>" (a child group, clist: (parent group,
+// suffix value, child leader)), so per-group counters plus per-group "base
+// taken" flags reproduce the sequential result in one O(nd) pass.
+__device__ __noinline__ void nm_dedup(Mod& m, uint32_t nd, const uint32_t* clist, uint32_t nc) {
+  auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
+    #pragma unroll 1
+    for (uint32_t q = 0; q < nc; ++q)
+      if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
+    return NONE32;
+  };
+  #pragma unroll 1
+  for (uint32_t k = 0; k < nd; ++k) {
+    const uint32_t g = (uint32_t)m.pos[k];
+    const uint32_t gs = m.ndl[g];
+    if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
+    uint32_t serial = NONE32;
+    const uint8_t fl = m.hfl[gs];
+    if (!(fl & HF_TB)) {
+      m.hfl[gs] = fl | HF_TB;
+    } else {
+      uint32_t sv = m.nP[gs];
+      if (fl & HF_HASCHILD) {
+        uint32_t c;
+        #pragma unroll 1
+        while ((c = child_of(g, sv)) != NONE32 && (m.hfl[m.ndl[c]] & HF_TB)) ++sv;
+        if (c != NONE32) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
+      }
+      serial = sv;
+      m.nP[gs] = sv + 1;
+    }
+    m.hser[m.ndl[k]] = serial;
+  }
+}
+
+// step 5 (named definition k, kept, arena offset off): the sanitized base into the arena
+__device__ __forceinline__ void nm_arena_write(Mod& m, uint32_t k, uint32_t off) {
+  const uint32_t slot = m.ndl[k];
+  m.hfl[slot] |= HF_FRIENDLY;
+  m.hnoff[slot] = off;
+  uint8_t* dst = m.narena + off;
+  uint32_t q = 0;
+  for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t c) { dst[q++] = (uint8_t)c; });
+}
+
+// friendly names of one module by one warp (disasm.py:159-206 via SURVEY A.3)
 __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
   const uint32_t lane = lane_id();
-  // 1. per slot: named definition / pinned (P0 = A - named definitions)
+  // 1. per slot flags; |P0|
   uint32_t nP0 = 0;
   #pragma unroll 1
-  for (uint32_t s = lane; s < m.S; s += 32) {
-    uint8_t f = 0;
-    if (m.hpres[s]) {
-      bool named_d = m.hname[s] != NONE32 && m.hdef[s] != NONE32;
-      if (named_d) f |= HF_NAMED_D;
-      if (m.hA[s] && !named_d) { f |= HF_P0; ++nP0; }
-    }
-    m.hfl[s] = f;
-  }
+  for (uint32_t s = lane; s < m.S; s += 32) nP0 += nm_slot_flags(m, s) ? 1 : 0;
   nP0 = warp_sum_u32(nP0);
   __syncwarp();
   // 2. definitions in document order: C = D without P0 (index j in ib), named list ndl
   uint32_t cj = 0, nd = 0;
   #pragma unroll 1
   for (uint32_t base = 0; base < m.I; base += 32) {
-    uint32_t i = base + lane;
+    const uint32_t i = base + lane;
     bool isC = false, isN = false;
     uint32_t slot = NONE32;
-    if (i < m.I) {
-      uint32_t d = m.idef[i];
-      if (d != NONE16 && T.has_result(d)) {
-        uint32_t idx = T.has_rtype(d) ? 1 : 0;
-        if (idx < inst_nops(m, i)) {
-          slot = ht_find(m, inst_ops(m, i)[idx]);
-          if (slot != NONE32 && m.hdef[slot] == i) {
-            isC = !(m.hfl[slot] & HF_P0);
-            isN = (m.hfl[slot] & HF_NAMED_D) != 0;
-          }
-        }
-      }
-    }
-    unsigned bc = __ballot_sync(FULL, isC), bn = __ballot_sync(FULL, isN);
-    uint32_t below = (1u << lane) - 1;
+    if (i < m.I) nm_def_pred(m, T, i, isC, isN, slot);
+    const unsigned bc = __ballot_sync(FULL, isC), bn = __ballot_sync(FULL, isN);
+    const uint32_t below = (1u << lane) - 1;
     if (isC) m.ib[i] = cj + __popc(bc & below);
     if (isN) m.ndl[nd + __popc(bn & below)] = slot;
     if (i < m.I) m.iflag[i] = (m.iflag[i] & ~IF_FIRSTDEF) | (isC ? IF_FIRSTDEF : 0);
@@ -263,23 +433,21 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
   #pragma unroll 1
   for (uint32_t s = lane; s < m.S; s += 32) {
     if (!(m.hfl[s] & HF_P0)) continue;
-    uint32_t key = slot_key(m, s);
+    const uint32_t key = slot_key(m, s);
     if (key >= 1 && key <= N) m.pos[key] = -1;
   }
   __syncwarp();
   #pragma unroll 1
-  for (uint32_t base = 0; base < m.I; base += 32) {
-    uint32_t i = base + lane;
-    if (i < m.I && (m.iflag[i] & IF_FIRSTDEF)) {
-      uint32_t key = inst_ops(m, i)[T.has_rtype(m.idef[i]) ? 1 : 0];
-      if (key >= 1 && key <= N) m.pos[key] = (int32_t)m.ib[i];
-    }
+  for (uint32_t i = lane; i < m.I; i += 32) {
+    if (!(m.iflag[i] & IF_FIRSTDEF)) continue;
+    const uint32_t key = nm_def_key(m, T, i);
+    if (key >= 1 && key <= N) m.pos[key] = (int32_t)m.ib[i];
   }
   __syncwarp();
   int32_t carry = -2;
   #pragma unroll 1
   for (uint32_t base = 1; base <= N; base += 32) {
-    uint32_t v = base + lane;
+    const uint32_t v = base + lane;
     int32_t x = v <= N ? m.pos[v] : -2;
     x = max(warp_incl_max(x), carry);
     if (v <= N) m.pos[v] = x;
@@ -287,140 +455,39 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
   }
   __syncwarp();
   #pragma unroll 1
-  for (uint32_t base = 0; base < m.I; base += 32) {
-    uint32_t i = base + lane;
-    if (i < m.I && (m.iflag[i] & IF_FIRSTDEF)) {
-      uint32_t key = inst_ops(m, i)[T.has_rtype(m.idef[i]) ? 1 : 0];
-      int32_t j = (int32_t)m.ib[i];
-      if (key >= 1 && key <= N && (key == 1 || m.pos[key - 1] < j)) m.hfl[ht_find(m, key)] |= HF_KEPT;
-    }
+  for (uint32_t i = lane; i < m.I; i += 32) {
+    if (!(m.iflag[i] & IF_FIRSTDEF)) continue;
+    const uint32_t key = nm_def_key(m, T, i);
+    const int32_t j = (int32_t)m.ib[i];
+    if (key >= 1 && key <= N && (key == 1 || m.pos[key - 1] < j)) m.hfl[ht_find(m, key)] |= HF_KEPT;
   }
   __syncwarp();
-  // 4. uniquify in D order (disasm.py:173-185): the k-th ident gets the first of
-  //    base, base_0, base_1, ... not taken yet.  Exact reformulation: group idents
-  //    by sanitized base; a candidate base_s can only collide with the *base* of
-  //    another group that reads "base_<s>" (a child group), so a per-group counter
-  //    plus per-group "base taken" flags reproduce the sequential result in one
-  //    O(nd) pass; only grouping/child detection needs string compares.
-  constexpr uint8_t HF_TB = 32, HF_HASCHILD = 64;
+  // 4. uniquify: base info, leaders (hash table of base -> first ident in the
+  //    spill area: capacity C = pow2 >= 2 nd, 8 C < 32 nd <= spill bytes), parents
   #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    uint32_t slot = m.ndl[k];
-    uint32_t h, len, ph;
-    bool suffix;
-    NameView nv = name_of(m, m.hname[slot]);
-    name_info(nv, h, len, ph, suffix);
-    m.nH[slot] = h; m.nP[slot] = ph; m.nLen[slot] = len;
-    uint32_t n = NONE32;
-    if (suffix) {   // numeric value of the canonical suffix (ignored if >= 2^32)
-      uint64_t v = 0;
-      uint32_t idx = 0, start = 0;
-      for_sanitized(nv, [&](uint32_t c) { if (c == '_') start = idx + 1; ++idx; });
-      idx = 0;
-      for_sanitized(nv, [&](uint32_t c) { if (idx >= start && v <= 0xFFFFFFFFull) v = v * 10 + (c - '0'); ++idx; });
-      if (v < 0xFFFFFFFFull) { n = (uint32_t)v; m.hfl[slot] |= HF_SUFFIX; }
-    }
-    m.ia[k] = n;
-  }
+  for (uint32_t k = lane; k < nd; k += 32) nm_info(m, k);
   __syncwarp();
-  // leader = first ident (D order) with the same sanitized base.  A hash table
-  // (in the spill area: capacity C = pow2 >= 2 nd, 8 C <= 32 nd bytes) keeps the
-  // smallest ident index per base hash; a candidate is verified by comparing the
-  // strings, and only a hash collision falls back to the ordered linear scan.
-  uint32_t C = 4;                     // 8 C < 32 nd <= spill_bytes(I)
+  uint32_t C = 4;
   while (C < 2 * nd) C <<= 1;
   uint32_t* htab = reinterpret_cast<uint32_t*>(m.spill);
   #pragma unroll 1
   for (uint32_t e = lane; e < C; e += 32) { __stcg(htab + 2 * e, EMPTY); __stcg(htab + 2 * e + 1, EMPTY); }
   __threadfence_block();
   __syncwarp();
-  auto hkey = [](uint32_t h) { return h == EMPTY ? EMPTY - 1 : h; };
   #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    const uint32_t key = hkey(m.nH[m.ndl[k]]);
-    uint32_t e = (key * 0x9E3779B1u) & (C - 1);
-    #pragma unroll 1
-    while (true) {
-      const uint32_t old = atomicCAS(&htab[2 * e], EMPTY, key);
-      if (old == EMPTY || old == key) { atomicMin(&htab[2 * e + 1], k); break; }
-      e = (e + 1) & (C - 1);
-    }
-  }
+  for (uint32_t k = lane; k < nd; k += 32) nm_hinsert(htab, C, m.nH[m.ndl[k]], k);
   __threadfence_block();
   __syncwarp();
-  auto hmin = [&](uint32_t h) -> uint32_t {   // smallest ident index with this base hash
-    const uint32_t key = hkey(h);
-    uint32_t e = (key * 0x9E3779B1u) & (C - 1);
-    #pragma unroll 1
-    while (true) {   // L2 reads: the table was filled with atomics (not in L1)
-      const uint32_t kk = __ldcg(htab + 2 * e);
-      if (kk == key) return __ldcg(htab + 2 * e + 1);
-      if (kk == EMPTY) return NONE32;
-      e = (e + 1) & (C - 1);
-    }
-  };
   #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    const uint32_t slot = m.ndl[k], h = m.nH[slot];
-    uint32_t lead = hmin(h);
-    if (lead != k && !(lead < k && cand_eq(m, slot, NONE32, m.ndl[lead], NONE32))) {
-      lead = k;   // hash collision with another base: exact ordered scan
-      #pragma unroll 1
-      for (uint32_t q = 0; q < k; ++q) {
-        const uint32_t o = m.ndl[q];
-        if (m.nH[o] == h && cand_eq(m, slot, NONE32, o, NONE32)) { lead = q; break; }
-      }
-    }
-    m.pos[k] = (int32_t)lead;
-  }
-  __syncwarp();
-  // child groups: leader c whose base is "<base of leader g>_<n>"
-  #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    uint32_t parent = NONE32;
-    uint32_t slot = m.ndl[k];
-    if (m.pos[k] == (int32_t)k && (m.hfl[slot] & HF_SUFFIX)) {
-      const uint32_t ph = m.nP[slot], n = m.ia[k];
-      // the parent (if any) is the leader of base hash ph: try the hash table's
-      // smallest index first, then the exact scan
-      const uint32_t hq = hmin(ph);
-      #pragma unroll 1
-      for (uint32_t it = 0; it <= nd && parent == NONE32; ++it) {
-        const uint32_t q = it == 0 ? hq : it - 1;
-        if (q == NONE32 || (it > 0 && q == hq)) continue;
-        if (it == 1 && hq == NONE32) break;   // no base with that hash: no parent
-        uint32_t o = m.ndl[q];
-        if (m.pos[q] != (int32_t)q || m.nH[o] != ph) continue;
-        if (m.nLen[o] + 1 + dec_len_u64(n) != m.nLen[slot]) continue;
-        // compare the first nLen[o] characters
-        bool eq = true;
-        const uint32_t L = m.nLen[o];
-        uint32_t ba[32], bb[32];
-        #pragma unroll 1
-        for (uint32_t from = 0; from < L && eq; from += 32) {
-          uint32_t na = 0, nb = 0, ia = 0, ib = 0;
-          for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t c) { if (ia >= from && ia < L && na < 32) ba[na++] = c; ++ia; });
-          for_sanitized(name_of(m, m.hname[o]), [&](uint32_t c) { if (ib >= from && nb < 32) bb[nb++] = c; ++ib; });
-          #pragma unroll 1
-          for (uint32_t z = 0; z < na; ++z) if (ba[z] != bb[z]) { eq = false; break; }
-        }
-        if (eq) parent = q;
-      }
-    }
-    m.ib[k] = parent;
-  }
+  for (uint32_t k = lane; k < nd; k += 32) m.pos[k] = (int32_t)nm_leader(m, htab, C, k);
   __syncwarp();
   #pragma unroll 1
-  for (uint32_t k = lane; k < nd; k += 32) {
-    if (m.ib[k] != NONE32) {
-      uint8_t* f = &m.hfl[m.ndl[m.ib[k]]];
-      atomicOr(reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(f) & ~(uintptr_t)3),
-               (unsigned)HF_HASCHILD << (8 * (reinterpret_cast<uintptr_t>(f) & 3)));
-    }
-  }
+  for (uint32_t k = lane; k < nd; k += 32) m.ib[k] = nm_parent(m, htab, C, nd, k);
   __syncwarp();
-  // child entries (parent group, suffix value, child leader), compacted into the
-  // spill area so the sequential pass finds a child with one ballot per 32
+  #pragma unroll 1
+  for (uint32_t k = lane; k < nd; k += 32) nm_mark_parent(m, k);
+  __syncwarp();
+  // child entries compacted into the spill area (the table is no longer needed)
   uint32_t nc = 0;
   uint32_t* clist = reinterpret_cast<uint32_t*>(m.spill);
   #pragma unroll 1
@@ -435,37 +502,7 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     nc += __popc(b);
   }
   __syncwarp();
-  // the sequential pass in D order (lane 0); child lookups scan the compact list
-  if (lane == 0) {
-    auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
-      #pragma unroll 1
-      for (uint32_t q = 0; q < nc; ++q)
-        if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
-      return NONE32;
-    };
-    #pragma unroll 1
-    for (uint32_t k = 0; k < nd; ++k) {
-      const uint32_t g = (uint32_t)m.pos[k];
-      const uint32_t gs = m.ndl[g];
-      if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
-      uint32_t serial = NONE32;
-      const uint8_t fl = m.hfl[gs];
-      if (!(fl & HF_TB)) {
-        m.hfl[gs] = fl | HF_TB;
-      } else {
-        uint32_t sv = m.nP[gs];
-        if (fl & HF_HASCHILD) {
-          uint32_t c;
-          #pragma unroll 1
-          while ((c = child_of(g, sv)) != NONE32 && (m.hfl[m.ndl[c]] & HF_TB)) ++sv;
-          if (c != NONE32) m.hfl[m.ndl[c]] |= HF_TB;  // our candidate is that child's base
-        }
-        serial = sv;
-        m.nP[gs] = sv + 1;
-      }
-      m.hser[m.ndl[k]] = serial;
-    }
-  }
+  if (lane == 0) nm_dedup(m, nd, clist, nc);
   __syncwarp();
   // 5. friendly = named definition that keeps its number; its sanitized base
   //    name goes into the module's name arena once (refs copy it from there)
@@ -477,14 +514,7 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     const bool kept = k < nd && (m.hfl[slot] & HF_KEPT);
     const uint32_t len = kept ? m.nLen[slot] : 0;
     const uint32_t incl = warp_incl_sum(len);
-    if (kept) {
-      m.hfl[slot] |= HF_FRIENDLY;
-      const uint32_t off = acarry + incl - len;
-      m.hnoff[slot] = off;
-      uint8_t* dst = m.narena + off;
-      uint32_t q = 0;
-      for_sanitized(name_of(m, m.hname[slot]), [&](uint32_t c) { dst[q++] = (uint8_t)c; });
-    }
+    if (kept) nm_arena_write(m, k, acarry + incl - len);
     acarry += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
@@ -639,10 +669,7 @@ struct ClassVis {
 };
 
 // walk every instruction once: word codes + per-instruction status
-__device__ __noinline__ void classify(Mod& m, const Tables& T) {
-  for (uint32_t base = 0; base < m.I; base += 32) {
-    const uint32_t i = base + lane_id();
-    if (i >= m.I) continue;
+__device__ __forceinline__ void classify_one(Mod& m, const Tables& T, uint32_t i) {
     const uint32_t s0 = m.ioff[i];
     const uint32_t n = inst_nops(m, i);
     const uint32_t d = m.idef[i];
@@ -661,19 +688,27 @@ __device__ __noinline__ void classify(Mod& m, const Tables& T) {
     m.ierr[i] = err;
     m.wk[s0] = C_OPC | (i << 6);
     m.wk[s0 + n] |= WK_LAST;          // n == 0: the opcode word itself
+}
+
+__device__ __noinline__ void classify(Mod& m, const Tables& T) {
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    const uint32_t i = base + lane_id();
+    if (i < m.I) classify_one(m, T, i);
   }
   __syncwarp();
 }
 
 // referenced ids (A, disasm.py:221-240), word-parallel
-__device__ __noinline__ void collect_ids(Mod& m) {
-  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) {
-    const uint32_t c = wk_code(m.wk[w]);
-    if (c == C_REF || c == C_RES || c == C_DECID) {
-      uint32_t s = ht_insert(m, m.w[w]);
-      if (s != NONE32) m.hA[s] = 1;
-    }
+__device__ __forceinline__ void collect_one(Mod& m, uint32_t w) {
+  const uint32_t c = wk_code(m.wk[w]);
+  if (c == C_REF || c == C_RES || c == C_DECID) {
+    uint32_t s = ht_insert(m, m.w[w]);
+    if (s != NONE32) m.hA[s] = 1;
   }
+}
+
+__device__ __noinline__ void collect_ids(Mod& m) {
+  for (uint32_t w = 5 + lane_id(); w < m.W; w += 32) collect_one(m, w);
   __syncwarp();
 }
 
@@ -950,12 +985,8 @@ __device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T
 }
 
 // result ref of every instruction -> irl/ib/iflag, module width (disasm.py:286-288)
-__device__ __noinline__ uint32_t result_refs(Mod& m, const Tables& T) {
-  fill_ref_lengths(m);
-  uint32_t width = 0;
-  for (uint32_t base = 0; base < m.I; base += 32) {
-    uint32_t i = base + lane_id();
-    if (i >= m.I) continue;
+__device__ __forceinline__ uint32_t result_ref_one(Mod& m, const Tables& T, uint32_t i) {
+    uint32_t width = 0;
     uint8_t fl = m.iflag[i] & ~IF_HAS_RESULT;
     uint32_t d = m.idef[i];
     if (d != NONE16 && T.has_result(d)) {
@@ -970,6 +1001,15 @@ __device__ __noinline__ uint32_t result_refs(Mod& m, const Tables& T) {
       }
     }
     m.iflag[i] = fl;
+    return width;
+}
+
+__device__ __noinline__ uint32_t result_refs(Mod& m, const Tables& T) {
+  fill_ref_lengths(m);
+  uint32_t width = 0;
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    const uint32_t i = base + lane_id();
+    if (i < m.I) width = max(width, result_ref_one(m, T, i));
   }
   return warp_max_u32(width);
 }
@@ -1002,31 +1042,43 @@ __device__ __noinline__ uint64_t text_size(const Mod& m, const Tables& T, uint32
 // nothing), every lane emits its word at its scanned offset (lengths from the
 // size pass), and the window is flushed with 16-byte stores.  A word too long
 // for the stage on its own is written straight to global memory.
+__device__ __noinline__ void text_write_range(const Mod& m, const Tables& T, uint32_t opts, uint32_t width,
+                                              uint8_t* out, uint8_t* stage, uint32_t cap, uint32_t w_begin,
+                                              uint32_t w_end, uint64_t pos0, bool header);
+
 __device__ __noinline__ void text_write(const Mod& m, const Tables& T, uint32_t opts, uint32_t width,
                                         uint8_t* out, uint8_t* stage, uint32_t cap) {
+  text_write_range(m, T, opts, width, out, stage, cap, 5, m.W, 0, !(opts & OPT_NO_HEADER));
+}
+
+// words [w_begin, w_end) whose text starts at out + pos0 (after the header when
+// `header`: then pos0 must be 0)
+__device__ __noinline__ void text_write_range(const Mod& m, const Tables& T, uint32_t opts, uint32_t width,
+                                              uint8_t* out, uint8_t* stage, uint32_t cap, uint32_t w_begin,
+                                              uint32_t w_end, uint64_t pos0, bool header) {
   const uint32_t lane = lane_id();
   const bool hl = opts & OPT_HIGHLIGHT;
-  uint64_t pos = 0;
+  uint64_t pos = pos0;
   const uint4 sp4 = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
-  if (!(opts & OPT_NO_HEADER)) {
+  if (header) {
     if (lane == 0) { Sink ms(stage); put_header(ms, m, hl); pos = ms.n; }
     pos = __shfl_sync(FULL, pos, 0);
     __syncwarp();
     flush_stage(out, out + pos, stage);
     __syncwarp();
   }
-  uint32_t w0 = 5;
-  while (w0 < m.W) {
+  uint32_t w0 = w_begin;
+  while (w0 < w_end) {
     const uint32_t w = w0 + lane;
     uint32_t x = 0, len = 0;
-    if (w < m.W) {
+    if (w < w_end) {
       x = m.wk[w];
       len = m.wl[w];
       if (len == 0xFFFF) len = word_len(m, T, w, x, width, hl);
     }
     const uint32_t incl = warp_incl_sum(len);
     const uint32_t shift = (uint32_t)(reinterpret_cast<uintptr_t>(out + pos) & 15);
-    const uint32_t take = __popc(__ballot_sync(FULL, w < m.W && shift + incl <= cap));
+    const uint32_t take = __popc(__ballot_sync(FULL, w < w_end && shift + incl <= cap));
     if (take == 0) {   // one word longer than the stage
       if (lane == 0) word_emit(out + pos, m, T, w, x, width, hl, false);
       __syncwarp();
