@@ -166,6 +166,21 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
                        uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
                        void* workspace, uint64_t workspace_bytes, void* stream);
 
+/* disassemble_module for ONE large module (config 3) over the whole GPU: the
+ * phases of skg_disasm as grid-wide kernels (tiled boundary pass, atomic id
+ * maps, per-instruction grammar walks, friendly names with device-wide scans
+ * and a prefix-max over id space, the text written per 1024-word range at
+ * scanned offsets; skg_disasm.cu / skg_big.cuh).  Host-synchronous.
+ * Replaces: Disassembler.to_text (reference disasm.py:117-127) for one module
+ * of nbytes bytes at `data` (device) with option bits `opts` (SKG_OPT_*).
+ * Returns 0: text[0:*text_bytes] and *status = SKG_ST_OK; 1: the exception the
+ * reference raises (*status, *error); 3: *text_bytes > text_cap (call again);
+ * 10 + s: the module does not decode (status s, *error); 2: ids at/above the
+ * header bound (use skg_disasm).  Workspace: skg_large_workspace_bytes. */
+int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
+                     uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
+                     void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,
  * and the text bytes the batch needs (allocator cursor). */

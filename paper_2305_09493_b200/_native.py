@@ -61,6 +61,8 @@ def lib():
     L.skg_large_workspace_bytes.restype = U64
     L.skg_validate_large.argtypes = [P, P, U64, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
     L.skg_validate_large.restype = I32
+    L.skg_disasm_large.argtypes = [P, P, U64, U32, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
+    L.skg_disasm_large.restype = I32
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
               L.skg_decode_large):
@@ -255,15 +257,18 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
         return []
     run = (lambda b: run_disasm(b, opts, spec, ext)) if kind == "disasm" else (lambda b: run_validate(b, spec))
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
-    if (n == 1 or need <= WS_BUDGET) and not (kind == "validate" and batch.max_words >= LARGE_MODULE_WORDS):
+    if (n == 1 or need <= WS_BUDGET) and batch.max_words < LARGE_MODULE_WORDS:
         return fetch_texts(run(batch), n)
     lens = batch.len.cpu().numpy()
     words = lens // 4
-    if kind == "validate":   # single large modules: the whole GPU on one module
+    if True:   # single large modules: the whole GPU on one module
         out = [None] * n
         rest = []
         for i in range(n):
-            r = _validate_large(batch, i, int(lens[i]), spec) if words[i] >= LARGE_MODULE_WORDS else None
+            r = None
+            if words[i] >= LARGE_MODULE_WORDS:
+                r = _validate_large(batch, i, int(lens[i]), spec) if kind == "validate" else \
+                    _disasm_large(batch, i, int(lens[i]), opts, spec, ext)
             if r is None:
                 rest.append(i)
             else:
@@ -293,6 +298,48 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
 
 LARGE_MODULE_WORDS = 1 << 20   # validate: modules this size and up run grid-wide (skg_validate_large)
 _DECODE_CODES = {ST_NOTSPIRV: "NotSpirv", ST_TRUNCATED: "TruncatedStream", ST_CORRUPT: "CorruptStream"}
+
+
+def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args):
+    """Shared driver of skg_validate_large / skg_disasm_large -> (rc, text bytes, errs)."""
+    torch = _torch()
+    L = lib()
+    o = int(batch.off[i].item())
+    data = batch.data.data_ptr() + o
+    W = nbytes // 4
+    head = batch.data[o:o + 20].cpu().numpy().tobytes()
+    bound = 0
+    if len(head) == 20:
+        w = np.frombuffer(head, dtype="<u4")
+        bound = int(w[3]) if w[0] == 0x07230203 else int(np.frombuffer(head, dtype=">u4")[3])
+    ws_bytes = int(L.skg_large_workspace_bytes(W, min(bound, 2 * W + 64)))
+    ws = _ws.get(ws_bytes)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    errs = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    cap = max(1 << 20, 4 * nbytes)
+    for _ in range(3):
+        text = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        need = ctypes.c_uint64(0)
+        rc = fn(data, nbytes, *args, text.data_ptr(), cap, ctypes.byref(need), status.data_ptr(), errs.data_ptr(),
+                ws.data_ptr(), ws_bytes, _stream())
+        if rc == 3:
+            cap = int(need.value) + 16
+            continue
+        break
+    _check(rc if rc < 0 else 0, fn.__name__)
+    return rc, (text[: int(need.value)].cpu().numpy().tobytes() if rc == 0 else None), errs
+
+
+def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext):
+    """skg_disasm_large on module i -> text bytes | exception | None (= use the batch path)."""
+    L = lib()
+    th = tables_handle(spec, ext)
+    rc, text, errs = _large_call(lambda *a: L.skg_disasm_large(th, a[0], a[1], *a[2:]), batch, i, nbytes, opts)
+    if rc == 2:
+        return None
+    if rc == 0:
+        return text
+    return decode_errors(errs.cpu().numpy())[0]
 
 
 def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec):

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
 #include "../../include/skgpu.h"
 #include "skg_module.cuh"
 #include "skg_sched.cuh"
@@ -397,7 +398,7 @@ LargeWs large_ws(uint8_t* ws, uint64_t W, uint32_t bound) {
   l.dec = ws + o; o += al256(skg_decode_large_workspace_bytes(W));
   l.mod = reinterpret_cast<skg::Mod*>(ws + o); o += al256(sizeof(skg::Mod));
   l.slot = ws + o; o += al256(skg::big_slot_bytes((uint32_t)W, bound));
-  l.sums = reinterpret_cast<uint32_t*>(ws + o); o += al256(4 * (W / skg::BS_BLOCK + 2));
+  l.sums = reinterpret_cast<uint32_t*>(ws + o); o += al256(4 * (3 * W / skg::BS_BLOCK + 4));   // N <= 2W + 64
   l.total = o;
   return l;
 }
@@ -506,6 +507,129 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
   *text_bytes = total;
   if (total > text_cap) return 3;                                  // grow the arena and call again
   skg::big_val_write<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl, text);
+  const int32_t ok = 0;
+  if (check(cudaMemcpyAsync(status, &ok, 4, cudaMemcpyHostToDevice, s))) return -1;
+  return check(cudaStreamSynchronize(s)) ? -1 : 0;
+}
+
+namespace {
+// exclusive scan of n uint32 in place; returns the total (host-synchronous)
+int64_t large_scan_total(uint32_t* a, uint32_t n, const LargeWs& l, cudaStream_t s) {
+  const uint32_t nb = (n + skg::BS_BLOCK - 1) / skg::BS_BLOCK;
+  if (nb) skg::scan_blocks<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
+  skg::scan_top<<<1, skg::BS_BLOCK, 0, s>>>(l.sums, nb, l.ctl + skg::BC_SCAN);
+  if (nb) skg::scan_apply<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
+  uint32_t tot = 0;
+  if (check(cudaMemcpyAsync(&tot, l.ctl + skg::BC_SCAN, 4, cudaMemcpyDeviceToHost, s)) ||
+      check(cudaStreamSynchronize(s)))
+    return -1;
+  return tot;
+}
+int read_ctl(const LargeWs& l, uint32_t* out64, cudaStream_t s) {
+  return check(cudaMemcpyAsync(out64, l.ctl, 256, cudaMemcpyDeviceToHost, s)) || check(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
+                     uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
+                     void* workspace, uint64_t workspace_bytes, void* stream) {
+  using namespace skg;
+  if (!t || !workspace || !data || !text_bytes || nbytes / 4 > 0xFFFFFFF0ull) return -1;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t W = nbytes / 4;
+  uint32_t hdr[5] = {0, 0, 0, 0, 0};
+  if (W >= 5 && check(cudaMemcpyAsync(hdr, data, 20, cudaMemcpyDeviceToHost, s))) return -1;
+  if (check(cudaStreamSynchronize(s))) return -1;
+  uint32_t bound = hdr[3];
+  if (hdr[0] == 0x03022307u) bound = __builtin_bswap32(bound);
+  if ((uint64_t)bound > 2 * W + 64) return 2;
+  const LargeWs l = large_ws((uint8_t*)workspace, W, bound);
+  if (workspace_bytes < l.total) return -3;
+  *text_bytes = 0;
+  ErrRec* rec = reinterpret_cast<ErrRec*>(error);
+  const int dst = large_front(data, nbytes, t->t.max_opcode, l, rec, s);
+  if (dst < 0) return -1;
+  if (dst > 0) return 10 + dst;                                    // decode exception (record in *error)
+  const Tables& T = t->t;
+  const uint32_t gW = grid_for(W), gS = grid_for(bound);
+  uint32_t ctl[64];
+  big_init_tables<<<gS, 256, 0, s>>>(l.mod);
+  big_prescan<<<gW, 256, 0, s>>>(l.mod, T, l.ctl);
+  big_fix_tables<<<gS, 256, 0, s>>>(l.mod);
+  bd_classify<<<gW, 256, 0, s>>>(l.mod, T);
+  if (read_ctl(l, ctl, s)) return -1;
+  if (ctl[BC_OVER]) return 2;
+  const bool names_mode = (opts & OPT_INLINE) && ctl[BC_ANYNAME];
+  Mod m;
+  if (check(cudaMemcpyAsync(&m, l.mod, sizeof(m), cudaMemcpyDeviceToHost, s))) return -1;
+  if (names_mode) bd_collect<<<gW, 256, 0, s>>>(l.mod);
+  bd_errors<<<gW, 256, 0, s>>>(l.mod, l.ctl, opts, names_mode);
+  uint32_t ovf = 0;
+  if (check(cudaMemcpyAsync(&ovf, m.overflow, 4, cudaMemcpyDeviceToHost, s))) return -1;
+  if (read_ctl(l, ctl, s)) return -1;
+  if (ovf) return 2;                                               // a referenced id at/above the bound
+  const uint32_t bad1 = ctl[BC_E1], bad2 = ctl[BC_E2], bad3 = ctl[BC_E3];
+  if (bad1 != NONE32 || bad2 != NONE32 || bad3 != NONE32) {
+    const uint32_t which = bad1 != NONE32 ? 1 : (bad2 != NONE32 ? 2 : 3);
+    bd_error_rec<<<1, 32, 0, s>>>(l.mod, T, which, which == 1 ? bad1 : (which == 2 ? bad2 : bad3), rec, status);
+    return check(cudaStreamSynchronize(s)) ? -1 : 1;
+  }
+  const uint32_t I = m.I;
+  if (names_mode) {
+    bn_flags<<<gS, 256, 0, s>>>(l.mod, l.ctl);
+    bn_mark<<<gW, 256, 0, s>>>(l.mod, T);
+    const int64_t cj = large_scan_total(m.ib, I, l, s);
+    const int64_t nd64 = large_scan_total(m.ia, I, l, s);
+    if (cj < 0 || nd64 < 0 || read_ctl(l, ctl, s)) return -1;
+    const uint32_t nd = (uint32_t)nd64, N = ctl[BC_NP0] + (uint32_t)cj;
+    bn_ndl<<<gW, 256, 0, s>>>(l.mod, T);
+    for (uint32_t step = 0; step < 3; ++step) bn_pos<<<grid_for(std::max<uint64_t>(N + 1, std::max<uint64_t>(I, bound))), 256, 0, s>>>(l.mod, T, N, step);
+    if (N >= 1) {   // inclusive prefix max over pos[1..N] from -2
+      int32_t* a = m.pos + 1;
+      const uint32_t nb = (N + BS_BLOCK - 1) / BS_BLOCK;
+      int32_t* maxes = reinterpret_cast<int32_t*>(l.sums);
+      maxscan_blocks<<<nb, BS_BLOCK, 0, s>>>(a, N, maxes);
+      maxscan_top<<<1, 32, 0, s>>>(maxes, nb, -2);
+      maxscan_apply<<<nb, BS_BLOCK, 0, s>>>(a, N, maxes);
+    }
+    bn_kept<<<gW, 256, 0, s>>>(l.mod, T, N);
+    uint32_t C = 4;
+    while (C < 2 * nd) C <<= 1;
+    uint32_t* htab = reinterpret_cast<uint32_t*>(m.spill);
+    const uint32_t gN = grid_for(nd), gC = grid_for(C);
+    bn_step<<<gN, 256, 0, s>>>(l.mod, htab, C, nd, 0);
+    bn_step<<<gC, 256, 0, s>>>(l.mod, htab, C, nd, 1);
+    for (uint32_t step = 2; step <= 5; ++step) bn_step<<<gN, 256, 0, s>>>(l.mod, htab, C, nd, step);
+    uint32_t* clist = reinterpret_cast<uint32_t*>(m.spill);       // the table is no longer needed
+    uint32_t* flags = clist + 4ull * nd;                            // spill holds >= 32 nd bytes
+    bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 0);
+    const int64_t nc = large_scan_total(flags, nd, l, s);
+    if (nc < 0) return -1;
+    bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 1);
+    bn_dedup<<<1, 32, 0, s>>>(l.mod, clist, (uint32_t)nc, nd);
+    bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 0);
+    if (large_scan_total(flags, nd, l, s) < 0) return -1;
+    bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 1);
+  }
+  bd_refs<<<gS, 256, 0, s>>>(l.mod, T, l.ctl, 0);
+  bd_refs<<<gW, 256, 0, s>>>(l.mod, T, l.ctl, 1);
+  if (opts & OPT_GROUP) {
+    bd_sections<<<1, 32, 0, s>>>(l.mod, T);
+    bd_blanks<<<gW, 256, 0, s>>>(l.mod);
+  }
+  bd_header_len<<<1, 32, 0, s>>>(l.mod, opts, l.ctl);
+  if (read_ctl(l, ctl, s)) return -1;
+  const uint32_t width = (opts & OPT_NO_INDENT) ? 0 : ctl[BC_WIDTH];
+  const uint32_t head = ctl[BC_TOTAL];
+  const uint32_t nr = (uint32_t)((W - 5 + BD_RANGE - 1) / BD_RANGE);
+  uint32_t* rsum = reinterpret_cast<uint32_t*>(m.spill);           // names are done with the spill area
+  bd_lengths<<<grid_for((uint64_t)nr * 32), 256, 0, s>>>(l.mod, T, opts, width, rsum);
+  const int64_t body = nr ? large_scan_total(rsum, nr, l, s) : 0;
+  if (body < 0) return -1;
+  const uint64_t total = (uint64_t)head + (uint64_t)body;
+  *text_bytes = total;
+  if (total > text_cap) return 3;
+  bd_render<<<grid_for((uint64_t)nr * 32 + 32), 256, 8 * 1024, s>>>(l.mod, T, opts, width, text, rsum, head);
   const int32_t ok = 0;
   if (check(cudaMemcpyAsync(status, &ok, 4, cudaMemcpyHostToDevice, s))) return -1;
   return check(cudaStreamSynchronize(s)) ? -1 : 0;

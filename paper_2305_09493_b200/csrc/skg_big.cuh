@@ -18,7 +18,9 @@ namespace skg {
 enum : uint32_t {
   BC_STATUS = 0, BC_ERRPOS = 1, BC_COUNT = 2, BC_SWAP = 3,        // shared with BigDecode.result
   BC_FLAGS = 8, BC_NMM = 9, BC_BAD = 10, BC_OVER = 11, BC_ANYNAME = 12, BC_ARENA = 13,
-  BC_TOTAL = 14, BC_EFF = 32                                       // eff: 8 x u64 at word 32
+  BC_TOTAL = 14, BC_SCAN = 16,                                     // BC_SCAN: u64 total of the last scan
+  BC_NP0 = 18, BC_E1 = 19, BC_E2 = 20, BC_E3 = 21, BC_WIDTH = 22, BC_SUM = 24,   // BC_SUM: u64
+  BC_EFF = 32                                                      // eff: 8 x u64 at word 32
 };
 enum : uint32_t { BF_FN = 1, BF_CAP = 2, BF_EP = 4 };
 
@@ -41,11 +43,12 @@ __global__ void big_setup(Mod* mp, uint8_t* slot, uint32_t W, uint32_t* ctl) {
   m.schema = m.w[4];
   m.arena_need = 0;
   for (uint32_t k = BC_FLAGS; k < 64; ++k) ctl[k] = 0;
-  ctl[BC_BAD] = NONE32;
+  ctl[BC_BAD] = NONE32; ctl[BC_E1] = NONE32; ctl[BC_E2] = NONE32; ctl[BC_E3] = NONE32;
   if (m.bound > 2 * m.W + 64) { ctl[BC_OVER] = 1; *mp = m; return; }   // not direct: host falls back
   layout_tables(m, true, m.bound, 0, 0);
   m.work_shared = false;
-  m.spill = m.work;   // unused by the big path
+  const uint32_t Imax = W > 5 ? W - 5 : 1;
+  m.spill = slot + big_slot_bytes(W, m.bound) - 256 - spill_bytes(Imax);
   *m.fill = 0; *m.overflow = 0; *m.top_present = 0;
   *mp = m;
 }
@@ -175,6 +178,58 @@ __global__ void __launch_bounds__(BS_BLOCK) scan_top(uint32_t* sums, uint32_t nb
 __global__ void __launch_bounds__(BS_BLOCK) scan_apply(uint32_t* a, uint32_t n, const uint32_t* sums) {
   const uint32_t i = blockIdx.x * BS_BLOCK + threadIdx.x;
   if (i < n) a[i] += sums[blockIdx.x];
+}
+
+// -- device-wide inclusive max-scan of int32 (in place), starting from `init` ------
+__device__ __forceinline__ int32_t block_incl_max(int32_t v, int32_t& total) {
+  __shared__ int32_t wmax[32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if (lane >= (uint32_t)d) x = max(x, y);
+  }
+  if (lane == 31) wmax[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t s = wmax[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xFFFFFFFFu, s, d);
+      if (lane >= (uint32_t)d) s = max(s, y);
+    }
+    wmax[lane] = s;
+  }
+  __syncthreads();
+  total = wmax[31];
+  const int32_t r = warp ? max(x, wmax[warp - 1]) : x;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(BS_BLOCK) maxscan_blocks(int32_t* a, uint32_t n, int32_t* maxes) {
+  const uint32_t i = blockIdx.x * BS_BLOCK + threadIdx.x;
+  int32_t tot;
+  const int32_t r = block_incl_max(i < n ? a[i] : INT32_MIN, tot);
+  if (i < n) a[i] = r;
+  if (threadIdx.x == 0) maxes[blockIdx.x] = tot;
+}
+
+// maxes[b] := max(init, maxes[0..b)) (exclusive); one thread (a few thousand blocks)
+__global__ void maxscan_top(int32_t* maxes, uint32_t nb, int32_t init) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int32_t c = init;
+  for (uint32_t b = 0; b < nb; ++b) {
+    const int32_t v = maxes[b];
+    maxes[b] = c;
+    c = max(c, v);
+  }
+}
+
+__global__ void __launch_bounds__(BS_BLOCK) maxscan_apply(int32_t* a, uint32_t n, const int32_t* maxes) {
+  const uint32_t i = blockIdx.x * BS_BLOCK + threadIdx.x;
+  if (i < n) a[i] = max(a[i], maxes[blockIdx.x]);
 }
 
 }  // namespace skg

@@ -1319,4 +1319,218 @@ __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(Disa
   }
 }
 
+
+
+// ---------------------------------------------------------------------------
+// One large module over the whole GPU (skg_big.cuh): the phases of disasm_one as
+// grid-stride kernels over instructions / words / ids / named definitions,
+// device-wide scans where the warp version carries a running offset, and the
+// text written per 1024-word range by one warp each at scanned offsets.
+#define SKG_GRID_FOR(i, n) \
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
+
+__device__ __forceinline__ void warp_add(uint32_t* dst, uint32_t v) {   // warp-aggregated atomicAdd
+  const unsigned act = __activemask();
+  const uint32_t sum = __reduce_add_sync(act, v);
+  if (lane_id() == (uint32_t)(__ffs(act) - 1) && sum) atomicAdd(dst, sum);
+}
+
+__global__ void bd_classify(const Mod* mp, Tables T) {
+  Mod m = *mp;
+  SKG_GRID_FOR(i, m.I) classify_one(m, T, i);
+}
+
+__global__ void bd_collect(const Mod* mp) {
+  Mod m = *mp;
+  SKG_GRID_FOR(k, m.W - 5) collect_one(m, 5 + k);
+}
+
+// first instruction of each error kind, in disasm_one's evaluation order
+__global__ void bd_errors(const Mod* mp, uint32_t* ctl, uint32_t opts, bool names_mode) {
+  const Mod m = *mp;
+  uint32_t e1 = NONE32, e2 = NONE32, e3 = NONE32;
+  SKG_GRID_FOR(i, m.I) {
+    const uint32_t d = m.idef[i], e = m.ierr[i];
+    if (m.iflag[i] & IF_PRESCAN_UTF8) e1 = min(e1, i);
+    if (names_mode && d != NONE16 && e != W_OK && !werr_is_codec(e)) e2 = min(e2, i);
+    if ((d == NONE16 && (opts & OPT_STRICT)) || (d != NONE16 && e != W_OK)) e3 = min(e3, i);
+  }
+  if (e1 != NONE32) atomicMin(&ctl[BC_E1], e1);
+  if (e2 != NONE32) atomicMin(&ctl[BC_E2], e2);
+  if (e3 != NONE32) atomicMin(&ctl[BC_E3], e3);
+}
+
+__global__ void bd_error_rec(const Mod* mp, Tables T, uint32_t which, uint32_t i, ErrRec* rec, int32_t* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const Mod m = *mp;
+  int32_t st;
+  if (which == 1) {
+    st = ST_UNICODE;
+    report_prescan_error(m, T, i, rec, 0);
+  } else if (m.idef[i] == NONE16) {
+    st = ST_CODEC;
+    if (rec) {
+      ErrWriter ew{rec};
+      put_cstr(ew, "unknown opcode "); put_u64(ew, inst_opcode(m, i));
+      rec->module = 0; rec->cls = ST_CODEC; rec->len = ew.n;
+    }
+  } else {
+    report_inst_error(m, T, i, rec, 0, st);
+  }
+  *status = st;
+}
+
+// -- names (resolve_names, step by step) -------------------------------------------
+__global__ void bn_flags(const Mod* mp, uint32_t* ctl) {
+  Mod m = *mp;
+  SKG_GRID_FOR(s, m.S) warp_add(&ctl[BC_NP0], nm_slot_flags(m, s) ? 1u : 0u);
+}
+
+// per instruction: ib = in C, ia = named definition (scanned into ranks next)
+__global__ void bn_mark(const Mod* mp, Tables T) {
+  Mod m = *mp;
+  SKG_GRID_FOR(i, m.I) {
+    bool isC, isN;
+    uint32_t slot;
+    nm_def_pred(m, T, i, isC, isN, slot);
+    m.ib[i] = isC ? 1 : 0;
+    m.ia[i] = isN ? 1 : 0;
+    m.iflag[i] = (m.iflag[i] & ~IF_FIRSTDEF) | (isC ? IF_FIRSTDEF : 0);
+  }
+}
+
+__global__ void bn_ndl(const Mod* mp, Tables T) {
+  Mod m = *mp;
+  SKG_GRID_FOR(i, m.I) {
+    bool isC, isN;
+    uint32_t slot;
+    nm_def_pred(m, T, i, isC, isN, slot);
+    if (isN) m.ndl[m.ia[i]] = slot;
+  }
+}
+
+__global__ void bn_pos(const Mod* mp, Tables T, uint32_t N, uint32_t step) {
+  Mod m = *mp;
+  if (step == 0) { SKG_GRID_FOR(v, N + 1) m.pos[v] = 0x7FFFFFFF; }
+  else if (step == 1) { SKG_GRID_FOR(s, m.S) if ((m.hfl[s] & HF_P0) && s >= 1 && s <= N) m.pos[s] = -1; }
+  else {
+    SKG_GRID_FOR(i, m.I) {
+      if (!(m.iflag[i] & IF_FIRSTDEF)) continue;
+      const uint32_t key = nm_def_key(m, T, i);
+      if (key >= 1 && key <= N) m.pos[key] = (int32_t)m.ib[i];
+    }
+  }
+}
+
+__global__ void bn_kept(const Mod* mp, Tables T, uint32_t N) {
+  Mod m = *mp;
+  SKG_GRID_FOR(i, m.I) {
+    if (!(m.iflag[i] & IF_FIRSTDEF)) continue;
+    const uint32_t key = nm_def_key(m, T, i);
+    const int32_t j = (int32_t)m.ib[i];
+    if (key >= 1 && key <= N && (key == 1 || m.pos[key - 1] < j)) m.hfl[key] |= HF_KEPT;
+  }
+}
+
+__global__ void bn_step(const Mod* mp, uint32_t* htab, uint32_t C, uint32_t nd, uint32_t step) {
+  Mod m = *mp;
+  if (step == 0) { SKG_GRID_FOR(k, nd) nm_info(m, k); }
+  else if (step == 1) { SKG_GRID_FOR(e, C) { htab[2 * e] = EMPTY; htab[2 * e + 1] = EMPTY; } }
+  else if (step == 2) { SKG_GRID_FOR(k, nd) nm_hinsert(htab, C, m.nH[m.ndl[k]], k); }
+  else if (step == 3) { SKG_GRID_FOR(k, nd) m.pos[k] = (int32_t)nm_leader(m, htab, C, k); }
+  else if (step == 4) { SKG_GRID_FOR(k, nd) m.ib[k] = nm_parent(m, htab, C, nd, k); }
+  else if (step == 5) { SKG_GRID_FOR(k, nd) nm_mark_parent(m, k); }
+}
+
+// child list: flags -> (scan) -> entries; then the sequential dedup (one thread)
+__global__ void bn_children(const Mod* mp, uint32_t* flags, uint32_t* clist, uint32_t nd, uint32_t step) {
+  Mod m = *mp;
+  if (step == 0) { SKG_GRID_FOR(k, nd) flags[k] = m.ib[k] != NONE32 ? 1 : 0; }
+  else {
+    SKG_GRID_FOR(k, nd) {
+      if (m.ib[k] == NONE32) continue;
+      const uint32_t at = flags[k];
+      clist[3 * at] = m.ib[k]; clist[3 * at + 1] = m.ia[k]; clist[3 * at + 2] = k;
+    }
+  }
+}
+
+__global__ void bn_dedup(const Mod* mp, const uint32_t* clist, uint32_t nc, uint32_t nd) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Mod m = *mp;
+  nm_dedup(m, nd, clist, nc);
+}
+
+__global__ void bn_arena(const Mod* mp, uint32_t* lens, uint32_t nd, uint32_t step) {
+  Mod m = *mp;
+  if (step == 0) {
+    SKG_GRID_FOR(k, nd) { const uint32_t s = m.ndl[k]; lens[k] = (m.hfl[s] & HF_KEPT) ? m.nLen[s] : 0; }
+  } else {
+    SKG_GRID_FOR(k, nd) if (m.hfl[m.ndl[k]] & HF_KEPT) nm_arena_write(m, k, lens[k]);
+  }
+}
+
+// -- refs, sizes, text -------------------------------------------------------------
+__global__ void bd_refs(const Mod* mp, Tables T, uint32_t* ctl, uint32_t step) {
+  Mod m = *mp;
+  if (step == 0) {
+    SKG_GRID_FOR(s, m.S) { const uint32_t r = ref_len_slow(m, s); m.hrl[s] = (uint16_t)(r > 0xFFFE ? 0xFFFF : r); }
+  } else {
+    uint32_t width = 0;
+    SKG_GRID_FOR(i, m.I) width = max(width, result_ref_one(m, T, i));
+    if (width) atomicMax(&ctl[BC_WIDTH], width);
+  }
+}
+
+__global__ void bd_blanks(const Mod* mp) {
+  Mod m = *mp;
+  SKG_GRID_FOR(i, m.I) if (i >= 1 && m.isec[i] != m.isec[i - 1]) m.wk[m.ioff[i]] |= WK_BLANK;
+}
+
+__global__ void bd_sections(const Mod* mp, Tables T) {   // one warp (sequential section state)
+  Mod m = *mp;
+  compute_sections(m, T);
+}
+
+__global__ void bd_header_len(const Mod* mp, uint32_t opts, uint32_t* ctl) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    ctl[BC_TOTAL] = (opts & OPT_NO_HEADER) ? 0 : header_len(*mp, opts & OPT_HIGHLIGHT);
+}
+
+constexpr uint32_t BD_RANGE = 1024;   // words per render range (one warp each)
+
+// word lengths (stored) and per-range sums
+__global__ void bd_lengths(const Mod* mp, Tables T, uint32_t opts, uint32_t width, uint32_t* rsum) {
+  const Mod m = *mp;
+  const bool hl = opts & OPT_HIGHLIGHT;
+  const uint32_t nr = (m.W - 5 + BD_RANGE - 1) / BD_RANGE;
+  const uint32_t wpb = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  for (uint32_t r = blockIdx.x * wpb + warp; r < nr; r += gridDim.x * wpb) {
+    const uint32_t w0 = 5 + r * BD_RANGE, w1 = min(w0 + BD_RANGE, m.W);
+    uint32_t sum = 0;
+    for (uint32_t w = w0 + lane_id(); w < w1; w += 32) {
+      const uint32_t l = word_len(m, T, w, m.wk[w], width, hl);
+      m.wl[w] = (uint16_t)(l > 0xFFFF ? 0xFFFF : l);
+      sum += l;
+    }
+    sum = warp_sum_u32(sum);
+    if (lane_id() == 0) rsum[r] = sum;
+  }
+}
+
+__global__ void bd_render(const Mod* mp, Tables T, uint32_t opts, uint32_t width, uint8_t* out,
+                          const uint32_t* roff, uint32_t head) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const Mod m = *mp;
+  const uint32_t nr = (m.W - 5 + BD_RANGE - 1) / BD_RANGE;
+  const uint32_t wpb = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  uint8_t* stage = smem + 1024 * warp;
+  if (nr == 0 && blockIdx.x == 0 && warp == 0 && head)
+    text_write_range(m, T, opts, width, out, stage, 1024, 5, 5, 0, true);
+  for (uint32_t r = blockIdx.x * wpb + warp; r < nr; r += gridDim.x * wpb) {
+    const uint32_t w0 = 5 + r * BD_RANGE, w1 = min(w0 + BD_RANGE, m.W);
+    text_write_range(m, T, opts, width, out, stage, 1024, w0, w1, (uint64_t)head + roff[r], r == 0 && head);
+  }
+}
+
 }  // namespace skg

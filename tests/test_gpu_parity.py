@@ -280,3 +280,46 @@ def test_validate_large_module_grid_wide(sk, monkeypatch):
     for c, g in zip(cases, got):
         want = [tuple(x) for x in oval.validate(c)]
         assert [(x.severity, x.code, x.location, x.message) for x in g] == want
+
+
+def test_disasm_large_module_grid_wide(sk, monkeypatch):
+    """disassembly of one large module runs grid-wide (skg_disasm_large): text
+    identical to the oracle under every option set, and the same exceptions."""
+    import struct
+    from oracle import disasm as odis
+    from paper_2305_09493_b200 import _native
+    from synth.families import FAMILIES, build_module
+    from synth.huge import build_huge
+    monkeypatch.setattr(_native, "LARGE_MODULE_WORDS", 1 << 12)
+    mods = [build_huge(12, chain=120, seed=7), build_huge(3, chain=400, seed=8)]
+    mods += [build_module(f, s) for f in FAMILIES for s in range(2)]   # small ones: batch path
+    opts = [sk.DisassemblerOptions(), sk.DisassemblerOptions(inline_names=False),
+            sk.DisassemblerOptions(highlight=True, group=True), sk.DisassemblerOptions(no_indent=True, no_header=True)]
+    for o in opts:
+        got = sk.disassemble_batch(mods, o)
+        for m, g in zip(mods, got):
+            assert g == odis.disassemble(m, o)
+    # exceptions: an unknown opcode under strict, invalid UTF-8 in an OpName
+    words = list(struct.unpack(f"<{len(mods[0]) // 4}I", mods[0]))
+    p, starts = 5, []
+    while p < len(words):
+        starts.append(p)
+        p += words[p] >> 16
+    w1 = list(words)
+    k = starts[len(starts) // 2]
+    w1[k] = (w1[k] & 0xFFFF0000) | 0x7FF0
+    name_at = next(s for s in starts if words[s] & 0xFFFF == 5)
+    w2 = list(words)
+    w2[name_at + 2] = 0x00FFFE61
+    bad = [struct.pack(f"<{len(w)}I", *w) for w in (w1, w2)]
+    for strict in (False, True):
+        got = sk.disassemble_batch(bad, None, strict=strict)
+        for m, g in zip(bad, got):
+            try:
+                want = odis.disassemble(m, strict=strict)
+            except Exception as exc:   # noqa: BLE001
+                want = exc
+            if isinstance(want, Exception):
+                assert (type(g).__name__, str(g)) == (type(want).__name__, str(want))
+            else:
+                assert g == want

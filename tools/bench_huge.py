@@ -52,6 +52,19 @@ def main():
             print(f"validate (skg_validate_large, grid-wide, incl. host syncs): {time.time() - t3:.3f} s "
                   f"{W / (time.time() - t3) / 1e6:.1f} Mwords/s -> {len(r) if isinstance(r, bytes) else r}",
                   flush=True)
+    from paper_2305_09493_b200.disasm import DisassemblerOptions, option_bits
+    for rep in range(2):   # disassembly, whole GPU on the one module (skg_disasm_large), device-resident
+        torch.cuda.synchronize()
+        t4 = time.time()
+        r = nat._disasm_large(dev, 0, len(m), option_bits(DisassemblerOptions()), None, None)
+        torch.cuda.synchronize()
+        if rep:
+            dt = time.time() - t4
+            print(f"disasm (skg_disasm_large, grid-wide, default options, incl. host syncs + text D2H): "
+                  f"{dt:.3f} s {W / dt / 1e6:.1f} Mwords/s -> {len(r) if isinstance(r, bytes) else r} bytes",
+                  flush=True)
+    if "--batch-path" not in sys.argv:
+        return
     for kind in ("disasm", "validate"):
         plan = _native.DisasmPlan(dev, 2, kind=kind, text_cap=24 * len(m) + 4096)
         t1 = time.time()
