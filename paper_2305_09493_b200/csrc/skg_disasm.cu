@@ -363,10 +363,26 @@ __device__ __noinline__ void nm_dedup(Mod& m, uint32_t nd, const uint32_t* clist
       if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
     return NONE32;
   };
+  // the (leader, leader slot, slot) of the next 8 idents are loaded ahead: they
+  // do not depend on the pass's state, only the group flags / counters do
+  constexpr uint32_t AHEAD = 8;
   #pragma unroll 1
-  for (uint32_t k = 0; k < nd; ++k) {
-    const uint32_t g = (uint32_t)m.pos[k];
-    const uint32_t gs = m.ndl[g];
+  for (uint32_t k0 = 0; k0 < nd; k0 += AHEAD) {
+  uint32_t gv[AHEAD], gsv[AHEAD], ksv[AHEAD];
+  #pragma unroll
+  for (uint32_t j = 0; j < AHEAD; ++j) {
+    const uint32_t kk = min(k0 + j, nd - 1);
+    gv[j] = (uint32_t)m.pos[kk];
+    ksv[j] = m.ndl[kk];
+  }
+  #pragma unroll
+  for (uint32_t j = 0; j < AHEAD; ++j) gsv[j] = m.ndl[gv[j]];
+  #pragma unroll
+  for (uint32_t j = 0; j < AHEAD; ++j) {
+    const uint32_t k = k0 + j;
+    if (k >= nd) break;
+    const uint32_t g = gv[j];
+    const uint32_t gs = gsv[j];
     if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
     uint32_t serial = NONE32;
     const uint8_t fl = m.hfl[gs];
@@ -383,7 +399,8 @@ __device__ __noinline__ void nm_dedup(Mod& m, uint32_t nd, const uint32_t* clist
       serial = sv;
       m.nP[gs] = sv + 1;
     }
-    m.hser[m.ndl[k]] = serial;
+    m.hser[ksv[j]] = serial;
+  }
   }
 }
 
