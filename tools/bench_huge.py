@@ -1,7 +1,8 @@
 """Config 3: disassembly + validation of ONE large module (synth/huge.py) on
 cuda:0, inputs resident in HBM; prints words/s for each kernel.
 
-usage: python tools/bench_huge.py <n_functions> [chain]   (~1840 words per function)
+usage: python tools/bench_huge.py <n_functions> [chain] [--batch-path]   (~1660 words per function)
+       (--batch-path also times the one-warp batch kernels on the same module)
 """
 import sys
 import time
@@ -12,8 +13,9 @@ sys.path.insert(0, str(ROOT))
 
 
 def main():
-    n_fn = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
-    chain = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    n_fn = int(args[0]) if len(args) > 0 else 5000
+    chain = int(args[1]) if len(args) > 1 else 200
     import numpy as np
     import torch
     from paper_2305_09493_b200 import _native
