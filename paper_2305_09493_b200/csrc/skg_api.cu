@@ -606,7 +606,10 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
     const int64_t nc = large_scan_total(flags, nd, l, s);
     if (nc < 0) return -1;
     bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 1);
-    bn_dedup<<<1, 32, 0, s>>>(l.mod, clist, (uint32_t)nc, nd);
+    // group counters of the parallel dedup: one per ident index (leaders), after the list
+    uint32_t* gcount = flags + nd;                                  // spill: 12 nc + 4 nd + 4 nd <= 32 nd bytes
+    if (check(cudaMemsetAsync(gcount, 0, 4ull * nd, s))) return -1;
+    bn_dedup_par<<<1, 1024, 0, s>>>(l.mod, clist, (uint32_t)nc, nd, gcount);
     bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 0);
     if (large_scan_total(flags, nd, l, s) < 0) return -1;
     bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 1);

@@ -1478,6 +1478,112 @@ __global__ void bn_dedup(const Mod* mp, const uint32_t* clist, uint32_t nc, uint
   nm_dedup(m, nd, clist, nc);
 }
 
+// The same pass with the independent groups in parallel (one CTA of 1024).  A
+// group that neither has child groups nor is one ("involved" otherwise) only
+// sees its own members: its k-th member (D order) gets the base for k = 0 and
+// serial k - 1 after.  Per chunk of 1024 idents, such members are sorted by
+// (leader, position) in shared memory (bitonic), ranked within the chunk and
+// offset by the group's running count; the involved idents of the chunk go
+// through the exact sequential logic (nm_dedup's body) on thread 0, in order.
+__global__ void __launch_bounds__(1024) bn_dedup_par(const Mod* mp, const uint32_t* clist, uint32_t nc,
+                                                     uint32_t nd, uint32_t* gcount) {
+  __shared__ uint64_t key[1024];
+  __shared__ uint32_t segstart[1024];
+  __shared__ uint32_t inv[1024];
+  __shared__ uint32_t ninv;
+  Mod m = *mp;
+  const uint32_t t = threadIdx.x;
+  auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
+    #pragma unroll 1
+    for (uint32_t q = 0; q < nc; ++q)
+      if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
+    return NONE32;
+  };
+  for (uint32_t base = 0; base < nd; base += 1024) {
+    const uint32_t k = base + t;
+    uint64_t kk = ~0ull;
+    bool involved = false;
+    if (k < nd) {
+      const uint32_t g = (uint32_t)m.pos[k];
+      involved = (m.hfl[m.ndl[g]] & HF_HASCHILD) || m.ib[g] != NONE32;
+      if (!involved) kk = ((uint64_t)g << 32) | t;
+    }
+    key[t] = kk;
+    if (t == 0) ninv = 0;
+    __syncthreads();
+    // involved idents of the chunk, in order
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, involved);
+    if ((t & 31) == 0) segstart[t >> 5] = __popc(b);
+    __syncthreads();
+    if (t == 0) {   // per-warp offsets (32 warps)
+      uint32_t run = 0;
+      for (uint32_t w = 0; w < 32; ++w) {
+        const uint32_t c = segstart[w];
+        segstart[w] = run;
+        run += c;
+      }
+      ninv = run;
+    }
+    __syncthreads();
+    if (involved) inv[segstart[t >> 5] + __popc(b & ((1u << (t & 31)) - 1))] = k;
+    __syncthreads();
+    // bitonic sort of the independent members by (leader, position)
+    for (uint32_t size = 2; size <= 1024; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        const uint32_t p = t ^ stride;
+        if (p > t) {
+          const bool up = (t & size) == 0;
+          const uint64_t a = key[t], c = key[p];
+          if ((a > c) == up) { key[t] = c; key[p] = a; }
+        }
+        __syncthreads();
+      }
+    }
+    const uint64_t me = key[t];
+    const uint32_t g = (uint32_t)(me >> 32);
+    const bool first = t == 0 || (uint32_t)(key[t - 1] >> 32) != g;
+    segstart[t] = first ? t : 0;
+    __syncthreads();
+    for (uint32_t d = 1; d < 1024; d <<= 1) {   // inclusive max-scan of segment starts
+      const uint32_t v = t >= d ? segstart[t - d] : 0;
+      __syncthreads();
+      segstart[t] = max(segstart[t], v);
+      __syncthreads();
+    }
+    if (me != ~0ull) {
+      const uint32_t r = gcount[g] + (t - segstart[t]);
+      m.hser[m.ndl[base + (uint32_t)(me & 0xFFFF)]] = r == 0 ? NONE32 : r - 1;
+      const bool last = t == 1023 || (uint32_t)(key[t + 1] >> 32) != g;
+      if (last) gcount[g] += t - segstart[t] + 1;
+    }
+    if (t == 0) {   // involved idents: the exact sequential logic, in D order
+      for (uint32_t q = 0; q < ninv; ++q) {
+        const uint32_t kq = inv[q];
+        const uint32_t gq = (uint32_t)m.pos[kq];
+        const uint32_t gs = m.ndl[gq];
+        if (gq == kq) m.nP[gs] = 0;
+        uint32_t serial = NONE32;
+        const uint8_t fl = m.hfl[gs];
+        if (!(fl & HF_TB)) {
+          m.hfl[gs] = fl | HF_TB;
+        } else {
+          uint32_t sv = m.nP[gs];
+          if (fl & HF_HASCHILD) {
+            uint32_t c;
+            #pragma unroll 1
+            while ((c = child_of(gq, sv)) != NONE32 && (m.hfl[m.ndl[c]] & HF_TB)) ++sv;
+            if (c != NONE32) m.hfl[m.ndl[c]] |= HF_TB;
+          }
+          serial = sv;
+          m.nP[gs] = sv + 1;
+        }
+        m.hser[m.ndl[kq]] = serial;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void bn_arena(const Mod* mp, uint32_t* lens, uint32_t nd, uint32_t step) {
   Mod m = *mp;
   if (step == 0) {
