@@ -878,125 +878,153 @@ __device__ __noinline__ uint32_t word_len(const Mod& m, const Tables& T, uint32_
   }
 }
 
-// emit word w's text at p; `spaces` = destination already holds spaces (skip padding)
+// emit word w's text at p; `spaces` = destination already holds spaces (skip padding).
+// Every code's text is prefix + [ref] + [" = "] + [table name] + [digits] +
+// [special] + ['\n'], so the stages run in that order with the expensive ones
+// (reference, table-name copy, decimal digits) reached by all lanes that need
+// them at the same program point: the warp runs each once, not once per code.
 __device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T, uint32_t w, uint32_t x,
                                        uint32_t width, bool hl, bool spaces) {
   const uint32_t v = m.w[w];
-  switch (wk_code(x)) {
-    case C_OPC: {
-      const uint32_t i = wk_pay(x);
-      if (x & WK_BLANK) *p++ = '\n';
-      uint32_t pad = 0;
-      const bool res = m.iflag[i] & IF_HAS_RESULT;
-      const uint32_t rl = res ? (m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i]) : 0;
-      if (res) pad = width ? width - rl : 0;
-      else pad = width ? width + 3 : 0;
-      if (!spaces) {
+  const uint32_t code = wk_code(x);
+  uint32_t ref = NONE32, tab_off = 0, tab_len = 0, num = 0;
+  bool has_ref = false, has_num = false, opc_res = false, special = false;
+  const char* ansi_tab = nullptr;
+  // stage 1: prefix and what the later stages emit
+  if (code == C_OPC) {
+    const uint32_t i = wk_pay(x);
+    if (x & WK_BLANK) *p++ = '\n';
+    opc_res = m.iflag[i] & IF_HAS_RESULT;
+    uint32_t pad;
+    if (opc_res) {
+      const uint32_t rl = m.irl[i] == 0xFFFF ? ref_len(m, m.ib[i]) : m.irl[i];
+      pad = width ? width - rl : 0;
+      has_ref = true;
+      ref = m.ib[i];
+    } else {
+      pad = width ? width + 3 : 0;
+    }
+    if (!spaces) {
 #pragma unroll 1
-        for (uint32_t q = 0; q < pad; ++q) p[q] = ' ';
-      }
-      p += pad;
-      if (res) {
-        if (hl) p = emit_cstr(p, ANSI_ID);
-        p = emit_ref(p, m, m.ib[i]);
+      for (uint32_t q = 0; q < pad; ++q) p[q] = ' ';
+    }
+    p += pad;
+    const uint32_t d = m.idef[i];
+    if (d == NONE16) { special = true; num = v & 0xFFFF; }
+    else { tab_off = T.iname_off(d); tab_len = T.iname_len(d); ansi_tab = hl ? ANSI_OPCODE : nullptr; }
+  } else if (code == C_REF) {
+    *p++ = ' ';
+    has_ref = true;
+    ref = v;
+  } else if (code == C_DEC || code == C_DECID) {
+    *p++ = ' ';
+    has_num = true;
+    num = v;
+  } else if (code == C_VEN) {
+    *p++ = ' ';
+    const uint32_t e = wk_pay(x);
+    tab_off = T.ename_off(e); tab_len = T.ename_len(e);
+  } else if (code == C_EXT) {
+    *p++ = ' ';
+    if (!(wk_pay(x) && T.ext_name(v, tab_off, tab_len))) { has_num = true; num = v; tab_len = 0; }
+  } else if (code == C_SPO) {
+    *p++ = ' ';
+    const uint32_t d = T.inst_of(v);
+    if (d != NONE32) { tab_off = T.iname_off(d) + 2; tab_len = T.iname_len(d) - 2; }
+    else { has_num = true; num = v; }
+  } else if (code != C_NONE && code != C_RES) {
+    special = true;
+  }
+  // stage 2: the reference (result of an instruction line, or an id operand)
+  if (has_ref) {
+    if (hl) p = emit_cstr(p, ANSI_ID);
+    p = emit_ref(p, m, ref);
+    if (hl) p = emit_cstr(p, ANSI_RESET);
+    if (opc_res) { p[0] = ' '; p[1] = '='; p[2] = ' '; p += 3; }
+  }
+  // stage 3: a name from the grammar tables (opcode, enumerant, ext instruction)
+  if (tab_len) {
+    if (ansi_tab) p = emit_cstr(p, ansi_tab);
+    p = emit_tab(p, T, tab_off, tab_len);
+    if (ansi_tab) p = emit_cstr(p, ANSI_RESET);
+  }
+  // stage 4: decimal digits
+  if (has_num) p = emit_u32(p, num);
+  // stage 5: the rest (bit masks, strings, typed literals, unknown opcodes / words)
+  if (special) {
+    switch (code) {
+      case C_OPC: {   // opcode outside the grammar
+        if (hl) p = emit_cstr(p, ANSI_OPCODE);
+        p = emit_cstr(p, "OpUnknown("); p = emit_u32(p, num); *p++ = ')';
         if (hl) p = emit_cstr(p, ANSI_RESET);
-        p[0] = ' '; p[1] = '='; p[2] = ' '; p += 3;
-      }
-      if (hl) p = emit_cstr(p, ANSI_OPCODE);
-      const uint32_t d = m.idef[i];
-      if (d == NONE16) { p = emit_cstr(p, "OpUnknown("); p = emit_u32(p, v & 0xFFFF); *p++ = ')'; }
-      else p = emit_tab(p, T, T.iname_off(d), T.iname_len(d));
-      if (hl) p = emit_cstr(p, ANSI_RESET);
-      break;
-    }
-    case C_NONE: case C_RES: break;
-    case C_REF:
-      *p++ = ' ';
-      if (hl) p = emit_cstr(p, ANSI_ID);
-      p = emit_ref(p, m, v);
-      if (hl) p = emit_cstr(p, ANSI_RESET);
-      break;
-    case C_DEC: case C_DECID: *p++ = ' '; p = emit_u32(p, v); break;
-    case C_VEN: { const uint32_t e = wk_pay(x); *p++ = ' '; p = emit_tab(p, T, T.ename_off(e), T.ename_len(e)); break; }
-    case C_BEN: {
-      const uint32_t k = wk_pay(x);
-      *p++ = ' ';
-      if (v == 0) {
-        const uint32_t z = T.kzero(k);
-        if (z != NONE32) p = emit_tab(p, T, T.ename_off(z), T.ename_len(z)); else *p++ = '0';
         break;
       }
-      uint32_t bytes, cnt;
-      if (!bit_cover(T, k, v, bytes, cnt)) {
-        const uint32_t hd = hex_digits(v);
-        *p++ = '0'; *p++ = 'x';
-#pragma unroll 1
-        for (uint32_t q = 0; q < hd; ++q) p[q] = (uint8_t)"0123456789abcdef"[(v >> (4 * (hd - 1 - q))) & 0xF];
-        p += hd;
-        break;
-      }
-      const uint32_t eo = T.kenum_off(k), ne = T.knenum(k);
-      uint32_t covered = 0;
-      bool first = true;
-#pragma unroll 1
-      for (uint32_t j = 0; j < ne; ++j) {
-        const uint32_t ev = T.evalue(eo + j);
-        if (covered == v) break;
-        if (ev && (v & ev) == ev && (covered & ev) != ev) {
-          covered |= ev;
-          if (!first) *p++ = '|';
-          first = false;
-          p = emit_tab(p, T, T.ename_off(eo + j), T.ename_len(eo + j));
+      case C_BEN: {
+        const uint32_t k = wk_pay(x);
+        *p++ = ' ';
+        if (v == 0) {
+          const uint32_t z = T.kzero(k);
+          if (z != NONE32) p = emit_tab(p, T, T.ename_off(z), T.ename_len(z)); else *p++ = '0';
+          break;
         }
-      }
-      break;
-    }
-    case C_STR: {
-      const uint32_t pl = wk_pay(x), nb = pl >> 2;
-      if (pl & 1) { *p++ = ' '; if (hl) p = emit_cstr(p, ANSI_STRING); *p++ = '"'; }
+        uint32_t bytes, cnt;
+        if (!bit_cover(T, k, v, bytes, cnt)) {
+          const uint32_t hd = hex_digits(v);
+          *p++ = '0'; *p++ = 'x';
 #pragma unroll 1
-      for (uint32_t q = 0; q < nb; ++q) {
-        const uint32_t b = (v >> (8 * q)) & 0xFF;
-        if (b == '\\' || b == '"') *p++ = '\\';
-        *p++ = (uint8_t)b;
-      }
-      if (pl & 2) { *p++ = '"'; if (hl) p = emit_cstr(p, ANSI_RESET); }
-      break;
-    }
-    case C_TYP: {
-      const uint32_t pl = wk_pay(x), width_t = pl >> 2;
-      Sink s(p);
-      s.put(' ');
-      if (pl & 1) put_repr_double(s, typed_float_bits(m, w, v, width_t));
-      else {
-        const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
-        if (lv.neg) put_i64(s, (int64_t)lv.bits); else put_u64(s, lv.bits);
-      }
-      p += s.n;
-      break;
-    }
-    case C_EXT: {
-      *p++ = ' ';
-      uint32_t off, ln;
-      if (wk_pay(x) && T.ext_name(v, off, ln)) p = emit_tab(p, T, off, ln);
-      else p = emit_u32(p, v);
-      break;
-    }
-    case C_SPO: {
-      *p++ = ' ';
-      const uint32_t d = T.inst_of(v);
-      if (d != NONE32) p = emit_tab(p, T, T.iname_off(d) + 2, T.iname_len(d) - 2);
-      else p = emit_u32(p, v);
-      break;
-    }
-    case C_UNK: {
-      *p++ = ' '; *p++ = '!'; *p++ = '0'; *p++ = 'x';
+          for (uint32_t q = 0; q < hd; ++q) p[q] = (uint8_t)"0123456789abcdef"[(v >> (4 * (hd - 1 - q))) & 0xF];
+          p += hd;
+          break;
+        }
+        const uint32_t eo = T.kenum_off(k), ne = T.knenum(k);
+        uint32_t covered = 0;
+        bool first = true;
 #pragma unroll 1
-      for (uint32_t q = 0; q < 8; ++q) p[q] = (uint8_t)"0123456789ABCDEF"[(v >> (28 - 4 * q)) & 0xF];
-      p += 8;
-      break;
+        for (uint32_t j = 0; j < ne; ++j) {
+          const uint32_t ev = T.evalue(eo + j);
+          if (covered == v) break;
+          if (ev && (v & ev) == ev && (covered & ev) != ev) {
+            covered |= ev;
+            if (!first) *p++ = '|';
+            first = false;
+            p = emit_tab(p, T, T.ename_off(eo + j), T.ename_len(eo + j));
+          }
+        }
+        break;
+      }
+      case C_STR: {
+        const uint32_t pl = wk_pay(x), nb = pl >> 2;
+        if (pl & 1) { *p++ = ' '; if (hl) p = emit_cstr(p, ANSI_STRING); *p++ = '"'; }
+#pragma unroll 1
+        for (uint32_t q = 0; q < nb; ++q) {
+          const uint32_t b = (v >> (8 * q)) & 0xFF;
+          if (b == '\\' || b == '"') *p++ = '\\';
+          *p++ = (uint8_t)b;
+        }
+        if (pl & 2) { *p++ = '"'; if (hl) p = emit_cstr(p, ANSI_RESET); }
+        break;
+      }
+      case C_TYP: {
+        const uint32_t pl = wk_pay(x), width_t = pl >> 2;
+        Sink sk(p);
+        sk.put(' ');
+        if (pl & 1) put_repr_double(sk, typed_float_bits(m, w, v, width_t));
+        else {
+          const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
+          if (lv.neg) put_i64(sk, (int64_t)lv.bits); else put_u64(sk, lv.bits);
+        }
+        p += sk.n;
+        break;
+      }
+      case C_UNK: {
+        *p++ = ' '; *p++ = '!'; *p++ = '0'; *p++ = 'x';
+#pragma unroll 1
+        for (uint32_t q = 0; q < 8; ++q) p[q] = (uint8_t)"0123456789ABCDEF"[(v >> (28 - 4 * q)) & 0xF];
+        p += 8;
+        break;
+      }
+      default: break;
     }
-    default: break;
   }
   if (x & WK_LAST) *p = '\n';
 }
