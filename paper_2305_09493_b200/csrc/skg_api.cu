@@ -330,7 +330,6 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.default_version = default_version;
   const Geom g = asm_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_ASM_GROUP", (int)g.warps));
-  a.sync_mask = (uint32_t)env_int("SKG_ASM_SYNC", 0x3FF);
   static bool carve = false;
   if (!carve) {
     const int pct = env_int("SKG_CARVEOUT", -2);

@@ -55,7 +55,6 @@ struct AsmArgs {
   uint32_t default_version;   // major << 16 | minor
   const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
   uint32_t group_warps;       // warps per phase-barrier group (divides the CTA's warps)
-  uint32_t sync_mask;         // phase barriers in use (bit k: after phase k); experiments
 };
 
 // token: off (text byte offset), lenf = len | TK_STR
@@ -1882,7 +1881,7 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   m.L = L;
 end_a:
   PHASE_MARK(0);
-  if (a.sync_mask & (1u << 0)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_b;
   {
   // per-line arrays (lt0: token-slot bases from split_lines)
@@ -1948,7 +1947,7 @@ end_a:
   }
 end_b:
   PHASE_MARK(2);
-  if (a.sync_mask & (1u << 1)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_c;
   // -- C: header comments; then the first reservation failure --------------------
   if (lane == 0) x = scan_header(m, X, a.default_version);
@@ -1967,7 +1966,7 @@ end_b:
   }
 end_c:
   PHASE_MARK(3);
-  if (a.sync_mask & (1u << 2)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_d;
   // -- D: unreserved prefix counts; symbolic result names in document order -------
   {
@@ -2034,7 +2033,7 @@ end_c:
   }
 end_d:
   PHASE_MARK(4);
-  if (a.sync_mask & (1u << 3)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_e;
   // -- E: opname lookup, width / value-type scans ---------------------------------
   for (uint32_t base = 0; base < L; base += 32) {
@@ -2063,7 +2062,7 @@ end_d:
   }
 end_e:
   PHASE_MARK(5);
-  if (a.sync_mask & (1u << 4)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_f;
   // -- F: encode pass 1 -------------------------------------------------------------
   {   // words of a line are bounded by 2 per token (4 string bytes per word)
@@ -2137,7 +2136,7 @@ end_e:
   }
 end_f:
   PHASE_MARK(6);
-  if (a.sync_mask & (1u << 5)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_g;
   // -- G: state machine ------------------------------------------------------------
   if (state_fast(m, X)) {
@@ -2158,7 +2157,7 @@ end_f:
   if (ndiag) { finish_error(a, m, X, t, X_ASSEMBLY, ndiag, fscratch, flimbs); done = true; goto end_g; }
 end_g:
   PHASE_MARK(7);
-  if (a.sync_mask & (1u << 6)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_h;
   // -- H: structure checks + layout (lane 0) ----------------------------------------
   if (lane == 0) {
@@ -2195,7 +2194,7 @@ end_g:
   total = m.misc[MS_TOTAL];
 end_h:
   PHASE_MARK(8);
-  if (a.sync_mask & (1u << 7)) CTA_SYNC();
+  CTA_SYNC();
   if (done) goto end_i;
   {
   // -- I: output ---------------------------------------------------------------------
@@ -2281,7 +2280,7 @@ end_h:
   }
 end_i:
   PHASE_MARK(9);
-  if (a.sync_mask & (1u << 8)) CTA_SYNC();
+  CTA_SYNC();
 }
 
 #ifndef SKG_ASM_MAXT
