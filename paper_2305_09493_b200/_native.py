@@ -119,7 +119,10 @@ class DeviceBatch:
     def from_host(cls, data: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, stream=None):
         torch = _torch()
         dev = torch.device("cuda")
-        d = torch.from_numpy(np.ascontiguousarray(data, dtype=np.uint8)).to(dev, non_blocking=False)
+        arr = np.ascontiguousarray(data, dtype=np.uint8)
+        if not arr.flags.writeable:   # torch.from_numpy wants a writable array (read-only bytes views)
+            arr = arr.copy()
+        d = torch.from_numpy(arr).to(dev, non_blocking=False)
         o = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
         ln = torch.from_numpy(np.ascontiguousarray(lengths, dtype=np.int64)).to(dev)
         mw = int(lengths.max()) // 4 if len(lengths) else 0

@@ -323,3 +323,38 @@ def test_disasm_large_module_grid_wide(sk, monkeypatch):
                 assert (type(g).__name__, str(g)) == (type(want).__name__, str(want))
             else:
                 assert g == want
+
+
+def test_large_paths_edge_cases(sk, monkeypatch):
+    """The whole-GPU single-module paths on degenerate inputs: header only, a
+    truncated stream, a foreign magic, big-endian, and an empty-string OpName."""
+    import struct
+    from oracle import core
+    from oracle import disasm as odis, validate as oval
+    from paper_2305_09493_b200 import _native
+    monkeypatch.setattr(_native, "LARGE_MODULE_WORDS", 1)
+    monkeypatch.setattr(_native, "LARGE_DECODE_WORDS", 1)
+    hdr = [0x07230203, 0x00010200, 0, 10, 0]
+    cases = [struct.pack("<5I", *hdr),
+             struct.pack("<5I", *hdr) + b"\x01\x02",
+             struct.pack("<5I", 0x12345678, *hdr[1:]),
+             struct.pack(">5I", *hdr) + struct.pack(">2I", (2 << 16) | 17, 6),
+             struct.pack("<5I", *hdr) + struct.pack("<3I", (3 << 16) | 5, 1, 0)]
+
+    def outcome(f, m):
+        try:
+            r = f(m)
+        except Exception as exc:   # noqa: BLE001
+            return ("exc", type(exc).__name__, str(exc))
+        return ("ok", r)
+
+    for m in cases:
+        got = sk.disassemble_batch([m])[0]
+        want = outcome(odis.disassemble, m)
+        assert (("exc", type(got).__name__, str(got)) if isinstance(got, BaseException) else ("ok", got)) == want
+        gv = sk.validate_batch([m])[0]
+        wv = [tuple(x) for x in oval.validate(m)]
+        assert [(x.severity, x.code, x.location, x.message) for x in gv] == wv
+        gd = outcome(lambda x: [(i.opcode, tuple(i.operands)) for i in sk.decode_module(x)[1]], m)
+        wd = outcome(lambda x: [(op, tuple(o)) for op, o in core.decode_module(x)[1]], m)
+        assert gd == wd
