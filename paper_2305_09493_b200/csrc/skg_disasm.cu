@@ -1206,7 +1206,7 @@ __device__ unsigned long long g_dis_phase[16];
 // time (CTA barrier between phases), so the instruction working set of the SM
 // is one phase rather than the whole program.
 __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
-                                        uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw) {
+                                        uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw, Mod& m) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   DPHASE_START();
@@ -1215,7 +1215,6 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
   int32_t status = live ? ST_OK : ST_INTERNAL;
   uint64_t total = 0;
   uint32_t width = 0;
-  Mod m;
   bool in_smem = false, direct = false, names_mode = false;
   // -- P0: load + boundary (A1, A2)
   if (live) {
@@ -1345,6 +1344,10 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
 __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(DisasmArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_base[16];
+  // the module descriptor, one per warp in shared memory (a per-thread copy would
+  // take 32 x sizeof(Mod) of L1 per warp as local memory); all lanes write the
+  // same values into it
+  __shared__ Mod s_mod[32];
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;                 // warps per barrier group
@@ -1360,7 +1363,7 @@ __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(Disa
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    disasm_one(a, base + gwarp_in, slab, gslot, stage, es, gid, gw);
+    disasm_one(a, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block]);
   }
 }
 
