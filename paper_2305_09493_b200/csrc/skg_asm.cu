@@ -1848,13 +1848,13 @@ __device__ __noinline__ void group_lines_by_opcode(AsmMod& m, uint32_t* perm) {
 }
 
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot,
-                                             uint32_t gid, uint32_t gw) {
+                                             uint32_t gid, uint32_t gw, AsmMod& m) {
   const uint32_t lane = lane_id_a();
   PHASE_START();
   bool done = t >= a.n_mod;
   const int64_t len64 = done ? 0 : a.mod_len[(size_t)t * a.mod_stride];
   const uint8_t* src = done ? a.text : a.text + a.mod_off[(size_t)t * a.mod_stride];
-  AsmMod m{};
+  m = AsmMod{};   // every lane writes the same (zero) values
   uint64_t used = 0;
   auto take = [&](uint64_t bytes) -> uint8_t* { uint8_t* r = slot + used; used += al16(bytes); return r; };
   uint32_t* fscratch = nullptr;
@@ -2144,6 +2144,7 @@ end_f:
   } else {
     state_reset(m);
     if (lane == 0) ndiag = state_machine(m, X);
+    __syncwarp();   // lane 0 may have grown the name table (m.nt / m.ncap, shared by the warp)
   }
   if (lane == 0 && ndiag != NONE32) {
     for (uint32_t li = 0; li < L; ++li) {
@@ -2289,6 +2290,7 @@ end_i:
 #endif
 __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs a) {
   __shared__ uint32_t s_base[16];
+  __shared__ AsmMod s_amod[32];   // the module descriptor, one per warp (not a per-thread local copy)
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;                 // warps per barrier group
@@ -2303,7 +2305,7 @@ __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
     const uint32_t tk = base + gwarp_in;
-    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw);
+    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block]);
   }
 }
 
