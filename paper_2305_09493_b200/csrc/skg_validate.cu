@@ -193,7 +193,7 @@ __device__ __noinline__ void shape_diags(S& s, const Shape& sh) {
 // One module per warp; the CTA's warps run each phase together (CTA barrier
 // between phases), like disasm_kernel.  Scratch in the per-warp global slot.
 __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket, uint8_t* gslot, ErrSink& es,
-                                          uint32_t gid, uint32_t gw) {
+                                          uint32_t gid, uint32_t gw, Mod& m) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   const bool live = ticket < a.n_mod;
@@ -201,7 +201,6 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
   int32_t status = live ? ST_OK : ST_INTERNAL;
   int32_t decode_status = ST_OK;
   uint64_t total = 0;
-  Mod m;
   Shape sh{};
   uint64_t eff[MAX_CAPW] = {0, 0, 0, 0, 0, 0};
   int64_t nbytes = 0;
@@ -385,6 +384,7 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
 #endif
 __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) {
   __shared__ uint32_t s_base[16];
+  __shared__ Mod s_mod[32];   // module descriptor, one per warp (not 32 per-thread local copies)
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) 
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    validate_one(a, base + gwarp_in, gslot, es, gid, gw);
+    validate_one(a, base + gwarp_in, gslot, es, gid, gw, s_mod[warp_in_block]);
   }
 }
 
