@@ -482,10 +482,10 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
 // Phase B: tokenize (asm.py:51-90), lane per line, into the line's token
 // slots (bound from split_lines); strings are unescaped into m.esc.
 
-struct AsmCtx {
-  const Tables& T;
-  const Uni& U;
-  const AsmTables& A;
+struct AsmCtx {   // one copy per CTA in shared memory (not a per-thread local copy)
+  Tables T;
+  Uni U;
+  AsmTables A;
 };
 
 __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
@@ -2288,7 +2288,7 @@ end_i:
 #define SKG_ASM_MAXT 1024
 #define SKG_ASM_MINB 1
 #endif
-__global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs a) {
+__global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(const __grid_constant__ AsmArgs a) {
   __shared__ uint32_t s_base[16];
   __shared__ AsmMod s_amod[32];   // the module descriptor, one per warp (not a per-thread local copy)
   const uint32_t warps = blockDim.x >> 5;
@@ -2297,7 +2297,11 @@ __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs
   const uint32_t gid = warp_in_block / gw, gwarp_in = warp_in_block % gw;
   const uint32_t gwarp = blockIdx.x * warps + warp_in_block;
   uint8_t* slot = a.gscratch + (size_t)gwarp * a.gslot_bytes;
-  const AsmCtx X{a.T, a.U, a.A};
+  __shared__ AsmCtx s_ctx;
+  __shared__ AsmArgs s_args;   // one copy per CTA: field reads are shared loads
+  if (threadIdx.x == 0) { s_ctx.T = a.T; s_ctx.U = a.U; s_ctx.A = a.A; s_args = a; }
+  __syncthreads();
+  const AsmCtx& X = s_ctx;
   while (true) {
     if (gwarp_in == 0 && (threadIdx.x & 31) == 0) s_base[gid] = atomicAdd(a.counters, gw);
     group_sync(gid, gw);
@@ -2305,7 +2309,7 @@ __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(AsmArgs
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
     const uint32_t tk = base + gwarp_in;
-    assemble_module(a, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block]);
+    assemble_module(s_args, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block]);
   }
 }
 

@@ -1341,7 +1341,10 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
 #define SKG_DIS_MAXT 1024
 #define SKG_DIS_MINB 1
 #endif
-__global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(DisasmArgs a) {
+__global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(const __grid_constant__ DisasmArgs a) {
+  __shared__ DisasmArgs s_args;   // one copy per CTA: field reads are shared loads
+  if (threadIdx.x == 0) s_args = a;
+  __syncthreads();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_base[16];
   // the module descriptor, one per warp in shared memory (a per-thread copy would
@@ -1363,7 +1366,7 @@ __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(Disa
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    disasm_one(a, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block]);
+    disasm_one(s_args, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block]);
   }
 }
 

@@ -382,7 +382,10 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
 #ifndef SKG_VAL_MAXT
 #define SKG_VAL_MAXT 1024
 #endif
-__global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) {
+__global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(const __grid_constant__ ValidateArgs a) {
+  __shared__ ValidateArgs s_args;   // one copy per CTA: field reads are shared loads
+  if (threadIdx.x == 0) s_args = a;
+  __syncthreads();
   __shared__ uint32_t s_base[16];
   __shared__ Mod s_mod[32];   // module descriptor, one per warp (not 32 per-thread local copies)
   const uint32_t warps = blockDim.x >> 5;
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(ValidateArgs a) 
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    validate_one(a, base + gwarp_in, gslot, es, gid, gw, s_mod[warp_in_block]);
+    validate_one(s_args, base + gwarp_in, gslot, es, gid, gw, s_mod[warp_in_block]);
   }
 }
 
