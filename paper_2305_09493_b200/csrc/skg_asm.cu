@@ -990,11 +990,10 @@ __device__ __forceinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st,
 // memory) and enc_one is inlined at a single call site: the slot sequence
 // ('*' repeats to the end, '?' skipped when no tokens remain, the
 // SpecConstantOp IdRef tail) is generated by a small state machine.
-__device__ __noinline__ void encode_line(EncCtx& cin) {
-  EncCtx c = cin;
+__device__ inline bool enc_setup(EncCtx& c, const AsmMod& m, uint32_t li);
+
+__device__ __forceinline__ void encode_walk(EncCtx& c) {
   const Tables& T = c.X.T;
-  c.r.nw = 0; c.r.ecode = E_OK; c.r.result_id = 0; c.r.word2 = NONE32; c.r.unres = false;
-  c.r.bad_ref = NONE32;
   c.pos = 0;
   uint32_t st[ESTACK];
   int sp = 0;
@@ -1024,10 +1023,36 @@ __device__ __noinline__ void encode_line(EncCtx& cin) {
       }
     }
     const uint32_t e = st[--sp];
-    if (!enc_one(c, e, st, sp)) { cin.r = c.r; return; }
+    if (!enc_one(c, e, st, sp)) return;
   }
   if (c.pos < c.nitems) enc_fail(c, E_EXTRA, 0, c.nitems - c.pos);
-  cin.r = c.r;
+}
+
+// One line through the encoder, the context built here in registers rather
+// than passed in through (per-lane) local memory.  Pass 1 (M_COUNT) stores the
+// line's results itself; the other modes return them through *ro.
+__device__ __noinline__ void encode_line(const AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t d, uint32_t mode,
+                                         uint32_t* out, uint32_t* rbits, uint32_t rbase, EncOut* ro) {
+  EncCtx c{m, X, li, d, mode, out};
+  c.rbits = rbits;
+  c.rbase = rbase;
+  c.r.nw = 0; c.r.ecode = E_OK; c.r.result_id = 0; c.r.word2 = NONE32; c.r.unres = false;
+  c.r.bad_ref = NONE32;
+  const bool setup = enc_setup(c, m, li);
+  if (setup) encode_walk(c);   // one inlined copy of the walk
+  if (ro) { *ro = c.r; return; }
+  m.lec[li] = c.r.ecode;
+  if (!setup) return;
+  if (c.r.ecode != E_OK) {
+    uint32_t* e = m.lerr + 4 * li;
+    e[0] = c.r.etok; e[1] = c.r.eaux; e[2] = c.r.eaux2; e[3] = c.r.eaux3;
+  }
+  m.lnw[li] = c.r.nw;
+  m.lrid[li] = c.r.result_id;
+  uint32_t f2 = m.lfl[li];
+  if (c.r.unres) f2 |= LF_UNRES;
+  if (X.T.special(d) == SP_VARIABLE && c.r.word2 == X.A.storage_fn) f2 |= LF_VARFN;
+  m.lfl[li] = f2;
 }
 
 // set up an encoder context for line li (d known, not OpLabel); false = pre-encode error
@@ -1456,10 +1481,9 @@ __device__ inline uint32_t result_id_of(const AsmMod& m, const AsmCtx& X, uint32
 
 // lane 0: re-run the encoder of line li assigning ids to unseen names in order
 __device__ __noinline__ bool resolve_line(AsmMod& m, const AsmCtx& X, uint32_t li) {
-  EncCtx c{m, X, li, m.ld[li], M_RESOLVE, nullptr};
-  if (!enc_setup(c, m, li)) return true;
-  encode_line(c);
-  return c.r.ecode != E_INTERNAL;
+  EncOut r;
+  encode_line(m, X, li, m.ld[li], M_RESOLVE, nullptr, nullptr, 0, &r);
+  return r.ecode != E_INTERNAL;
 }
 
 // Phase G (lane 0): the scope state machine of Assembler._emit / builder scopes.
@@ -2103,22 +2127,8 @@ end_e:
       if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
       continue;
     }
-    EncCtx c{m, X, li, d, M_COUNT, m.sw + m.lwo[li] + 1};
-    c.rbits = m.swr;
-    c.rbase = m.lwo[li] + 1;
-    if (!enc_setup(c, m, li)) { m.lec[li] = c.r.ecode; continue; }
-    encode_line(c);
-    m.lec[li] = c.r.ecode;
-    if (c.r.ecode != E_OK) {
-      uint32_t* e = m.lerr + 4 * li;
-      e[0] = c.r.etok; e[1] = c.r.eaux; e[2] = c.r.eaux2; e[3] = c.r.eaux3;
-    }
-    m.lnw[li] = c.r.nw;
-    m.lrid[li] = c.r.result_id;
-    uint32_t f2 = fl;
-    if (c.r.unres) f2 |= LF_UNRES;
-    if (X.T.special(d) == SP_VARIABLE && c.r.word2 == X.A.storage_fn) f2 |= LF_VARFN;
-    m.lfl[li] = f2;
+    const uint32_t w0 = m.lwo[li] + 1;
+    encode_line(m, X, li, d, M_COUNT, m.sw + w0, m.swr, w0, nullptr);
   }
   __syncwarp();
   // first OverflowError (escapes the emit loop's except clause)
@@ -2240,10 +2250,9 @@ end_h:
     if (1 + m.lnw[li] > 0xFFFF) wc_off = min(wc_off, at);
     uint32_t bad_ref = NONE32;
     if (m.lfl[li] & LF_UNRES) {   // ids of names first seen in the state machine: re-encode
-      EncCtx c{m, X, li, d, M_WRITE, fits ? ow + at + 1 : nullptr};   // M_WRITE also checks references
-      enc_setup(c, m, li);
-      encode_line(c);
-      bad_ref = c.r.bad_ref;
+      EncOut r;   // M_WRITE also checks references
+      encode_line(m, X, li, d, M_WRITE, fits ? ow + at + 1 : nullptr, nullptr, 0, &r);
+      bad_ref = r.bad_ref;
     } else {                      // copy pass-1 words; check the referenced ids
       const uint32_t w0 = m.lwo[li] + 1, nw = m.lnw[li];
       for (uint32_t k = 0; k < nw; ++k) {
