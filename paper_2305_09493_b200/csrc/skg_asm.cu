@@ -649,16 +649,12 @@ struct EncCtx {
   bool is_switch;
   uint32_t* rbits;        // pass 1: bit per scratch word, set for referenced ids
   uint32_t rbase;         // bit index of operand word 0
-  const uint32_t* tok;    // register copies of the module arrays the walk reads
-  const uint8_t* txt;
-  const uint8_t* esc;
-  const uint32_t* tid;
 };
 
 __device__ __forceinline__ Tok tok_of(const EncCtx& c, uint32_t t) {
-  const uint32_t off = c.tok[2 * t], lf = c.tok[2 * t + 1];
+  const uint32_t off = c.m.tok[2 * t], lf = c.m.tok[2 * t + 1];
   Tok k;
-  k.p = ((lf & TK_ESC) ? c.esc : c.txt) + off;
+  k.p = ((lf & TK_ESC) ? c.m.esc : c.m.txt) + off;
   k.n = lf & TK_LEN;
   k.str = (lf & TK_STR) != 0;
   k.raw = off - (k.str ? 1 : 0);
@@ -736,7 +732,7 @@ __device__ inline bool ext_by_name(const AsmCtx& X, const uint8_t* p, uint32_t n
 // id of an %name token for coerce (asm.py:106-120); false on error
 __device__ inline bool enc_id(EncCtx& c, uint32_t t, const Tok& k, uint32_t& id) {
   if (c.mode != M_RESOLVE) {   // resolved once per token after the result names are bound
-    const uint32_t cached = c.tid[t];
+    const uint32_t cached = c.m.tid[t];
     if (cached) { id = cached; return true; }
   }
   if (!(k.n >= 2 && k.p[0] == '%')) return enc_fail(c, E_EXPECT_ID, t);
@@ -1058,7 +1054,6 @@ __device__ __noinline__ void encode_line(const AsmMod& m, const AsmCtx& X, uint3
 // set up an encoder context for line li (d known, not OpLabel); false = pre-encode error
 __device__ inline bool enc_setup(EncCtx& c, const AsmMod& m, uint32_t li) {
   const Tables& T = c.X.T;
-  c.tok = m.tok; c.txt = m.txt; c.esc = m.esc; c.tid = m.tid;
   const uint32_t fl = m.lfl[li];
   const bool has_res = fl & LF_RESULT;
   c.rtok = has_res ? m.lt0[li] : NONE32;

@@ -96,4 +96,4 @@ for k, d in enumerate(data):
     agg_s[key] += num(d, "Warp Stall Sampling (All Samples)")
 ti, ts = sum(agg_i.values()) or 1, sum(agg_s.values()) or 1
 for key in sorted(agg_s, key=lambda k: -agg_s[k])[:topn]:
-    print(f"{100 * agg_s[key] / ts:5.1f}% stall {100 * agg_i[key] / ti:5.1f}% inst  {key}")
+    print(f"{100 * agg_s[key] / ts:5.1f}% stall {100 * agg_i[key] / ti:5.1f}% inst {agg_i[key] / 1e6:8.1f}M  {key}")
