@@ -533,11 +533,16 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       ++nt;
       continue;
     }
-    while (i < e0) {
-      const uint32_t d = t[i];
-      if (d < 64 && ((0x0800000500002600ull >> d) & 1)) break;   // \t \n \r ' ' '"' ';'
-      ++i;
+    // token end: the first \t \n \r ' ' '"' ';' -- four independent loads per step
+    auto delim = [](uint32_t d) -> bool { return d < 64 && ((0x0800000500002600ull >> d) & 1); };
+    while (i + 4 <= e0) {
+      const uint32_t d0 = __ldg(t + i), d1 = __ldg(t + i + 1), d2 = __ldg(t + i + 2), d3 = __ldg(t + i + 3);
+      const uint32_t k = delim(d0) ? 0 : delim(d1) ? 1 : delim(d2) ? 2 : delim(d3) ? 3 : 4;
+      i += k;
+      if (k < 4) goto token_end;
     }
+    while (i < e0 && !delim(__ldg(t + i))) ++i;
+  token_end:
     if (nt < cap) {   // cap = candidate bound of this line (split_lines)
       m.tok[2 * (tb + nt)] = start;
       m.tok[2 * (tb + nt) + 1] = i - start;
