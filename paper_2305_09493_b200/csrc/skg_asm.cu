@@ -442,7 +442,17 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
     const uint32_t cm = ~eq_bytes(word, ' ') & (lt21_bytes(prev) | (prev & 0x80808080u)) & valid;
     const uint32_t qm = eq_bytes(word, '"') & valid;
     const uint32_t nc = __popc(cm) + __popc(qm);
-    if (w < nw && word_maybe_sep(word)) {
+    // common case: the word's only separator candidates are bare '\n' bytes
+    const uint32_t nl = eq_bytes(word, '\n') & valid;
+    const uint32_t rest = (~(((word & 0x7F7F7F7Fu) + 0x60606060u) | word) & 0x80808080u & ~nl) |
+                          eq_bytes(word, 0xC2) | eq_bytes(word, 0xE2) | (eq_bytes(prev, '\r') & nl);
+    if (!(rest & valid)) {
+      for (uint32_t bits = nl; bits; bits &= bits - 1) {
+        const uint32_t b = (__ffs(bits) - 1) >> 3;
+        const uint32_t below = b ? (0xFFFFFFFFu >> (32 - 8 * b)) : 0u;
+        pos[cnt] = 4 * w + b; len[cnt] = 1; cb[cnt] = __popc(cm & below) + __popc(qm & below); ++cnt;
+      }
+    } else if (w < nw && word_maybe_sep(word)) {
       for (uint32_t b = 0; b < 4; ++b) {
         const uint32_t i = 4 * w + b;
         if (i >= T) break;
