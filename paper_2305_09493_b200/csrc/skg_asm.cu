@@ -463,8 +463,8 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
         }
       }
     }
-    const uint32_t incl = wincl(cnt);
-    const uint32_t cincl = wincl(nc);
+    const uint32_t both = wincl((cnt << 16) | nc);   // one scan for both counts (each < 2^16 per step)
+    const uint32_t incl = both >> 16, cincl = both & 0xFFFF;
     const uint32_t c0 = ccarry + cincl - nc;
     uint32_t k = nsep + incl - cnt;
     for (uint32_t q = 0; q < cnt; ++q, ++k) {
@@ -1628,8 +1628,7 @@ __device__ __noinline__ bool state_fast(AsmMod& m, const AsmCtx& X) {
   uint32_t last_struct_kind = K_SKIP;         // kind of the previous structural line
   uint32_t last_struct_term = 0;
   uint32_t last_func_line = NONE32, last_label_line = NONE32;
-  uint32_t bucket_run[11];
-  for (int b = 0; b < 11; ++b) bucket_run[b] = 0;
+  uint32_t brun = 0;   // lane b < 11: words placed so far in bucket b
   uint32_t P = 0;                             // words of function-group lines so far
   bool ok = true;
   for (uint32_t base = 0; base < m.L && ok; base += 32) {
@@ -1711,12 +1710,18 @@ __device__ __noinline__ bool state_fast(AsmMod& m, const AsmCtx& X) {
     if (__any_sync(FULLM, bad)) { ok = false; break; }
     // placement: buckets
     uint32_t off = 0;
-#pragma unroll
-    for (int b = 0; b < 11; ++b) {
-      const uint32_t v = (kind == K_MOD && route == (uint32_t)b) ? words : 0;
+    // one scan per bucket present in this group of lines (usually one or two)
+    const bool placed = kind == K_MOD && route < 11;
+    for (uint32_t pend = __ballot_sync(FULLM, placed && words); pend;) {
+      const uint32_t r = __shfl_sync(FULLM, route, __ffs(pend) - 1);
+      const bool mine = placed && route == r;
+      const uint32_t v = mine ? words : 0;
       const uint32_t incl = wincl(v);
-      if (v) off = bucket_run[b] + incl - v;
-      bucket_run[b] += __shfl_sync(FULLM, incl, 31);
+      const uint32_t base = __shfl_sync(FULLM, brun, r);
+      const uint32_t tot = __shfl_sync(FULLM, incl, 31);
+      if (mine) off = base + incl - v;
+      if (lane == r) brun += tot;
+      pend &= ~__ballot_sync(FULLM, mine);
     }
     // placement: function lines, offset from the function's first line
     const bool fline = kind == K_FUNC || kind == K_PARAM || kind == K_LABEL || kind == K_BLOCK || kind == K_BLOCKVAR;
@@ -1746,8 +1751,8 @@ __device__ __noinline__ bool state_fast(AsmMod& m, const AsmCtx& X) {
   }
   if (ok && nF != nE) ok = false;                 // a function without OpFunctionEnd
   if (!ok) return false;
+  if (lane < 11) m.misc[MS_BUCKET0 + lane] = brun;
   if (lane == 0) {
-    for (int b = 0; b < 11; ++b) m.misc[MS_BUCKET0 + b] = bucket_run[b];
     m.misc[MS_NFN] = nF;
     m.misc[MS_NBLK] = 0;                          // every block was checked terminated above
   }
