@@ -498,6 +498,8 @@ struct AsmCtx {   // one copy per CTA in shared memory (not a per-thread local c
   AsmTables A;
 };
 
+__device__ __forceinline__ bool str_stop(uint32_t d) { return d == '"' || d == '\\'; }
+
 __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t li, uint32_t tb,
                                            uint32_t cap, uint32_t& npct) {
   const uint8_t* t = m.txt;
@@ -516,6 +518,13 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
     const uint32_t start = i;
     if (c == '"') {
       ++i;
+      // up to the first '"' or '\\' four bytes per step (no escape so far: w == i)
+      while (i + 4 <= e0) {
+        const uint32_t d0 = __ldg(t + i), d1 = __ldg(t + i + 1), d2 = __ldg(t + i + 2), d3 = __ldg(t + i + 3);
+        const uint32_t k = str_stop(d0) ? 0 : str_stop(d1) ? 1 : str_stop(d2) ? 2 : str_stop(d3) ? 3 : 4;
+        i += k;
+        if (k < 4) break;
+      }
       uint32_t w = i;
       bool esc = false;
       while (i < e0 && t[i] != '"') {
@@ -544,7 +553,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
       continue;
     }
     // token end: the first \t \n \r ' ' '"' ';' -- four independent loads per step
-    auto delim = [](uint32_t d) -> bool { return d < 64 && ((0x0800000500002600ull >> d) & 1); };
+    auto delim = [](uint32_t d) -> bool {   // bit d of 0x0800000500002600 (d < 64), in 32-bit halves
+      const uint32_t h = d < 32 ? 0x00002600u : (d < 64 ? 0x08000005u : 0u);
+      return __funnelshift_r(h, h, d) & 1;
+    };
     while (i + 4 <= e0) {
       const uint32_t d0 = __ldg(t + i), d1 = __ldg(t + i + 1), d2 = __ldg(t + i + 2), d3 = __ldg(t + i + 3);
       const uint32_t k = delim(d0) ? 0 : delim(d1) ? 1 : delim(d2) ? 2 : delim(d3) ? 3 : 4;
