@@ -512,8 +512,8 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
   while (i + 4 <= e0 && (reinterpret_cast<uintptr_t>(t + i) & 3) == 0 &&
          *reinterpret_cast<const uint32_t*>(t + i) == 0x20202020u) i += 4;
   while (i < e0) {
-    const uint8_t c = t[i];
-    if (c == ' ' || c == '\t' || c == '\r' || c == '\n') { ++i; continue; }
+    const uint32_t c = __ldg(t + i);
+    if (c <= ' ' && ((c == ' ' ? 1u : 0x2600u >> c) & 1)) { ++i; continue; }   // ' ' \t \r \n
     if (c == ';') break;
     const uint32_t start = i;
     if (c == '"') {

@@ -169,6 +169,13 @@ EDGE = [
     "%f = OpFunction %v None %t\n%l = OpLabel\n%x = OpVariable %p Function\nOpReturn\nOpFunctionEnd\n",
     "OpEntryPoint Kernel %f \"main\" %a %b\nOpExecutionMode %f LocalSize 1 2 3\nOpSource OpenCL_C 120\n",
     "OpLine %1 2 3\nOpNoLine\n%5 = OpUndef %1\nOpModuleProcessed \"x\"\nOpString \"s\"\n",
+    # four-bytes-per-step scans: quotes / escapes / delimiters at every offset mod 4
+    "".join(f"OpSourceExtension \"{'abcdefgh'[:k]}\\\"{'xyz'[:k % 4]}\\\\q\"\n" for k in range(9)),
+    "".join(f"%{'s' * (k + 1)} = OpString \"{'s' * k}\"\nOpName %{'s' * (k + 1)} \"{'t' * (k + 2)}\";{'c' * k}\n"
+            for k in range(9)),
+    "".join(f"%{'a' * k}\t=\tOpTypeInt 32 0\n%{'b' * (k + 1)}\t=\tOpConstant\t%{'a' * k} {7 * k}\r\n"
+            for k in range(1, 9)),
+    "OpName %x \"abcdefghij\nOpName %y \"abcdefg\\\nOpName %z \"abc\"def\"\n",
 ]
 
 
