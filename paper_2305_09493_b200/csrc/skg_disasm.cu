@@ -731,19 +731,19 @@ __device__ __noinline__ void collect_ids(Mod& m) {
 
 // ---------------------------------------------------------------------------
 // Per-word length (arithmetic only) and emission (register-resident pointer).
-__device__ __forceinline__ uint8_t* emit_u32(uint8_t* p, uint32_t v) {
+__device__ __forceinline__ uint8_t* emit_u32(uint8_t* __restrict__ p, uint32_t v) {
   uint8_t* e = p + dlen32(v);
   uint8_t* q = e;
 #pragma unroll 1
   do { *--q = (uint8_t)('0' + v % 10); v /= 10; } while (v);
   return e;
 }
-__device__ __forceinline__ uint8_t* emit_cstr(uint8_t* p, const char* z) {
+__device__ __forceinline__ uint8_t* emit_cstr(uint8_t* __restrict__ p, const char* z) {
 #pragma unroll 1
   while (*z) *p++ = (uint8_t)*z++;
   return p;
 }
-__device__ __forceinline__ uint8_t* emit_tab(uint8_t* p, const Tables& T, uint32_t off, uint32_t len) {
+__device__ __forceinline__ uint8_t* emit_tab(uint8_t* __restrict__ p, const Tables& T, uint32_t off, uint32_t len) {
   const uint8_t* src = T.str + off;
   uint32_t q = 0;
 #pragma unroll 1
@@ -756,7 +756,7 @@ __device__ __forceinline__ uint8_t* emit_tab(uint8_t* p, const Tables& T, uint32
   return p + len;
 }
 
-__device__ __noinline__ uint8_t* emit_ref(uint8_t* p, const Mod& m, uint32_t id) {
+__device__ __noinline__ uint8_t* emit_ref(uint8_t* __restrict__ p, const Mod& m, uint32_t id) {
   *p++ = '%';
   // direct mode: a slot that is not present has hfl == 0 (init_tables)
   const uint32_t slot = m.direct ? (id < m.S ? id : NONE32) : ht_find(m, id);
@@ -883,7 +883,7 @@ __device__ __noinline__ uint32_t word_len(const Mod& m, const Tables& T, uint32_
 // [special] + ['\n'], so the stages run in that order with the expensive ones
 // (reference, table-name copy, decimal digits) reached by all lanes that need
 // them at the same program point: the warp runs each once, not once per code.
-__device__ __noinline__ void word_emit(uint8_t* p, const Mod& m, const Tables& T, uint32_t w, uint32_t x,
+__device__ __noinline__ void word_emit(uint8_t* __restrict__ p, const Mod& m, const Tables& T, uint32_t w, uint32_t x,
                                        uint32_t width, bool hl, bool spaces) {
   const uint32_t v = m.w[w];
   const uint32_t code = wk_code(x);
@@ -1113,12 +1113,14 @@ __device__ __noinline__ void text_write_range(const Mod& m, const Tables& T, uin
     __syncwarp();
   }
   uint32_t w0 = w_begin;
+  const uint32_t* __restrict__ wk = m.wk;   // held in registers across the stage stores
+  const uint16_t* __restrict__ wl = m.wl;
   while (w0 < w_end) {
     const uint32_t w = w0 + lane;
     uint32_t x = 0, len = 0;
     if (w < w_end) {
-      x = m.wk[w];
-      len = m.wl[w];
+      x = wk[w];
+      len = wl[w];
       if (len == 0xFFFF) len = word_len(m, T, w, x, width, hl);
     }
     const uint32_t incl = warp_incl_sum(len);
