@@ -249,7 +249,7 @@ def run_ours(args, rank, world, local_rank):
                 assert got == odis.disassemble(m), f"module {i} differs from oracle"
 
     # e2e through the host-buffer public API
-    sess = RoundTripSession()
+    sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "8")))   # pipeline depth (experiments)
     sess.stage(batch.data, batch.offsets, batch.lengths)
     sess.run_staged(max_text)
     e2e_steps = max(1, min(args.steps, 3))
