@@ -325,6 +325,24 @@ def test_disasm_large_module_grid_wide(sk, monkeypatch):
                 assert g == want
 
 
+def test_disasm_large_module_many_name_families(sk, monkeypatch):
+    """grid-wide name de-duplication with many parent / child / grandchild name
+    groups (x, x_0, x_1, x_0_0 ...) over several 1024-ident chunks, so the ordered
+    pass's group-state cache sees collisions and evictions: text == oracle."""
+    from oracle import disasm as odis
+    from paper_2305_09493_b200 import _native
+    import synth.huge as huge
+    monkeypatch.setattr(_native, "LARGE_MODULE_WORDS", 1 << 12)
+    vocab = [f"p{i}" for i in range(700)] + [f"p{i}_0" for i in range(0, 700, 2)]
+    vocab += [f"p{i}_1" for i in range(0, 700, 3)] + [f"p{i}_0_0" for i in range(0, 100, 4)]
+    vocab += ["x", "x_0", "x_1", "x_0_0", "x_2"]
+    monkeypatch.setattr(huge, "VOCAB", tuple(vocab))
+    for seed in (3, 4):
+        m = huge.build_huge(8, chain=200, seed=seed)
+        got = sk.disassemble_batch([m])[0]
+        assert got == odis.disassemble(m)
+
+
 def test_large_paths_edge_cases(sk, monkeypatch):
     """The whole-GPU single-module paths on degenerate inputs: header only, a
     truncated stream, a foreign magic, big-endian, and an empty-string OpName."""
