@@ -119,33 +119,75 @@ __global__ void tile_spec(BigDecode b) {
   }
 }
 
+// One warp.  The walk is sequential over tiles, so its cost is latency: the
+// lanes first load 32 tiles' speculative results (exits, errors, and the first
+// 16 bytes of their chain maps, where an entry nearly always lands) in one
+// round, then every lane runs the same walk, taking tile j's data from lane j by
+// shuffles; only an entry past those 16 bytes, or an unmarked one, reads memory.
 __global__ void tile_link(BigDecode b) {
-  if (blockIdx.x != 0 || threadIdx.x != 0 || b.result[0] != ST_OK) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  if (b.result[0] != ST_OK) return;   // (the same value for every lane)
+  const uint32_t lane = threadIdx.x;
   uint32_t e = 5, status = ST_OK, errpos = 0;
-  for (uint32_t t = 0; t < b.ntiles; ++t) {
-    const uint32_t lo = t * BD_TILE, hi = min(lo + BD_TILE, b.W);
-    if (status != ST_OK || e >= hi) { b.entry[t] = BD_NONE; continue; }
-    b.entry[t] = e;
-    const uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;
-    uint32_t p = e, c = 0;
-    while (p < hi) {
-      if ((c = cm[p - lo]) != 0) break;
-      const uint32_t wc = b.words[p] >> 16;
-      if (wc == 0) { status = ST_CORRUPT; errpos = p; break; }
-      if ((uint64_t)p + wc > b.W) { status = ST_TRUNCATED; errpos = p; break; }
-      p += wc;
+  for (uint32_t t0 = 0; t0 < b.ntiles; t0 += 32) {
+    const uint32_t tl = t0 + lane;
+    uint32_t ex[BD_K], er[BD_K], ec[BD_K];
+    uint4 c16 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (uint32_t k = 0; k < BD_K; ++k) { ex[k] = BD_NONE; er[k] = BD_NONE; ec[k] = 0; }
+    if (tl < b.ntiles) {
+#pragma unroll
+      for (uint32_t k = 0; k < BD_K; ++k) {
+        ex[k] = b.spec_exit[(uint64_t)tl * BD_K + k];
+        er[k] = b.spec_err[(uint64_t)tl * BD_K + k];
+        ec[k] = b.spec_errc[(uint64_t)tl * BD_K + k];
+      }
+      c16 = *reinterpret_cast<const uint4*>(b.chain + (uint64_t)tl * BD_TILE);
     }
-    if (status != ST_OK) continue;
-    if (c) {   // on speculative chain c - 1 from here on
-      const uint64_t q = (uint64_t)t * BD_K + (c - 1);
-      if (b.spec_err[q] != BD_NONE) { status = b.spec_errc[q]; errpos = b.spec_err[q]; continue; }
-      e = b.spec_exit[q];
-    } else {
-      e = p;
+    const uint32_t nt = min(32u, b.ntiles - t0);
+#pragma unroll 1
+    for (uint32_t j = 0; j < nt; ++j) {
+      const uint32_t t = t0 + j;
+      const uint32_t lo = t * BD_TILE, hi = min(lo + BD_TILE, b.W);
+      const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, c16.x, j), w1 = __shfl_sync(0xFFFFFFFFu, c16.y, j);
+      const uint32_t w2 = __shfl_sync(0xFFFFFFFFu, c16.z, j), w3 = __shfl_sync(0xFFFFFFFFu, c16.w, j);
+      if (status != ST_OK || e >= hi) { if (lane == 0) b.entry[t] = BD_NONE; continue; }
+      if (lane == 0) b.entry[t] = e;
+      const uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;
+      uint32_t p = e, c = 0;
+#pragma unroll 1
+      while (p < hi) {
+        const uint32_t o = p - lo;
+        if (o < 16) {
+          const uint32_t w = o < 8 ? (o < 4 ? w0 : w1) : (o < 12 ? w2 : w3);
+          c = (w >> (8 * (o & 3))) & 0xFF;
+        } else {
+          c = cm[o];
+        }
+        if (c) break;
+        const uint32_t wc = b.words[p] >> 16;
+        if (wc == 0) { status = ST_CORRUPT; errpos = p; break; }
+        if ((uint64_t)p + wc > b.W) { status = ST_TRUNCATED; errpos = p; break; }
+        p += wc;
+      }
+      // chain c - 1's exit / first error, from lane j (selected without a dynamic register index)
+      const uint32_t kk = c ? c - 1 : 0;
+      uint32_t sx = ex[0], sr = er[0], sc = ec[0];
+#pragma unroll
+      for (uint32_t k = 1; k < BD_K; ++k) if (kk == k) { sx = ex[k]; sr = er[k]; sc = ec[k]; }
+      sx = __shfl_sync(0xFFFFFFFFu, sx, j);
+      sr = __shfl_sync(0xFFFFFFFFu, sr, j);
+      sc = __shfl_sync(0xFFFFFFFFu, sc, j);
+      if (status != ST_OK) continue;
+      if (c) {   // on speculative chain c - 1 from here on
+        if (sr != BD_NONE) { status = sc; errpos = sr; continue; }
+        e = sx;
+      } else {
+        e = p;
+      }
     }
   }
-  b.result[0] = status;
-  b.result[1] = errpos;
+  if (lane == 0) { b.result[0] = status; b.result[1] = errpos; }
 }
 
 __global__ void tile_count(BigDecode b) {

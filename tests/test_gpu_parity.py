@@ -250,6 +250,45 @@ def test_decode_large_module_tiled(sk):
         assert (type(e1.value).__name__, str(e1.value)) == (type(e2.value).__name__, str(e2.value))
 
 
+def test_decode_large_random_word_counts(sk):
+    """the tiled boundary pass under corrupted word counts anywhere in the stream (the
+    true chain re-enters tiles at arbitrary offsets, merges late or hits an error):
+    instructions or the exact first error, as the oracle."""
+    import random
+    import struct
+    from oracle import core
+    from synth.huge import build_huge
+    m = build_huge(120, chain=150, seed=9, string_kib=(1, 24))
+    words = list(struct.unpack(f"<{len(m) // 4}I", m))
+    assert len(words) >= 1 << 16
+    starts, p = [], 5
+    while p < len(words):
+        starts.append(p)
+        p += words[p] >> 16
+    rng = random.Random(5)
+    for _ in range(10):
+        w = list(words)
+        for _ in range(rng.choice((1, 3))):
+            at = rng.choice(starts)
+            w[at] = (rng.choice((0, 1, 2, 3, 7, 4096, 5000)) << 16) | (w[at] & 0xFFFF)
+        data = struct.pack(f"<{len(w)}I", *w)
+        try:
+            want = core.decode_module(data)
+        except Exception as exc:   # noqa: BLE001
+            want = exc
+        try:
+            got = sk.decode_module(data)
+        except Exception as exc:   # noqa: BLE001
+            got = exc
+        if isinstance(want, Exception):
+            assert (type(got).__name__, str(got)) == (type(want).__name__, str(want))
+        else:
+            from dataclasses import astuple
+            h, insts = got
+            assert astuple(h) == tuple(want[0])
+            assert [(i.opcode, tuple(i.operands)) for i in insts] == [(op, tuple(o)) for op, o in want[1]]
+
+
 def test_validate_large_module_grid_wide(sk, monkeypatch):
     """validate on one large module runs grid-wide (skg_validate_large): same diagnostics
     as the batch path / oracle, including decode errors and instruction diagnostics."""
