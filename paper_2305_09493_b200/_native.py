@@ -155,6 +155,40 @@ class _Workspace:
 _ws = _Workspace()
 
 
+class _PinnedStage:
+    """Pinned host staging for large device -> host results (a pageable .cpu() copy of a
+    ~1 GB text runs at a fraction of the link rate); grown on demand, reused."""
+
+    def __init__(self):
+        self.buf = None
+
+    def to_bytes(self, dev_u8) -> bytes:
+        torch = _torch()
+        n = int(dev_u8.numel())
+        if n < (16 << 20):   # small results: the plain copy is cheaper than pinning
+            return dev_u8.cpu().numpy().tobytes()
+        if self.buf is None or self.buf.numel() < n:
+            self.buf = torch.empty(n + (n >> 3), dtype=torch.uint8).pin_memory()
+        self.buf[:n].copy_(dev_u8, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.buf[:n].numpy().tobytes()
+
+    def to_u32(self, dev_i32, count: int):
+        """the first `count` elements of a device int32 tensor as a host uint32 array"""
+        torch = _torch()
+        n = 4 * count
+        if n < (16 << 20):
+            return dev_i32[:count].cpu().numpy().view(np.uint32)
+        if self.buf is None or self.buf.numel() < n:
+            self.buf = torch.empty(n + (n >> 3), dtype=torch.uint8).pin_memory()
+        self.buf[:n].copy_(dev_i32[:count].view(torch.uint8), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.buf[:n].numpy().view(np.uint32).copy()
+
+
+_pinned = _PinnedStage()
+
+
 def _stream():
     torch = _torch()
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -330,7 +364,7 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args):
             continue
         break
     _check(rc if rc < 0 else 0, fn.__name__)
-    return rc, (text[: int(need.value)].cpu().numpy().tobytes() if rc == 0 else None), errs
+    return rc, (_pinned.to_bytes(text[: int(need.value)]) if rc == 0 else None), errs
 
 
 def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext):
@@ -456,7 +490,7 @@ def _run_decode_large(d, n: int):
         raise decode_errors(errs.cpu().numpy())[0]
     k = int(cnt.item())
     return tuple(int(x) for x in header.cpu().numpy().view(np.uint32)), \
-        words.cpu().numpy().view(np.uint32)[:W], inst_off.cpu().numpy().view(np.uint32)[:k]
+        _pinned.to_u32(words, W), _pinned.to_u32(inst_off, k)
 
 
 __all__ = ["lib", "DeviceBatch", "run_disasm", "run_validate", "run_decode", "fetch_texts",
