@@ -165,7 +165,8 @@ class _PinnedStage:
     def to_bytes(self, dev_u8) -> bytes:
         torch = _torch()
         n = int(dev_u8.numel())
-        if n < (16 << 20):   # small results: the plain copy is cheaper than pinning
+        if n < (16 << 20) or dev_u8.dtype != torch.uint8 or not dev_u8.is_contiguous():
+            # small results: the plain copy is cheaper than pinning
             return dev_u8.cpu().numpy().tobytes()
         if self.buf is None or self.buf.numel() < n:
             self.buf = torch.empty(n + (n >> 3), dtype=torch.uint8).pin_memory()
@@ -408,7 +409,7 @@ def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec):
         return None
     _check(rc if rc < 0 else 0, "validate_large")
     if rc == 0:
-        return text[: int(need.value)].cpu().numpy().tobytes()
+        return _pinned.to_bytes(text[: int(need.value)])
     exc = decode_errors(errs.cpu().numpy())[0]
     if rc == 1:
         return exc
@@ -420,7 +421,7 @@ def fetch_texts(res: TextResult, n: int):
     """Host copies: list of (text bytes | exception) per module."""
     span = res.span.cpu().numpy()
     status = res.status.cpu().numpy()
-    text = res.text.cpu().numpy().tobytes()
+    text = _pinned.to_bytes(res.text)
     errs = decode_errors(res.errors.cpu().numpy()) if res.errors.numel() else {}
     out = []
     for m in range(n):
@@ -684,7 +685,7 @@ def run_asm(texts, spec=None, ext=None, default_version=(1, 2)):
     plan.fit()
     status = plan.status[:n].cpu().numpy()
     span = plan.span[: 2 * n].cpu().numpy()
-    out = plan.out.cpu().numpy().tobytes()
+    out = _pinned.to_bytes(plan.out)
     res = []
     retry = []
     for m in range(n):
