@@ -190,6 +190,11 @@ class _PinnedStage:
 _pinned = _PinnedStage()
 
 
+def release_host_staging():
+    """Free the pinned host staging buffer (it grows to the largest result fetched)."""
+    _pinned.buf = None
+
+
 def _stream():
     torch = _torch()
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
