@@ -79,8 +79,15 @@ def _torch():
 
 
 def _check(rc, what):
+    if rc == -4:
+        raise RuntimeError(f"libskgpu {what}: the output exceeds 4 GiB (32-bit text offsets)")
     if rc != 0:
         raise RuntimeError(f"libskgpu {what} failed with code {rc}")
+
+
+def _device():
+    """index of the current CUDA device: table handles and workspaces are per device"""
+    return _torch().cuda.current_device()
 
 
 # -- grammar tables --------------------------------------------------------------
@@ -92,7 +99,7 @@ def tables_handle(spec, ext):
     from . import grammar, tables
     spec = spec if spec is not None else grammar.load_pinned()
     ext = ext if ext is not None else grammar.load_pinned_extended()
-    key = (id(spec), id(ext))
+    key = (id(spec), id(ext), _device())
     hit = _tables.get(key)
     if hit is not None and hit[1] is spec and hit[2] is ext:
         return hit[0]
@@ -142,14 +149,18 @@ class DeviceBatch:
 
 
 class _Workspace:
+    """One grow-only device scratch buffer per CUDA device."""
+
     def __init__(self):
-        self.buf = None
+        self.bufs = {}
 
     def get(self, nbytes):
         torch = _torch()
-        if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
-        return self.buf
+        dev = _device()
+        buf = self.bufs.get(dev)
+        if buf is None or buf.numel() < nbytes:
+            buf = self.bufs[dev] = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+        return buf
 
 
 _ws = _Workspace()
@@ -304,7 +315,7 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
         return fetch_texts(run(batch), n)
     lens = batch.len.cpu().numpy()
     words = lens // 4
-    if True:   # single large modules: the whole GPU on one module
+    if batch.max_words >= LARGE_MODULE_WORDS:   # single large modules: the whole GPU on one module
         out = [None] * n
         rest = []
         for i in range(n):
@@ -343,23 +354,27 @@ LARGE_MODULE_WORDS = 1 << 20   # validate: modules this size and up run grid-wid
 _DECODE_CODES = {ST_NOTSPIRV: "NotSpirv", ST_TRUNCATED: "TruncatedStream", ST_CORRUPT: "CorruptStream"}
 
 
-def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args):
+def _header_bound(head: bytes) -> int:
+    """the header bound as skg_*_large read it: byte-swapped only when the magic is"""
+    if len(head) < 20:
+        return 0
+    w = np.frombuffer(head[:20], dtype="<u4")
+    return int(np.frombuffer(head[:20], dtype=">u4")[3]) if w[0] == 0x03022307 else int(w[3])
+
+
+def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None):
     """Shared driver of skg_validate_large / skg_disasm_large -> (rc, text bytes, errs)."""
     torch = _torch()
     L = lib()
     o = int(batch.off[i].item())
     data = batch.data.data_ptr() + o
     W = nbytes // 4
-    head = batch.data[o:o + 20].cpu().numpy().tobytes()
-    bound = 0
-    if len(head) == 20:
-        w = np.frombuffer(head, dtype="<u4")
-        bound = int(w[3]) if w[0] == 0x07230203 else int(np.frombuffer(head, dtype=">u4")[3])
+    bound = _header_bound(batch.data[o:o + 20].cpu().numpy().tobytes())
     ws_bytes = int(L.skg_large_workspace_bytes(W, min(bound, 2 * W + 64)))
     ws = _ws.get(ws_bytes)
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     errs = torch.zeros(256, dtype=torch.uint8, device="cuda")
-    cap = max(1 << 20, 4 * nbytes)
+    cap = cap if cap is not None else max(1 << 20, 4 * nbytes)
     for _ in range(3):
         text = torch.empty(cap, dtype=torch.uint8, device="cuda")
         need = ctypes.c_uint64(0)
@@ -369,7 +384,7 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args):
             cap = int(need.value) + 16
             continue
         break
-    _check(rc if rc < 0 else 0, fn.__name__)
+    _check(rc if rc < 0 else 0, getattr(fn, "__name__", "large call"))
     return rc, (_pinned.to_bytes(text[: int(need.value)]) if rc == 0 else None), errs
 
 
@@ -377,7 +392,10 @@ def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext)
     """skg_disasm_large on module i -> text bytes | exception | None (= use the batch path)."""
     L = lib()
     th = tables_handle(spec, ext)
-    rc, text, errs = _large_call(lambda *a: L.skg_disasm_large(th, a[0], a[1], *a[2:]), batch, i, nbytes, opts)
+
+    def disasm_large(*a):
+        return L.skg_disasm_large(th, a[0], a[1], *a[2:])
+    rc, text, errs = _large_call(disasm_large, batch, i, nbytes, opts)
     if rc == 2:
         return None
     if rc == 0:
@@ -387,34 +405,16 @@ def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext)
 
 def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec):
     """skg_validate_large on module i of a device batch -> text bytes | exception | None (= not handled)."""
-    torch = _torch()
     L = lib()
-    data = batch.data.data_ptr() + int(batch.off[i].item())
-    W = nbytes // 4
-    head = batch.data[int(batch.off[i].item()):int(batch.off[i].item()) + 20].cpu().numpy().tobytes()
-    bound = 0
-    if len(head) == 20:
-        w = np.frombuffer(head, dtype="<u4")
-        bound = int(w[3]) if w[0] == 0x07230203 else int(np.frombuffer(head, dtype=">u4")[3])
-    ws_bytes = int(L.skg_large_workspace_bytes(W, min(bound, 2 * W + 64)))
-    ws = _ws.get(ws_bytes)
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    errs = torch.zeros(256, dtype=torch.uint8, device="cuda")
-    cap = 1 << 20
-    for _ in range(3):
-        text = torch.empty(cap, dtype=torch.uint8, device="cuda")
-        need = ctypes.c_uint64(0)
-        rc = L.skg_validate_large(tables_handle(spec, None), data, nbytes, text.data_ptr(), cap, ctypes.byref(need),
-                                  status.data_ptr(), errs.data_ptr(), ws.data_ptr(), ws_bytes, _stream())
-        if rc == 3:
-            cap = int(need.value) + 16
-            continue
-        break
+    th = tables_handle(spec, None)
+
+    def validate_large(*a):
+        return L.skg_validate_large(th, *a)
+    rc, text, errs = _large_call(validate_large, batch, i, nbytes, cap=1 << 20)
     if rc == 2:
         return None
-    _check(rc if rc < 0 else 0, "validate_large")
     if rc == 0:
-        return _pinned.to_bytes(text[: int(need.value)])
+        return text
     exc = decode_errors(errs.cpu().numpy())[0]
     if rc == 1:
         return exc

@@ -116,6 +116,10 @@ class RoundTripSession:
         import torch
         if self.chunks is None:
             raise RuntimeError("stage() first")
+        if self.n == 0 or not self.chunks:
+            z8, z32 = np.zeros(0, np.uint8), np.zeros(0, np.int32)
+            zs = np.zeros((0, 2), np.int64)
+            return z8, zs, z32, z8.copy(), zs.copy(), z32.copy()
         comp = torch.cuda.current_stream()
         cs = _native.ctypes.c_void_p(comp.cuda_stream)
         evs = []

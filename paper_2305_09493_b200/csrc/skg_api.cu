@@ -31,16 +31,28 @@ struct skg_tables {
 namespace {
 
 
-int g_sms = 0;
+int g_sms[64] = {};
 
 int sm_count() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = g_sms[dev & 63];
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  return g_sms;
+  return n;
+}
+
+// true the first time it is called for the current device (function attributes are
+// per device)
+bool first_on_device(uint64_t& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done & bit) return false;
+  done |= bit;
+  return true;
 }
 
 uint64_t gslot_bytes(uint32_t max_words) {
@@ -238,16 +250,14 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   a.group_warps = group_warps((int)g.warps, env_int("SKG_DIS_GROUP", (int)g.warps));
   const size_t smem_max = (size_t)(kDisSlab + kDisStage) * kDisWarps;
   const size_t smem = (size_t)(kDisSlab + kDisStage) * g.warps;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (first_on_device(attr)) {
     cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-    attr = true;
   }
-  static bool carve = false;
-  if (!carve) {   // smallest shared-memory carveout that fits: the rest is L1 for the scratch
+  static uint64_t carve = 0;
+  if (first_on_device(carve)) {   // smallest shared-memory carveout that fits: the rest is L1 for the scratch
     const int pct = env_int("SKG_CARVEOUT", -2);
     if (pct != -2) cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    carve = true;
   }
   skg::disasm_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
   return check(cudaGetLastError());
@@ -278,11 +288,10 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   const Geom g = val_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_VAL_GROUP", (int)g.warps));
-  static bool carve = false;
-  if (!carve) {
+  static uint64_t carve = 0;
+  if (first_on_device(carve)) {
     const int pct = env_int("SKG_CARVEOUT", -2);
     if (pct != -2) cudaFuncSetAttribute(skg::validate_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    carve = true;
   }
   skg::validate_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
@@ -330,11 +339,10 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.default_version = default_version;
   const Geom g = asm_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_ASM_GROUP", (int)g.warps));
-  static bool carve = false;
-  if (!carve) {
+  static uint64_t carve = 0;
+  if (first_on_device(carve)) {
     const int pct = env_int("SKG_CARVEOUT", -2);
     if (pct != -2) cudaFuncSetAttribute(skg::asm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    carve = true;
   }
   skg::asm_kernel<<<g.blocks, 32 * g.warps, 0, s>>>(a);
   return check(cudaGetLastError());
@@ -440,20 +448,16 @@ int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const
   return check(cudaGetLastError()) ? -1 : 0;
 }
 
-// device-wide exclusive scan of n uint32 in place; total into ctl[BC_TOTAL + 2..3]
-void large_scan(uint32_t* a, uint32_t n, const LargeWs& l, cudaStream_t s) {
-  const uint32_t nb = (n + skg::BS_BLOCK - 1) / skg::BS_BLOCK;
-  if (nb) skg::scan_blocks<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
-  skg::scan_top<<<1, skg::BS_BLOCK, 0, s>>>(l.sums, nb, l.ctl + skg::BC_TOTAL + 2);
-  if (nb) skg::scan_apply<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
-}
-
 uint32_t grid_for(uint64_t n) {
   const uint64_t b = (n + 255) / 256;
   const uint64_t cap = (uint64_t)sm_count() * 8;
   return (uint32_t)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 }  // namespace
+
+namespace {
+int64_t large_scan_total(uint32_t* a, uint32_t n, const LargeWs& l, cudaStream_t s);
+}
 
 uint64_t skg_large_workspace_bytes(uint64_t n_words, uint32_t bound) {
   return large_ws(nullptr, n_words, bound).total;
@@ -497,12 +501,14 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
   skg::Mod m;
   if (check(cudaMemcpyAsync(&m, l.mod, sizeof(m), cudaMemcpyDeviceToHost, s))) return -1;
   if (check(cudaStreamSynchronize(s))) return -1;
-  large_scan(m.ia, I, l, s);
+  const int64_t body = large_scan_total(m.ia, I, l, s);
+  if (body < 0) return (int)body;
   uint32_t tot[4];
   if (check(cudaMemcpyAsync(tot, l.ctl + skg::BC_TOTAL, 16, cudaMemcpyDeviceToHost, s)) ||
       check(cudaStreamSynchronize(s)))
     return -1;
-  const uint64_t total = (uint64_t)tot[0] + tot[2];
+  const uint64_t total = (uint64_t)tot[0] + (uint64_t)body;
+  if (total > 0xFFFFFFFFull) return -4;                            // diagnostics offsets are 32-bit
   *text_bytes = total;
   if (total > text_cap) return 3;                                  // grow the arena and call again
   skg::big_val_write<<<grid_for(W), 256, 0, s>>>(l.mod, t->t, l.ctl, text);
@@ -513,7 +519,15 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
 
 namespace {
 // exclusive scan of n uint32 in place; returns the total (host-synchronous)
+// returns -1 on a CUDA error, -4 when the total does not fit the 32-bit offsets
 int64_t large_scan_total(uint32_t* a, uint32_t n, const LargeWs& l, cudaStream_t s) {
+  unsigned long long* sum = reinterpret_cast<unsigned long long*>(l.ctl + skg::BC_SUM);
+  unsigned long long tot64 = 0;
+  if (check(cudaMemsetAsync(sum, 0, 8, s))) return -1;
+  if (n) skg::sum_u64<<<grid_for(n), 256, 0, s>>>(a, n, sum);
+  if (check(cudaMemcpyAsync(&tot64, sum, 8, cudaMemcpyDeviceToHost, s)) || check(cudaStreamSynchronize(s)))
+    return -1;
+  if (tot64 > 0xFFFFFFFFull) return -4;
   const uint32_t nb = (n + skg::BS_BLOCK - 1) / skg::BS_BLOCK;
   if (nb) skg::scan_blocks<<<nb, skg::BS_BLOCK, 0, s>>>(a, n, l.sums);
   skg::scan_top<<<1, skg::BS_BLOCK, 0, s>>>(l.sums, nb, l.ctl + skg::BC_SCAN);
@@ -579,7 +593,8 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
     bn_mark<<<gW, 256, 0, s>>>(l.mod, T);
     const int64_t cj = large_scan_total(m.ib, I, l, s);
     const int64_t nd64 = large_scan_total(m.ia, I, l, s);
-    if (cj < 0 || nd64 < 0 || read_ctl(l, ctl, s)) return -1;
+    if (cj < 0 || nd64 < 0) return (int)std::min(cj, nd64);
+    if (read_ctl(l, ctl, s)) return -1;
     const uint32_t nd = (uint32_t)nd64, N = ctl[BC_NP0] + (uint32_t)cj;
     bn_ndl<<<gW, 256, 0, s>>>(l.mod, T);
     for (uint32_t step = 0; step < 3; ++step) bn_pos<<<grid_for(std::max<uint64_t>(N + 1, std::max<uint64_t>(I, bound))), 256, 0, s>>>(l.mod, T, N, step);
@@ -603,14 +618,15 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
     uint32_t* flags = clist + 4ull * nd;                            // spill holds >= 32 nd bytes
     bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 0);
     const int64_t nc = large_scan_total(flags, nd, l, s);
-    if (nc < 0) return -1;
+    if (nc < 0) return (int)nc;
     bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 1);
     // group counters of the parallel dedup: one per ident index (leaders), after the list
     uint32_t* gcount = flags + nd;                                  // spill: 12 nc + 4 nd + 4 nd <= 32 nd bytes
     if (check(cudaMemsetAsync(gcount, 0, 4ull * nd, s))) return -1;
     bn_dedup_par<<<1, 1024, 0, s>>>(l.mod, clist, (uint32_t)nc, nd, gcount);
     bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 0);
-    if (large_scan_total(flags, nd, l, s) < 0) return -1;
+    const int64_t arena = large_scan_total(flags, nd, l, s);
+    if (arena < 0) return (int)arena;
     bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 1);
   }
   bd_refs<<<gS, 256, 0, s>>>(l.mod, T, l.ctl, 0);
@@ -627,8 +643,9 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
   uint32_t* rsum = reinterpret_cast<uint32_t*>(m.spill);           // names are done with the spill area
   bd_lengths<<<grid_for((uint64_t)nr * 32), 256, 0, s>>>(l.mod, T, opts, width, rsum);
   const int64_t body = nr ? large_scan_total(rsum, nr, l, s) : 0;
-  if (body < 0) return -1;
+  if (body < 0) return (int)body;
   const uint64_t total = (uint64_t)head + (uint64_t)body;
+  if (total > 0xFFFFFFFFull) return -4;                            // text offsets are 32-bit
   *text_bytes = total;
   if (total > text_cap) return 3;
   bd_render<<<grid_for((uint64_t)nr * 32 + 32), 256, 8 * 1024, s>>>(l.mod, T, opts, width, text, rsum, head);

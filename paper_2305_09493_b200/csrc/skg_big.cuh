@@ -175,6 +175,16 @@ __global__ void __launch_bounds__(BS_BLOCK) scan_top(uint32_t* sums, uint32_t nb
   if (threadIdx.x == 0) { total_u64[0] = carry; total_u64[1] = 0; }
 }
 
+// 64-bit sum of n uint32 (the exclusive scans above are 32-bit: the host refuses totals
+// that do not fit instead of letting the offsets wrap)
+__global__ void sum_u64(const uint32_t* a, uint32_t n, unsigned long long* out) {
+  unsigned long long v = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v += a[i];
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
 __global__ void __launch_bounds__(BS_BLOCK) scan_apply(uint32_t* a, uint32_t n, const uint32_t* sums) {
   const uint32_t i = blockIdx.x * BS_BLOCK + threadIdx.x;
   if (i < n) a[i] += sums[blockIdx.x];

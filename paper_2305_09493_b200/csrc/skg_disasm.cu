@@ -1606,11 +1606,15 @@ __global__ void __launch_bounds__(1024) bn_dedup_par(const Mod* mp, const uint32
       segstart[t] = max(segstart[t], v);
       __syncthreads();
     }
+    // every member reads its group's running count before any segment's last member
+    // advances it (a segment can span warps)
+    const uint32_t gc0 = me != ~0ull ? gcount[g] : 0;
+    __syncthreads();
     if (me != ~0ull) {
-      const uint32_t r = gcount[g] + (t - segstart[t]);
+      const uint32_t r = gc0 + (t - segstart[t]);
       m.hser[m.ndl[base + (uint32_t)(me & 0xFFFF)]] = r == 0 ? NONE32 : r - 1;
       const bool last = t == 1023 || (uint32_t)(key[t + 1] >> 32) != g;
-      if (last) gcount[g] += t - segstart[t] + 1;
+      if (last) gcount[g] = gc0 + t - segstart[t] + 1;
     }
     if ((t & 31) == 0) {   // involved idents: the exact sequential logic, in D order per family
       const uint32_t wq = t >> 5;
