@@ -1,0 +1,66 @@
+"""Config 3 at its configured size (BASELINE.json configs[2]):
+one ~91M-word module (synth/huge.py, OpName on every id, long OpStrings, ids
+up to ~1.1e7) disassembled and validated on the GPU through the public API,
+which routes modules of 2^20 words and more to the grid-wide kernels
+(skg_disasm_large / skg_validate_large) -- no monkeypatched thresholds.
+
+The expected outputs are SHA-256 digests recorded in the build container by
+tools/make_config3_fixtures.py:
+
+* validation and ``inline_names=False`` disassembly: the REFERENCE's own
+  ``validate_module`` / ``disassemble_module`` run over the full module;
+* ``inline_names=True`` disassembly: the oracle's linear closed form of
+  ``_assign_refs`` (the reference's fixpoint is O(n^2) here).
+
+A mid-size module (640 functions, ~1.1M words, just above the threshold) is
+pinned the same way and runs first.
+"""
+
+import hashlib
+import json
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).parent / "golden"
+
+
+def _fixture(n_fn):
+    p = GOLDEN / f"config3_{n_fn}.json"
+    if not p.exists():
+        pytest.skip(f"{p.name} not recorded")
+    return json.loads(p.read_text())
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2305_09493_b200 as sk
+    return sk
+
+
+def _digest(text):
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    return hashlib.sha256(data).hexdigest(), len(data)
+
+
+@pytest.mark.parametrize("n_fn", [640, 55000])
+def test_config3_full_size(sk, n_fn):
+    from paper_2305_09493_b200 import _native
+    from synth.huge import build_huge
+    fx = _fixture(n_fn)
+    m = build_huge(n_fn)
+    assert hashlib.sha256(m).hexdigest() == fx["ref_validate"]["module_sha256"]
+    assert len(m) // 4 >= _native.LARGE_MODULE_WORDS        # the grid-wide kernels, not the warp path
+    diags = sk.validate_module(m)
+    text = sk.diagnostics_text(diags)
+    assert _digest(text) == (fx["ref_validate"]["sha256"], fx["ref_validate"]["bytes"])
+    got = sk.disassemble_module(m, sk.DisassemblerOptions(inline_names=False))
+    assert _digest(got) == (fx["ref_disasm_numeric"]["sha256"], fx["ref_disasm_numeric"]["bytes"])
+    del got
+    got = sk.disassemble_module(m)
+    assert _digest(got) == (fx["oracle_disasm_named"]["sha256"], fx["oracle_disasm_named"]["bytes"])

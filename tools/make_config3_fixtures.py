@@ -7,7 +7,9 @@
 
 for the ~91M-word module ``synth.huge.build_huge(55000)``.  Build container
 only (needs /root/reference); each leg runs in its own process (RAM-heavy:
-tens of GB), the results are merged into ``tests/golden/config3.json``.
+tens of GB), the results are merged into ``tests/golden/config3_<n_fn>.json``.
+A mid-size module (n_fn = 640, just above the 2^20-word threshold of the
+grid-wide large-module kernels) is recorded the same way for a quicker test.
 
 usage: python tools/make_config3_fixtures.py [n_fn] [leg ...]
        legs: ref_validate ref_disasm_numeric oracle_disasm_named
@@ -23,7 +25,7 @@ import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-OUT = ROOT / "tests" / "golden" / "config3.json"
+GOLDEN = ROOT / "tests" / "golden"
 LEGS = ("ref_validate", "ref_disasm_numeric", "oracle_disasm_named")
 
 
@@ -61,9 +63,8 @@ def main():
         return
     n_fn = int(args[0]) if args else 55000
     legs = args[1:] or list(LEGS)
-    res = json.loads(OUT.read_text()) if OUT.exists() else {}
-    if res.get("n_fn") not in (None, n_fn):
-        res = {}
+    out = GOLDEN / f"config3_{n_fn}.json"
+    res = json.loads(out.read_text()) if out.exists() else {}
     res["n_fn"] = n_fn
     res["generator"] = "synth.huge.build_huge(n_fn) (chain=200, seed=1)"
     procs = {leg: subprocess.Popen([sys.executable, __file__, "--leg", str(n_fn), leg],
@@ -75,7 +76,7 @@ def main():
             continue
         res[leg] = json.loads(line[-1])
         print(leg, res[leg], flush=True)
-        OUT.write_text(json.dumps(res, indent=1, sort_keys=True) + "\n")
+        out.write_text(json.dumps(res, indent=1, sort_keys=True) + "\n")
 
 
 if __name__ == "__main__":
