@@ -87,6 +87,18 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
                void* stream);
 
+/* skg_disasm with explicit id refs for every module of the batch: the text of
+ * format_instruction(spec, inst, context) with a RenderContext whose `refs`
+ * name some ids (reference disasm.py:57-67, 380-389).  ref_ids: n_refs
+ * entries of 3 uint32 (id, byte offset into ref_text, byte length), ascending
+ * by id; an id listed there renders as exactly that text (result column and
+ * operands); all other ids render as usual. */
+int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                    const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+                    uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
+                    skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
+                    void* stream, const uint32_t* ref_ids, const uint8_t* ref_text, uint32_t n_refs);
+
 /* Batch structural + capability validation.
  * Replaces: validate_module(bytes) (reference validate.py:73-94).
  * Output: diagnostics_text-formatted lines ("severity code location message\n")
@@ -180,6 +192,55 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
 int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
                      uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
                      void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* tokenize_line for a batch of lines (reference asm.py:51-90).
+ * Input: UTF-8 byte arena `text` with int64 per-line offsets/lengths (one
+ * logical line each, no line separators inside).  Output, line l with its
+ * tokens in slots line_off[l] + k (k < ntok[l]; the arrays are sized like
+ * `text`): tok_off = byte offset of the token text -- in `text` for bare
+ * tokens, in `esc` (same size as `text`) for string tokens, which are stored
+ * with their backslash escapes resolved; tok_len = bytes; tok_col = 1-based
+ * code-point column of the token start (the quote for strings); tok_flags bit 0
+ * = string token.  kind[l]: 0 blank/comment line (None), 1 instruction, 2
+ * instruction with a "%r =" result, 3 unterminated string literal (err_col[l]
+ * = column of its opening quote). */
+int skg_tokenize(const uint8_t* text, const int64_t* line_off, const int64_t* line_len, uint32_t n_lines,
+                 uint64_t* tok_off, uint32_t* tok_len, uint32_t* tok_col, uint8_t* tok_flags, uint8_t* esc,
+                 int32_t* kind, int32_t* ntok, uint32_t* err_col, void* stream);
+
+/* encode_module for a batch (reference codec.py:192-196 with encode_header
+ * :61-79 and encode_instruction :92-101; the words of ModuleScope.serialize,
+ * builder.py:208-224).  header: 5 int64 per module (major, minor,
+ * generator_magic & 0xFFFFFFFF, bound, schema & 0xFFFFFFFF); module m owns
+ * instructions [inst_base[m], inst_base[m+1]); instruction i has opcode[i] and
+ * the operand words ops[op_off[i] : op_off[i+1]] (already masked to 32 bits;
+ * op_off has n_inst + 1 entries).  Module m's words start at word
+ * 5m + inst_base[m] + op_off[inst_base[m]] of `out`.  err[m] = all ones when
+ * the module encodes, else (k << 8 | code) for its first error: code 1 bound 0,
+ * 2 bound out of range, 3 version bytes (k = 0), 4 instruction length
+ * overflows 16 bits, 5 opcode out of range (k = 1 + instruction index in the
+ * module). */
+int skg_encode_modules(const int64_t* header, uint32_t n_mod, const int64_t* inst_base, const int64_t* opcode,
+                       uint64_t n_inst, const int64_t* op_off, const uint32_t* ops, uint64_t n_ops,
+                       uint32_t* out, uint64_t* err, void* stream);
+
+/* encode_string_literal for a batch of UTF-8 strings (reference codec.py:104-114):
+ * string s = bytes[off[s] : off[s] + len[s]] packs into len[s] / 4 + 1
+ * little-endian words (NUL-terminated, zero padded) at out[word_off[s]...];
+ * bad[s] is set to 1 (caller zeroes it) when the string holds a NUL byte
+ * (CodecError). */
+int skg_pack_strings(const uint8_t* bytes, const int64_t* off, const int64_t* len, const int64_t* word_off,
+                     uint32_t n_str, uint64_t n_words, uint32_t* out, int32_t* bad, void* stream);
+
+/* encode_context_dependent_literal for a batch (reference codec.py:132-168).
+ * width[k]: bit width, -1 for None; flags[k]: 1 signed, 2 floating, 4 negative
+ * integer, 8 integer magnitude >= 2^64; val[k]: |integer| or the IEEE-754
+ * double bits of the float.  Output words[2k], words[2k+1] (nwords[k] of them)
+ * and status[k]: 0 ok, 1 unresolved width, 2 unsupported width, 3 unsupported
+ * float width, 4 OverflowError (e format), 5 OverflowError (f format), 6 / 7 the
+ * value does not fit a signed / unsigned literal of that width. */
+int skg_ctx_literals(const int64_t* width, const uint32_t* flags, const uint64_t* val, uint32_t n,
+                     uint32_t* words, int32_t* nwords, int32_t* status, void* stream);
 
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,

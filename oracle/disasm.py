@@ -91,16 +91,27 @@ def referenced_ids(spec, insts, maps):
 
 
 def unique_names(order, names):
-    """disasm.py:173-185: sanitize, then base, base_0, base_1, ... in D order."""
-    out, taken = {}, set()
+    """disasm.py:173-185: sanitize, then base, base_0, base_1, ... in D order.
+
+    The reference retries every serial from 0 for each duplicate (quadratic in
+    the duplicates of one base).  The taken set only grows, so serials that
+    were taken at a base's previous duplicate still are: restarting from the
+    serial after the one that base took last gives the same names in linear
+    time (needed for the config-3 module, ~10^7 named ids over a dozen bases).
+    """
+    out, taken, nxt = {}, set(), {}
     for ident in order:
         if ident not in names:
             continue
         base = sanitize(names[ident])
-        cand, serial = base, 0
-        while cand in taken:
+        cand = base
+        if cand in taken:
+            serial = nxt.get(base, 0)
             cand = f"{base}_{serial}"
-            serial += 1
+            while cand in taken:
+                serial += 1
+                cand = f"{base}_{serial}"
+            nxt[base] = serial + 1
         taken.add(cand)
         out[ident] = cand
     return out

@@ -1,18 +1,22 @@
 """B200-native SPIR-V codec path (disassemble / assemble / validate / decode) behind the
 ``spirvkit`` (arXiv 2305.09493 reference) API.  See DESIGN.md."""
 
-from .asm import Assembler, assemble_batch, assemble_module
-from .codec import ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module
-from .disasm import (Disassembler, DisassemblerOptions, disassemble_batch, disassemble_module,
-                     format_instruction)
+from .asm import (Assembler, SymbolTable, TextInstruction, Token, assemble_batch, assemble_module,
+                  tokenize_line, tokenize_lines)
+from .codec import (ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module,
+                    encode_context_dependent_literal, encode_context_dependent_literals, encode_header,
+                    encode_instruction, encode_module, encode_modules, encode_string_literal,
+                    encode_string_literals)
+from .disasm import (Disassembler, DisassemblerOptions, RenderContext, disassemble_batch,
+                     disassemble_module, format_instruction)
 from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,
                      GenerationError, GrammarError, GrammarParseError, GrammarSchemaError,
                      IdExhaustedError, NotFoundError, NotSpirvError, ScopeError,
                      SerializationError, SpirvKitError, SsaError, StructureError,
                      TruncatedStreamError)
-from .grammar import (EnumerantDef, ExtInstGrammar, GrammarSpec, InstructionDef, OperandKindDef,
-                      OperandSlot, load_core_grammar, load_extended_grammar, load_pinned,
-                      load_pinned_extended, transitive_capabilities)
+from .grammar import (DependencyReport, EnumerantDef, ExtInstGrammar, GrammarSpec, InstructionDef,
+                      OperandKindDef, OperandSlot, capability_dependency_graph, load_core_grammar,
+                      load_extended_grammar, load_pinned, load_pinned_extended, transitive_capabilities)
 from .validate import (Diagnostic, check_capability_closure, diagnostics_text, validate_batch,
                        validate_module)
 

@@ -63,6 +63,14 @@ def lib():
     L.skg_validate_large.restype = I32
     L.skg_disasm_large.argtypes = [P, P, U64, U32, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
     L.skg_disasm_large.restype = I32
+    L.skg_disasm_refs.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P, P, P, U32]
+    L.skg_disasm_refs.restype = I32
+    L.skg_tokenize.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, P]
+    L.skg_encode_modules.argtypes = [P, U32, P, P, U64, P, P, U64, P, P, P]
+    L.skg_pack_strings.argtypes = [P, P, P, P, U32, U64, P, P, P]
+    L.skg_ctx_literals.argtypes = [P, P, P, U32, P, P, P, P]
+    for f in (L.skg_tokenize, L.skg_encode_modules, L.skg_pack_strings, L.skg_ctx_literals):
+        f.restype = I32
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
               L.skg_decode_large):
@@ -226,7 +234,7 @@ def last_counts(ws):
     return int(nerr.value), bool(over.value), int(used.value)
 
 
-def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, err_cap=None):
+def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, err_cap=None, refs=None):
     torch = _torch()
     L = lib()
     th = tables_handle(spec, ext)
@@ -240,7 +248,12 @@ def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, e
         span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
         status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         errs = torch.empty(ecap * 256, dtype=torch.uint8, device="cuda")
-        if kind == "disasm":
+        if kind == "disasm" and refs is not None:   # (ids u32[n, 3] device, text u8 device, n)
+            rc = L.skg_disasm_refs(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
+                                   opts, batch.max_words, text.data_ptr(), cap, span.data_ptr(),
+                                   status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes, _stream(),
+                                   refs[0].data_ptr(), refs[1].data_ptr(), refs[2])
+        elif kind == "disasm":
             rc = L.skg_disasm(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n,
                               opts, batch.max_words, text.data_ptr(), cap, span.data_ptr(),
                               status.data_ptr(), errs.data_ptr(), ecap, ws.data_ptr(), ws_bytes, _stream())
@@ -303,13 +316,15 @@ def make_exception(status, msg, a=0, b=0, c=0, d=0):
 WS_BUDGET = 8 << 30
 
 
-def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None):
-    """disasm / validate of a device batch -> list of (text bytes | exception)."""
+def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None, refs=None):
+    """disasm / validate of a device batch -> list of (text bytes | exception).
+    refs: explicit id refs for skg_disasm_refs (format_instruction with a context)."""
     torch = _torch()
     n = batch.n
     if n == 0:
         return []
-    run = (lambda b: run_disasm(b, opts, spec, ext)) if kind == "disasm" else (lambda b: run_validate(b, spec))
+    run = (lambda b: run_disasm(b, opts, spec, ext, refs=refs)) if kind == "disasm" else \
+        (lambda b: run_validate(b, spec))
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
     if (n == 1 or need <= WS_BUDGET) and batch.max_words < LARGE_MODULE_WORDS:
         return fetch_texts(run(batch), n)
@@ -497,6 +512,125 @@ def _run_decode_large(d, n: int):
     k = int(cnt.item())
     return tuple(int(x) for x in header.cpu().numpy().view(np.uint32)), \
         _pinned.to_u32(words, W), _pinned.to_u32(inst_off, k)
+
+
+# -- standalone codec / tokenizer kernels (skg_codec.cuh) -------------------------------
+def _dev(arr, dtype):
+    """host numpy array -> device tensor (at least one element)"""
+    torch = _torch()
+    a = np.ascontiguousarray(arr, dtype=dtype)
+    if a.size == 0:
+        a = np.zeros(1, dtype=dtype)
+    return torch.from_numpy(a).to("cuda")
+
+
+def run_tokenize(raws):
+    """list[bytes] (one logical line each) -> per line (kind, [(text bytes, column, is_string)],
+    err_col): kind 0 blank, 1 instruction, 2 with result, 3 unterminated string."""
+    torch = _torch()
+    n = len(raws)
+    if n == 0:
+        return []
+    lens = np.array([len(r) for r in raws], dtype=np.int64)
+    offs = np.zeros(n, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)[:-1]
+    total = int(lens.sum())
+    text = _dev(np.frombuffer(b"".join(raws) + b"\0", dtype=np.uint8), np.uint8)
+    d_off, d_len = _dev(offs, np.int64), _dev(lens, np.int64)
+    cap = max(total, 1)
+    tok_off = torch.zeros(cap, dtype=torch.int64, device="cuda")
+    tok_len = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tok_col = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tok_fl = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+    esc = torch.zeros(cap + 1, dtype=torch.uint8, device="cuda")
+    kind = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ntok = torch.zeros(n, dtype=torch.int32, device="cuda")
+    err = torch.zeros(n, dtype=torch.int32, device="cuda")
+    _check(lib().skg_tokenize(text.data_ptr(), d_off.data_ptr(), d_len.data_ptr(), n, tok_off.data_ptr(),
+                              tok_len.data_ptr(), tok_col.data_ptr(), tok_fl.data_ptr(), esc.data_ptr(),
+                              kind.data_ptr(), ntok.data_ptr(), err.data_ptr(), _stream()), "tokenize")
+    h_text, h_esc = text.cpu().numpy().tobytes(), esc.cpu().numpy().tobytes()
+    h_off, h_len = tok_off.cpu().numpy(), tok_len.cpu().numpy()
+    h_col, h_fl = tok_col.cpu().numpy(), tok_fl.cpu().numpy()
+    h_kind, h_nt, h_err = kind.cpu().numpy(), ntok.cpu().numpy(), err.cpu().numpy()
+    out = []
+    for li in range(n):
+        toks = []
+        for k in range(int(offs[li]), int(offs[li]) + int(h_nt[li])):
+            src = h_esc if h_fl[k] & 1 else h_text
+            o = int(h_off[k])
+            toks.append((src[o:o + int(h_len[k])], int(h_col[k]), bool(h_fl[k] & 1)))
+        out.append((int(h_kind[li]), toks, int(h_err[li])))
+    return out
+
+
+ENC_MESSAGES = {1: "header bound is 0; recompute the bound before serializing"}
+
+
+def run_encode_modules(headers, opcodes, op_counts, operands, inst_counts):
+    """Batch encode_module: headers int64[n, 5] (major, minor, generator & mask, bound,
+    schema & mask), per instruction opcode / operand count, operand words uint32 (masked),
+    instructions per module.  -> (words uint32 arena, word offset per module (n + 1),
+    err uint64 per module: all ones = ok, else (k << 8) | code)."""
+    torch = _torch()
+    headers = np.ascontiguousarray(headers, dtype=np.int64).reshape(-1, 5)
+    n = len(headers)
+    if n == 0:
+        return np.zeros(0, np.uint32), np.zeros(1, np.int64), np.zeros(0, np.uint64)
+    inst_counts = np.asarray(inst_counts, dtype=np.int64)
+    inst_base = np.zeros(n + 1, dtype=np.int64)
+    inst_base[1:] = np.cumsum(inst_counts)
+    op_counts = np.asarray(op_counts, dtype=np.int64)
+    n_inst = int(inst_base[-1])
+    op_off = np.zeros(n_inst + 1, dtype=np.int64)
+    op_off[1:] = np.cumsum(op_counts)
+    n_ops = int(op_off[-1])
+    mod_words = 5 * np.arange(n + 1, dtype=np.int64) + inst_base + op_off[inst_base]
+    total = int(mod_words[-1])
+    out = torch.zeros(max(total, 1), dtype=torch.int32, device="cuda")
+    err = torch.zeros(n, dtype=torch.int64, device="cuda")
+    d_hdr, d_ib = _dev(headers.reshape(-1), np.int64), _dev(inst_base, np.int64)
+    d_opc, d_oo = _dev(opcodes, np.int64), _dev(op_off, np.int64)
+    d_ops = _dev(np.asarray(operands, dtype=np.uint32).view(np.int32), np.int32)
+    _check(lib().skg_encode_modules(d_hdr.data_ptr(), n, d_ib.data_ptr(), d_opc.data_ptr(), n_inst,
+                                    d_oo.data_ptr(), d_ops.data_ptr(), n_ops, out.data_ptr(), err.data_ptr(),
+                                    _stream()), "encode_modules")
+    return (_pinned.to_u32(out, total) if total else np.zeros(0, np.uint32)), mod_words, \
+        err.cpu().numpy().view(np.uint64)
+
+
+def run_pack_strings(raws):
+    """list[bytes] -> (words uint32 arena, word offsets (n + 1), has-NUL flags)."""
+    torch = _torch()
+    n = len(raws)
+    lens = np.array([len(r) for r in raws], dtype=np.int64)
+    offs = np.zeros(n, dtype=np.int64)
+    if n > 1:
+        offs[1:] = np.cumsum(lens)[:-1]
+    wo = np.zeros(n + 1, dtype=np.int64)
+    wo[1:] = np.cumsum(lens // 4 + 1)
+    total = int(wo[-1])
+    data = _dev(np.frombuffer(b"".join(raws) + b"\0", dtype=np.uint8), np.uint8)
+    out = torch.zeros(max(total, 1), dtype=torch.int32, device="cuda")
+    bad = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    d_off, d_len, d_wo = _dev(offs, np.int64), _dev(lens, np.int64), _dev(wo, np.int64)
+    _check(lib().skg_pack_strings(data.data_ptr(), d_off.data_ptr(), d_len.data_ptr(), d_wo.data_ptr(), n, total,
+                                  out.data_ptr(), bad.data_ptr(), _stream()), "pack_strings")
+    return out.cpu().numpy().view(np.uint32)[:total], wo, bad.cpu().numpy()[:n]
+
+
+def run_ctx_literals(widths, flags, vals):
+    """Batch encode_context_dependent_literal -> (words uint32[n, 2], nwords, status)."""
+    torch = _torch()
+    n = len(widths)
+    words = torch.zeros(2 * max(n, 1), dtype=torch.int32, device="cuda")
+    nw = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    st = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+    d_w, d_f = _dev(widths, np.int64), _dev(np.asarray(flags, dtype=np.uint32).view(np.int32), np.int32)
+    d_v = _dev(np.asarray(vals, dtype=np.uint64).view(np.int64), np.int64)
+    _check(lib().skg_ctx_literals(d_w.data_ptr(), d_f.data_ptr(), d_v.data_ptr(), n, words.data_ptr(),
+                                  nw.data_ptr(), st.data_ptr(), _stream()), "ctx_literals")
+    return words.cpu().numpy().view(np.uint32).reshape(-1, 2)[:n], nw.cpu().numpy()[:n], st.cpu().numpy()[:n]
 
 
 __all__ = ["lib", "DeviceBatch", "run_disasm", "run_validate", "run_decode", "fetch_texts",

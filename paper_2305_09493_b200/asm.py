@@ -11,7 +11,84 @@ ValueError, OverflowError, StructureError, SerializationError, CodecError).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 from . import _native
+from .errors import AsmDiagnostic, AssemblyError
+
+
+@dataclass(frozen=True)
+class Token:
+    """asm.py:34-38."""
+    text: str
+    column: int  # 1-based (code points)
+    is_string: bool = False
+
+
+@dataclass
+class TextInstruction:
+    """asm.py:41-48: one parsed source line."""
+    result: Token | None
+    opname: Token
+    operands: list
+    line: int
+
+
+def tokenize_lines(lines, first_lineno: int = 1):
+    """Batch tokenize_line over many lines on the GPU (skg_tokenize, one thread per
+    line): list[str] -> list[TextInstruction | None | AssemblyError] (line numbers
+    first_lineno, first_lineno + 1, ...; exception instances, not raised)."""
+    raws = [ln.encode("utf-8", "surrogatepass") for ln in lines]
+    out = []
+    for k, (kind, toks, col) in enumerate(_native.run_tokenize(raws)):
+        lineno = first_lineno + k
+        if kind == 3:
+            out.append(AssemblyError([AsmDiagnostic(lineno, col, "unterminated string literal")]))
+            continue
+        if kind == 0:
+            out.append(None)
+            continue
+        tokens = [Token(b.decode("utf-8", "surrogatepass"), c, s) for b, c, s in toks]
+        result = None
+        if kind == 2:
+            result, tokens = tokens[0], tokens[2:]
+        out.append(TextInstruction(result=result, opname=tokens[0], operands=tokens[1:], line=lineno))
+    return out
+
+
+def tokenize_line(line: str, lineno: int = 1):
+    """asm.py:51-90 on the GPU: None for blank / comment lines, AssemblyError for an
+    unterminated string literal (column of the opening quote)."""
+    r = tokenize_lines([line], lineno)[0]
+    if isinstance(r, BaseException):
+        raise r
+    return r
+
+
+class SymbolTable:
+    """asm.py:93-120: names <-> ids of a builder module.  Numeric names (%13) pin
+    their value (module.reserve_id), symbolic names take module.new_id() at first
+    mention.  The assembler kernel runs this logic on the device for whole
+    documents (skg_asm phase D: a name hash map, the reservation bitmap and a
+    select over unreserved ids); this class is the reference's per-name interface
+    over a caller-owned builder module."""
+
+    def __init__(self, module):
+        self.module = module
+        self.by_name = {}
+        self.by_id = {}
+
+    def resolve(self, name: str):
+        if not name.startswith("%") or len(name) == 1:
+            raise ValueError(f"expected an id like %name, got {name!r}")
+        hit = self.by_name.get(name)
+        if hit is not None:
+            return hit
+        body = name[1:]
+        ident = self.module.reserve_id(int(body)) if body.isdigit() else self.module.new_id()
+        self.by_name[name] = ident
+        self.by_id[int(ident)] = name
+        return ident
 
 
 def assemble_batch(texts, spec=None, ext=None, default_version=(1, 2)):

@@ -9,6 +9,7 @@
 #include "skg_sched.cuh"
 #include "skg_bigdecode.cuh"
 #include "skg_big.cuh"
+#include "skg_codec.cuh"
 
 namespace skg {
 struct DisasmArgs;
@@ -226,7 +227,16 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
                skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
                void* stream) {
-  if (!t || !workspace) return -1;
+  return skg_disasm_refs(t, data, mod_off, mod_len, n_mod, opts, max_words, text, text_cap, text_span, status,
+                         errors, err_cap, workspace, workspace_bytes, stream, nullptr, nullptr, 0);
+}
+
+int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                    const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+                    uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
+                    skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
+                    void* stream, const uint32_t* ref_ids, const uint8_t* ref_text, uint32_t n_refs) {
+  if (!t || !workspace || (n_refs && (!ref_ids || !ref_text))) return -1;
   WsLayout l = ws_layout(n_mod, max_words);
   if (workspace_bytes < l.total) return -3;
   cudaStream_t s = (cudaStream_t)stream;
@@ -243,6 +253,7 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
   a.gscratch = ws + l.scratch;
   a.gslot_bytes = l.slot;
   a.smem_slab = kDisSlab;
+  a.ovr = ref_ids; a.ovr_text = ref_text; a.n_ovr = n_refs;
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   a.stage_bytes = kDisStage;
@@ -673,6 +684,61 @@ int skg_decode(const uint8_t* data, const int64_t* mod_off, const int64_t* mod_l
   const uint32_t threads = 256;
   uint32_t blocks = (n_mod + threads - 1) / threads;
   skg::decode_kernel<<<blocks, threads, 0, s>>>(a);
+  return check(cudaGetLastError());
+}
+
+
+// -- standalone codec / tokenizer entries (skg_codec.cuh) --------------------------------
+namespace {
+uint32_t item_grid(uint64_t n) {
+  const uint64_t b = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)sm_count() * 16;
+  return (uint32_t)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+}  // namespace
+
+int skg_tokenize(const uint8_t* text, const int64_t* line_off, const int64_t* line_len, uint32_t n_lines,
+                 uint64_t* tok_off, uint32_t* tok_len, uint32_t* tok_col, uint8_t* tok_flags, uint8_t* esc,
+                 int32_t* kind, int32_t* ntok, uint32_t* err_col, void* stream) {
+  if (n_lines == 0) return 0;
+  if (!text || !line_off || !line_len || !tok_off || !tok_len || !tok_col || !tok_flags || !esc || !kind ||
+      !ntok || !err_col)
+    return -1;
+  skg::tokenize_kernel<<<item_grid(n_lines), 256, 0, (cudaStream_t)stream>>>(
+      text, line_off, line_len, n_lines, tok_off, tok_len, tok_col, tok_flags, esc, kind, ntok, err_col);
+  return check(cudaGetLastError());
+}
+
+int skg_encode_modules(const int64_t* header, uint32_t n_mod, const int64_t* inst_base, const int64_t* opcode,
+                       uint64_t n_inst, const int64_t* op_off, const uint32_t* ops, uint64_t n_ops,
+                       uint32_t* out, uint64_t* err, void* stream) {
+  if (n_mod == 0) return 0;
+  if (!header || !inst_base || !op_off || !out || !err || n_inst >= 0xFFFFFFFFull) return -1;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* e = reinterpret_cast<unsigned long long*>(err);
+  skg::encode_headers_kernel<<<item_grid(n_mod), 256, 0, s>>>(header, n_mod, inst_base, op_off, out, e);
+  if (n_inst) skg::encode_insts_kernel<<<item_grid(n_inst), 256, 0, s>>>(opcode, op_off, n_inst, inst_base,
+                                                                          n_mod, out, e);
+  if (n_ops) skg::encode_operands_kernel<<<item_grid(n_ops), 256, 0, s>>>(ops, n_ops, op_off, (uint32_t)n_inst,
+                                                                           inst_base, n_mod, out);
+  return check(cudaGetLastError());
+}
+
+int skg_pack_strings(const uint8_t* bytes, const int64_t* off, const int64_t* len, const int64_t* word_off,
+                     uint32_t n_str, uint64_t n_words, uint32_t* out, int32_t* bad, void* stream) {
+  if (n_str == 0 || n_words == 0) return 0;
+  if (!bytes || !off || !len || !word_off || !out || !bad) return -1;
+  skg::pack_strings_kernel<<<item_grid(n_words), 256, 0, (cudaStream_t)stream>>>(bytes, off, len, word_off, n_str,
+                                                                                  n_words, out, bad);
+  return check(cudaGetLastError());
+}
+
+int skg_ctx_literals(const int64_t* width, const uint32_t* flags, const uint64_t* val, uint32_t n,
+                     uint32_t* words, int32_t* nwords, int32_t* status, void* stream) {
+  if (n == 0) return 0;
+  if (!width || !flags || !val || !words || !nwords || !status) return -1;
+  skg::ctx_literals_kernel<<<item_grid(n), 256, 0, (cudaStream_t)stream>>>(width, flags, val, n, words, nwords,
+                                                                            status);
   return check(cudaGetLastError());
 }
 

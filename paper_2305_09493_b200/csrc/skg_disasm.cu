@@ -46,6 +46,9 @@ struct DisasmArgs {
   uint32_t stage_bytes;       // bytes per warp of text stage (dynamic shared memory, first)
   const uint32_t* order;      // ticket -> module index (skg_sched.cuh)
   uint32_t group_warps;       // warps per phase-barrier group (divides the CTA's warps)
+  const uint32_t* ovr;        // explicit refs (Mod::ovr), n_ovr entries; nullptr = none
+  const uint8_t* ovr_text;
+  uint32_t n_ovr;
 };
 
 // -- sanitized friendly names (disasm.py:82-86) --------------------------------
@@ -104,7 +107,23 @@ __device__ __forceinline__ uint32_t dlen32(uint32_t v) {
 // per-slot ref text lengths for direct-mode modules (P5, before any length is needed)
 __device__ __noinline__ void fill_ref_lengths(Mod& m);
 
+// explicit ref of `id` (Mod::ovr): entry index or NONE32
+__device__ __noinline__ uint32_t ovr_find(const Mod& m, uint32_t id) {
+  uint32_t lo = 0, hi = m.n_ovr;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint32_t v = m.ovr[3 * mid];
+    if (v == id) return mid;
+    if (v < id) lo = mid + 1; else hi = mid;
+  }
+  return NONE32;
+}
+
 __device__ __forceinline__ uint32_t ref_len_slow(const Mod& m, uint32_t id) {
+  if (m.n_ovr) {
+    const uint32_t k = ovr_find(m, id);
+    if (k != NONE32) return m.ovr[3 * k + 2];
+  }
   const uint32_t slot = ht_find(m, id);
   if (slot != NONE32 && (m.hfl[slot] & HF_FRIENDLY)) {
     const uint32_t ser = m.hser[slot];
@@ -757,6 +776,15 @@ __device__ __forceinline__ uint8_t* emit_tab(uint8_t* __restrict__ p, const Tabl
 }
 
 __device__ __noinline__ uint8_t* emit_ref(uint8_t* __restrict__ p, const Mod& m, uint32_t id) {
+  if (m.n_ovr) {
+    const uint32_t k = ovr_find(m, id);
+    if (k != NONE32) {
+      const uint8_t* src = m.ovr_text + m.ovr[3 * k + 1];
+      const uint32_t n = m.ovr[3 * k + 2];
+      for (uint32_t q = 0; q < n; ++q) p[q] = src[q];
+      return p + n;
+    }
+  }
   *p++ = '%';
   // direct mode: a slot that is not present has hfl == 0 (init_tables)
   const uint32_t slot = m.direct ? (id < m.S ? id : NONE32) : ht_find(m, id);
@@ -1229,6 +1257,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
       report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
     } else {
       layout_head(m, in_smem ? slab : gslot, W);
+      m.ovr = a.ovr; m.ovr_text = a.ovr_text; m.n_ovr = a.n_ovr;
       status = load_and_split(m, src, (uint64_t)nbytes, &es, (int32_t)t);
     }
   }

@@ -90,6 +90,11 @@ struct Mod {
   uint32_t* overflow;
   uint32_t* top_present;
   uint32_t major, minor, gen, bound, schema;
+  // explicit refs (format_instruction with a RenderContext, disasm.py:57-67): ids in
+  // ascending order with (text offset, length) of their full ref text; 0 = none
+  const uint32_t* ovr;        // 3 words per entry
+  const uint8_t* ovr_text;
+  uint32_t n_ovr;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -140,6 +145,7 @@ __device__ inline void layout_head(Mod& m, uint8_t* base, uint32_t W) {
   m.w = reinterpret_cast<uint32_t*>(base + 64);
   m.W = W;
   m.ioff = reinterpret_cast<uint32_t*>(base + 64 + align16(4ull * W));
+  m.ovr = nullptr; m.ovr_text = nullptr; m.n_ovr = 0;
 }
 
 __device__ inline size_t tables_need(const Mod& m, bool direct, uint32_t S_or_C, size_t work_min) {
@@ -482,6 +488,7 @@ __device__ inline void move_to_global(Mod& m, uint8_t* gslot) {
   for (uint32_t k = lane_id(); k < m.W; k += 32) g.w[k] = m.w[k];
   for (uint32_t k = lane_id(); k < m.I; k += 32) g.ioff[k] = m.ioff[k];
   g.I = m.I; g.arena_need = m.arena_need; g.major = m.major; g.minor = m.minor; g.gen = m.gen; g.bound = m.bound; g.schema = m.schema;
+  g.ovr = m.ovr; g.ovr_text = m.ovr_text; g.n_ovr = m.n_ovr;
   __syncwarp();
   m = g;
 }

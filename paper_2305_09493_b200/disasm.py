@@ -8,7 +8,8 @@ repr, layout -- happens in ``skg_disasm`` (csrc/skg_disasm.cu).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import struct
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -44,31 +45,99 @@ def disassemble_batch(modules, options=None, spec=None, ext=None, strict=False):
             for r in _native.run_texts("disasm", batch, option_bits(options, strict), spec, ext)]
 
 
+@dataclass
+class RenderContext:
+    """disasm.py:57-79: the per-module maps the per-instruction renderer draws from."""
+    refs: dict = field(default_factory=dict)          # id -> %ref text
+    type_info: dict = field(default_factory=dict)     # type id -> (width, signed, floating)
+    value_type: dict = field(default_factory=dict)    # value id -> type id
+    import_sets: dict = field(default_factory=dict)   # set id -> import name
+
+    def ref(self, ident: int) -> str:
+        return self.refs.get(ident) or f"%{ident}"
+
+    def literal_resolver(self, opdef, decoded):
+        if opdef.name == "OpSwitch":
+            if not decoded:
+                return None
+            return self.type_info.get(self.value_type.get(decoded[0].value, -1))
+        for operand in decoded:
+            if operand.role == "result_type":
+                return self.type_info.get(operand.value)
+        return None
+
+
+def _u32(v) -> bool:
+    return isinstance(v, int) and 0 <= v <= 0xFFFFFFFF
+
+
+def _str_words(text: str):
+    data = text.encode("utf-8") + b"\0"
+    data += b"\0" * (-len(data) % 4)
+    return list(struct.unpack(f"<{len(data) // 4}I", data))
+
+
 def format_instruction(spec, inst, context=None, ext=None) -> str:
-    """One raw instruction as one plain-text line (reference disasm.py:380-389)
-    with the default, empty RenderContext: no friendly names, no type map, no
-    extended-instruction sets.  Rendered by skg_disasm on a one-instruction
-    module (no header, no indentation, numeric ids), which sees exactly that
-    empty context; decode errors raise the reference's exceptions."""
+    """One raw instruction as one plain-text line (reference disasm.py:380-389).
+
+    Rendered by skg_disasm on a synthesized module: the instruction, preceded by
+    the declarations that make the kernel's own prescan reproduce the context's
+    maps -- OpTypeInt / OpTypeFloat per ``type_info`` entry, OpUndef per
+    ``value_type`` entry and an OpExtInstImport "OpenCL.std" per such
+    ``import_sets`` entry (only when an ``ext`` grammar is given, as the reference
+    names extended instructions only then) -- with no header, no indentation and
+    numeric ids, except that the context's ``refs`` are passed to the kernel as
+    explicit ref texts (skg_disasm_refs).  Decode errors raise the reference's
+    exceptions."""
+    import numpy as np
     from . import grammar as _grammar
-    if context is not None:
-        raise NotImplementedError("format_instruction: only the default (empty) RenderContext "
-                                  "is supported by the GPU path")
     spec = spec if spec is not None else _grammar.load_pinned()
     spec.instruction(inst.opcode)          # NotFoundError outside the grammar, as the reference
     ops = [int(w) & 0xFFFFFFFF for w in inst.operands]
     if len(ops) + 1 > 0xFFFF:
         raise ValueError("format_instruction: more than 65534 operand words")
-    bound = max(ops, default=0) + 1
-    words = [0x07230203, 0x00010200, 0, bound & 0xFFFFFFFF, 0,
-             ((len(ops) + 1) << 16) | (int(inst.opcode) & 0xFFFF), *ops]
-    import struct
+    ctx = context if context is not None else RenderContext()
+    pre, ids = [], list(ops)
+    for tid, info in ctx.type_info.items():
+        if not _u32(tid) or info is None:
+            continue
+        width, signed, floating = info
+        if floating:
+            pre += [(3 << 16) | 22, tid, int(width) & 0xFFFFFFFF]                       # OpTypeFloat
+        else:
+            pre += [(4 << 16) | 21, tid, int(width) & 0xFFFFFFFF, 1 if signed else 0]    # OpTypeInt
+        ids.append(tid)
+    for vid, tid in ctx.value_type.items():
+        if _u32(vid) and _u32(tid):
+            pre += [(3 << 16) | 1, tid, vid]                                            # OpUndef
+            ids += [vid, tid]
+    if ext is not None:
+        for sid, name in ctx.import_sets.items():
+            if _u32(sid) and name == "OpenCL.std":
+                w = _str_words(name)
+                pre += [((2 + len(w)) << 16) | 11, sid, *w]                              # OpExtInstImport
+                ids.append(sid)
+    bound = min(max(ids, default=0) + 1, 0xFFFFFFFF)
+    words = [0x07230203, 0x00010200, 0, bound, 0, *pre, ((len(ops) + 1) << 16) | (int(inst.opcode) & 0xFFFF), *ops]
     module = struct.pack(f"<{len(words)}I", *words)
+    refs = sorted((k, v.encode("utf-8", "surrogatepass")) for k, v in ctx.refs.items() if _u32(k) and v)
     opts = DisassemblerOptions(inline_names=False, no_indent=True, no_header=True)
-    out = disassemble_batch([module], opts, spec, ext)[0]
-    if isinstance(out, BaseException):
-        raise out
-    return out[:-1] if out.endswith("\n") else out
+    batch = _native.DeviceBatch.from_modules([module])
+    dev_refs = None
+    if refs:
+        blob = b"".join(r for _, r in refs)
+        tab = np.zeros((len(refs), 3), dtype=np.uint32)
+        pos = 0
+        for k, (i, r) in enumerate(refs):
+            tab[k] = (i, pos, len(r))
+            pos += len(r)
+        dev_refs = (_native._dev(tab.reshape(-1), np.uint32), _native._dev(np.frombuffer(blob, np.uint8), np.uint8),
+                    len(refs))
+    res = _native.run_texts("disasm", batch, option_bits(opts), spec, ext, refs=dev_refs)[0]
+    if isinstance(res, BaseException):
+        raise res
+    out = res.decode("utf-8")
+    return out.rsplit("\n", 2)[-2] if out.endswith("\n") else out
 
 
 class Disassembler:

@@ -48,19 +48,30 @@ def _digest(text):
     return hashlib.sha256(data).hexdigest(), len(data)
 
 
-@pytest.mark.parametrize("n_fn", [640, 55000])
-def test_config3_full_size(sk, n_fn):
+@pytest.mark.parametrize("n_fn,mut", [(640, ""), (640, "_mut"), (55000, ""), (55000, "_mut")])
+def test_config3_full_size(sk, n_fn, mut):
+    """mut: the seeded mutations of tools/make_config3_fixtures.mutate (duplicate result
+    ids, unknown opcodes): validation reports them, disassembly renders OpUnknown."""
     from paper_2305_09493_b200 import _native
     from synth.huge import build_huge
     fx = _fixture(n_fn)
+    if "ref_validate" + mut not in fx:
+        pytest.skip(f"config3_{n_fn}.json has no {mut or 'plain'} records")
     m = build_huge(n_fn)
-    assert hashlib.sha256(m).hexdigest() == fx["ref_validate"]["module_sha256"]
+    if mut:
+        import sys
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+        from make_config3_fixtures import mutate
+        m = mutate(m)
+    assert hashlib.sha256(m).hexdigest() == fx["ref_validate" + mut]["module_sha256"]
     assert len(m) // 4 >= _native.LARGE_MODULE_WORDS        # the grid-wide kernels, not the warp path
     diags = sk.validate_module(m)
     text = sk.diagnostics_text(diags)
-    assert _digest(text) == (fx["ref_validate"]["sha256"], fx["ref_validate"]["bytes"])
+    assert _digest(text) == (fx["ref_validate" + mut]["sha256"], fx["ref_validate" + mut]["bytes"])
     got = sk.disassemble_module(m, sk.DisassemblerOptions(inline_names=False))
-    assert _digest(got) == (fx["ref_disasm_numeric"]["sha256"], fx["ref_disasm_numeric"]["bytes"])
+    want = fx["ref_disasm_numeric" + mut]
+    assert _digest(got) == (want["sha256"], want["bytes"])
     del got
     got = sk.disassemble_module(m)
-    assert _digest(got) == (fx["oracle_disasm_named"]["sha256"], fx["oracle_disasm_named"]["bytes"])
+    want = fx["oracle_disasm_named" + mut]
+    assert _digest(got) == (want["sha256"], want["bytes"])

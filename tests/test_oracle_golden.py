@@ -48,3 +48,19 @@ ASM = asm_texts()
 def test_oracle_assemble(rec):
     got = outcome(lambda: oasm.assemble(rec["text"]).hex())
     assert same(got, rec["asm"])
+
+
+def test_capability_dependency_graph_golden():
+    """grammar.capability_dependency_graph (host, grammar-constant) == the reference's
+    DependencyReport for both pinned grammars (tests/golden/boundary.json.gz)."""
+    import gzip
+    import json
+    from pathlib import Path
+    from paper_2305_09493_b200 import capability_dependency_graph, load_pinned
+    with gzip.open(Path(__file__).parent / "golden" / "boundary.json.gz", "rt", encoding="utf-8") as fh:
+        want = json.load(fh)["dependency"]
+    for version, rec in want.items():
+        rep = capability_dependency_graph(load_pinned(version))
+        assert list(rep.nodes) == rec["nodes"]
+        assert {k: list(v) for k, v in rep.edges.items()} == rec["edges"]
+        assert [list(c) for c in rep.cycles] == rec["cycles"]

@@ -12,7 +12,9 @@ A mid-size module (n_fn = 640, just above the 2^20-word threshold of the
 grid-wide large-module kernels) is recorded the same way for a quicker test.
 
 usage: python tools/make_config3_fixtures.py [n_fn] [leg ...]
-       legs: ref_validate ref_disasm_numeric oracle_disasm_named
+       legs: ref_validate ref_disasm_numeric oracle_disasm_named (default), and the same
+       with a _mut suffix for the mutated module (mutate(): duplicate result ids and
+       unknown opcodes)
 """
 
 from __future__ import annotations
@@ -26,7 +28,27 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = ROOT / "tests" / "golden"
-LEGS = ("ref_validate", "ref_disasm_numeric", "oracle_disasm_named")
+LEGS = ("ref_validate", "ref_disasm_numeric", "oracle_disasm_named",
+        "ref_validate_mut", "ref_disasm_numeric_mut", "oracle_disasm_named_mut")
+
+
+def mutate(m: bytes) -> bytes:
+    """Seeded mutations of the config-3 module that keep every word count: some
+    OpIAdd results re-define the previous OpIAdd's result (DuplicateResultId), some
+    opcodes become unknown (UnknownOpcode; OpUnknown(N) in the disassembly)."""
+    import numpy as np
+    w = np.frombuffer(m, dtype="<u4").copy()
+    pos, starts = 5, []
+    while pos < len(w):
+        starts.append(pos)
+        pos += int(w[pos] >> 16)
+    starts = np.array(starts)
+    iadd = starts[w[starts] == ((5 << 16) | 128)]
+    for k in range(1, len(iadd), 997):
+        w[iadd[k] + 2] = w[iadd[k - 1] + 2]
+    for k in range(5, len(iadd), 1499):
+        w[iadd[k]] = (5 << 16) | 0xFFF0
+    return w.tobytes()
 
 
 def _digest(text: str) -> dict:
@@ -39,6 +61,9 @@ def run_leg(n_fn: int, leg: str) -> dict:
     sys.path.insert(0, str(ROOT))
     from synth.huge import build_huge
     m = build_huge(n_fn)
+    if leg.endswith("_mut"):
+        m = mutate(m)
+        leg = leg[:-4]
     t0 = time.time()
     if leg.startswith("ref_"):
         sys.path.insert(0, "/root/reference/pkg/src")
@@ -62,7 +87,7 @@ def main():
         print(json.dumps(run_leg(int(args[1]), args[2])), flush=True)
         return
     n_fn = int(args[0]) if args else 55000
-    legs = args[1:] or list(LEGS)
+    legs = args[1:] or list(LEGS[:3])
     out = GOLDEN / f"config3_{n_fn}.json"
     res = json.loads(out.read_text()) if out.exists() else {}
     res["n_fn"] = n_fn
