@@ -233,8 +233,8 @@ int skg_pack_strings(const uint8_t* bytes, const int64_t* off, const int64_t* le
                      uint32_t n_str, uint64_t n_words, uint32_t* out, int32_t* bad, void* stream);
 
 /* encode_context_dependent_literal for a batch (reference codec.py:132-168).
- * width[k]: bit width, -1 for None; flags[k]: 1 signed, 2 floating, 4 negative
- * integer, 8 integer magnitude >= 2^64; val[k]: |integer| or the IEEE-754
+ * width[k]: bit width; flags[k]: 1 signed, 2 floating, 4 negative integer, 8
+ * integer magnitude >= 2^64, 16 width is None (unresolved); val[k]: |integer| or the IEEE-754
  * double bits of the float.  Output words[2k], words[2k+1] (nwords[k] of them)
  * and status[k]: 0 ok, 1 unresolved width, 2 unsupported width, 3 unsupported
  * float width, 4 OverflowError (e format), 5 OverflowError (f format), 6 / 7 the

@@ -6,7 +6,7 @@ from .asm import (Assembler, SymbolTable, TextInstruction, Token, assemble_batch
 from .codec import (ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_module,
                     encode_context_dependent_literal, encode_context_dependent_literals, encode_header,
                     encode_instruction, encode_module, encode_modules, encode_string_literal,
-                    encode_string_literals)
+                    encode_string_literals, serialize_modules)
 from .disasm import (Disassembler, DisassemblerOptions, RenderContext, disassemble_batch,
                      disassemble_module, format_instruction)
 from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,

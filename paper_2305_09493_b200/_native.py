@@ -521,6 +521,8 @@ def _dev(arr, dtype):
     a = np.ascontiguousarray(arr, dtype=dtype)
     if a.size == 0:
         a = np.zeros(1, dtype=dtype)
+    elif not a.flags.writeable:
+        a = a.copy()
     return torch.from_numpy(a).to("cuda")
 
 

@@ -163,7 +163,7 @@ def encode_string_literal(text: str) -> list[int]:
     return _raise_or(encode_string_literals([text])[0])
 
 
-_LIT_SIGNED, _LIT_FLOAT, _LIT_NEG, _LIT_BIG = 1, 2, 4, 8
+_LIT_SIGNED, _LIT_FLOAT, _LIT_NEG, _LIT_BIG, _LIT_NONE = 1, 2, 4, 8, 16
 
 
 def encode_context_dependent_literals(items):
@@ -171,13 +171,14 @@ def encode_context_dependent_literals(items):
     -> list[list[int] | exception]."""
     widths, flags, vals, conv = [], [], [], []
     for value, bit_width, signed, floating in items:
-        w = -1 if bit_width is None else _i64(bit_width)
-        widths.append(w if w != _I64_MIN else 0)
-        f = (_LIT_SIGNED if signed else 0) | (_LIT_FLOAT if floating else 0)
+        w = 0 if bit_width is None else _i64(bit_width)
+        widths.append(w if w != _I64_MIN else 0)          # (out of int64: unsupported, as 0)
+        f = (_LIT_SIGNED if signed else 0) | (_LIT_FLOAT if floating else 0) | \
+            (_LIT_NONE if bit_width is None else 0)
         v, err, shown = 0, None, None
         try:                           # argument conversion; any failure surfaces only if
             if floating:               # the device accepts the width first (codec.py order)
-                if isinstance(value, bool) or not isinstance(value, (int, float)):
+                if not isinstance(value, (int, float)):
                     raise struct.error("required argument is not a float")
                 try:
                     v = struct.unpack("<Q", struct.pack("<d", float(value)))[0]
@@ -241,3 +242,25 @@ def decode_header(words) -> ModuleHeader:
 def literal_word_count(bit_width: int) -> int:
     """codec.py:188-189."""
     return 2 if bit_width == 64 else 1
+
+
+def serialize_modules(scopes):
+    """Batch ModuleScope.serialize (builder.py:187-224) -> list[bytes | exception].
+
+    The builder objects stay the caller's (host) structure: each scope's
+    instruction stream in logical-layout order, its structure / reference checks
+    (StructureError / SerializationError) and its header (bound recomputed) come
+    from the builder as in the reference; the words of every module -- header
+    and instruction encoding with the codec.py range checks -- are produced by
+    ONE skg_encode_modules launch for the whole batch."""
+    out, work = [None] * len(scopes), []
+    for k, scope in enumerate(scopes):
+        try:
+            stream = scope.instruction_stream()
+            scope._check_references(stream)
+            work.append((k, scope.header(), [inst.raw() for inst in stream]))
+        except Exception as exc:  # noqa: BLE001 - the builder's own errors, per module
+            out[k] = exc
+    for (k, _, _), res in zip(work, encode_modules([(h, insts) for _, h, insts in work])):
+        out[k] = res
+    return out

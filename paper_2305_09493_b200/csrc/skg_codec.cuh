@@ -181,9 +181,9 @@ enum : int32_t {
   LIT_OK = 0, LIT_UNRESOLVED = 1, LIT_WIDTH = 2, LIT_FWIDTH = 3, LIT_OVF_E = 4, LIT_OVF_F = 5,
   LIT_FIT_SIGNED = 6, LIT_FIT_UNSIGNED = 7
 };
-enum : uint32_t { LITF_SIGNED = 1, LITF_FLOAT = 2, LITF_NEG = 4, LITF_BIG = 8 };
+enum : uint32_t { LITF_SIGNED = 1, LITF_FLOAT = 2, LITF_NEG = 4, LITF_BIG = 8, LITF_NONE = 16 };
 
-// literal k: width[k] (-1 = None), flags[k], val[k] = |int value| (u64; LITF_NEG / LITF_BIG
+// literal k: width[k] (LITF_NONE in flags[k] = None), flags[k], val[k] = |int value| (u64; LITF_NEG / LITF_BIG
 // for the sign / a magnitude of 2^64 or more) or the IEEE double bits (LITF_FLOAT)
 __global__ void ctx_literals_kernel(const int64_t* __restrict__ width, const uint32_t* __restrict__ flags,
                                     const uint64_t* __restrict__ val, uint32_t n, uint32_t* __restrict__ words,
@@ -193,7 +193,7 @@ __global__ void ctx_literals_kernel(const int64_t* __restrict__ width, const uin
     const uint32_t f = flags[k];
     uint32_t lo = 0, hi = 0;
     int32_t nw = 0, st = LIT_OK;
-    if (w < 0) st = LIT_UNRESOLVED;                                          // codec.py:140-141
+    if (f & LITF_NONE) st = LIT_UNRESOLVED;                                  // codec.py:140-141
     else if (!(w == 8 || w == 16 || w == 32 || w == 64)) st = LIT_WIDTH;     // :142-143
     else if (f & LITF_FLOAT) {                                               // :144-151
       const uint64_t bits = val[k];

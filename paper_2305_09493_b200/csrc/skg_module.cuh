@@ -498,9 +498,12 @@ __device__ inline void move_to_global(Mod& m, uint8_t* gslot) {
 // Returns false if even the global slot cannot hold the module.
 __device__ __noinline__ bool place_tables(Mod& m, bool direct, bool& in_smem, uint8_t* gslot,
                                     uint64_t gslot_bytes, uint32_t slab_bytes, size_t work_min) {
+  const size_t greg = gslot_bytes - spill_bytes(m.I);
+  // the slot is sized for hash mode (worst_bytes); a direct table for a bound above the
+  // hash capacity (small modules: bound <= 2W + 64) may not fit, hash mode always does
+  if (direct && tables_need(m, true, m.bound, work_min) > greg) direct = false;
   const uint32_t SC = direct ? m.bound : hash_capacity(m.W);
   const size_t need = tables_need(m, direct, SC, work_min);
-  const size_t greg = gslot_bytes - spill_bytes(m.I);
   if (in_smem && need > slab_bytes) {
     if (need > greg) return false;
     move_to_global(m, gslot);

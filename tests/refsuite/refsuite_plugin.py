@@ -18,11 +18,12 @@ sys.path.insert(0, ROOT)
 
 import spirvkit as R  # noqa: E402  (the reference: builder / grammar / codegen for inputs)
 from spirvkit import asm as R_asm, codec as R_codec, disasm as R_disasm, errors as R_errors  # noqa: E402
-from spirvkit import grammar as R_grammar, validate as R_validate  # noqa: E402
+from spirvkit import cli as R_cli, grammar as R_grammar, validate as R_validate  # noqa: E402
 
 import paper_2305_09493_b200 as G  # noqa: E402
 from paper_2305_09493_b200 import asm as G_asm, codec as G_codec, disasm as G_disasm  # noqa: E402
-from paper_2305_09493_b200 import errors as G_errors, grammar as G_grammar, validate as G_validate  # noqa: E402
+from paper_2305_09493_b200 import cli as G_cli, errors as G_errors, grammar as G_grammar  # noqa: E402
+from paper_2305_09493_b200 import validate as G_validate  # noqa: E402
 
 BINDINGS = {
     R_codec: (G_codec, ["decode_module", "encode_header", "encode_instruction", "encode_string_literal",
@@ -32,6 +33,7 @@ BINDINGS = {
     R_validate: (G_validate, ["validate_module", "check_capability_closure", "diagnostics_text", "Diagnostic"]),
     R_asm: (G_asm, ["Assembler", "assemble_module", "tokenize_line", "TextInstruction", "Token", "SymbolTable"]),
     R_grammar: (G_grammar, ["capability_dependency_graph", "DependencyReport"]),
+    R_cli: (G_cli, ["run_cli", "build_parser"]),
 }
 ERRORS = ["SpirvKitError", "CodecError", "CorruptStreamError", "TruncatedStreamError", "NotSpirvError",
           "AssemblyError", "AsmDiagnostic", "StructureError", "SerializationError", "NotFoundError"]

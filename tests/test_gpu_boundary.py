@@ -182,3 +182,29 @@ def test_format_instruction_with_context(sk):
         if not check(got, c["out"]):
             bad.append((c, got))
     assert not bad, bad[:5]
+
+
+def test_serialize_modules_batch(sk):
+    """Batch builder serialization: modules built with the reference's
+    builder (inputs only; oracle/_ref) serialize through skg_encode_modules to the bytes
+    the builder's own ModuleScope.to_bytes writes."""
+    import sys
+    from pathlib import Path
+    ref = Path(__file__).resolve().parents[1] / "oracle" / "_ref"
+    if not (ref / "spirvkit").is_dir():
+        pytest.skip("reference builder not installed (oracle/_ref)")
+    sys.path.insert(0, str(ref))
+    sys.path.insert(0, str(ref / "ref_tests"))
+    try:
+        import corpus
+    except ImportError:
+        pytest.skip("reference corpus not staged")
+    scopes = list(corpus.crafted_modules().values()) + [corpus.random_module(s) for s in range(40)]
+    got = sk.serialize_modules(scopes)
+    for scope, g in zip(scopes, got):
+        try:
+            want = scope.to_bytes()
+        except Exception as exc:  # noqa: BLE001
+            assert isinstance(g, BaseException) and type(g).__name__ == type(exc).__name__ and str(g) == str(exc)
+            continue
+        assert g == want

@@ -415,3 +415,30 @@ def test_large_paths_edge_cases(sk, monkeypatch):
         gd = outcome(lambda x: [(i.opcode, tuple(i.operands)) for i in sk.decode_module(x)[1]], m)
         wd = outcome(lambda x: [(op, tuple(o)) for op, o in core.decode_module(x)[1]], m)
         assert gd == wd
+
+
+def test_small_module_with_large_bound(sk):
+    """A small module whose header bound exceeds the hash capacity its per-warp slot is
+    sized for (bound up to 2W + 64 still takes the direct id tables) falls back to the
+    hash tables instead of failing (regression: "module exceeds the per-warp scratch
+    slot" for format_instruction contexts)."""
+    import struct as st
+    from oracle import disasm as odis, validate as oval
+    done = 0
+    for rec in CASES:
+        data = rec["bytes"]
+        if "ok" not in rec["disasm"]["default"] or len(data) < 24 or len(data) > 400:
+            continue
+        w = list(st.unpack(f"<{len(data) // 4}I", data))
+        if w[0] != 0x07230203:
+            continue
+        for bound in (2 * len(w) + 40, 2 * len(w) + 64):
+            w[3] = bound
+            m = st.pack(f"<{len(w)}I", *w)
+            assert sk.disassemble_batch([m])[0] == odis.disassemble(m)
+            d = sk.validate_batch([m])[0]
+            assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(m)]
+        done += 1
+        if done >= 25:
+            break
+    assert done >= 10

@@ -1,5 +1,5 @@
 """Conformance: the reference's own test files (pkg/tests/test_{codec,disasm,asm,
-validate,acceptance}.py, copied to oracle/_ref/ref_tests by __graft_entry__.build)
+validate,acceptance,cli}.py, copied to oracle/_ref/ref_tests by __graft_entry__.build)
 run with every hot-path name bound to this package (tests/refsuite/refsuite_plugin.py):
 decode / encode / disassemble / format / validate / tokenize / assemble all go
 through the CUDA kernels; the reference builder only constructs inputs.
@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parents[1]
 SUITE = ROOT / "oracle" / "_ref" / "ref_tests"
-FILES = ["test_codec.py", "test_disasm.py", "test_asm.py", "test_validate.py", "test_acceptance.py"]
+FILES = ["test_codec.py", "test_disasm.py", "test_asm.py", "test_validate.py", "test_acceptance.py", "test_cli.py"]
 FAIL_BY_DESIGN = {"test_acceptance.py::test_criterion_1_generator_counts",
                   "test_acceptance.py::test_criterion_5_capability_cycles"}
 
