@@ -400,34 +400,51 @@ def run_config5(args, rank, world, local_rank):
     max_n = max(b.n for _, b in chunks)
     text = torch.empty(4 * max_bytes + 4096, dtype=torch.uint8, device="cuda")
     out = torch.empty(max_bytes + 64 * max_n + 4096, dtype=torch.uint8, device="cuda")
+    vtext = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")   # clean batch: no diagnostics
+
+    def asm_plan(b, span, aws):
+        mx = int(span[1::2].max().item())
+        tb = _native.DeviceBatch(text, span[0::2], span[1::2], (mx + 3) // 4, 0)
+        tb.n = b.n
+        ap = _native.AsmPlan(tb, out_cap=16, stride=2, ws=aws)
+        ap.out, ap.cap = out, out.numel()
+        return ap
+
     plans, ws, aws = [], None, None
     for c0, b in chunks:
+        # fused: decode -> validate -> disassemble in one pass (skg_disasm_validate), then asm
+        fp = _native.DisasmPlan(b, opts, kind="pipeline", text_cap=16, ws=ws)
+        ws = fp.ws
+        fp.text, fp.cap, fp.vtext, fp.vcap = text, text.numel(), vtext, vtext.numel()
+        fp.launch()
+        finfo = fp.check()
+        assert not finfo["overflow"] and finfo["errors"] == 0 and finfo["vtext_bytes"] == 0, finfo
+        apf = asm_plan(b, fp.span, aws)
+        aws = apf.ws
+        apf.launch()
+        ainfo = apf.check()
+        st_ok = bool((fp.status[: b.n] == 0).all() and (fp.vstatus[: b.n] == 0).all()
+                     and (apf.status[: b.n] == 0).all())
+        assert st_ok and not ainfo["overflow"], (finfo, ainfo)
+        # unfused, for comparison: skg_validate + skg_disasm + skg_asm
         vp = _native.DisasmPlan(b, 0, kind="validate", text_cap=1 << 20, ws=ws)
-        ws = vp.ws
-        vinfo = vp.fit()
+        vp.text, vp.cap = vtext, vtext.numel()
         dp = _native.DisasmPlan(b, opts, text_cap=16, ws=ws)
         dp.text, dp.cap = text, text.numel()
         dp.launch()
-        dinfo = dp.check()
-        assert not dinfo["overflow"] and dinfo["errors"] == 0, dinfo
-        mx = int(dp.span[1::2].max().item())
-        tb = _native.DeviceBatch(text, dp.span[0::2], dp.span[1::2], (mx + 3) // 4, 0)
-        tb.n = b.n
-        ap = _native.AsmPlan(tb, out_cap=16, stride=2, ws=aws)
-        aws = ap.ws
-        ap.out, ap.cap = out, out.numel()
-        ap.launch()
-        ainfo = ap.check()
-        st_ok = bool((vp.status[: b.n] == 0).all() and (dp.status[: b.n] == 0).all()
-                     and (ap.status[: b.n] == 0).all())
-        assert st_ok and vinfo["text_bytes"] == 0 and not ainfo["overflow"], (vinfo, dinfo, ainfo)
-        plans.append((b, vp, dp, ap))
+        apu = asm_plan(b, dp.span, aws)
+        plans.append((b, fp, apf, vp, dp, apu))
 
     def step():
-        for b, vp, dp, ap in plans:
+        for b, fp, apf, vp, dp, apu in plans:
+            fp.launch()
+            apf.launch()
+
+    def step_unfused():
+        for b, fp, apf, vp, dp, apu in plans:
             vp.launch()
             dp.launch()
-            ap.launch()
+            apu.launch()
 
     for _ in range(args.warmup):
         step()
@@ -449,12 +466,26 @@ def run_config5(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    # parity of the last step (sampled): validation clean, text == oracle, binaries == inputs
+    for _ in range(2):
+        step_unfused()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step_unfused()
+    e1.record()
+    torch.cuda.synchronize()
+    tu = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tu, op=dist.ReduceOp.MAX)
+    ms_unfused = float(tu.item()) / args.steps
+    # parity of the fused step (sampled): validation clean, text == oracle, binaries == inputs
     from oracle import disasm as odis, validate as oval
     checked, text_bytes = 0, 0
-    for ci, (b, vp, dp, ap) in enumerate(plans):
+    for ci, (b, dp, ap, _, _, _) in enumerate(plans):
         dp.launch()               # the arenas are shared: re-run this chunk, then check it
-        text_bytes += int(dp.check()["text_bytes"])
+        info = dp.check()
+        assert info["vtext_bytes"] == 0 and (dp.vstatus[: b.n] == 0).all()
+        text_bytes += int(info["text_bytes"])
         ap.launch()
         torch.cuda.synchronize()
         dspan = dp.span[: 2 * b.n].cpu().numpy().reshape(-1, 2)
@@ -477,7 +508,7 @@ def run_config5(args, rank, world, local_rank):
     if rank != 0:
         return None
     peak, peak_src = peak_hbm()
-    alg = 4 * words + text_bytes + text_bytes + 4 * words + 4 * words   # validate + disasm + asm
+    alg = 4 * words + text_bytes + text_bytes + 4 * words   # fused validate+disasm, then asm
     ach = alg / (ms_step / 1e3) / 1e9
     return {
         "metric": METRIC, "value": total_words / (ms_step / 1e3), "unit": "words/s",
@@ -487,18 +518,21 @@ def run_config5(args, rank, world, local_rank):
         "config": {
             "workload": "configs[4]: full decode/validate/encode pipeline over ONE seeded batch "
                         f"of {args.modules} modules split across {world} GPU(s) by "
-                        "shard.shard_ranges; per rank: skg_validate + skg_disasm + skg_asm over "
-                        f"its shard in device-resident chunks of {args.chunk} modules",
+                        "shard.shard_ranges; per rank, per device-resident chunk of "
+                        f"{args.chunk} modules: the fused decode->validate->disassemble pass "
+                        "(skg_disasm_validate) + skg_asm on its text",
+            "ms_per_step_unfused": ms_unfused,
+            "unfused": "skg_validate + skg_disasm + skg_asm (three reads of every module)",
             "modules_total": args.modules, "modules_rank0": m1 - m0, "words_total": total_words,
             "chunks_rank0": len(chunks), "parity_sampled_rank0": checked,
             "l2": "inputs and text exceed the 126 MB L2; no flush needed",
             "parallelism": f"module-sharded x{world} (no collective on the data path)",
         },
-        "roofline": {"bound": "hbm", "kernel": "pipeline (validate+disasm+asm, unfused)",
+        "roofline": {"bound": "hbm", "kernel": "pipeline (fused validate+disasm, then asm)",
                      "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "peak_source": peak_src, "traffic": None,
                      "algorithmic_bytes_per_step_rank0": alg},
-        "gpu_launches": 3 * 4 * len(chunks) * args.steps,
+        "gpu_launches": 2 * 4 * len(chunks) * args.steps,
         "clocks": clocks.summary(),
     }
 

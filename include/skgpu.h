@@ -99,6 +99,19 @@ int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod
                     skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
                     void* stream, const uint32_t* ref_ids, const uint8_t* ref_text, uint32_t n_refs);
 
+/* Fused decode -> validate -> disassemble: ONE pass over the batch
+ * produces both skg_disasm's outputs (text, text_span, status, errors) and
+ * skg_validate's (vtext, vtext_span, vstatus, verrors) from a single read and a
+ * single decode of every module (shared boundary pass, grammar walk, id tables
+ * and prescan).  Counters: skg_last_counts(workspace) for the text,
+ * skg_last_counts((char*)workspace + 128) for the diagnostics arena. */
+int skg_disasm_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                        const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+                        uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
+                        skg_error* errors, uint32_t err_cap, uint8_t* vtext, uint64_t vtext_cap,
+                        int64_t* vtext_span, int32_t* vstatus, skg_error* verrors, uint32_t verr_cap,
+                        void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Batch structural + capability validation.
  * Replaces: validate_module(bytes) (reference validate.py:73-94).
  * Output: diagnostics_text-formatted lines ("severity code location message\n")

@@ -8,7 +8,7 @@ from .codec import (ModuleHeader, RawInstruction, TypedFloat, TypedInt, decode_m
                     encode_instruction, encode_module, encode_modules, encode_string_literal,
                     encode_string_literals, serialize_modules)
 from .disasm import (Disassembler, DisassemblerOptions, RenderContext, disassemble_batch,
-                     disassemble_module, format_instruction)
+                     disassemble_module, disassemble_validate_batch, format_instruction)
 from .errors import (AsmDiagnostic, AssemblyError, CodecError, CorruptStreamError,
                      GenerationError, GrammarError, GrammarParseError, GrammarSchemaError,
                      IdExhaustedError, NotFoundError, NotSpirvError, ScopeError,

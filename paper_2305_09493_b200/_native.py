@@ -65,6 +65,9 @@ def lib():
     L.skg_disasm_large.restype = I32
     L.skg_disasm_refs.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P, P, P, U32]
     L.skg_disasm_refs.restype = I32
+    L.skg_disasm_validate.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P, P, P, U32,
+                                      P, U64, P]
+    L.skg_disasm_validate.restype = I32
     L.skg_tokenize.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, P]
     L.skg_encode_modules.argtypes = [P, U32, P, P, U64, P, P, U64, P, P, P]
     L.skg_pack_strings.argtypes = [P, P, P, P, U32, U64, P, P, P]
@@ -270,6 +273,58 @@ def _run_text_kernel(kind, batch: DeviceBatch, opts, spec, ext, text_cap=None, e
             continue
         return TextResult(text[:used], span[: 2 * n], status[:n], errs[: nerr * 256])
     raise RuntimeError(f"libskgpu {kind}: output capacity retry failed")
+
+
+VAL_COUNTERS = 128   # byte offset of the fused validator's counters in the workspace
+
+
+def run_pipeline(batch: DeviceBatch, opts, spec=None, ext=None):
+    """skg_disasm_validate: one pass -> (disasm TextResult, validate TextResult)."""
+    torch = _torch()
+    L = lib()
+    th = tables_handle(spec, ext)
+    n = batch.n
+    ws_bytes = int(L.skg_workspace_bytes(n, max(batch.max_words, 1)))
+    ws = _ws.get(ws_bytes)
+    cap, vcap = 6 * batch.total_bytes + 4096, batch.total_bytes + 4096
+    ecap = max(16, min(n, 1 << 16))
+    for _ in range(3):
+        text = torch.empty(max(cap, 16), dtype=torch.uint8, device="cuda")
+        vtext = torch.empty(max(vcap, 16), dtype=torch.uint8, device="cuda")
+        span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
+        vspan = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
+        status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        vstatus = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        errs = torch.empty(ecap * 256, dtype=torch.uint8, device="cuda")
+        verrs = torch.empty(ecap * 256, dtype=torch.uint8, device="cuda")
+        _check(L.skg_disasm_validate(th, batch.data.data_ptr(), batch.off.data_ptr(), batch.len.data_ptr(), n, opts,
+                                     batch.max_words, text.data_ptr(), cap, span.data_ptr(), status.data_ptr(),
+                                     errs.data_ptr(), ecap, vtext.data_ptr(), vcap, vspan.data_ptr(),
+                                     vstatus.data_ptr(), verrs.data_ptr(), ecap, ws.data_ptr(), ws_bytes,
+                                     _stream()), "disasm_validate")
+        nerr, over, used = last_counts(ws)
+        vnerr, vover, vused = last_counts(ws[VAL_COUNTERS:])
+        if over or vover or nerr > ecap or vnerr > ecap:
+            cap, vcap = max(cap, used + 16), max(vcap, vused + 16)
+            ecap = max(ecap, nerr, vnerr)
+            continue
+        return (TextResult(text[:used], span[: 2 * n], status[:n], errs[: nerr * 256]),
+                TextResult(vtext[:vused], vspan[: 2 * n], vstatus[:n], verrs[: vnerr * 256]))
+    raise RuntimeError("libskgpu disasm_validate: output capacity retry failed")
+
+
+def run_texts_pipeline(batch: DeviceBatch, opts=0, spec=None, ext=None):
+    """Fused disassembly + validation of a device batch -> (texts, diagnostics texts), each
+    a list of (bytes | exception).  Batches with large modules (grid-wide kernels) or
+    beyond the one-launch workspace budget take the two separate batch paths."""
+    n = batch.n
+    if n == 0:
+        return [], []
+    need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
+    if batch.max_words >= LARGE_MODULE_WORDS or (n > 1 and need > WS_BUDGET):
+        return run_texts("disasm", batch, opts, spec, ext), run_texts("validate", batch, 0, spec)
+    d, v = run_pipeline(batch, opts, spec, ext)
+    return fetch_texts(d, n), fetch_texts(v, n)
 
 
 def run_disasm(batch, opts, spec=None, ext=None, **kw):
@@ -665,11 +720,24 @@ class DisasmPlan:
         self.status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         self.ecap = max(16, min(n, 1 << 16))
         self.errs = torch.empty(self.ecap * 256, dtype=torch.uint8, device="cuda")
+        if kind == "pipeline":   # fused validation outputs (skg_disasm_validate)
+            self.vcap = batch.total_bytes + 4096
+            self.vtext = torch.empty(self.vcap, dtype=torch.uint8, device="cuda")
+            self.vspan = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
+            self.vstatus = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+            self.verrs = torch.empty(self.ecap * 256, dtype=torch.uint8, device="cuda")
 
     def launch(self, stream=None):
         b = self.batch
         s = stream if stream is not None else _stream()
-        if self.kind == "disasm":
+        if self.kind == "pipeline":
+            rc = lib().skg_disasm_validate(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n,
+                                           self.opts, b.max_words, self.text.data_ptr(), self.cap,
+                                           self.span.data_ptr(), self.status.data_ptr(), self.errs.data_ptr(),
+                                           self.ecap, self.vtext.data_ptr(), self.vcap, self.vspan.data_ptr(),
+                                           self.vstatus.data_ptr(), self.verrs.data_ptr(), self.ecap,
+                                           self.ws.data_ptr(), self.ws_bytes, s)
+        elif self.kind == "disasm":
             rc = lib().skg_disasm(self.th, b.data.data_ptr(), b.off.data_ptr(), b.len.data_ptr(), b.n,
                                   self.opts, b.max_words, self.text.data_ptr(), self.cap,
                                   self.span.data_ptr(), self.status.data_ptr(), self.errs.data_ptr(),
@@ -683,7 +751,12 @@ class DisasmPlan:
 
     def check(self):
         nerr, over, used = last_counts(self.ws)
-        return {"errors": nerr, "overflow": over, "text_bytes": used}
+        info = {"errors": nerr, "overflow": over, "text_bytes": used}
+        if self.kind == "pipeline":
+            vnerr, vover, vused = last_counts(self.ws[VAL_COUNTERS:])
+            info.update(verrors=vnerr, voverflow=vover, vtext_bytes=vused)
+            info["overflow"] = over or vover
+        return info
 
     def grow(self, need):
         torch = _torch()

@@ -17,8 +17,8 @@ struct ValidateArgs;
 struct DecodeArgs;
 }
 
-#include "skg_disasm.cu"
 #include "skg_validate.cu"
+#include "skg_disasm.cu"
 #include "skg_decode.cu"
 #include "skg_asm.cu"
 
@@ -120,6 +120,10 @@ Geom fit_geom(uint32_t blocks, uint32_t warps, uint32_t n_mod, bool shrink_warps
 }
 Geom dis_geom(uint32_t n_mod) { return fit_geom(dis_blocks(), (uint32_t)kDisWarps, n_mod, true); }
 Geom val_geom(uint32_t n_mod) { return fit_geom(dis_blocks(), (uint32_t)kDisWarps, n_mod, true); }
+
+// the fused validator's counters (error records, overflow, cursor) inside the
+// 256-byte counter block, after the disassembler's
+constexpr uint32_t kValCounters = 128;
 
 WsLayout ws_layout(uint32_t n_mod, uint32_t max_words) {
   WsLayout l;
@@ -231,12 +235,18 @@ int skg_disasm(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
                          errors, err_cap, workspace, workspace_bytes, stream, nullptr, nullptr, 0);
 }
 
-int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
-                    const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
-                    uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
-                    skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
-                    void* stream, const uint32_t* ref_ids, const uint8_t* ref_text, uint32_t n_refs) {
+namespace {
+struct ValOut {   // the fused validator's outputs (skg_disasm_validate)
+  uint8_t* text; uint64_t cap; int64_t* span; int32_t* status; skg_error* errors; uint32_t err_cap;
+};
+
+int disasm_launch(const skg_tables* t, const uint8_t* data, const int64_t* mod_off, const int64_t* mod_len,
+                  uint32_t n_mod, uint32_t opts, uint32_t max_words, uint8_t* text, uint64_t text_cap,
+                  int64_t* text_span, int32_t* status, skg_error* errors, uint32_t err_cap, void* workspace,
+                  uint64_t workspace_bytes, void* stream, const uint32_t* ref_ids, const uint8_t* ref_text,
+                  uint32_t n_refs, const ValOut* vo) {
   if (!t || !workspace || (n_refs && (!ref_ids || !ref_text))) return -1;
+  if (vo && (!vo->span || !vo->status || !vo->text)) return -1;
   WsLayout l = ws_layout(n_mod, max_words);
   if (workspace_bytes < l.total) return -3;
   cudaStream_t s = (cudaStream_t)stream;
@@ -254,6 +264,11 @@ int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod
   a.gslot_bytes = l.slot;
   a.smem_slab = kDisSlab;
   a.ovr = ref_ids; a.ovr_text = ref_text; a.n_ovr = n_refs;
+  a.vtext = vo ? vo->text : nullptr; a.vtext_cap = vo ? vo->cap : 0;
+  a.vspan = vo ? vo->span : nullptr; a.vstatus = vo ? vo->status : nullptr;
+  a.vctr = reinterpret_cast<uint32_t*>(ws + l.counters + kValCounters);
+  a.verrs = reinterpret_cast<skg::ErrRec*>(vo ? vo->errors : nullptr);
+  a.verr_cap = vo ? vo->err_cap : 0;
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
   a.stage_bytes = kDisStage;
@@ -264,14 +279,40 @@ int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod
   static uint64_t attr = 0;
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+    cudaFuncSetAttribute(skg::pipeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
   }
   static uint64_t carve = 0;
   if (first_on_device(carve)) {   // smallest shared-memory carveout that fits: the rest is L1 for the scratch
     const int pct = env_int("SKG_CARVEOUT", -2);
-    if (pct != -2) cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    if (pct != -2) {
+      cudaFuncSetAttribute(skg::disasm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaFuncSetAttribute(skg::pipeline_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    }
   }
-  skg::disasm_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
+  if (vo) skg::pipeline_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
+  else skg::disasm_kernel<<<g.blocks, 32 * g.warps, smem, s>>>(a);
   return check(cudaGetLastError());
+}
+}  // namespace
+
+int skg_disasm_refs(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                    const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+                    uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
+                    skg_error* errors, uint32_t err_cap, void* workspace, uint64_t workspace_bytes,
+                    void* stream, const uint32_t* ref_ids, const uint8_t* ref_text, uint32_t n_refs) {
+  return disasm_launch(t, data, mod_off, mod_len, n_mod, opts, max_words, text, text_cap, text_span, status, errors,
+                       err_cap, workspace, workspace_bytes, stream, ref_ids, ref_text, n_refs, nullptr);
+}
+
+int skg_disasm_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,
+                        const int64_t* mod_len, uint32_t n_mod, uint32_t opts, uint32_t max_words,
+                        uint8_t* text, uint64_t text_cap, int64_t* text_span, int32_t* status,
+                        skg_error* errors, uint32_t err_cap, uint8_t* vtext, uint64_t vtext_cap,
+                        int64_t* vtext_span, int32_t* vstatus, skg_error* verrors, uint32_t verr_cap,
+                        void* workspace, uint64_t workspace_bytes, void* stream) {
+  const ValOut vo{vtext, vtext_cap, vtext_span, vstatus, verrors, verr_cap};
+  return disasm_launch(t, data, mod_off, mod_len, n_mod, opts, max_words, text, text_cap, text_span, status, errors,
+                       err_cap, workspace, workspace_bytes, stream, nullptr, nullptr, 0, &vo);
 }
 
 int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_off,

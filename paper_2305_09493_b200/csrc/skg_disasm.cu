@@ -49,6 +49,14 @@ struct DisasmArgs {
   const uint32_t* ovr;        // explicit refs (Mod::ovr), n_ovr entries; nullptr = none
   const uint8_t* ovr_text;
   uint32_t n_ovr;
+  // fused validation (pipeline_kernel): the validate_kernel outputs
+  uint8_t* vtext;
+  uint64_t vtext_cap;
+  int64_t* vspan;
+  int32_t* vstatus;
+  uint32_t* vctr;             // [1] error records, [2] overflow, [4..5] cursor
+  ErrRec* verrs;
+  uint32_t verr_cap;
 };
 
 // -- sanitized friendly names (disasm.py:82-86) --------------------------------
@@ -1235,8 +1243,13 @@ __device__ unsigned long long g_dis_phase[16];
 // One module per warp; all warps of the CTA run the same phase at the same
 // time (CTA barrier between phases), so the instruction working set of the SM
 // is one phase rather than the whole program.
+// VAL (pipeline_kernel): the same pass also validates the module (validate_one's V2/V3
+// on the tables, prescan and decode this pass already built), writing the validator's
+// outputs next to the text: one read and one decode of every module for both results.
+template <bool VAL>
 __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
-                                        uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw, Mod& m) {
+                                        uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw, Mod& m,
+                                        uint64_t* veff) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   DPHASE_START();
@@ -1246,9 +1259,14 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
   uint64_t total = 0;
   uint32_t width = 0;
   bool in_smem = false, direct = false, names_mode = false;
+  int32_t vstatus = status, decode_status = ST_OK;   // VAL: the validator's status / decode error
+  uint64_t vtotal = 0;
+  uint32_t vfast = 0;
+  Shape sh{};
+  int64_t nbytes = 0;
   // -- P0: load + boundary (A1, A2)
   if (live) {
-    const int64_t nbytes = a.mod_len[t];
+    nbytes = a.mod_len[t];
     const uint8_t* src = a.data + a.mod_off[t];
     const uint32_t W = (nbytes >= 0 && nbytes % 4 == 0) ? (uint32_t)(nbytes / 4) : 0;
     in_smem = head_bytes(W) <= a.smem_slab;
@@ -1259,7 +1277,13 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
       layout_head(m, in_smem ? slab : gslot, W);
       m.ovr = a.ovr; m.ovr_text = a.ovr_text; m.n_ovr = a.n_ovr;
       status = load_and_split(m, src, (uint64_t)nbytes, &es, (int32_t)t);
+      if (VAL) {
+        if (status == ST_TRUNCATED || status == ST_NOTSPIRV || status == ST_CORRUPT) decode_status = status;
+        else vstatus = status;
+      }
     }
+  } else if (VAL) {
+    vstatus = ST_INTERNAL;
   }
   DPHASE_MARK(0);
   group_sync(gid, gw);
@@ -1269,6 +1293,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     direct = m.bound <= 2 * m.W + 64;
     if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, RENDER_MIN)) {
       status = ST_INTERNAL;
+      if (VAL) vstatus = ST_INTERNAL;
       report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
     } else {
       init_tables(m);
@@ -1288,6 +1313,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
       direct = false;
       if (!place_tables(m, direct, in_smem, gslot, a.gslot_bytes, a.smem_slab, RENDER_MIN)) {
         status = ST_INTERNAL;
+        if (VAL) vstatus = ST_INTERNAL;
         report_internal(es, (int32_t)t, "internal: module exceeds the per-warp scratch slot");
       } else {
         init_tables(m);
@@ -1343,6 +1369,30 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
   if (status == ST_OK && names_mode) resolve_names(m, T);
   DPHASE_MARK(4);
   group_sync(gid, gw);
+  // -- P5 (VAL): the validator's shape, capabilities, diagnostic sizes and offsets
+  //    (validate_one V2); m.ia is free once the friendly names are resolved
+  if (VAL && live && vstatus == ST_OK && decode_status == ST_OK) {
+    for (int k = 0; k < MAX_CAPW; ++k) veff[k] = 0;
+    __syncwarp();
+    uint64_t eff[MAX_CAPW];
+    for (int k = 0; k < MAX_CAPW; ++k) eff[k] = 0;
+    ErrSink ves{a.verrs, a.vctr + 1, a.verr_cap};
+    // the classification walk's status is the validator's first walk; BoundTooSmall
+    // needs an id operand at/above the bound (word-parallel check of the id words)
+    bool big = false;
+    if (status != ST_INTERNAL) {
+      for (uint32_t w = 5 + lane; w < m.W; w += 32) {
+        const uint32_t c = wk_code(m.wk[w]);
+        big |= (c == C_REF || c == C_RES || c == C_DECID) && m.w[w] >= m.bound;
+      }
+    }
+    big = __any_sync(FULL, big);
+    vfast = VF_IERR_KNOWN | (big ? 0u : VF_NO_BIG_IDS);
+    vtotal = val_sizes(m, T, eff, sh, vstatus, ves, (int32_t)t, vfast);
+    if (lane == 0) for (int k = 0; k < MAX_CAPW; ++k) veff[k] = eff[k];
+    __syncwarp();
+  }
+  if (VAL) group_sync(gid, gw);   // a phase of its own: the SM runs one phase's code at a time
   // -- P5: result refs, width, sections, text size (A17-A19)
   if (status == ST_OK) {
     width = result_refs(m, T);
@@ -1364,6 +1414,42 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     }
     if (status == ST_OK && total > 0 && fits) text_write(m, T, a.opts, width, a.text + off, stage, a.stage_bytes);
   }
+  if (VAL) group_sync(gid, gw);
+  if (VAL && live) {
+    {   // validate_one V3: the diagnostics, or the decode error as the only one
+      uint64_t vt = vstatus == ST_OK ? vtotal : 0;
+      ErrRec tmp;
+      const char* code = nullptr;
+      if (vstatus == ST_OK && decode_status != ST_OK) {
+        code = decode_code(decode_status);
+        CountSink cs;
+        diag_head(cs, true, code, NONE32);
+        ErrWriter ew{&tmp};
+        put_decode_msg(ew, m, nbytes, decode_status);
+        tmp.len = ew.n;
+        vt = cs.n + (uint32_t)tmp.len + 1;
+      }
+      bool vfits;
+      const uint64_t voff = alloc_text(a.vctr, vt, a.vtext_cap, vfits);
+      if (lane == 0) {
+        a.vspan[2 * t] = (int64_t)voff;
+        a.vspan[2 * t + 1] = (int64_t)vt;
+        a.vstatus[t] = vstatus;
+      }
+      if (vstatus == ST_OK && vfits && vt > 0) {
+        if (code) {
+          if (lane == 0) {
+            MemSink ms(a.vtext + voff);
+            diag_head(ms, true, code, NONE32);
+            ms.putn((const uint8_t*)tmp.msg, (uint32_t)tmp.len);
+            ms.put('\n');
+          }
+        } else {
+          val_write(a.vtext + voff, m, T, veff, sh, vfast);
+        }
+      }
+    }
+  }
   DPHASE_MARK(6);
   group_sync(gid, gw);
 }
@@ -1372,7 +1458,20 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
 #define SKG_DIS_MAXT 1024
 #define SKG_DIS_MINB 1
 #endif
+template <bool VAL>
+__device__ __forceinline__ void disasm_persistent(const DisasmArgs& a);
+
 __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(const __grid_constant__ DisasmArgs a) {
+  disasm_persistent<false>(a);
+}
+
+// decode -> validate -> disassemble in one pass (skg_disasm_validate)
+__global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) pipeline_kernel(const __grid_constant__ DisasmArgs a) {
+  disasm_persistent<true>(a);
+}
+
+template <bool VAL>
+__device__ __forceinline__ void disasm_persistent(const DisasmArgs& a) {
   __shared__ DisasmArgs s_args;   // one copy per CTA: field reads are shared loads
   if (threadIdx.x == 0) s_args = a;
   __syncthreads();
@@ -1382,6 +1481,7 @@ __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(cons
   // take 32 x sizeof(Mod) of L1 per warp as local memory); all lanes write the
   // same values into it
   __shared__ Mod s_mod[32];
+  __shared__ uint64_t s_eff[VAL ? 32 : 1][MAX_CAPW];   // VAL: effective capabilities per warp
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;                 // warps per barrier group
@@ -1397,7 +1497,8 @@ __global__ void __launch_bounds__(SKG_DIS_MAXT, SKG_DIS_MINB) disasm_kernel(cons
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    disasm_one(s_args, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block]);
+    disasm_one<VAL>(s_args, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block],
+                    VAL ? s_eff[warp_in_block] : nullptr);
   }
 }
 

@@ -65,6 +65,8 @@ struct Tables {
   __device__ __forceinline__ uint32_t special(uint32_t i) const { return (iflags(i) >> 8) & 0xFF; }
   __device__ __forceinline__ uint32_t section(uint32_t i) const { return (iflags(i) >> 16) & 0xFF; }
   __device__ __forceinline__ uint32_t ireq(uint32_t i) const { return __ldg(irec(i) + 4); }
+  // some operand kind of the instruction can carry a capability requirement (tables.py)
+  __device__ __forceinline__ bool ireqops(uint32_t i) const { return __ldg(irec(i) + 6) & 1; }
 
   // -- kinds -----------------------------------------------------------------
   __device__ __forceinline__ const uint32_t* krec(uint32_t k) const { return kind + 8 * k; }

@@ -103,10 +103,14 @@ struct ReqVis : NullVis {
   }
 };
 
+// inst_diags shortcuts (fused pass): the walk status is already in m.ierr (the
+// disassembler's classification walk), no id operand reaches the header bound
+enum : uint32_t { VF_IERR_KNOWN = 1, VF_NO_BIG_IDS = 2 };
+
 // all located diagnostics of instruction i; returns the walk status
 template <class S>
 __device__ __noinline__ WalkErr inst_diags(S& s, const Mod& m, const Tables& T, uint32_t i,
-                                     const uint64_t* eff) {
+                                     const uint64_t* eff, uint32_t fast = 0) {
   const uint32_t d = m.idef[i];
   const uint32_t* ops = inst_ops(m, i);
   const uint32_t n = inst_nops(m, i);
@@ -128,12 +132,15 @@ __device__ __noinline__ WalkErr inst_diags(S& s, const Mod& m, const Tables& T, 
   }
   Resolver res{&m, &T};
   NullVis nv;
-  WalkErr e = walk(T, d, ops, n, nv, res);
+  WalkErr e{};
+  if (!(fast & VF_IERR_KNOWN) || m.ierr[i] != W_OK) e = walk(T, d, ops, n, nv, res);
   if (e.code != W_OK && !werr_is_codec(e.code)) return e;
   if (e.code == W_OK) {
-    BoundVis<S> bv;
-    bv.s = &s; bv.i = i; bv.bound = m.bound;
-    walk(T, d, ops, n, bv, res);
+    if (!(fast & VF_NO_BIG_IDS)) {
+      BoundVis<S> bv;
+      bv.s = &s; bv.i = i; bv.bound = m.bound;
+      walk(T, d, ops, n, bv, res);
+    }
   } else {
     diag_head(s, true, "OperandMismatch", i);
     put_walk_error(s, T, d, e);
@@ -150,9 +157,11 @@ __device__ __noinline__ WalkErr inst_diags(S& s, const Mod& m, const Tables& T, 
     s.put('\n');
   }
   if (e.code != W_OK) return e;
-  ReqVis<S> rv;
-  rv.s = &s; rv.T = &T; rv.eff = eff; rv.i = i; rv.d = d;
-  walk(T, d, ops, n, rv, res);
+  if (T.ireqops(d)) {
+    ReqVis<S> rv;
+    rv.s = &s; rv.T = &T; rv.eff = eff; rv.i = i; rv.d = d;
+    walk(T, d, ops, n, rv, res);
+  }
   uint32_t wr = NONE32;
   if ((sp == SP_TYPEINT || sp == SP_TYPEFLOAT) && n >= 2) {
     uint32_t wd = ops[1];
@@ -187,6 +196,125 @@ __device__ __noinline__ void shape_diags(S& s, const Shape& sh) {
   if (!sh.has_ep) {
     diag_head(s, !sh.linkage, "MissingEntryPoint", NONE32);
     put_cstr(s, "module declares no entry point\n");
+  }
+}
+
+// the validator's single diagnostic for a module that does not decode (validate.py:76-83):
+// its code and the decode error's message, identical to load_and_split's
+__device__ inline const char* decode_code(int32_t decode_status) {
+  return decode_status == ST_NOTSPIRV ? "NotSpirv" : decode_status == ST_TRUNCATED ? "TruncatedStream"
+                                                                                  : "CorruptStream";
+}
+
+template <class S>
+__device__ __noinline__ void put_decode_msg(S& ew, const Mod& m, int64_t nbytes, int32_t decode_status) {
+  if (nbytes % 4 != 0 || nbytes < 20) {
+    put_u64(ew, (uint64_t)nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
+  } else if (decode_status == ST_NOTSPIRV) {
+    put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, m.w[0]); put_cstr(ew, " is not SPIR-V");
+  } else {
+    uint32_t p = 5;   // re-walk to the failing position
+    while (p < m.W) {
+      uint32_t wc = m.w[p] >> 16;
+      if (wc == 0 || p + wc > m.W) break;
+      p += wc;
+    }
+    put_cstr(ew, "instruction at word "); put_u64(ew, p);
+    put_cstr(ew, decode_status == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
+  }
+}
+
+// V2 (warp): module shape + effective capabilities (validate.py:101-136), per-instruction
+// diagnostic sizes, the first escaping exception (status, error record), then the
+// per-instruction offsets in m.ia; returns the module's diagnostics bytes
+__device__ __noinline__ uint64_t val_sizes(Mod& m, const Tables& T, uint64_t* eff, Shape& sh, int32_t& status,
+                                           ErrSink& es, int32_t t, uint32_t fast = 0) {
+  const uint32_t lane = lane_id();
+  uint64_t total = 0;
+  bool fn = false, cap = false, ep = false;
+  uint32_t mm = 0;
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    uint32_t i = base + lane;
+    if (i >= m.I || m.idef[i] == NONE16) continue;
+    uint32_t sp = T.special(m.idef[i]);
+    fn |= sp == SP_FUNCTION;
+    ep |= sp == SP_ENTRYPOINT;
+    mm += sp == SP_MEMORYMODEL;
+    if (sp == SP_CAPABILITY) {
+      cap = true;
+      if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
+        uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
+        uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
+        if (cn != NONE32)
+          for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k) eff[k] |= __ldg(T.closure + cn * T.cap_words + k);
+      }
+    }
+  }
+  sh.has_fn = __any_sync(FULL, fn);
+  sh.has_cap = __any_sync(FULL, cap);
+  sh.has_ep = __any_sync(FULL, ep);
+  sh.n_mm = warp_sum_u32(mm);
+  for (int k = 0; k < MAX_CAPW; ++k) {
+#pragma unroll
+    for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
+  }
+  sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    uint32_t i = base + lane;
+    if (i < m.I) {
+      CountSink cs;
+      WalkErr e = inst_diags(cs, m, T, i, eff, fast);
+      m.ierr[i] = (uint8_t)e.code;
+      m.ia[i] = cs.n;
+    }
+  }
+  __syncwarp();
+  uint32_t bad = NONE32;
+  for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
+    uint32_t i = base + lane;
+    unsigned b = __ballot_sync(FULL, i < m.I && m.ierr[i] != W_OK && !werr_is_codec(m.ierr[i]));
+    if (b) bad = base + __ffs(b) - 1;
+  }
+  if (bad != NONE32) {
+    if (lane == 0) {
+      ErrRec* rec = es.alloc();
+      CountSink cs;
+      WalkErr e = inst_diags(cs, m, T, bad, eff);
+      status = walk_status(e.code);
+      if (rec) {
+        ErrWriter ew{rec};
+        put_walk_error(ew, T, m.idef[bad], e);
+        rec->module = t; rec->cls = status; rec->len = ew.n;
+        rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
+      }
+    }
+    status = __shfl_sync(FULL, status, 0);
+    return 0;
+  }
+  CountSink hs;
+  shape_diags(hs, sh);
+  uint64_t run = hs.n;
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    uint32_t i = base + lane;
+    uint32_t len = i < m.I ? m.ia[i] : 0;
+    uint32_t incl = warp_incl_sum(len);
+    if (i < m.I) m.ia[i] = (uint32_t)(run + incl - len);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  __syncwarp();
+  total = run;
+  return total;
+}
+
+// V3 (warp): the diagnostics text at the offsets val_sizes left in m.ia
+__device__ __noinline__ void val_write(uint8_t* out, const Mod& m, const Tables& T, const uint64_t* eff,
+                                       const Shape& sh, uint32_t fast = 0) {
+  if (lane_id() == 0) { MemSink ms(out); shape_diags(ms, sh); }
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    uint32_t i = base + lane_id();
+    if (i >= m.I) continue;
+    MemSink ms(out + m.ia[i]);
+    inst_diags(ms, m, T, i, eff, fast);
   }
 }
 
@@ -239,106 +367,18 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
   group_sync(gid, gw);
   // -- V2: module shape + effective capabilities (validate.py:101-136), sizes,
   //        escaping exceptions, offsets
-  if (go && status == ST_OK) {
-    bool fn = false, cap = false, ep = false;
-    uint32_t mm = 0;
-    for (uint32_t base = 0; base < m.I; base += 32) {
-      uint32_t i = base + lane;
-      if (i >= m.I || m.idef[i] == NONE16) continue;
-      uint32_t sp = T.special(m.idef[i]);
-      fn |= sp == SP_FUNCTION;
-      ep |= sp == SP_ENTRYPOINT;
-      mm += sp == SP_MEMORYMODEL;
-      if (sp == SP_CAPABILITY) {
-        cap = true;
-        if (inst_nops(m, i) >= 1 && T.cap_kind != NONE32) {
-          uint32_t e = T.venum_lookup(T.cap_kind, inst_ops(m, i)[0]);
-          uint32_t cn = e == NONE32 ? NONE32 : T.ecapname(e);
-          if (cn != NONE32)
-            for (uint32_t k = 0; k < T.cap_words && k < MAX_CAPW; ++k) eff[k] |= __ldg(T.closure + cn * T.cap_words + k);
-        }
-      }
-    }
-    sh.has_fn = __any_sync(FULL, fn);
-    sh.has_cap = __any_sync(FULL, cap);
-    sh.has_ep = __any_sync(FULL, ep);
-    sh.n_mm = warp_sum_u32(mm);
-    for (int k = 0; k < MAX_CAPW; ++k) {
-#pragma unroll
-      for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
-    }
-    sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
-    for (uint32_t base = 0; base < m.I; base += 32) {
-      uint32_t i = base + lane;
-      if (i < m.I) {
-        CountSink cs;
-        WalkErr e = inst_diags(cs, m, T, i, eff);
-        m.ierr[i] = (uint8_t)e.code;
-        m.ia[i] = cs.n;
-      }
-    }
-    __syncwarp();
-    uint32_t bad = NONE32;
-    for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
-      uint32_t i = base + lane;
-      unsigned b = __ballot_sync(FULL, i < m.I && m.ierr[i] != W_OK && !werr_is_codec(m.ierr[i]));
-      if (b) bad = base + __ffs(b) - 1;
-    }
-    if (bad != NONE32) {
-      if (lane == 0) {
-        ErrRec* rec = es.alloc();
-        CountSink cs;
-        WalkErr e = inst_diags(cs, m, T, bad, eff);
-        status = walk_status(e.code);
-        if (rec) {
-          ErrWriter ew{rec};
-          put_walk_error(ew, T, m.idef[bad], e);
-          rec->module = (int32_t)t; rec->cls = status; rec->len = ew.n;
-          rec->a = e.a; rec->b = e.b; rec->c = e.c; rec->d = e.d;
-        }
-      }
-      status = __shfl_sync(FULL, status, 0);
-    } else {
-      CountSink hs;
-      shape_diags(hs, sh);
-      uint64_t run = hs.n;
-      for (uint32_t base = 0; base < m.I; base += 32) {
-        uint32_t i = base + lane;
-        uint32_t len = i < m.I ? m.ia[i] : 0;
-        uint32_t incl = warp_incl_sum(len);
-        if (i < m.I) m.ia[i] = (uint32_t)(run + incl - len);
-        run += __shfl_sync(FULL, incl, 31);
-      }
-      __syncwarp();
-      total = run;
-    }
-  }
+  if (go && status == ST_OK) total = val_sizes(m, T, eff, sh, status, es, (int32_t)t);
   group_sync(gid, gw);
   // -- V3: output
   if (live && status == ST_OK && decode_status != ST_OK) {
     // the decode error of the module is its only diagnostic line
-    const char* code = decode_status == ST_NOTSPIRV ? "NotSpirv"
-                       : decode_status == ST_TRUNCATED ? "TruncatedStream" : "CorruptStream";
+    const char* code = decode_code(decode_status);
     CountSink cs;
     diag_head(cs, true, code, NONE32);
     ErrRec tmp;
     {
       ErrWriter ew{&tmp};
-      // identical text to load_and_split's
-      if (nbytes % 4 != 0 || nbytes < 20) {
-        put_u64(ew, (uint64_t)nbytes); put_cstr(ew, " bytes is not a whole word stream of at least 5 words");
-      } else if (decode_status == ST_NOTSPIRV) {
-        put_cstr(ew, "magic word 0x"); put_hex8_upper(ew, m.w[0]); put_cstr(ew, " is not SPIR-V");
-      } else {
-        uint32_t p = 5;   // re-walk to the failing position
-        while (p < m.W) {
-          uint32_t wc = m.w[p] >> 16;
-          if (wc == 0 || p + wc > m.W) break;
-          p += wc;
-        }
-        put_cstr(ew, "instruction at word "); put_u64(ew, p);
-        put_cstr(ew, decode_status == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
-      }
+      put_decode_msg(ew, m, nbytes, decode_status);
       tmp.len = ew.n;
     }
     total = cs.n + (uint32_t)tmp.len + 1;
@@ -364,16 +404,7 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
       a.text_span[2 * t + 1] = (int64_t)total;
       a.status[t] = status;
     }
-    if (status == ST_OK && total > 0 && fits) {
-      uint8_t* out = a.text + off;
-      if (lane == 0) { MemSink ms(out); shape_diags(ms, sh); }
-      for (uint32_t base = 0; base < m.I; base += 32) {
-        uint32_t i = base + lane;
-        if (i >= m.I) continue;
-        MemSink ms(out + m.ia[i]);
-        inst_diags(ms, m, T, i, eff);
-      }
-    }
+    if (status == ST_OK && total > 0 && fits) val_write(a.text + off, m, T, eff, sh);
   }
   __syncwarp();
   group_sync(gid, gw);

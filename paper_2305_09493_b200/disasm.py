@@ -77,6 +77,19 @@ def _str_words(text: str):
     return list(struct.unpack(f"<{len(data) // 4}I", data))
 
 
+def disassemble_validate_batch(modules, options=None, spec=None, ext=None, strict=False):
+    """Fused decode -> validate -> disassemble: every module is read and
+    decoded once (skg_disasm_validate) for both results.  -> list of (text | exception,
+    list[Diagnostic] | exception) pairs, each element exactly what
+    disassemble_batch / validate_batch return for the module."""
+    from .validate import _parse
+    batch = modules if isinstance(modules, _native.DeviceBatch) else \
+        _native.DeviceBatch.from_modules([bytes(m) for m in modules])
+    texts, diags = _native.run_texts_pipeline(batch, option_bits(options, strict), spec, ext)
+    return [(t if isinstance(t, BaseException) else t.decode("utf-8"),
+             d if isinstance(d, BaseException) else _parse(d.decode("utf-8"))) for t, d in zip(texts, diags)]
+
+
 def format_instruction(spec, inst, context=None, ext=None) -> str:
     """One raw instruction as one plain-text line (reference disasm.py:380-389).
 

@@ -142,6 +142,30 @@ def pack(spec=None, ext=None) -> PackedTables:
             requirements.append(names)
         return req_index[names]
 
+    # kinds whose operands can carry a capability requirement (an enumerant with required
+    # capabilities, directly, through an enumerant parameter or a composite part): the
+    # validator's operand-requirement walk is skipped for instructions without any
+    kind_by_name = {}
+    for k in kinds:
+        kind_by_name.setdefault(k.kind, k)
+    req_memo = {}
+
+    def kind_has_req(name, stack=()):
+        if name in req_memo:
+            return req_memo[name]
+        if name in stack:
+            return False
+        k = kind_by_name.get(name)
+        r = False
+        if k is not None:
+            for e in k.enumerants or ():
+                if e.required_capabilities or any(kind_has_req(p.kind, stack + (name,)) for p in e.parameters):
+                    r = True
+            for b in k.bases or ():
+                r = r or kind_has_req(b, stack + (name,))
+        req_memo[name] = r
+        return r
+
     # instructions
     insts = list(spec.instructions)
     inst_rec = []
@@ -151,8 +175,9 @@ def pack(spec=None, ext=None) -> PackedTables:
         flags = (1 if inst.has_result else 0) | (2 if inst.has_result_type else 0)
         flags |= SPECIAL.get(inst.name, 0) << 8
         flags |= _section(inst) << 16
+        flags2 = 1 if any(kind_has_req(sl.kind) for sl in inst.operands) else 0
         inst_rec.append([name_off, name_len | (len(inst.operands) << 16), slot_off, flags,
-                         req(inst.required_capabilities), inst.opcode, 0, 0])
+                         req(inst.required_capabilities), inst.opcode, flags2, 0])
     max_opcode = max((i.opcode for i in insts), default=0)
     opidx = np.full(max_opcode + 2, 0xFFFF, dtype=np.uint16)
     for i, inst in enumerate(insts):

@@ -442,3 +442,37 @@ def test_small_module_with_large_bound(sk):
         if done >= 25:
             break
     assert done >= 10
+
+
+def test_fused_disasm_validate_goldens(sk):
+    """the fused decode -> validate -> disassemble pass gives, for every
+    golden module and every option set, exactly the reference's text (or exception) AND
+    its diagnostics (or exception) -- both goldens from one kernel."""
+    datas = [r["bytes"] for r in CASES]
+    for key, opts in OPTION_SETS.items():
+        got = sk.disassemble_validate_batch(datas, sk.DisassemblerOptions(**opts))
+        bad = []
+        for r, (t, d) in zip(CASES, got):
+            if not same(_as_outcome(t), r["disasm"][key]):
+                bad.append((r["name"], "disasm"))
+            o = _as_outcome(d)
+            if "ok" in o:
+                o = {"ok": [[x.severity, x.code, x.location, x.message] for x in o["ok"]]}
+            if not same(o, r["validate"]):
+                bad.append((r["name"], "validate"))
+        assert not bad, (key, bad[:10])
+    got = sk.disassemble_validate_batch(datas, strict=True)
+    bad = [r["name"] for r, (t, _) in zip(CASES, got) if not same(_as_outcome(t), r["disasm_strict"])]
+    assert not bad, bad[:10]
+
+
+def test_fused_matches_separate_on_families(sk):
+    """the fused pass on a shuffled synthetic batch equals the two separate kernels"""
+    from synth.families import sample_batch
+    b = sample_batch(3000, 300, 77)
+    mods = [b.module(i) for i in range(b.n)]
+    fused = sk.disassemble_validate_batch(mods)
+    texts = sk.disassemble_batch(mods)
+    diags = sk.validate_batch(mods)
+    assert [t for t, _ in fused] == texts
+    assert [d for _, d in fused] == diags

@@ -35,8 +35,12 @@ def main():
     asm = _native.AsmPlan(tb, out_cap=int(b.lengths.sum()) + 64 * dev.n + 4096, stride=2)
     asm.fit()
     assert (asm.span[1: 2 * dev.n: 2].cpu().numpy() == b.lengths).all()
+    fus = _native.DisasmPlan(dev, option_bits(DisassemblerOptions()), kind="pipeline", text_cap=dis.cap)
+    fus.launch()
+    finfo = fus.check()
+    assert not finfo["overflow"] and finfo["vtext_bytes"] == 0, finfo
     for _ in range(2):
-        val.launch(); dis.launch(); asm.launch()
+        val.launch(); dis.launch(); asm.launch(); fus.launch()
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     tv = td = ta = 0.0
@@ -45,10 +49,17 @@ def main():
         torch.cuda.synchronize()
         tv += ev[0].elapsed_time(ev[1]); td += ev[1].elapsed_time(ev[2]); ta += ev[2].elapsed_time(ev[3])
     tv, td, ta = tv / steps, td / steps, ta / steps
+    ev[0].record()
+    for _ in range(steps):
+        fus.launch()
+    ev[1].record()
+    torch.cuda.synchronize()
+    tf = ev[0].elapsed_time(ev[1]) / steps
     W = b.words
     print(f"validate {tv:.1f} ms ({W / tv / 1e6:.2f} Gwords/s, diagnostics {vinfo['text_bytes']} B)\n"
           f"disasm   {td:.1f} ms ({W / td / 1e6:.2f} Gwords/s, text {dinfo['text_bytes']} B)\n"
           f"asm      {ta:.1f} ms ({W / ta / 1e6:.2f} Gwords/s)\n"
+          f"fused validate+disasm (skg_disasm_validate) {tf:.1f} ms vs {tv + td:.1f} ms separate\n"
           f"pipeline {tv + td + ta:.1f} ms/step: {W / (tv + td + ta) / 1e6:.2f} Gwords/s per GPU "
           f"(each word validated, disassembled and re-assembled)", flush=True)
 
