@@ -81,12 +81,16 @@ def ref_kind():
 
 
 class CpuReference:
-    """The reference disassembler + assembler on all host cores (multiprocessing)."""
+    """The reference disassembler + assembler on all host cores (multiprocessing).
+
+    Workers are spawned (fresh interpreters), not forked: a fork of the GPU arm's
+    process would carry its CUDA context, pinned buffers and the 1M-module batch,
+    and ran measurably slower than the driver's reference arm."""
 
     def __init__(self, cores=None):
         import multiprocessing as mp
         self.cores = cores or len(os.sched_getaffinity(0))
-        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_ref_init)
+        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_ref_init)
 
     def run(self, mods):
         chunks = [mods[i::self.cores] for i in range(self.cores)]
@@ -248,17 +252,19 @@ def run_ours(args, rank, world, local_rank):
                 got = txt[span[2 * i]:span[2 * i] + span[2 * i + 1]].tobytes().decode()
                 assert got == odis.disassemble(m), f"module {i} differs from oracle"
 
-    # e2e through the host-buffer public API
+    # e2e through the host-buffer public API: RoundTripSession.run on the batch in pinned
+    # host memory -- no sizing pass (capacity-bounded arenas, per-chunk counters read
+    # back before each D2H), H2D of the binaries and D2H of text + binaries timed
     sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "8")))   # pipeline depth (experiments)
-    sess.stage(batch.data, batch.offsets, batch.lengths)
-    sess.run_staged(max_text)
+    h_batch = torch.from_numpy(batch.data).pin_memory()
+    sess.run(h_batch, batch.offsets, batch.lengths)          # warm-up: buffer allocation
     e2e_steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t1 = time.perf_counter()
     for _ in range(e2e_steps):
-        text, tspan, tst, binv, bspan, bst = sess.run_staged(max_text)
+        text, tspan, tst, binv, bspan, bst = sess.run(h_batch, batch.offsets, batch.lengths)
     e2e_s = (time.perf_counter() - t1) / e2e_steps
     et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -315,7 +321,8 @@ def run_ours(args, rank, world, local_rank):
         },
         "e2e": {"value": total_words / e2e_s, "unit": "words/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "paper_2305_09493_b200.asm.RoundTripSession.run_staged"},
+                "api": "paper_2305_09493_b200.asm.RoundTripSession.run (fresh batch: no sizing "
+                       "pass, host arrays of the results returned)"},
         # per step: skg_disasm + skg_asm, each = 3 scheduling kernels (size sort) + the main kernel
         "gpu_launches": 8 * args.steps,
         "clocks": clocks.summary(),
@@ -537,6 +544,81 @@ def run_config5(args, rank, world, local_rank):
     }
 
 
+# -- config 3: one ~91M-word module, disassembled and validated over the whole GPU ----------
+def run_config3(args, rank, world, local_rank):
+    """BASELINE configs[2]: the synth/huge.py module (55,000 functions, ~91M words, an
+    OpName on every id, long OpStrings) disassembled (default options: friendly names)
+    and validated by the grid-wide kernels (skg_disasm_large / skg_validate_large),
+    the module resident in HBM.  One step = disassembly + validation; value = words /
+    step time.  The text is checked against the recorded SHA-256 (reference validate,
+    oracle closed-form named disassembly: tests/golden/config3_55000.json).  Replicas
+    only: every rank runs its own copy (the module does not shard)."""
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    from paper_2305_09493_b200 import _native
+    from paper_2305_09493_b200.disasm import DisassemblerOptions, option_bits
+    from synth.huge import build_huge
+    t0 = time.perf_counter()
+    m = build_huge(args.functions)
+    W = len(m) // 4
+    log(f"[rank {rank}] config 3 module: {W} words ({time.perf_counter() - t0:.1f}s)")
+    data = np.frombuffer(m + b"\0" * 16, dtype=np.uint8)
+    dev = _native.DeviceBatch.from_host(data, np.array([0], np.int64), np.array([len(m)], np.int64))
+    opts = option_bits(DisassemblerOptions())
+
+    def step():
+        text = _native._disasm_large(dev, 0, len(m), opts, None, None)
+        diags = _native._validate_large(dev, 0, len(m), None)
+        return text, diags
+
+    for _ in range(args.warmup):
+        text, diags = step()
+    fx = ROOT / "tests" / "golden" / f"config3_{args.functions}.json"
+    checked = None
+    if fx.exists():
+        rec = json.loads(fx.read_text())
+        checked = (hashlib.sha256(text).hexdigest() == rec["oracle_disasm_named"]["sha256"]
+                   and hashlib.sha256(diags).hexdigest() == rec["ref_validate"]["sha256"])
+        assert checked, "config-3 output differs from the recorded digests"
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    if rank != 0:
+        return None
+    peak, peak_src = peak_hbm()
+    alg = 4 * W + len(text) + 4 * W
+    ach = alg / (ms_step / 1e3) / 1e9
+    return {
+        "metric": METRIC, "value": world * W / (ms_step / 1e3), "unit": "words/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: synth/huge.py (seeded; canonicality checked on slices against the reference)",
+        "config": {"workload": "configs[2]: one ~91M-word module (OpName on every id, long OpStrings, ids > "
+                               "2^16) disassembled (default options) + validated on the GPU, module resident "
+                               "in HBM; step = skg_disasm_large + skg_validate_large (host-synchronous "
+                               "calls, results copied to host memory inside the step)",
+                   "functions": args.functions, "words": W, "text_bytes": len(text),
+                   "digests_match_recorded": checked, "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "kernel": "skg_disasm_large + skg_validate_large", "achieved": ach,
+                     "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src, "traffic": None,
+                     "algorithmic_bytes_per_step": alg},
+        "clocks": clocks.summary(),
+    }
+
+
 def run_reference(args, rank):
     if rank != 0:
         return None
@@ -593,8 +675,10 @@ def main():
     ap.add_argument("--cpu-per-core", type=int, default=60)
     ap.add_argument("--ref-modules", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 5],
-                    help="2: configs[1]+[3] round trip per GPU (default); 5: configs[4] sharded pipeline")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="2: configs[1]+[3] round trip per GPU (default); 3: configs[2] one huge module; "
+                         "5: configs[4] sharded pipeline")
+    ap.add_argument("--functions", type=int, default=55000, help="config 3: functions of the module")
     ap.add_argument("--chunk", type=int, default=1_000_000, help="config 5: modules per device chunk")
     args = ap.parse_args()
     if args.config == 5 and "--modules" not in sys.argv:
@@ -624,6 +708,8 @@ def main():
         line = run_reference(args, rank)
     elif args.config == 5:
         line = run_config5(args, rank, world, local_rank)
+    elif args.config == 3:
+        line = run_config3(args, rank, world, local_rank)
     else:
         line = run_ours(args, rank, world, local_rank)
     if line is not None:

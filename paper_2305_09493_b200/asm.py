@@ -115,153 +115,195 @@ def assemble_module(text: str, spec=None, ext=None) -> bytes:
 class RoundTripSession:
     """Host-buffer batch API for binary -> text -> binary (disassemble + assemble).
 
-    ``stage(data, offsets, lengths)`` copies the host batch (module starts
-    16-byte aligned in one byte arena, int64 offsets/lengths) into pinned
-    staging buffers and sizes the device plans with one untimed pass.
-    ``run_staged()`` then runs the whole round trip as a pipeline over
-    ``chunks`` contiguous module ranges on three CUDA streams: the H2D copy of
-    chunk k+1 and the D2H copies of chunk k-1's text and binaries overlap
-    ``skg_disasm`` + ``skg_asm`` of chunk k (the assembler reads the
-    disassembler's text arena directly, spans with stride 2).  Returns
-    (text uint8[], text spans int64[n, 2], disasm status int32[n],
-    binaries uint8[], binary spans int64[n, 2], asm status int32[n]) with spans
-    relative to the returned arenas.
+    ``run(data, offsets, lengths)`` takes a host batch (byte arena with module
+    starts 16-byte aligned, int64 offsets / lengths; ``data`` may be a pinned
+    torch uint8 tensor, otherwise it is copied into pinned staging first) and runs
+    the round trip as a pipeline over ``chunks`` contiguous module ranges on three
+    CUDA streams: the H2D copy of chunk k+1 and the D2H copies of chunk k-1's
+    text and binaries overlap ``skg_disasm`` + ``skg_asm`` of chunk k (the
+    assembler reads the disassembler's text arena directly, spans with stride 2).
+    No sizing pass: the device arenas are capacity bounds (6x the chunk's input
+    bytes for text, 1x + slack for binaries); after each chunk's kernels its
+    counters are copied to pinned memory and the host, one chunk behind, issues
+    D2H copies of exactly the bytes used (a chunk that overflows is re-run with
+    grown arenas).  Returns (text uint8[], text spans int64[n, 2], disasm status
+    int32[n], binaries uint8[], binary spans int64[n, 2], asm status int32[n])
+    with spans relative to the returned arenas.  ``stage()`` + ``run_staged()``
+    split the same call (pinned staging, then the pipeline).
     """
+
+    TEXT_FACTOR = 6
 
     def __init__(self, options=None, spec=None, ext=None, chunks=8):
         from .disasm import DisassemblerOptions, option_bits
         self.opts = option_bits(options if options is not None else DisassemblerOptions())
         self.spec, self.ext = spec, ext
         self.nchunks = max(1, int(chunks))
-        self.chunks = None
+        self._buf = {}
+        self._staged = None
+
+    def _get(self, name, n, dtype, pinned=False):
+        """grow-only buffer (device, or pinned host)"""
+        import torch
+        b = self._buf.get(name)
+        if b is None or b.numel() < n:
+            n = max(int(n), 16)
+            b = torch.empty(n, dtype=dtype).pin_memory() if pinned else \
+                torch.empty(n, dtype=dtype, device="cuda")
+            self._buf[name] = b
+        return b
 
     def stage(self, data, offsets, lengths):
+        """Pinned staging of the host inputs (what run() does first for non-pinned data)."""
         import numpy as np
         import torch
         offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        if isinstance(data, torch.Tensor) and data.is_pinned():
+            h = data
+        else:
+            arr = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8) if not isinstance(data, np.ndarray) \
+                else data.view(np.uint8).reshape(-1)
+            h = self._get("h_data", arr.size + 16, torch.uint8, pinned=True)
+            h.numpy()[: arr.size] = arr
+        self._staged = (h, offsets, lengths)
+
+    def run_staged(self, max_text=None):
+        if self._staged is None:
+            raise RuntimeError("stage() first")
+        return self._pipeline(*self._staged)
+
+    def run(self, data, offsets, lengths):
+        self.stage(data, offsets, lengths)
+        return self.run_staged()
+
+    def _pipeline(self, h_data, offsets, lengths):
+        import numpy as np
+        import torch
         n = len(offsets)
-        self.n = n
-        self.h_data = torch.empty(max(data.nbytes, 16), dtype=torch.uint8).pin_memory()
-        self.h_data.numpy()[: data.nbytes] = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)
-        self.h_meta = torch.empty(2 * max(n, 1), dtype=torch.int64).pin_memory()
-        self.h_meta.numpy()[:n] = offsets
-        self.h_meta.numpy()[n: 2 * n] = lengths
-        self.d_data = torch.empty(max(data.nbytes, 16), dtype=torch.uint8, device="cuda")
-        self.d_meta = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
-        self.d_meta.copy_(self.h_meta)
-        self.d_data.copy_(self.h_data)
+        if n == 0:
+            z8, z32 = np.zeros(0, np.uint8), np.zeros(0, np.int32)
+            zs = np.zeros((0, 2), np.int64)
+            return z8, zs, z32, z8.copy(), zs.copy(), z32.copy()
+        nbytes = int(offsets[-1] + lengths[-1] + 15) // 16 * 16
         # contiguous module ranges by bytes; the first and last chunks are half size, so the
         # copy-in before the first kernel and the copy-out after the last one are short
-        cum = np.cumsum(lengths) if n else np.zeros(0, dtype=np.int64)
-        total = int(cum[-1]) if n else 0
+        cum = np.cumsum(lengths)
+        total = int(cum[-1])
         w = np.ones(self.nchunks)
         if self.nchunks >= 3:
             w[0] = w[-1] = 0.5
         frac = np.cumsum(w) / w.sum()
-        cuts = [0]
-        for k in range(1, self.nchunks):
-            cuts.append(int(np.searchsorted(cum, total * frac[k - 1])))
-        cuts.append(n)
+        cuts = [0] + [int(np.searchsorted(cum, total * frac[k - 1])) for k in range(1, self.nchunks)] + [n]
         cuts = sorted(set(cuts))
-        self.chunks = []
-        dis_ws = asm_ws = None
-        for a, b in zip(cuts[:-1], cuts[1:]):
-            if b <= a:
-                continue
-            c = _Chunk(self, a, b, offsets, lengths, dis_ws, asm_ws)
-            dis_ws, asm_ws = c.dplan.ws, c.aplan.ws
-            self.chunks.append(c)
-        torch.cuda.synchronize()
-        self.h_text = torch.empty(max(sum(c.text_used for c in self.chunks), 16), dtype=torch.uint8).pin_memory()
-        self.h_out = torch.empty(max(sum(c.out_used for c in self.chunks), 16), dtype=torch.uint8).pin_memory()
-        self.h_tspan = torch.empty(2 * max(n, 1), dtype=torch.int64).pin_memory()
-        self.h_bspan = torch.empty(2 * max(n, 1), dtype=torch.int64).pin_memory()
-        self.h_tst = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
-        self.h_bst = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
-        self.h_counts = torch.empty(max(len(self.chunks), 1) * 16, dtype=torch.int32).pin_memory()
-        self.d_counts = torch.zeros(max(len(self.chunks), 1) * 16, dtype=torch.int32, device="cuda")
-        tb = ob = 0
-        for c in self.chunks:
-            c.text_base, c.out_base = tb, ob
-            tb += c.text_used
-            ob += c.out_used
-        self.s_in, self.s_out = torch.cuda.Stream(), torch.cuda.Stream()
-
-    def run_staged(self, max_text=None):
-        import numpy as np
-        import torch
-        if self.chunks is None:
-            raise RuntimeError("stage() first")
-        if self.n == 0 or not self.chunks:
-            z8, z32 = np.zeros(0, np.uint8), np.zeros(0, np.int32)
-            zs = np.zeros((0, 2), np.int64)
-            return z8, zs, z32, z8.copy(), zs.copy(), z32.copy()
+        chunks = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+        d_data = self._get("d_data", nbytes + 16, torch.uint8)
+        h_meta = self._get("h_meta", 2 * n, torch.int64, pinned=True)
+        h_meta.numpy()[:n] = offsets
+        h_meta.numpy()[n: 2 * n] = lengths
+        d_meta = self._get("d_meta", 2 * n, torch.int64)
+        h_tspan = self._get("h_tspan", 2 * n, torch.int64, pinned=True)
+        h_bspan = self._get("h_bspan", 2 * n, torch.int64, pinned=True)
+        h_tst = self._get("h_tst", n, torch.int32, pinned=True)
+        h_bst = self._get("h_bst", n, torch.int32, pinned=True)
+        h_cnt = self._get("h_cnt", 16 * len(chunks), torch.int32, pinned=True)
         comp = torch.cuda.current_stream()
+        s_in = self._buf.setdefault("s_in", torch.cuda.Stream())
+        s_out = self._buf.setdefault("s_out", torch.cuda.Stream())
         cs = _native.ctypes.c_void_p(comp.cuda_stream)
-        evs = []
-        for k, c in enumerate(self.chunks):
-            ev_in, ev_dis, ev_asm = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
-            with torch.cuda.stream(self.s_in):
-                self.d_data[c.b0:c.b1].copy_(self.h_data[c.b0:c.b1], non_blocking=True)
-                ev_in.record(self.s_in)
-            comp.wait_event(ev_in)
-            c.dplan.launch(cs)
-            self.d_counts[16 * k: 16 * k + 8].copy_(c.dplan.ws[:32].view(torch.int32), non_blocking=True)
-            ev_dis.record(comp)
-            c.aplan.launch(cs)
-            self.d_counts[16 * k + 8: 16 * k + 16].copy_(c.aplan.ws[:32].view(torch.int32), non_blocking=True)
-            ev_asm.record(comp)
-            with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(ev_dis)
-                self.h_text[c.text_base:c.text_base + c.text_used].copy_(c.dplan.text[: c.text_used],
-                                                                          non_blocking=True)
-                self.h_tspan[2 * c.m0:2 * c.m1].copy_(c.dplan.span[: 2 * c.n], non_blocking=True)
-                self.h_tst[c.m0:c.m1].copy_(c.dplan.status[: c.n], non_blocking=True)
-                self.s_out.wait_event(ev_asm)
-                self.h_out[c.out_base:c.out_base + c.out_used].copy_(c.aplan.out[: c.out_used], non_blocking=True)
-                self.h_bspan[2 * c.m0:2 * c.m1].copy_(c.aplan.span[: 2 * c.n], non_blocking=True)
-                self.h_bst[c.m0:c.m1].copy_(c.aplan.status[: c.n], non_blocking=True)
-            evs.append(ev_asm)
-        with torch.cuda.stream(self.s_out):
-            self.s_out.wait_event(evs[-1])
-            self.h_counts.copy_(self.d_counts, non_blocking=True)
-        self.s_out.synchronize()
-        cnt = self.h_counts.numpy().reshape(-1, 16)
-        for k, c in enumerate(self.chunks):
-            dused = int(cnt[k, 4]) & 0xFFFFFFFF | (int(cnt[k, 5]) & 0xFFFFFFFF) << 32
-            aused = int(cnt[k, 12]) & 0xFFFFFFFF | (int(cnt[k, 13]) & 0xFFFFFFFF) << 32
-            if cnt[k, 2] or cnt[k, 10] or dused != c.text_used or aused != c.out_used:
-                raise RuntimeError("RoundTripSession: staged sizes changed; call stage() again")
-        n = self.n
-        tspan = self.h_tspan[: 2 * n].numpy().reshape(n, 2).copy()
-        bspan = self.h_bspan[: 2 * n].numpy().reshape(n, 2).copy()
-        for c in self.chunks:   # chunk-relative -> arena-relative offsets
-            tspan[c.m0:c.m1, 0] += c.text_base
-            bspan[c.m0:c.m1, 0] += c.out_base
-        return (self.h_text[: sum(c.text_used for c in self.chunks)].numpy(), tspan,
-                self.h_tst[:n].numpy(), self.h_out[: sum(c.out_used for c in self.chunks)].numpy(), bspan,
-                self.h_bst[:n].numpy())
+        with torch.cuda.stream(s_in):
+            d_meta[: 2 * n].copy_(h_meta[: 2 * n], non_blocking=True)
+        ev_meta = torch.cuda.Event()
+        ev_meta.record(s_in)
+        comp.wait_event(ev_meta)
+        plans, bases, state = [], [0, 0], {}
+        text_host, out_host = [], []
 
+        def launch(k, grow=None):
+            a, b = chunks[k]
+            b0 = int(offsets[a])
+            b1 = int(offsets[b - 1] + lengths[b - 1] + 15) // 16 * 16
+            cb = int(lengths[a:b].sum())
+            mw = int(lengths[a:b].max()) // 4
+            tcap, ocap = self.TEXT_FACTOR * cb + 4096, cb + 64 * (b - a) + 4096
+            max_text = self.TEXT_FACTOR * mw * 4 + 4096      # per-module text bound: sizes the asm slots
+            if grow:
+                tcap, ocap = max(tcap, grow[0] + 16), max(ocap, grow[1] + 16)
+                max_text = max(max_text, grow[2])
+            batch = _native.DeviceBatch(d_data, d_meta[a:b], d_meta[n + a:n + b], mw, cb)
+            dp = _native.DisasmPlan(batch, self.opts, self.spec, self.ext, text_cap=16,
+                                    ws=self._buf.get("ws_d"))
+            self._buf["ws_d"] = dp.ws
+            dp.text, dp.cap = self._get(f"text{k}", tcap, torch.uint8), tcap
+            tb = _native.DeviceBatch(dp.text, dp.span[0::2], dp.span[1::2], 0, 0)
+            tb.n = b - a
+            tb.max_words = (max_text + 3) // 4
+            ap = _native.AsmPlan(tb, self.spec, self.ext, out_cap=16, stride=2, ws=self._buf.get("ws_a"))
+            self._buf["ws_a"] = ap.ws
+            ap.out, ap.cap = self._get(f"out{k}", ocap, torch.uint8), ocap
+            if grow is None:
+                ev_in = torch.cuda.Event()
+                with torch.cuda.stream(s_in):
+                    d_data[b0:b1].copy_(h_data[b0:b1], non_blocking=True)
+                    ev_in.record(s_in)
+                comp.wait_event(ev_in)
+            dp.launch(cs)
+            h_cnt[16 * k: 16 * k + 8].copy_(dp.ws[:32].view(torch.int32), non_blocking=True)
+            ap.launch(cs)
+            h_cnt[16 * k + 8: 16 * k + 16].copy_(ap.ws[:32].view(torch.int32), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            return dp, ap, ev
 
-class _Chunk:
-    """One contiguous module range of a RoundTripSession with its fitted plans."""
+        def drain(k):
+            dp, ap, ev = plans[k]
+            ev.synchronize()
+            c = h_cnt[16 * k: 16 * k + 16].numpy()
+            tused = int(c[4]) & 0xFFFFFFFF | (int(c[5]) & 0xFFFFFFFF) << 32
+            oused = int(c[12]) & 0xFFFFFFFF | (int(c[13]) & 0xFFFFFFFF) << 32
+            if c[2] or c[10]:          # an arena overflowed: re-run this chunk with grown arenas
+                plans[k] = launch(k, grow=(tused, oused, 0))
+                return drain(k)
+            a, b = chunks[k]
+            ht = self._get(f"h_text{k}", tused, torch.uint8, pinned=True)
+            ho = self._get(f"h_out{k}", oused, torch.uint8, pinned=True)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev)
+                ht[:tused].copy_(dp.text[:tused], non_blocking=True)
+                h_tspan[2 * a:2 * b].copy_(dp.span[: 2 * (b - a)], non_blocking=True)
+                h_tst[a:b].copy_(dp.status[: b - a], non_blocking=True)
+                ho[:oused].copy_(ap.out[:oused], non_blocking=True)
+                h_bspan[2 * a:2 * b].copy_(ap.span[: 2 * (b - a)], non_blocking=True)
+                h_bst[a:b].copy_(ap.status[: b - a], non_blocking=True)
+            text_host.append((ht, tused, a, b))
+            out_host.append((ho, oused, a, b))
 
-    def __init__(self, sess, m0, m1, offsets, lengths, dis_ws, asm_ws):
-        self.m0, self.m1, self.n = m0, m1, m1 - m0
-        self.b0 = int(offsets[m0])
-        self.b1 = int((offsets[m1 - 1] + lengths[m1 - 1] + 15) // 16 * 16)
-        mw = int(lengths[m0:m1].max()) // 4
-        batch = _native.DeviceBatch(sess.d_data, sess.d_meta[m0:m1], sess.d_meta[sess.n + m0: sess.n + m1],
-                                    mw, int(lengths[m0:m1].sum()))
-        self.dplan = _native.DisasmPlan(batch, sess.opts, sess.spec, sess.ext, ws=dis_ws)
-        info = self.dplan.fit()
-        self.text_used = int(info["text_bytes"])
-        max_text = int(self.dplan.span[1::2].max().item()) if self.n else 0
-        tb = _native.DeviceBatch(self.dplan.text, self.dplan.span[0::2], self.dplan.span[1::2],
-                                 (max_text + 3) // 4, 0)
-        tb.n = self.n
-        self.aplan = _native.AsmPlan(tb, sess.spec, sess.ext, out_cap=int(lengths[m0:m1].sum()) + 64 * self.n + 4096,
-                                     stride=2, ws=asm_ws)
-        ainfo = self.aplan.fit()
-        self.out_used = int(ainfo["bytes"])
+        for k in range(len(chunks)):
+            plans.append(launch(k))
+            if k >= 1:
+                drain(k - 1)          # host one chunk behind: chunk k's kernels are queued
+        drain(len(chunks) - 1)
+        s_out.synchronize()
+        # a module whose text outgrew the per-module bound the assembler slots were sized
+        # for reports an internal status: re-run its chunk with slots for the real maximum
+        for k, (a, b) in enumerate(chunks):
+            if (h_bst[a:b].numpy() == _native.ST_INTERNAL).any():
+                mx = int(h_tspan[2 * a + 1:2 * b:2].numpy().max())
+                _, tused, _, _ = text_host[k]
+                _, oused, _, _ = out_host[k]
+                plans[k] = launch(k, grow=(tused, max(oused, 4 * mx), mx))
+                pos_t, pos_o = len(text_host), len(out_host)
+                drain(k)
+                text_host[k], out_host[k] = text_host.pop(pos_t), out_host.pop(pos_o)
+                s_out.synchronize()
+        tspan = h_tspan[: 2 * n].numpy().reshape(n, 2).copy()
+        bspan = h_bspan[: 2 * n].numpy().reshape(n, 2).copy()
+        text = np.empty(sum(u for _, u, _, _ in text_host), dtype=np.uint8)
+        binv = np.empty(sum(u for _, u, _, _ in out_host), dtype=np.uint8)
+        for arena, parts, spans in ((text, text_host, tspan), (binv, out_host, bspan)):
+            pos = 0
+            for h, used, a, b in parts:
+                arena[pos:pos + used] = h.numpy()[:used]
+                spans[a:b, 0] += pos
+                pos += used
+        return text, tspan, h_tst[:n].numpy().copy(), binv, bspan, h_bst[:n].numpy().copy()

@@ -4,6 +4,10 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
+#ifdef W_OK   // <unistd.h> access() mode (via CUB): the walk status enum uses the name
+#undef W_OK
+#endif
 #include "../../include/skgpu.h"
 #include "skg_module.cuh"
 #include "skg_sched.cuh"
@@ -595,6 +599,92 @@ int read_ctl(const LargeWs& l, uint32_t* out64, cudaStream_t s) {
 }
 }  // namespace
 
+namespace {
+// closed-form name de-duplication (skg_disasm.cu bnc_*): stable radix sorts of the
+// named idents by group leader and of the child list by (parent, serial), group and
+// child ranges, one kernel per level of the parent / child tree, then the serials
+int name_dedup_closed(const LargeWs& l, uint32_t nd, const uint32_t* clist, uint32_t nc, cudaStream_t s) {
+  using namespace skg;
+  if (nd == 0) return 0;
+  const uint32_t ncx = nc ? nc : 1;
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) < nd) ++bits;
+  const bool dbg = getenv("SKG_DEBUG_SYNC") != nullptr;
+  size_t tmp_sort = 0, tmp_csort = 0;
+  const cudaError_t q1 = cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (const uint32_t*)nullptr,
+                                                         (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                                         (uint32_t*)nullptr, (int)nd, 0, bits, s);
+  const cudaError_t q2 = cub::DeviceRadixSort::SortPairs(nullptr, tmp_csort, (const unsigned long long*)nullptr,
+                                                         (unsigned long long*)nullptr, (const uint32_t*)nullptr,
+                                                         (uint32_t*)nullptr, (int)ncx, 0, 64, s);
+  if (int e = check(q1 != cudaSuccess ? q1 : q2)) return e;
+  const size_t tmp = std::max(tmp_sort, tmp_csort);
+  // buffers: 4 x nd members, 6 x nd per-leader arrays, nd flags, 4 x nc children, skips
+  // (+ 256-byte alignment of each of the 17 pieces)
+  const size_t bytes = 16ull * nd + 24ull * nd + ((nd + 15) & ~15ull) + 24ull * ncx + 4ull * ncx + tmp + 17 * 256;
+  uint8_t* buf = nullptr;
+  if (int e = check(cudaMalloc(reinterpret_cast<void**>(&buf), bytes))) return e;   // (host-synchronous path)
+  uint8_t* p = buf;
+  auto take = [&](size_t b) { uint8_t* r = p; p += (b + 255) & ~255ull; return r; };
+  uint32_t* keys = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* vals = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* svals = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint8_t* zero0 = p;                                              // zero-initialised from here
+  uint32_t* gstart = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* gend = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* cstart = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* cend = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* depth = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint32_t* nskip = reinterpret_cast<uint32_t*>(take(4ull * nd));
+  uint8_t* btaken = take(nd);
+  uint8_t* zero1 = p;
+  auto* ckeys = reinterpret_cast<unsigned long long*>(take(8ull * ncx));
+  auto* sckeys = reinterpret_cast<unsigned long long*>(take(8ull * ncx));
+  uint32_t* cvals = reinterpret_cast<uint32_t*>(take(4ull * ncx));
+  uint32_t* scvals = reinterpret_cast<uint32_t*>(take(4ull * ncx));
+  uint32_t* skipq = reinterpret_cast<uint32_t*>(take(4ull * ncx));
+  void* ctmp = take(tmp);
+  int rc = 0;
+  const uint32_t gN = grid_for(nd), gC = grid_for(ncx);
+  auto step_ok = [&](const char* what) -> bool {   // SKG_DEBUG_SYNC: synchronise and name a failing step
+    if (!dbg) return true;
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { fprintf(stderr, "skgpu: name_dedup_closed %s: %s\n", what, cudaGetErrorString(e)); rc = (int)e; }
+    return e == cudaSuccess;
+  };
+  do {
+    if ((rc = check(cudaMemsetAsync(zero0, 0, (size_t)(zero1 - zero0), s)))) break;
+    if (!step_ok("memset")) break;
+    bnc_keys<<<gN, 256, 0, s>>>(l.mod, nd, keys, vals, clist, nc, ckeys, cvals);
+    if (!step_ok("keys")) break;
+    size_t t1 = tmp;
+    if ((rc = check(cub::DeviceRadixSort::SortPairs(ctmp, t1, keys, skeys, vals, svals, (int)nd, 0, bits, s)))) break;
+    if (nc) {
+      size_t t2 = tmp;
+      if ((rc = check(cub::DeviceRadixSort::SortPairs(ctmp, t2, ckeys, sckeys, cvals, scvals, (int)nc, 0, 64, s))))
+        break;
+    }
+    if (!step_ok("sorts")) break;
+    bnc_ranges<<<gN, 256, 0, s>>>(l.mod, nd, skeys, gstart, gend, nc, sckeys, cstart, cend, depth, l.ctl);
+    uint32_t maxd = 0;
+    if ((rc = check(cudaMemcpyAsync(&maxd, l.ctl + BC_DEPTH, 4, cudaMemcpyDeviceToHost, s)))) break;
+    if ((rc = check(cudaStreamSynchronize(s)))) break;
+    if (nc)
+      for (uint32_t lv = 0; lv <= maxd; ++lv)
+        bnc_level<<<gC, 256, 0, s>>>(nc, sckeys, scvals, svals, gstart, gend, cstart, cend, depth, lv, btaken, skipq,
+                                     nskip);
+    if (!step_ok("levels")) break;
+    bnc_assign<<<gN, 256, 0, s>>>(l.mod, nd, skeys, svals, gstart, btaken, cstart, skipq, nskip);
+    rc = check(cudaGetLastError());
+    step_ok("assign");
+  } while (false);
+  if (!rc) rc = check(cudaStreamSynchronize(s));
+  cudaFree(buf);
+  return rc;
+}
+}  // namespace
+
 int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
                      uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
                      void* workspace, uint64_t workspace_bytes, void* stream) {
@@ -672,10 +762,7 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
     const int64_t nc = large_scan_total(flags, nd, l, s);
     if (nc < 0) return (int)nc;
     bn_children<<<gN, 256, 0, s>>>(l.mod, flags, clist, nd, 1);
-    // group counters of the parallel dedup: one per ident index (leaders), after the list
-    uint32_t* gcount = flags + nd;                                  // spill: 12 nc + 4 nd + 4 nd <= 32 nd bytes
-    if (check(cudaMemsetAsync(gcount, 0, 4ull * nd, s))) return -1;
-    bn_dedup_par<<<1, 1024, 0, s>>>(l.mod, clist, (uint32_t)nc, nd, gcount);
+    if (int e = name_dedup_closed(l, nd, clist, (uint32_t)nc, s)) return e;
     bn_arena<<<gN, 256, 0, s>>>(l.mod, flags, nd, 0);
     const int64_t arena = large_scan_total(flags, nd, l, s);
     if (arena < 0) return (int)arena;

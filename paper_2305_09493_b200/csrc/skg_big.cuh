@@ -20,6 +20,7 @@ enum : uint32_t {
   BC_FLAGS = 8, BC_NMM = 9, BC_BAD = 10, BC_OVER = 11, BC_ANYNAME = 12, BC_ARENA = 13,
   BC_TOTAL = 14, BC_SCAN = 16,                                     // BC_SCAN: u64 total of the last scan
   BC_NP0 = 18, BC_E1 = 19, BC_E2 = 20, BC_E3 = 21, BC_WIDTH = 22, BC_SUM = 24,   // BC_SUM: u64
+  BC_DEPTH = 26,                                                   // closed-form name dedup: max tree depth
   BC_EFF = 32                                                      // eff: 8 x u64 at word 32
 };
 enum : uint32_t { BF_FN = 1, BF_CAP = 2, BF_EP = 4 };

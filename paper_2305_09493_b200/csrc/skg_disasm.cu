@@ -1798,6 +1798,97 @@ __global__ void __launch_bounds__(1024) bn_dedup_par(const Mod* mp, const uint32
   }
 }
 
+// ---- name de-duplication of one large module in closed form (replaces the
+// ordered pass of bn_dedup_par).  disasm.py:173-185 gives the k-th named ident
+// (D order) the first free of base, base_0, base_1, ...  A candidate "B_s" of
+// group B (idents with sanitized base B) can only be taken by an earlier member of
+// B or by the bare name of the child group C whose literal base reads "B_s" (no
+// other group generates that string); C's bare name can only be taken by B's
+// serial s.  So with B's members sorted in D order, B's requests (all members but
+// the first when B's bare name is free) take serials 0, 1, 2 ... skipping serial s
+// exactly when child "B_s"'s first member comes before the request that would take
+// s; otherwise B takes s and the child's bare name is taken.  Groups are decided
+// top-down over the parent / child tree (one thread per group per tree level),
+// then every member's serial is q + (skips at requests <= q).
+__global__ void bnc_keys(const Mod* mp, uint32_t nd, uint32_t* keys, uint32_t* vals, const uint32_t* clist,
+                         uint32_t nc, unsigned long long* ckeys, uint32_t* cvals) {
+  const Mod m = *mp;
+  SKG_GRID_FOR(k, nd) { keys[k] = (uint32_t)m.pos[k]; vals[k] = k; }
+  SKG_GRID_FOR(j, nc) {
+    ckeys[j] = ((unsigned long long)clist[3 * j] << 32) | clist[3 * j + 1];   // (parent leader, serial)
+    cvals[j] = clist[3 * j + 2];                                               // child leader
+  }
+}
+
+// group ranges in the sorted member list and in the sorted child list (indexed by
+// leader); depth of every group with children (parent chain length)
+__global__ void bnc_ranges(const Mod* mp, uint32_t nd, const uint32_t* skeys, uint32_t* gstart, uint32_t* gend,
+                           uint32_t nc, const unsigned long long* sckeys, uint32_t* cstart, uint32_t* cend,
+                           uint32_t* depth, uint32_t* ctl) {
+  const Mod m = *mp;
+  SKG_GRID_FOR(i, nd) {
+    const uint32_t g = skeys[i];
+    if (i == 0 || skeys[i - 1] != g) gstart[g] = i;
+    if (i + 1 == nd || skeys[i + 1] != g) gend[g] = i + 1;
+  }
+  SKG_GRID_FOR(j, nc) {
+    const uint32_t p = (uint32_t)(sckeys[j] >> 32);
+    if (j == 0 || (uint32_t)(sckeys[j - 1] >> 32) != p) {
+      cstart[p] = j;
+      uint32_t d = 0;
+      for (uint32_t q = m.ib[p]; q != NONE32 && d < nd; q = m.ib[q]) ++d;
+      depth[p] = d;
+      atomicMax(&ctl[BC_DEPTH], d);
+    }
+    if (j + 1 == nc || (uint32_t)(sckeys[j + 1] >> 32) != p) cend[p] = j + 1;
+  }
+}
+
+// one thread per group with children at tree level `level`: its skips and its
+// children's bare-name status
+__global__ void bnc_level(uint32_t nc, const unsigned long long* sckeys, const uint32_t* scvals,
+                          const uint32_t* svals, const uint32_t* gstart, const uint32_t* gend,
+                          const uint32_t* cstart, const uint32_t* cend, const uint32_t* depth, uint32_t level,
+                          uint8_t* btaken, uint32_t* skipq, uint32_t* nskip) {
+  SKG_GRID_FOR(j0, nc) {
+    const uint32_t g = (uint32_t)(sckeys[j0] >> 32);
+    if (cstart[g] != j0 || depth[g] != level) continue;
+    const bool bfree = !btaken[g];
+    const uint32_t n = gend[g] - gstart[g];
+    const uint32_t nreq = bfree ? n - 1 : n, off = gstart[g] + (bfree ? 1u : 0u);
+    uint32_t delta = 0, ns = 0;
+    #pragma unroll 1
+    for (uint32_t j = j0; j < cend[g]; ++j) {
+      const uint32_t sigma = (uint32_t)sckeys[j], c = scvals[j];
+      const uint32_t q = sigma - delta;
+      if (q >= nreq) break;                        // g never reaches this serial (nor the later ones)
+      if (c < svals[off + q]) { skipq[j0 + ns++] = q; ++delta; }   // the child's bare name came first
+      else btaken[c] = 1;                          // g took serial sigma before the child appeared
+    }
+    nskip[g] = ns;
+  }
+}
+
+__global__ void bnc_assign(const Mod* mp, uint32_t nd, const uint32_t* skeys, const uint32_t* svals,
+                           const uint32_t* gstart, const uint8_t* btaken, const uint32_t* cstart,
+                           const uint32_t* skipq, const uint32_t* nskip) {
+  const Mod m = *mp;
+  SKG_GRID_FOR(i, nd) {
+    const uint32_t g = skeys[i], k = svals[i];
+    const bool bfree = !btaken[g];
+    const uint32_t j = i - gstart[g];
+    uint32_t serial = NONE32;
+    if (!(bfree && j == 0)) {
+      const uint32_t q = j - (bfree ? 1u : 0u);
+      uint32_t lo = 0, hi = nskip[g];               // skips at requests <= q (ascending)
+      const uint32_t* sk = skipq + cstart[g];
+      while (lo < hi) { const uint32_t mid = (lo + hi) >> 1; if (sk[mid] <= q) lo = mid + 1; else hi = mid; }
+      serial = q + lo;
+    }
+    m.hser[m.ndl[k]] = serial;
+  }
+}
+
 __global__ void bn_arena(const Mod* mp, uint32_t* lens, uint32_t nd, uint32_t step) {
   Mod m = *mp;
   if (step == 0) {

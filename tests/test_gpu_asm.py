@@ -233,3 +233,25 @@ def test_asm_mixed_batch_with_large_text(sk, monkeypatch):
             except Exception as exc:   # noqa: BLE001
                 want = exc
             assert (type(g), str(g)) == (type(want), str(want)) if isinstance(want, Exception) else g == want
+
+
+def test_roundtrip_session_fresh_batches_and_regrowth(sk, monkeypatch):
+    """RoundTripSession.run on new batches with no sizing pass: different batches through
+    one session; a text-arena bound too small (overflow: the chunk is re-run with grown
+    arenas) and an assembler slot too small (internal status: re-run with slots for the
+    real maximum) give the same results."""
+    from oracle import disasm as odis
+    from paper_2305_09493_b200.asm import RoundTripSession
+    from synth.families import sample_batch
+    sess = RoundTripSession(chunks=4)
+    for seed, factor in ((11, 6), (12, 6), (13, 1)):
+        monkeypatch.setattr(RoundTripSession, "TEXT_FACTOR", factor)
+        b = sample_batch(2000 + 500 * (seed - 11), 200, seed)
+        text, tspan, tst, binv, bspan, bst = sess.run(b.data, b.offsets, b.lengths)
+        assert (tst == 0).all() and (bst == 0).all()
+        assert (bspan[:, 1] == b.lengths).all()
+        for i in range(0, b.n, 29):
+            m = b.module(i)
+            assert binv[bspan[i, 0]:bspan[i, 0] + bspan[i, 1]].tobytes() == m
+            if i % 87 == 0:
+                assert text[tspan[i, 0]:tspan[i, 0] + tspan[i, 1]].tobytes().decode() == odis.disassemble(m)
