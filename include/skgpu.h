@@ -185,11 +185,14 @@ int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, 
  * larger arena); 10 + s: the module does not decode (status s, *error = the
  * message: the validator's only diagnostic); 2: ids at/above the header bound
  * (use skg_validate).  `workspace` must hold skg_large_workspace_bytes(nbytes
- * / 4, bound) for the module's header bound. */
+ * / 4, S) with S = max(header bound, min_table).  min_table (0 = the header
+ * bound) widens the direct id tables: a module with ids at or above its header
+ * bound (return 2) can be redone with min_table = 2 * nbytes / 4 + 64 instead of
+ * falling back to the one-warp path; messages keep the header bound. */
 uint64_t skg_large_workspace_bytes(uint64_t n_words, uint32_t bound);
 int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint8_t* text,
                        uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
-                       void* workspace, uint64_t workspace_bytes, void* stream);
+                       void* workspace, uint64_t workspace_bytes, void* stream, uint32_t min_table);
 
 /* disassemble_module for ONE large module (config 3) over the whole GPU: the
  * phases of skg_disasm as grid-wide kernels (tiled boundary pass, atomic id
@@ -204,7 +207,7 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
  * header bound (use skg_disasm).  Workspace: skg_large_workspace_bytes. */
 int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
                      uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
-                     void* workspace, uint64_t workspace_bytes, void* stream);
+                     void* workspace, uint64_t workspace_bytes, void* stream, uint32_t min_table);
 
 /* tokenize_line for a batch of lines (reference asm.py:51-90).
  * Input: UTF-8 byte arena `text` with int64 per-line offsets/lengths (one
@@ -254,6 +257,15 @@ int skg_pack_strings(const uint8_t* bytes, const int64_t* off, const int64_t* le
  * value does not fit a signed / unsigned literal of that width. */
 int skg_ctx_literals(const int64_t* width, const uint32_t* flags, const uint64_t* val, uint32_t n,
                      uint32_t* words, int32_t* nwords, int32_t* status, void* stream);
+
+/* Self-test (tests only): repr() of every float32 bit pattern in [start, start +
+ * count) as the disassembler renders it, checked on the device against the
+ * assembler's independent float() parser -- the text reads back as the same
+ * double and no (n-1)-significant-digit neighbour does (shortest round trip);
+ * nan / inf / zero spelled as CPython does.  *fails += failures (caller zeroes),
+ * *first_fail = min failing bit pattern (caller sets 0xFFFFFFFF). */
+int skg_selftest_repr_f32(const skg_tables* t, uint64_t start, uint64_t count, uint64_t* fails,
+                          uint32_t* first_fail, void* stream);
 
 /* Counters of the last call on `workspace` (device->host copy, synchronous on
  * `stream`): number of error records wanted, 1 if the text arena overflowed,

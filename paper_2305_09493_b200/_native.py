@@ -59,15 +59,17 @@ def lib():
     L.skg_decode_large.argtypes = [P, U64, U32, P, P, P, P, P, P, P, U64, P]
     L.skg_large_workspace_bytes.argtypes = [U64, U32]
     L.skg_large_workspace_bytes.restype = U64
-    L.skg_validate_large.argtypes = [P, P, U64, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
+    L.skg_validate_large.argtypes = [P, P, U64, P, U64, ctypes.POINTER(U64), P, P, P, U64, P, U32]
     L.skg_validate_large.restype = I32
-    L.skg_disasm_large.argtypes = [P, P, U64, U32, P, U64, ctypes.POINTER(U64), P, P, P, U64, P]
+    L.skg_disasm_large.argtypes = [P, P, U64, U32, P, U64, ctypes.POINTER(U64), P, P, P, U64, P, U32]
     L.skg_disasm_large.restype = I32
     L.skg_disasm_refs.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P, P, P, U32]
     L.skg_disasm_refs.restype = I32
     L.skg_disasm_validate.argtypes = [P, P, P, P, U32, U32, U32, P, U64, P, P, P, U32, P, U64, P, P, P, U32,
                                       P, U64, P]
     L.skg_disasm_validate.restype = I32
+    L.skg_selftest_repr_f32.argtypes = [P, U64, U64, P, P, P]
+    L.skg_selftest_repr_f32.restype = I32
     L.skg_tokenize.argtypes = [P, P, P, U32, P, P, P, P, P, P, P, P, P]
     L.skg_encode_modules.argtypes = [P, U32, P, P, U64, P, P, U64, P, P, P]
     L.skg_pack_strings.argtypes = [P, P, P, P, U32, U64, P, P, P]
@@ -440,20 +442,27 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None):
     data = batch.data.data_ptr() + o
     W = nbytes // 4
     bound = _header_bound(batch.data[o:o + 20].cpu().numpy().tobytes())
-    ws_bytes = int(L.skg_large_workspace_bytes(W, min(bound, 2 * W + 64)))
-    ws = _ws.get(ws_bytes)
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     errs = torch.zeros(256, dtype=torch.uint8, device="cuda")
     cap = cap if cap is not None else max(1 << 20, 4 * nbytes)
-    for _ in range(3):
-        text = torch.empty(cap, dtype=torch.uint8, device="cuda")
-        need = ctypes.c_uint64(0)
-        rc = fn(data, nbytes, *args, text.data_ptr(), cap, ctypes.byref(need), status.data_ptr(), errs.data_ptr(),
-                ws.data_ptr(), ws_bytes, _stream())
-        if rc == 3:
-            cap = int(need.value) + 16
-            continue
-        break
+    # id tables sized by the header bound first; ids at/above it (rc 2): once more with
+    # tables for every id below 2W + 64 (the header bound still names BoundTooSmall)
+    for min_table in (0, 2 * W + 64):
+        if min_table and bound >= min_table:
+            break
+        ws_bytes = int(L.skg_large_workspace_bytes(W, min(max(bound, min_table), 2 * W + 64)))
+        ws = _ws.get(ws_bytes)
+        for _ in range(3):
+            text = torch.empty(cap, dtype=torch.uint8, device="cuda")
+            need = ctypes.c_uint64(0)
+            rc = fn(data, nbytes, *args, text.data_ptr(), cap, ctypes.byref(need), status.data_ptr(),
+                    errs.data_ptr(), ws.data_ptr(), ws_bytes, _stream(), min_table)
+            if rc == 3:
+                cap = int(need.value) + 16
+                continue
+            break
+        if rc != 2:
+            break
     _check(rc if rc < 0 else 0, getattr(fn, "__name__", "large call"))
     return rc, (_pinned.to_bytes(text[: int(need.value)]) if rc == 0 else None), errs
 

@@ -469,7 +469,7 @@ LargeWs large_ws(uint8_t* ws, uint64_t W, uint32_t bound) {
 // tiled boundary pass into the module scratch + layout; returns the decode status
 // (host-synchronous) or -1 on a CUDA error
 int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const LargeWs& l, skg::ErrRec* derr,
-                cudaStream_t s) {
+                cudaStream_t s, uint32_t min_table) {
   skg::BigDecode b;
   const uint64_t W = nbytes / 4;
   b.src = data; b.nbytes = nbytes; b.W = (uint32_t)W;
@@ -500,7 +500,7 @@ int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const
   uint32_t st = 0;
   if (check(cudaMemcpyAsync(&st, l.ctl, 4, cudaMemcpyDeviceToHost, s)) || check(cudaStreamSynchronize(s))) return -1;
   if (st != 0) return (int)st;
-  skg::big_setup<<<1, 1, 0, s>>>(l.mod, l.slot, (uint32_t)W, l.ctl);
+  skg::big_setup<<<1, 1, 0, s>>>(l.mod, l.slot, (uint32_t)W, l.ctl, min_table);
   return check(cudaGetLastError()) ? -1 : 0;
 }
 
@@ -521,7 +521,7 @@ uint64_t skg_large_workspace_bytes(uint64_t n_words, uint32_t bound) {
 
 int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint8_t* text,
                        uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
-                       void* workspace, uint64_t workspace_bytes, void* stream) {
+                       void* workspace, uint64_t workspace_bytes, void* stream, uint32_t min_table) {
   if (!t || !workspace || !data || !text_bytes || nbytes / 4 > 0xFFFFFFF0ull) return -1;
   cudaStream_t s = (cudaStream_t)stream;
   const uint64_t W = nbytes / 4;
@@ -531,11 +531,12 @@ int skg_validate_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes
   if (check(cudaStreamSynchronize(s))) return -1;
   uint32_t bound = hdr[3];
   if (hdr[0] == 0x03022307u) bound = __builtin_bswap32(bound);
+  if (min_table > bound) bound = min_table;                         // direct table size
   if ((uint64_t)bound > 2 * W + 64) return 2;                      // not direct: use skg_validate
   const LargeWs l = large_ws((uint8_t*)workspace, W, bound);
   if (workspace_bytes < l.total) return -3;
   *text_bytes = 0;
-  const int dst = large_front(data, nbytes, t->t.max_opcode, l, reinterpret_cast<skg::ErrRec*>(error), s);
+  const int dst = large_front(data, nbytes, t->t.max_opcode, l, reinterpret_cast<skg::ErrRec*>(error), s, min_table);
   if (dst < 0) return -1;
   if (dst > 0) return 10 + dst;                                    // decode error: caller formats it
   skg::big_init_tables<<<grid_for(bound), 256, 0, s>>>(l.mod);
@@ -687,7 +688,7 @@ int name_dedup_closed(const LargeWs& l, uint32_t nd, const uint32_t* clist, uint
 
 int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, uint32_t opts, uint8_t* text,
                      uint64_t text_cap, uint64_t* text_bytes, int32_t* status, skg_error* error,
-                     void* workspace, uint64_t workspace_bytes, void* stream) {
+                     void* workspace, uint64_t workspace_bytes, void* stream, uint32_t min_table) {
   using namespace skg;
   if (!t || !workspace || !data || !text_bytes || nbytes / 4 > 0xFFFFFFF0ull) return -1;
   cudaStream_t s = (cudaStream_t)stream;
@@ -697,12 +698,13 @@ int skg_disasm_large(const skg_tables* t, const uint8_t* data, uint64_t nbytes, 
   if (check(cudaStreamSynchronize(s))) return -1;
   uint32_t bound = hdr[3];
   if (hdr[0] == 0x03022307u) bound = __builtin_bswap32(bound);
+  if (min_table > bound) bound = min_table;                         // direct table size
   if ((uint64_t)bound > 2 * W + 64) return 2;
   const LargeWs l = large_ws((uint8_t*)workspace, W, bound);
   if (workspace_bytes < l.total) return -3;
   *text_bytes = 0;
   ErrRec* rec = reinterpret_cast<ErrRec*>(error);
-  const int dst = large_front(data, nbytes, t->t.max_opcode, l, rec, s);
+  const int dst = large_front(data, nbytes, t->t.max_opcode, l, rec, s, min_table);
   if (dst < 0) return -1;
   if (dst > 0) return 10 + dst;                                    // decode exception (record in *error)
   const Tables& T = t->t;
@@ -867,6 +869,15 @@ int skg_ctx_literals(const int64_t* width, const uint32_t* flags, const uint64_t
   if (!width || !flags || !val || !words || !nwords || !status) return -1;
   skg::ctx_literals_kernel<<<item_grid(n), 256, 0, (cudaStream_t)stream>>>(width, flags, val, n, words, nwords,
                                                                             status);
+  return check(cudaGetLastError());
+}
+
+int skg_selftest_repr_f32(const skg_tables* t, uint64_t start, uint64_t count, uint64_t* fails,
+                          uint32_t* first_fail, void* stream) {
+  if (!t || !fails || !first_fail || start + count > (1ull << 32)) return -1;
+  if (count == 0) return 0;
+  skg::selftest_repr_f32_kernel<<<sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(
+      t->u, start, count, reinterpret_cast<unsigned long long*>(fails), first_fail);
   return check(cudaGetLastError());
 }
 

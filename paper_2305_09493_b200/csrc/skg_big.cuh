@@ -33,7 +33,9 @@ __host__ __device__ inline size_t big_slot_bytes(uint32_t W, uint32_t bound) {
 }
 
 // layout of the module scratch once I is known (one thread)
-__global__ void big_setup(Mod* mp, uint8_t* slot, uint32_t W, uint32_t* ctl) {
+// min_table: direct id tables of at least this many slots (a module whose ids reach
+// its header bound is redone with tables for every id below 2W + 64)
+__global__ void big_setup(Mod* mp, uint8_t* slot, uint32_t W, uint32_t* ctl, uint32_t min_table) {
   Mod m;
   layout_head(m, slot, W);
   m.I = ctl[BC_COUNT];
@@ -45,11 +47,12 @@ __global__ void big_setup(Mod* mp, uint8_t* slot, uint32_t W, uint32_t* ctl) {
   m.arena_need = 0;
   for (uint32_t k = BC_FLAGS; k < 64; ++k) ctl[k] = 0;
   ctl[BC_BAD] = NONE32; ctl[BC_E1] = NONE32; ctl[BC_E2] = NONE32; ctl[BC_E3] = NONE32;
-  if (m.bound > 2 * m.W + 64) { ctl[BC_OVER] = 1; *mp = m; return; }   // not direct: host falls back
-  layout_tables(m, true, m.bound, 0, 0);
+  const uint32_t S = m.bound > min_table ? m.bound : min_table;
+  if (S > 2 * m.W + 64) { ctl[BC_OVER] = 1; *mp = m; return; }   // not direct: host falls back
+  layout_tables(m, true, S, 0, 0);
   m.work_shared = false;
   const uint32_t Imax = W > 5 ? W - 5 : 1;
-  m.spill = slot + big_slot_bytes(W, m.bound) - 256 - spill_bytes(Imax);
+  m.spill = slot + big_slot_bytes(W, S) - 256 - spill_bytes(Imax);
   *m.fill = 0; *m.overflow = 0; *m.top_present = 0;
   *mp = m;
 }

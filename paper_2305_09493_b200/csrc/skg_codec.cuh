@@ -229,4 +229,58 @@ __global__ void ctx_literals_kernel(const int64_t* __restrict__ width, const uin
   }
 }
 
+// ---- self-test: repr(float) of every float32 value (SURVEY.md 7 hard part 2) ---------------
+// disasm renders f32 literals as CPython repr() of the value widened to double
+// (codec.py:174-178, disasm.py:93-94; skg_fmt.cuh).  For each f32 bit pattern the
+// kernel checks the two properties that define the shortest round-trip repr, with
+// the assembler's independent float() parser (skg_text.cuh parse_float): the text
+// parses back to exactly the same double, and neither (n-1)-digit neighbour of its
+// n significant digits does.  nan / inf / zero must read "nan" / "inf" / "0.0".
+struct BufSink {
+  uint8_t b[48];
+  uint32_t n = 0;
+  __device__ void put(uint8_t c) { if (n < sizeof(b)) b[n] = c; ++n; }
+  __device__ void putn(const uint8_t* s, uint32_t k) { for (uint32_t i = 0; i < k; ++i) put(s[i]); }
+  __device__ void fill(uint8_t c, uint32_t k) { for (uint32_t i = 0; i < k; ++i) put(c); }
+};
+
+__device__ __forceinline__ bool sci_parses_to(bool neg, uint64_t digits, int32_t exp, const Uni& U, uint64_t bits) {
+  BufSink s;
+  if (neg) s.put('-');
+  put_u64(s, digits);
+  s.put('e');
+  if (exp < 0) { s.put('-'); put_u64(s, (uint64_t)(-exp)); } else put_u64(s, (uint64_t)exp);
+  uint64_t got = 0;
+  return parse_float(s.b, s.n, U, got) == FLT_OK && got == bits;
+}
+
+__global__ void selftest_repr_f32_kernel(Uni U, uint64_t start, uint64_t count, unsigned long long* ctr,
+                                         unsigned int* first_fail) {
+  unsigned long long fails = 0;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = (uint32_t)(start + k);
+    const uint64_t bits = f32_to_f64_bits(f);
+    const FloatParts p = repr_parts(bits);
+    BufSink s;
+    put_repr_parts(s, p);
+    bool ok;
+    if (p.kind == 1) ok = s.n == 3 && s.b[0] == 'n' && s.b[1] == 'a' && s.b[2] == 'n';
+    else if (p.kind == 2) ok = s.n == 3u + p.neg && s.b[p.neg] == 'i';
+    else if (p.kind == 3) ok = s.n == 3u + p.neg && s.b[p.neg] == '0' && s.b[p.neg + 2] == '0';
+    else {
+      uint64_t got = 0;
+      ok = s.n <= sizeof(s.b) && parse_float(s.b, s.n, U, got) == FLT_OK && got == bits;
+      if (ok && p.digits >= 10) {   // shortest: no (n-1)-digit string reads back as the value
+        const uint64_t lo = p.digits / 10;
+        ok = !sci_parses_to(p.neg, lo, p.exp + 1, U, bits) && !sci_parses_to(p.neg, lo + 1, p.exp + 1, U, bits);
+      }
+    }
+    if (!ok) { ++fails; atomicMin(first_fail, f); }
+  }
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fails += __shfl_xor_sync(0xFFFFFFFFu, fails, o);
+  if ((threadIdx.x & 31) == 0 && fails) atomicAdd(ctr, fails);
+}
+
 }  // namespace skg

@@ -476,3 +476,63 @@ def test_fused_matches_separate_on_families(sk):
     diags = sk.validate_batch(mods)
     assert [t for t, _ in fused] == texts
     assert [d for _, d in fused] == diags
+
+
+def test_large_module_ids_above_header_bound_stay_grid_wide(sk, monkeypatch):
+    """A large module whose ids reach its header bound is redone grid-wide with id tables
+    widened to 2W + 64 (BoundTooSmall still names the header bound) instead of the
+    one-warp batch path (which this test disables)."""
+    import struct
+    from oracle import disasm as odis, validate as oval
+    from paper_2305_09493_b200 import _native
+    from synth.huge import build_huge
+    monkeypatch.setattr(_native, "LARGE_MODULE_WORDS", 1 << 14)
+
+    def no_warp_path(*a, **k):
+        raise AssertionError("the one-warp batch path was used")
+    monkeypatch.setattr(_native, "run_disasm", no_warp_path)
+    monkeypatch.setattr(_native, "run_validate", no_warp_path)
+    m = build_huge(40, chain=100, seed=9)
+    w = list(struct.unpack(f"<{len(m) // 4}I", m))
+    for bound in (100, w[3] - 1):
+        w[3] = bound
+        mm = struct.pack(f"<{len(w)}I", *w)
+        d = sk.validate_batch([mm])[0]
+        assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(mm)]
+        for o in (sk.DisassemblerOptions(), sk.DisassemblerOptions(inline_names=False)):
+            assert sk.disassemble_batch([mm], o)[0] == odis.disassemble(mm, o)
+
+
+def test_f32_repr_exhaustive_on_device(sk):
+    """All 2^32 float32 bit patterns (SURVEY.md 7 hard part 2): the disassembler's repr of
+    the widened value reads back exactly through the assembler's independent float()
+    parser and is the shortest such text (skg_selftest_repr_f32); plus an exact
+    comparison with CPython repr on 300k random patterns through the disasm kernel."""
+    import ctypes
+    import random
+    import struct as st
+    import torch
+    from paper_2305_09493_b200 import _native
+    L = _native.lib()
+    th = _native.tables_handle(None, None)
+    fails = torch.zeros(1, dtype=torch.int64, device="cuda")
+    first = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    step = 1 << 28
+    for start in range(0, 1 << 32, step):
+        assert L.skg_selftest_repr_f32(th, start, step, fails.data_ptr(), first.data_ptr(),
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    torch.cuda.synchronize()
+    assert int(fails.item()) == 0, hex(int(first.item()) & 0xFFFFFFFF)
+    rng = random.Random(5)
+    vals = [rng.getrandbits(32) for _ in range(300_000)]
+    vals = [v for v in vals if (v >> 23) & 0xFF != 0xFF]
+    want = [repr(st.unpack("<f", st.pack("<I", v))[0]) for v in vals]
+    # one OpConstant per value under a 32-bit float type, numeric refs, no header/indent
+    words = [0x07230203, 0x00010200, 0, len(vals) + 3, 0, (3 << 16) | 22, 1, 32]
+    for k, v in enumerate(vals):
+        words += [(4 << 16) | 43, 1, 2 + k, v]
+    m = st.pack(f"<{len(words)}I", *words)
+    text = sk.disassemble_batch([m], sk.DisassemblerOptions(inline_names=False, no_indent=True,
+                                                             no_header=True))[0]
+    got = [ln.rsplit(" ", 1)[1] for ln in text.splitlines()[1:]]
+    assert got == want
