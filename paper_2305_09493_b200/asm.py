@@ -128,8 +128,11 @@ class RoundTripSession:
     D2H copies of exactly the bytes used (a chunk that overflows is re-run with
     grown arenas).  Returns (text uint8[], text spans int64[n, 2], disasm status
     int32[n], binaries uint8[], binary spans int64[n, 2], asm status int32[n])
-    with spans relative to the returned arenas.  ``stage()`` + ``run_staged()``
-    split the same call (pinned staging, then the pipeline).
+    with spans relative to the returned arenas.  The arrays are views of the
+    session's pinned host arenas (each chunk's D2H lands at its running offset,
+    no host-side concatenation): they stay valid until the next call.
+    ``stage()`` + ``run_staged()`` split the same call (pinned staging, then the
+    pipeline).
     """
 
     TEXT_FACTOR = 6
@@ -141,6 +144,7 @@ class RoundTripSession:
         self.nchunks = max(1, int(chunks))
         self._buf = {}
         self._staged = None
+        self._ratio = (4.0, 1.1)   # host arena sizes per input byte (grown from the runs seen)
 
     def _get(self, name, n, dtype, pinned=False):
         """grow-only buffer (device, or pinned host)"""
@@ -216,8 +220,7 @@ class RoundTripSession:
         ev_meta = torch.cuda.Event()
         ev_meta.record(s_in)
         comp.wait_event(ev_meta)
-        plans, bases, state = [], [0, 0], {}
-        text_host, out_host = [], []
+        plans = []
 
         def launch(k, grow=None):
             a, b = chunks[k]
@@ -265,19 +268,38 @@ class RoundTripSession:
                 plans[k] = launch(k, grow=(tused, oused, 0))
                 return drain(k)
             a, b = chunks[k]
-            ht = self._get(f"h_text{k}", tused, torch.uint8, pinned=True)
-            ho = self._get(f"h_out{k}", oused, torch.uint8, pinned=True)
+            # the results land in one host arena each, at running offsets (no host-side
+            # concatenation: the returned arrays are views of the session's pinned arenas)
+            ht = arena("h_text", pos[0], tused)
+            ho = arena("h_out", pos[1], oused)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev)
-                ht[:tused].copy_(dp.text[:tused], non_blocking=True)
+                ht[pos[0]:pos[0] + tused].copy_(dp.text[:tused], non_blocking=True)
                 h_tspan[2 * a:2 * b].copy_(dp.span[: 2 * (b - a)], non_blocking=True)
                 h_tst[a:b].copy_(dp.status[: b - a], non_blocking=True)
-                ho[:oused].copy_(ap.out[:oused], non_blocking=True)
+                ho[pos[1]:pos[1] + oused].copy_(ap.out[:oused], non_blocking=True)
                 h_bspan[2 * a:2 * b].copy_(ap.span[: 2 * (b - a)], non_blocking=True)
                 h_bst[a:b].copy_(ap.status[: b - a], non_blocking=True)
-            text_host.append((ht, tused, a, b))
-            out_host.append((ho, oused, a, b))
+            parts[k] = (pos[0], tused, pos[1], oused)
+            pos[0] += tused
+            pos[1] += oused
 
+        def arena(name, used, need):
+            """grow-only pinned host arena; growing keeps the bytes already copied"""
+            h = self._buf.get(name)
+            if h is None or h.numel() < used + need:
+                s_out.synchronize()
+                est = int(hint.get(name, 0) * 1.05) + 4096
+                nh = torch.empty(max(est, 2 * (used + need)) if h is not None else max(est, used + need),
+                                 dtype=torch.uint8).pin_memory()
+                if h is not None and used:
+                    nh[:used].copy_(h[:used])
+                self._buf[name] = h = nh
+            return h
+
+        total_in = int(lengths.sum())
+        hint = {"h_text": total_in * self._ratio[0], "h_out": total_in * self._ratio[1]}
+        pos, parts = [0, 0], {}
         for k in range(len(chunks)):
             plans.append(launch(k))
             if k >= 1:
@@ -286,24 +308,22 @@ class RoundTripSession:
         s_out.synchronize()
         # a module whose text outgrew the per-module bound the assembler slots were sized
         # for reports an internal status: re-run its chunk with slots for the real maximum
+        # (its results are appended to the arenas; spans are rebased below)
         for k, (a, b) in enumerate(chunks):
             if (h_bst[a:b].numpy() == _native.ST_INTERNAL).any():
                 mx = int(h_tspan[2 * a + 1:2 * b:2].numpy().max())
-                _, tused, _, _ = text_host[k]
-                _, oused, _, _ = out_host[k]
+                _, tused, _, oused = parts[k]
                 plans[k] = launch(k, grow=(tused, max(oused, 4 * mx), mx))
-                pos_t, pos_o = len(text_host), len(out_host)
                 drain(k)
-                text_host[k], out_host[k] = text_host.pop(pos_t), out_host.pop(pos_o)
                 s_out.synchronize()
-        tspan = h_tspan[: 2 * n].numpy().reshape(n, 2).copy()
-        bspan = h_bspan[: 2 * n].numpy().reshape(n, 2).copy()
-        text = np.empty(sum(u for _, u, _, _ in text_host), dtype=np.uint8)
-        binv = np.empty(sum(u for _, u, _, _ in out_host), dtype=np.uint8)
-        for arena, parts, spans in ((text, text_host, tspan), (binv, out_host, bspan)):
-            pos = 0
-            for h, used, a, b in parts:
-                arena[pos:pos + used] = h.numpy()[:used]
-                spans[a:b, 0] += pos
-                pos += used
-        return text, tspan, h_tst[:n].numpy().copy(), binv, bspan, h_bst[:n].numpy().copy()
+        tspan = h_tspan[: 2 * n].numpy().reshape(n, 2)
+        bspan = h_bspan[: 2 * n].numpy().reshape(n, 2)
+        for k, (a, b) in enumerate(chunks):
+            tp, _, op, _ = parts[k]
+            tspan[a:b, 0] += tp
+            bspan[a:b, 0] += op
+        if total_in:
+            self._ratio = (max(self._ratio[0], pos[0] / total_in), max(self._ratio[1], pos[1] / total_in))
+        text = self._buf["h_text"].numpy()[: pos[0]]
+        binv = self._buf["h_out"].numpy()[: pos[1]]
+        return text, tspan, h_tst[:n].numpy(), binv, bspan, h_bst[:n].numpy()

@@ -1429,62 +1429,107 @@ __device__ __noinline__ void put_module_error(S& s, const FmtCtx& F, uint32_t x,
 }
 
 // ============================================================================
-// Phase C: header comments (lane 0).  Returns X_NONE / X_VERSION_LIMIT and
-// fills major/minor validity, generator and schema (asm.py:184-206).
-__device__ __noinline__ uint32_t scan_header(AsmMod& m, const AsmCtx& X, uint32_t dv) {
+// Phase C: header comments (asm.py:184-206), one line per lane in rounds of 32
+// lines; the outcome is the reference's sequential loop: lines up to the first
+// non-comment line, the first int() digit-limit error stops the scan, and a later
+// match of a pattern overrides an earlier one.  Returns X_NONE / X_VERSION_LIMIT /
+// X_VERSION / X_VERSION_DEFAULT and fills major/minor validity, generator, schema.
+struct HdrLine {
+  uint32_t key;        // 0 none, 1 version, 2 generator, 3 schema, 4 digit-limit error, 5 stop
+  uint32_t a, b, c, d; // version: d1.s, d1.e, d2.s, d2.e (line-relative) | generator word | schema
+  uint32_t f;          // version: major/minor validity (major ok << 16 | minor + 1) | limit: digits
+};
+
+__device__ __forceinline__ HdrLine header_line(const AsmMod& m, const AsmCtx& X, uint32_t li) {
   const Uni& U = X.U;
+  HdrLine r{0, 0, 0, 0, 0, 0};
+  const uint8_t* p = m.txt + m.ls[li];
+  const uint32_t n = m.le[li] - m.ls[li];
+  uint32_t a, b;
+  py_strip(p, n, U, a, b);
+  if (b > a && p[a] != ';') { r.key = 5; return r; }
+  if (b == a) return r;
+  // the three patterns, anchored at a, must consume up to b
+  for (int key = 0; key < 3; ++key) {
+    uint32_t i = a;
+    if (!match_lit(p, b, i, ";")) break;
+    i = skip_ws(p, b, i, U);
+    const char* kw = key == 0 ? "Version:" : key == 1 ? "Generator:" : "Schema:";
+    if (!match_lit(p, b, i, kw)) continue;
+    i = skip_ws(p, b, i, U);
+    Dec d1, d2;
+    if (!match_dec(p, b, i, U, d1)) continue;
+    if (key == 0) {
+      if (!match_lit(p, b, i, ".")) continue;
+      if (!match_dec(p, b, i, U, d2)) continue;
+    } else if (key == 1) {
+      if (!match_lit(p, b, i, ";")) continue;
+      i = skip_ws(p, b, i, U);
+      if (!match_dec(p, b, i, U, d2)) continue;
+    }
+    i = skip_ws(p, b, i, U);
+    if (i != b) continue;
+    // int() of each group, in order (the 4300-digit limit raises here)
+    if (d1.ndig > PY_MAX_STR_DIGITS) { r.key = 4; r.f = d1.ndig; return r; }
+    if (key != 2 && d2.ndig > PY_MAX_STR_DIGITS) { r.key = 4; r.f = d2.ndig; return r; }
+    if (key == 0) {
+      r.key = 1;
+      r.a = d1.s; r.b = d1.e; r.c = d2.s; r.d = d2.e;
+      r.f = ((d1.fits && d1.mod32 == 1) ? 1u << 16 : 0u) | ((d2.fits && d2.mod32 <= 6) ? d2.mod32 + 1 : 0u);
+    } else if (key == 1) {
+      r.key = 2;
+      r.a = ((d1.mod32 & 0xFFFFu) << 16) | d2.mod32;
+    } else {
+      r.key = 3;
+      r.a = d1.mod32;
+    }
+    break;
+  }
+  return r;
+}
+
+__device__ __noinline__ uint32_t scan_header(AsmMod& m, const AsmCtx& X, uint32_t dv) {
+  const uint32_t lane = lane_id_a();
   uint32_t* ms = m.misc;
   bool vset = false;
-  for (uint32_t li = 0; li < m.L; ++li) {
-    const uint8_t* p = m.txt + m.ls[li];
-    const uint32_t n = m.le[li] - m.ls[li];
-    uint32_t a, b;
-    py_strip(p, n, U, a, b);
-    if (b > a && p[a] != ';') break;
-    if (b == a) continue;
-    // the three patterns, anchored at a, must consume up to b
-    for (int key = 0; key < 3; ++key) {
-      uint32_t i = a;
-      if (!match_lit(p, b, i, ";")) break;
-      i = skip_ws(p, b, i, U);
-      const char* kw = key == 0 ? "Version:" : key == 1 ? "Generator:" : "Schema:";
-      if (!match_lit(p, b, i, kw)) continue;
-      i = skip_ws(p, b, i, U);
-      Dec d1, d2;
-      if (!match_dec(p, b, i, U, d1)) continue;
-      if (key == 0) {
-        if (!match_lit(p, b, i, ".")) continue;
-        if (!match_dec(p, b, i, U, d2)) continue;
-      } else if (key == 1) {
-        if (!match_lit(p, b, i, ";")) continue;
-        i = skip_ws(p, b, i, U);
-        if (!match_dec(p, b, i, U, d2)) continue;
-      }
-      i = skip_ws(p, b, i, U);
-      if (i != b) continue;
-      // int() of each group, in order (the 4300-digit limit raises here)
-      if (d1.ndig > PY_MAX_STR_DIGITS) { ms[MS_XA] = d1.ndig; return X_VERSION_LIMIT; }
-      if (key != 2 && d2.ndig > PY_MAX_STR_DIGITS) { ms[MS_XA] = d2.ndig; return X_VERSION_LIMIT; }
-      const uint32_t base = m.ls[li];
-      if (key == 0) {
-        vset = true;
-        ms[MS_MAJOR] = (d1.fits && d1.mod32 == 1) ? 1 : 0;
-        ms[MS_MINOR] = (d2.fits && d2.mod32 <= 6) ? d2.mod32 + 1 : 0;
-        ms[MS_V0] = base + d1.s; ms[MS_V0 + 1] = base + d1.e;
-        ms[MS_V0 + 2] = base + d2.s; ms[MS_V0 + 3] = base + d2.e;
-      } else if (key == 1) {
-        ms[MS_GEN] = ((d1.mod32 & 0xFFFFu) << 16) | d2.mod32;
-        ms[MS_GENSET] = 1;
-      } else {
-        ms[MS_SCHEMA] = d1.mod32;
-      }
-      break;
+  for (uint32_t base = 0; base < m.L; base += 32) {
+    const uint32_t li = base + lane;
+    const HdrLine h = li < m.L ? header_line(m, X, li) : HdrLine{0, 0, 0, 0, 0, 0};
+    const uint32_t stop = __ballot_sync(FULLM, h.key == 5);
+    const uint32_t upto = stop ? (1u << (__ffs(stop) - 1)) - 1 : FULLM;   // lanes before the stop line
+    const uint32_t lim = __ballot_sync(FULLM, h.key == 4) & upto;
+    // the last match of each key among lanes [0, first limit error) wins
+    const uint32_t valid = lim ? (1u << (__ffs(lim) - 1)) - 1 : upto;
+    const uint32_t kv = __ballot_sync(FULLM, h.key == 1) & valid;
+    const uint32_t kg = __ballot_sync(FULLM, h.key == 2) & valid;
+    const uint32_t ks = __ballot_sync(FULLM, h.key == 3) & valid;
+    if (kv && lane == 31 - __clz(kv)) {
+      const uint32_t lb = m.ls[li];
+      ms[MS_MAJOR] = h.f >> 16;
+      ms[MS_MINOR] = h.f & 0xFFFF;
+      ms[MS_V0] = lb + h.a; ms[MS_V0 + 1] = lb + h.b;
+      ms[MS_V0 + 2] = lb + h.c; ms[MS_V0 + 3] = lb + h.d;
     }
+    if (kg && lane == 31 - __clz(kg)) { ms[MS_GEN] = h.a; ms[MS_GENSET] = 1; }
+    if (ks && lane == 31 - __clz(ks)) ms[MS_SCHEMA] = h.a;
+    vset |= kv != 0;
+    if (lim) {
+      if (lane == __ffs(lim) - 1) ms[MS_XA] = h.f;
+      __syncwarp();
+      return X_VERSION_LIMIT;
+    }
+    if (stop) break;
   }
+  __syncwarp();
   if (!vset) {   // Assembler.default_version
     const uint32_t mj = dv >> 16, mn = dv & 0xFFFF;
-    if (!(mj == 1 && mn <= 6)) { ms[MS_V0] = mj; ms[MS_V0 + 1] = mn; return X_VERSION_DEFAULT; }
-    ms[MS_MAJOR] = 1; ms[MS_MINOR] = mn + 1;
+    if (!(mj == 1 && mn <= 6)) {
+      if (lane == 0) { ms[MS_V0] = mj; ms[MS_V0 + 1] = mn; }
+      __syncwarp();
+      return X_VERSION_DEFAULT;
+    }
+    if (lane == 0) { ms[MS_MAJOR] = 1; ms[MS_MINOR] = mn + 1; }
+    __syncwarp();
     return X_NONE;
   }
   if (!(ms[MS_MAJOR] == 1 && ms[MS_MINOR] != 0)) return X_VERSION;
@@ -2001,8 +2046,7 @@ end_b:
   CTA_SYNC();
   if (done) goto end_c;
   // -- C: header comments; then the first reservation failure --------------------
-  if (lane == 0) x = scan_header(m, X, a.default_version);
-  x = __shfl_sync(FULLM, x, 0);
+  x = scan_header(m, X, a.default_version);
   if (x != X_NONE) { finish_error(a, m, X, t, x, 0, fscratch, flimbs); done = true; goto end_c; }
   for (uint32_t base = 0; base < L; base += 32) {
     const uint32_t li = base + lane;

@@ -440,31 +440,45 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
   m.gen = m.w[2];
   m.bound = m.w[3];
   m.schema = m.w[4];
-  // instruction-boundary walk (pointer chase: pos += wc)
+  // instruction-boundary walk (codec.py:212-229: pos += wc), warp-cooperative: the
+  // window [p, p + 32) is loaded one word per lane (coalesced), the chase inside it
+  // runs on shuffles (no dependent memory loads), and the lanes that hold a start
+  // write their offsets; the next window starts at the next instruction.
   int32_t st = ST_OK;
   uint32_t I = 0, bad = 0, arena = 0;
-  if (lane == 0) {
-    uint32_t p = 5;
-    while (p < W) {
-      const uint32_t x = m.w[p];
-      const uint32_t wc = x >> 16;
+  uint32_t p = 5;
+  while (p < W) {
+    const uint32_t base = p;
+    const uint32_t x = base + lane < W ? m.w[base + lane] : 0;
+    uint32_t starts = 0;
+    while (p < W && p < base + 32) {   // p is warp-uniform
+      const uint32_t wc = __shfl_sync(FULL, x, p - base) >> 16;
       if (wc == 0) { st = ST_CORRUPT; bad = p; break; }
       if (p + wc > W) { st = ST_TRUNCATED; bad = p; break; }
-      if ((x & 0xFFFF) == 5 && wc > 2) arena += 4 * (wc - 2) + 1;   // OpName: sanitized name bound
-      m.ioff[I++] = p;
+      starts |= 1u << (p - base);
       p += wc;
     }
-    if (st != ST_OK && es) err = es->alloc();
-    if (st != ST_OK && err) {
+    const bool mine = (starts >> lane) & 1;
+    if (mine) {
+      m.ioff[I + __popc(starts & ((1u << lane) - 1))] = base + lane;
+      const uint32_t wc = x >> 16;
+      if ((x & 0xFFFF) == 5 && wc > 2) arena += 4 * (wc - 2) + 1;   // OpName: sanitized name bound
+    }
+    I += __popc(starts);
+    if (st != ST_OK) break;
+  }
+  arena = warp_sum_u32(arena);
+  if (st != ST_OK && lane == 0) {
+    if (es) err = es->alloc();
+    if (err) {
       ErrWriter ew{err};
       put_cstr(ew, "instruction at word "); put_u64(ew, bad);
       put_cstr(ew, st == ST_CORRUPT ? " has word count 0" : " runs past the end of the stream");
       err->module = module; err->cls = st; err->len = ew.n;
     }
   }
-  st = __shfl_sync(FULL, st, 0);
-  m.I = __shfl_sync(FULL, I, 0);
-  m.arena_need = __shfl_sync(FULL, arena, 0);
+  m.I = I;
+  m.arena_need = arena;
   __syncwarp();
   return st;
 }

@@ -239,13 +239,17 @@ def test_roundtrip_session_fresh_batches_and_regrowth(sk, monkeypatch):
     """RoundTripSession.run on new batches with no sizing pass: different batches through
     one session; a text-arena bound too small (overflow: the chunk is re-run with grown
     arenas) and an assembler slot too small (internal status: re-run with slots for the
-    real maximum) give the same results."""
+    real maximum) give the same results; host arenas that start too small grow
+    mid-run keeping the chunks already copied."""
     from oracle import disasm as odis
     from paper_2305_09493_b200.asm import RoundTripSession
     from synth.families import sample_batch
     sess = RoundTripSession(chunks=4)
     for seed, factor in ((11, 6), (12, 6), (13, 1)):
         monkeypatch.setattr(RoundTripSession, "TEXT_FACTOR", factor)
+        if seed == 12:   # host arenas grown chunk by chunk
+            sess._buf.pop("h_text", None), sess._buf.pop("h_out", None)
+            sess._ratio = (0.01, 0.01)
         b = sample_batch(2000 + 500 * (seed - 11), 200, seed)
         text, tspan, tst, binv, bspan, bst = sess.run(b.data, b.offsets, b.lengths)
         assert (tst == 0).all() and (bst == 0).all()

@@ -85,7 +85,7 @@ def num(d, k):
         return 0.0
 
 
-agg_i, agg_s = collections.Counter(), collections.Counter()
+agg_i, agg_s, agg_t = collections.Counter(), collections.Counter(), collections.Counter()
 for k, d in enumerate(data):
     key = locs[k] if k < len(locs) else None
     if op_prefix:
@@ -94,6 +94,8 @@ for k, d in enumerate(data):
             continue
     agg_i[key] += num(d, "Instructions Executed")
     agg_s[key] += num(d, "Warp Stall Sampling (All Samples)")
+    agg_t[key] += num(d, "Thread Instructions Executed")
 ti, ts = sum(agg_i.values()) or 1, sum(agg_s.values()) or 1
 for key in sorted(agg_s, key=lambda k: -agg_s[k])[:topn]:
-    print(f"{100 * agg_s[key] / ts:5.1f}% stall {100 * agg_i[key] / ti:5.1f}% inst {agg_i[key] / 1e6:8.1f}M  {key}")
+    print(f"{100 * agg_s[key] / ts:5.1f}% stall {100 * agg_i[key] / ti:5.1f}% inst {agg_i[key] / 1e6:8.1f}M "
+          f"{agg_t[key] / max(agg_i[key], 1):5.1f} lanes  {key}")
