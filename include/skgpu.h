@@ -273,6 +273,14 @@ int skg_selftest_repr_f32(const skg_tables* t, uint64_t start, uint64_t count, u
 int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow,
                     uint64_t* text_bytes, void* stream);
 
+/* Copy n_words 32-bit words from device memory into page-locked host memory
+ * (host_dst from cudaHostAlloc / a pinned tensor) with a kernel on `stream`:
+ * the stores travel over PCIe without a copy engine, so a pipeline can read a
+ * chunk's counters while a large D2H copy of the previous chunk is in flight
+ * (a cudaMemcpyAsync of the counters would queue behind it).  Not a reference
+ * interface: plumbing of the host-buffer round-trip session. */
+int skg_store_counters(void* host_dst, const void* dev_src, uint32_t n_words, void* stream);
+
 /* Version / build info string. */
 const char* skg_version(void);
 

@@ -76,6 +76,8 @@ def lib():
     L.skg_ctx_literals.argtypes = [P, P, P, U32, P, P, P, P]
     for f in (L.skg_tokenize, L.skg_encode_modules, L.skg_pack_strings, L.skg_ctx_literals):
         f.restype = I32
+    L.skg_store_counters.argtypes = [P, P, U32, P]
+    L.skg_store_counters.restype = I32
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
               L.skg_decode_large):

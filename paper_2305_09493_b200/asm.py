@@ -145,6 +145,7 @@ class RoundTripSession:
         self._buf = {}
         self._staged = None
         self._ratio = (4.0, 1.1)   # host arena sizes per input byte (grown from the runs seen)
+        self.kernel_events = None  # a list: (start, disasm end, asm end) CUDA events per chunk launch
 
     def _get(self, name, n, dtype, pinned=False):
         """grow-only buffer (device, or pinned host)"""
@@ -222,6 +223,16 @@ class RoundTripSession:
         comp.wait_event(ev_meta)
         plans = []
 
+        L = _native.lib()
+
+        def store_counters(h, at, ws):
+            # the chunk's allocator counters straight into pinned memory by a kernel: a
+            # copy-engine D2H here would queue behind the previous chunk's text copy
+            rc = L.skg_store_counters(_native.ctypes.c_void_p(h.data_ptr() + 4 * at),
+                                      _native.ctypes.c_void_p(ws.data_ptr()), 8, cs)
+            if rc:
+                raise RuntimeError(f"skg_store_counters failed ({rc})")
+
         def launch(k, grow=None):
             a, b = chunks[k]
             b0 = int(offsets[a])
@@ -250,10 +261,18 @@ class RoundTripSession:
                     d_data[b0:b1].copy_(h_data[b0:b1], non_blocking=True)
                     ev_in.record(s_in)
                 comp.wait_event(ev_in)
+            if self.kernel_events is not None:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(comp)
             dp.launch(cs)
-            h_cnt[16 * k: 16 * k + 8].copy_(dp.ws[:32].view(torch.int32), non_blocking=True)
+            store_counters(h_cnt, 16 * k, dp.ws)
+            if self.kernel_events is not None:
+                e1.record(comp)
             ap.launch(cs)
-            h_cnt[16 * k + 8: 16 * k + 16].copy_(ap.ws[:32].view(torch.int32), non_blocking=True)
+            if self.kernel_events is not None:
+                e2.record(comp)
+                self.kernel_events.append((e0, e1, e2))
+            store_counters(h_cnt, 16 * k + 8, ap.ws)
             ev = torch.cuda.Event()
             ev.record(comp)
             return dp, ap, ev

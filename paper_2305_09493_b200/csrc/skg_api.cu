@@ -155,6 +155,14 @@ int check(cudaError_t e) {
 
 }  // namespace
 
+namespace skg {
+// device -> mapped pinned host words (skg_store_counters)
+__global__ void store_words_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+}  // namespace skg
+
 extern "C" {
 
 const char* skg_version(void) { return "skgpu 0.1 (sm_100a)"; }
@@ -216,6 +224,19 @@ void skg_tables_destroy(skg_tables* t) {
 
 uint64_t skg_workspace_bytes(uint32_t n_mod, uint32_t max_words) {
   return ws_layout(n_mod, max_words).total;
+}
+
+int skg_store_counters(void* host_dst, const void* dev_src, uint32_t n_words, void* stream) {
+  if (!host_dst || !dev_src || n_words == 0 || n_words > 1024) return -1;
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
+    cudaGetLastError();   // not mapped: a plain async copy
+    return check(cudaMemcpyAsync(host_dst, dev_src, 4ull * n_words, cudaMemcpyDeviceToHost,
+                                 static_cast<cudaStream_t>(stream)));
+  }
+  skg::store_words_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint32_t*>(dptr), static_cast<const uint32_t*>(dev_src), n_words);
+  return check(cudaGetLastError());
 }
 
 int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_overflow,

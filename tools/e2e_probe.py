@@ -30,7 +30,14 @@ def main():
                 t0 = time.perf_counter()
                 sess.run(h, b.offsets, b.lengths)
                 best = min(best, time.perf_counter() - t0)
-            print(f"factor {f} chunks {chunks}: {best * 1e3:.1f} ms  {b.words / best / 1e9:.3f} Gw/s", flush=True)
+            sess.kernel_events = []
+            sess.run(h, b.offsets, b.lengths)
+            torch.cuda.synchronize()
+            kd = sum(e0.elapsed_time(e1) for e0, e1, _ in sess.kernel_events)
+            ka = sum(e1.elapsed_time(e2) for _, e1, e2 in sess.kernel_events)
+            span = sess.kernel_events[0][0].elapsed_time(sess.kernel_events[-1][2])
+            print(f"factor {f} chunks {chunks}: {best * 1e3:.1f} ms  {b.words / best / 1e9:.3f} Gw/s  "
+                  f"kernels: disasm {kd:.1f} ms asm {ka:.1f} ms, first start -> last end {span:.1f} ms", flush=True)
             del sess
             torch.cuda.empty_cache()
 
