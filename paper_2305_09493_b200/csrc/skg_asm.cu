@@ -504,6 +504,10 @@ __device__ __noinline__ void tokenize_line(AsmMod& m, const AsmCtx& X, uint32_t 
                                            uint32_t cap, uint32_t& npct) {
   const uint8_t* t = m.txt;
   const uint32_t s0 = m.ls[li], e0 = m.le[li];
+#ifndef SKG_EXP_NO_PREFETCH
+  prefetch_l1(t + s0);
+  if (e0 > s0 + 64) prefetch_l1(t + e0 - 1);
+#endif
   uint32_t nt = 0;
   uint32_t fl = 0;
   uint32_t i = s0;
@@ -1973,6 +1977,9 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
   if (used > a.gslot_bytes || len64 < 0 || len64 > 0x3FFFFFFF) { fail_internal(); done = true; goto end_a; }
   for (uint32_t k = lane; k < 64; k += 32) m.misc[k] = 0;
   __syncwarp();
+#ifndef SKG_EXP_NO_PREFETCH
+  prefetch_l2(src, T);
+#endif
   L = split_lines(m, src, T + 1, m.lt0, ntb0);
   m.L = L;
 end_a:

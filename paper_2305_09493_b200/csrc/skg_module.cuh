@@ -403,6 +403,9 @@ __device__ __noinline__ int32_t load_and_split(Mod& m, const uint8_t* src, uint6
     return ST_TRUNCATED;
   }
   const uint32_t W = (uint32_t)(nbytes / 4);
+#ifndef SKG_EXP_NO_PREFETCH
+  prefetch_l2(src, nbytes);
+#endif
   // little-endian, word-aligned input (the batch case): read the words in place
   // (the input arena is read-only for the kernel; no scratch copy)
   if ((reinterpret_cast<uintptr_t>(src) & 3) == 0 &&

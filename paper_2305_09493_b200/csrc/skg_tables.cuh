@@ -17,6 +17,18 @@ __device__ __forceinline__ void group_sync(uint32_t group, uint32_t warps) {
 }
 
 
+// Ask L2 for every 128-byte line of [p, p + n), one prefetch per lane per 4 KB:
+// a module's bytes are then in flight at once instead of one load round trip per
+// step of the (dependent) scans that read them.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint64_t n) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~127ull, e = reinterpret_cast<uint64_t>(p) + n;
+  for (uint64_t q = a + 128ull * (threadIdx.x & 31); q < e; q += 128ull * 32)
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(q));
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
+}
+
 // instruction special codes (tables.py SPECIAL)
 enum : uint32_t {
   SP_NONE = 0, SP_TYPEINT = 1, SP_TYPEFLOAT = 2, SP_EXTINSTIMPORT = 3, SP_NAME = 4, SP_SWITCH = 5,
