@@ -36,7 +36,9 @@ def _parse(text: str):
 def _as_bytes(module):
     if isinstance(module, (bytes, bytearray)):
         return bytes(module)
-    to_bytes = getattr(module, "to_bytes", None)     # a builder ModuleScope
+    # a builder ModuleScope (serialized as the reference does, validate.py:64-70);
+    # int also has a to_bytes method but is not a module
+    to_bytes = None if isinstance(module, int) else getattr(module, "to_bytes", None)
     if callable(to_bytes):
         return to_bytes()
     raise TypeError("validate_module expects bytes or a ModuleScope")
