@@ -1919,6 +1919,7 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
 // Line order grouped by instruction (counting sort over a hash of the
 // instruction index; order within a bucket is arbitrary): perm[0..L).
 constexpr uint32_t OPG_BUCKETS = 64;
+constexpr uint32_t FX_KEYS = 1024;   // phase F cross-module sort: one key per instruction (clamped)
 template <class K>
 __device__ __forceinline__ void group_lines(AsmMod& m, uint32_t* perm, K&& key) {
   const uint32_t lane = lane_id_a();
@@ -1948,7 +1949,7 @@ __device__ __noinline__ void group_lines_by_opcode(AsmMod& m, uint32_t* perm) {
 }
 
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot,
-                                             uint32_t gid, uint32_t gw, AsmMod& m) {
+                                             uint32_t gid, uint32_t gw, AsmMod& m, const AsmMod* all) {
   const uint32_t lane = lane_id_a();
   PHASE_START();
   bool done = t >= a.n_mod;
@@ -2165,49 +2166,154 @@ end_d:
 end_e:
   PHASE_MARK(5);
   CTA_SYNC();
-  if (done) goto end_f;
   // -- F: encode pass 1 -------------------------------------------------------------
-  {   // words of a line are bounded by 2 per token (4 string bytes per word)
-    uint32_t carry = 0;
-    m.lwo = reinterpret_cast<uint32_t*>(take(4ull * L + 4));
-    for (uint32_t base = 0; base < L; base += 32) {
-      const uint32_t li = base + lane;
-      uint32_t ub = 0;
-      if (li < L) {
-        ub = 1;
-        for (uint32_t k = 0; k < m.lnt[li]; ++k) {
-          const uint32_t lf = m.tok[2 * (m.lt0[li] + k) + 1];
-          ub += (lf & TK_STR) ? (lf & TK_LEN) / 4 + 1 : 2;
+  // When the barrier group is the whole CTA, the lines of all its modules are encoded
+  // together: every warp lists its lines that need the Encoder walk, the CTA sorts
+  // them by instruction (shared-memory counting sort), and each warp then encodes 32
+  // consecutive lines of that order -- lanes of one warp run the same instruction's
+  // walk, mostly for different modules, and warps whose module is finished (or
+  // smaller) take their share of the others' lines.  Results go to each line's own
+  // module scratch, exactly as in the per-module loop (kept for other group sizes).
+  {
+    const uint32_t nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+    const bool fcross = gw == nwb;
+    __shared__ uint32_t s_fhist[FX_KEYS];
+    __shared__ uint32_t s_fpre[33];
+    __shared__ uint32_t* s_fout[32];
+    uint32_t nent = 0;
+    uint32_t* fin = nullptr;
+    uint32_t* fout = nullptr;
+    bool local = !fcross;
+    if (fcross) {
+      for (uint32_t k = threadIdx.x; k < FX_KEYS; k += blockDim.x) s_fhist[k] = 0;
+      CTA_SYNC();
+    }
+    if (!done) {   // words of a line are bounded by 2 per token (4 string bytes per word)
+      uint32_t carry = 0;
+      m.lwo = reinterpret_cast<uint32_t*>(take(4ull * L + 4));
+      for (uint32_t base = 0; base < L; base += 32) {
+        const uint32_t li = base + lane;
+        uint32_t ub = 0;
+        if (li < L) {
+          ub = 1;
+          for (uint32_t k = 0; k < m.lnt[li]; ++k) {
+            const uint32_t lf = m.tok[2 * (m.lt0[li] + k) + 1];
+            ub += (lf & TK_STR) ? (lf & TK_LEN) / 4 + 1 : 2;
+          }
+        }
+        const uint32_t incl = wincl(ub);
+        if (li < L) m.lwo[li] = carry + incl - ub;
+        carry += __shfl_sync(FULLM, incl, 31);
+      }
+      m.sw = reinterpret_cast<uint32_t*>(take(4ull * carry + 4));
+      m.swr = reinterpret_cast<uint32_t*>(take(carry / 8 + 8));
+      if (used > a.gslot_bytes) {
+        fail_internal();
+        done = true;
+      } else {
+        m.sused = used;
+        for (uint32_t k = lane; k <= carry / 32; k += 32) m.swr[k] = 0;
+        if (fcross) {   // the line lists (input, sorted share) fit the slot, else this module stays local
+          const uint64_t used0 = used;
+          fin = reinterpret_cast<uint32_t*>(take(4ull * L + 16));
+          fout = reinterpret_cast<uint32_t*>(take(4ull * L + 16));
+          if (used > a.gslot_bytes || L >= (1u << 27)) { used = used0; local = true; fin = fout = nullptr; }
+          m.sused = used;
+        }
+        if (fcross && !local) {
+          for (uint32_t base = 0; base < L; base += 32) {
+            const uint32_t li = base + lane;
+            bool enc = false;
+            uint32_t d = NONE32;
+            if (li < L) {
+              const uint32_t fl = m.lfl[li];
+              m.lnw[li] = 0; m.lrid[li] = 0;
+              if (!(fl & (LF_TOKERR | LF_EMPTY))) {
+                d = m.ld[li];
+                if (d == NONE32) m.lec[li] = E_NOINST;
+                else if (X.T.special(d) == SP_LABEL) {
+                  if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
+                } else {
+                  enc = true;
+                }
+              }
+            }
+            const unsigned bm = __ballot_sync(FULLM, enc);
+            if (enc) {
+              fin[nent + __popc(bm & ((1u << lane) - 1))] = (wib << 27) | li;
+              atomicAdd(&s_fhist[min(d, FX_KEYS - 1)], 1u);
+            }
+            nent += __popc(bm);
+          }
+        } else {
+          group_lines_by_opcode(m, lperm);
         }
       }
-      const uint32_t incl = wincl(ub);
-      if (li < L) m.lwo[li] = carry + incl - ub;
-      carry += __shfl_sync(FULLM, incl, 31);
     }
-    m.sw = reinterpret_cast<uint32_t*>(take(4ull * carry + 4));
-    m.swr = reinterpret_cast<uint32_t*>(take(carry / 8 + 8));
-    if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_f; }
-    m.sused = used;
-    for (uint32_t k = lane; k <= carry / 32; k += 32) m.swr[k] = 0;
-    group_lines_by_opcode(m, lperm);
-  }
-  // lanes take lines grouped by instruction (one code path per group instead of
-  // the union of 32 different encoders); results are stored per line
-  for (uint32_t base = 0; base < L; base += 32) {
-    if (base + lane >= L) continue;
-    const uint32_t li = lperm[base + lane];
-    const uint32_t fl = m.lfl[li];
-    m.lnw[li] = 0; m.lrid[li] = 0;
-    if (fl & (LF_TOKERR | LF_EMPTY)) continue;
-    const uint32_t d = m.ld[li];
-    if (d == NONE32) { m.lec[li] = E_NOINST; continue; }
-    if (X.T.special(d) == SP_LABEL) {
-      if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
-      continue;
+    if (fcross) {
+      if (lane == 0) { s_fout[wib] = fout; s_fpre[wib + 1] = nent; }
+      CTA_SYNC();
+      if (wib == 0) {   // bucket cursors (exclusive scan of the histogram) and the per-warp prefix
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < FX_KEYS; base += 32) {
+          const uint32_t c = s_fhist[base + lane];
+          const uint32_t incl = wincl(c);
+          s_fhist[base + lane] = carry + incl - c;
+          carry += __shfl_sync(FULLM, incl, 31);
+        }
+        const uint32_t c = lane < nwb ? s_fpre[lane + 1] : 0;
+        const uint32_t incl = wincl(c);
+        if (lane < nwb) s_fpre[lane + 1] = incl;
+        if (lane == 0) s_fpre[0] = 0;
+      }
+      CTA_SYNC();
+      for (uint32_t k = lane; k < nent; k += 32) {   // scatter into sorted order
+        const uint32_t e = fin[k];
+        const uint32_t p = atomicAdd(&s_fhist[min(m.ld[e & ((1u << 27) - 1)], FX_KEYS - 1)], 1u);
+        uint32_t o = 0;
+#pragma unroll
+        for (uint32_t step = 16; step; step >>= 1)
+          if (o + step < nwb && s_fpre[o + step] <= p) o += step;
+        s_fout[o][p - s_fpre[o]] = e;
+      }
+      CTA_SYNC();
+      const uint32_t total = s_fpre[nwb];
+      for (uint32_t c0 = 32 * wib; c0 < total; c0 += 32 * nwb) {
+        const uint32_t p = c0 + lane;
+        if (p >= total) continue;
+        uint32_t o = 0;
+#pragma unroll
+        for (uint32_t step = 16; step; step >>= 1)
+          if (o + step < nwb && s_fpre[o + step] <= p) o += step;
+        const uint32_t e = s_fout[o][p - s_fpre[o]];
+        const AsmMod& mm = all[e >> 27];
+        const uint32_t li = e & ((1u << 27) - 1);
+        const uint32_t w0 = mm.lwo[li] + 1;
+        encode_line(mm, X, li, mm.ld[li], M_COUNT, mm.sw + w0, mm.swr, w0, nullptr);
+      }
+      CTA_SYNC();
     }
-    const uint32_t w0 = m.lwo[li] + 1;
-    encode_line(m, X, li, d, M_COUNT, m.sw + w0, m.swr, w0, nullptr);
+    if (!done && local) {
+      // lanes take lines grouped by instruction (one code path per group instead of
+      // the union of 32 different encoders); results are stored per line
+      for (uint32_t base = 0; base < L; base += 32) {
+        if (base + lane >= L) continue;
+        const uint32_t li = lperm[base + lane];
+        const uint32_t fl = m.lfl[li];
+        m.lnw[li] = 0; m.lrid[li] = 0;
+        if (fl & (LF_TOKERR | LF_EMPTY)) continue;
+        const uint32_t d = m.ld[li];
+        if (d == NONE32) { m.lec[li] = E_NOINST; continue; }
+        if (X.T.special(d) == SP_LABEL) {
+          if ((fl & LF_RESULT) && !(fl & LF_RESOLVE_ERR)) m.lrid[li] = result_id_of(m, X, m.lt0[li]);
+          continue;
+        }
+        const uint32_t w0 = m.lwo[li] + 1;
+        encode_line(m, X, li, d, M_COUNT, m.sw + w0, m.swr, w0, nullptr);
+      }
+    }
   }
+  if (done) goto end_f;
   __syncwarp();
   // first OverflowError (escapes the emit loop's except clause)
   for (uint32_t base = 0; base < L; base += 32) {
@@ -2396,7 +2502,7 @@ __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(const _
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
     const uint32_t tk = base + gwarp_in;
-    assemble_module(s_args, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block]);
+    assemble_module(s_args, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block], s_amod);
   }
 }
 
