@@ -1919,7 +1919,6 @@ __device__ __noinline__ void finish_error(const AsmArgs& a, AsmMod& m, const Asm
 // Line order grouped by instruction (counting sort over a hash of the
 // instruction index; order within a bucket is arbitrary): perm[0..L).
 constexpr uint32_t OPG_BUCKETS = 64;
-constexpr uint32_t FX_KEYS = 1024;   // phase F cross-module sort: one key per instruction (clamped)
 template <class K>
 __device__ __forceinline__ void group_lines(AsmMod& m, uint32_t* perm, K&& key) {
   const uint32_t lane = lane_id_a();
@@ -1949,7 +1948,7 @@ __device__ __noinline__ void group_lines_by_opcode(AsmMod& m, uint32_t* perm) {
 }
 
 __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, uint32_t t, uint8_t* slot,
-                                             uint32_t gid, uint32_t gw, AsmMod& m, const AsmMod* all) {
+                                             uint32_t gid, uint32_t gw, AsmMod& m, AsmMod* all, CtaSort& cs) {
   const uint32_t lane = lane_id_a();
   PHASE_START();
   bool done = t >= a.n_mod;
@@ -1986,8 +1985,9 @@ __device__ __noinline__ void assemble_module(const AsmArgs& a, const AsmCtx& X, 
 end_a:
   PHASE_MARK(0);
   CTA_SYNC();
-  if (done) goto end_b;
   {
+  bool bready = false;
+  if (!done) {
   // per-line arrays (lt0: token-slot bases from split_lines)
   m.lnt = reinterpret_cast<uint32_t*>(take(4ull * L));
   m.lfl = reinterpret_cast<uint32_t*>(take(4ull * L));
@@ -2012,27 +2012,38 @@ end_a:
   m.blk = reinterpret_cast<uint32_t*>(take(12ull * L + 16));
   m.big_cap = BIG_CAP;
   m.big = reinterpret_cast<uint32_t*>(take(4ull * (2 + 2 * BIG_CAP)));
-  if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_b; }
-  for (uint32_t k = lane; k < m.RB / 32; k += 32) { m.rbm[k] = 0; m.reg[k] = 0; m.lab[k] = 0; }
-  if (lane < 2) m.big[lane] = 0;
-  __syncwarp();
-  if (lane == 0) m.rbm[0] = 1;   // id 0 is never allocated
-  __syncwarp();
+  if (used > a.gslot_bytes || L >= (1u << 27)) {
+    fail_internal();
+    done = true;
+  } else {
+    for (uint32_t k = lane; k < m.RB / 32; k += 32) { m.rbm[k] = 0; m.reg[k] = 0; m.lab[k] = 0; }
+    if (lane < 2) m.big[lane] = 0;
+    __syncwarp();
+    if (lane == 0) m.rbm[0] = 1;   // id 0 is never allocated
+    __syncwarp();
+    bready = true;
+  }
+  }
 
   PHASE_MARK(1);
   // -- B: tokenize + reservations ------------------------------------------------
+  // (lane per line within the module: a cross-module assignment of the lines,
+  // sorted by length or not, measured 2-3% slower -- the module's text stays in L1)
   uint32_t nres = 0;
-  for (uint32_t base = 0; base < L; base += 32) {
-    const uint32_t li = base + lane;
-    if (li < L) {
-      m.lec[li] = E_OK;
-      const uint32_t cap = (li + 1 < L ? m.lt0[li + 1] : ntb) - m.lt0[li];
-      tokenize_line(m, X, li, m.lt0[li], cap, npct);
-      nres += (m.lfl[li] & LF_RESULT) ? 1 : 0;
+  if (bready) {
+    for (uint32_t base = 0; base < L; base += 32) {
+      const uint32_t li = base + lane;
+      if (li < L) {
+        m.lec[li] = E_OK;
+        const uint32_t cap = (li + 1 < L ? m.lt0[li + 1] : m.ntb) - m.lt0[li];
+        tokenize_line(m, X, li, m.lt0[li], cap, npct);
+        nres += (m.lfl[li] & LF_RESULT) ? 1 : 0;
+      }
     }
+    npct = wsum(npct);
+    nres = wsum(nres);
   }
-  npct = wsum(npct);
-  nres = wsum(nres);
+  if (bready) {
   m.ncap = 32;   // result names at load <= 2/3 (+ unresolved operand names: lane 0 grows the table)
   while (2 * m.ncap < 3 * nres + 48) m.ncap <<= 1;
   if (lane == 0) m.misc[MS_NTCOUNT] = nres;
@@ -2041,15 +2052,18 @@ end_a:
   flimbs = T / 2 + 64;
   fscratch = reinterpret_cast<uint32_t*>(take(4ull * flimbs));
   m.sbase = slot; m.sused = used; m.scap = a.gslot_bytes;
-  if (used > a.gslot_bytes) { fail_internal(); done = true; goto end_b; }
-  for (uint32_t k = lane; k < m.ncap; k += 32) {
-    uint32_t* e = m.nt + NT_W * k;
-    e[0] = EMPTYK; e[1] = 0; e[2] = NONE32; e[3] = 0; e[4] = 0; e[5] = 0;
+  if (used > a.gslot_bytes) {
+    fail_internal();
+    done = true;
+  } else {
+    for (uint32_t k = lane; k < m.ncap; k += 32) {
+      uint32_t* e = m.nt + NT_W * k;
+      e[0] = EMPTYK; e[1] = 0; e[2] = NONE32; e[3] = 0; e[4] = 0; e[5] = 0;
+    }
+    __syncwarp();
   }
-  __syncwarp();
-
   }
-end_b:
+  }
   PHASE_MARK(2);
   CTA_SYNC();
   if (done) goto end_c;
@@ -2177,17 +2191,10 @@ end_e:
   {
     const uint32_t nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
     const bool fcross = gw == nwb;
-    __shared__ uint32_t s_fhist[FX_KEYS];
-    __shared__ uint32_t s_fpre[33];
-    __shared__ uint32_t* s_fout[32];
     uint32_t nent = 0;
     uint32_t* fin = nullptr;
     uint32_t* fout = nullptr;
     bool local = !fcross;
-    if (fcross) {
-      for (uint32_t k = threadIdx.x; k < FX_KEYS; k += blockDim.x) s_fhist[k] = 0;
-      CTA_SYNC();
-    }
     if (!done) {   // words of a line are bounded by 2 per token (4 string bytes per word)
       uint32_t carry = 0;
       m.lwo = reinterpret_cast<uint32_t*>(take(4ull * L + 4));
@@ -2241,7 +2248,6 @@ end_e:
             const unsigned bm = __ballot_sync(FULLM, enc);
             if (enc) {
               fin[nent + __popc(bm & ((1u << lane) - 1))] = (wib << 27) | li;
-              atomicAdd(&s_fhist[min(d, FX_KEYS - 1)], 1u);
             }
             nent += __popc(bm);
           }
@@ -2251,47 +2257,14 @@ end_e:
       }
     }
     if (fcross) {
-      if (lane == 0) { s_fout[wib] = fout; s_fpre[wib + 1] = nent; }
-      CTA_SYNC();
-      if (wib == 0) {   // bucket cursors (exclusive scan of the histogram) and the per-warp prefix
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < FX_KEYS; base += 32) {
-          const uint32_t c = s_fhist[base + lane];
-          const uint32_t incl = wincl(c);
-          s_fhist[base + lane] = carry + incl - c;
-          carry += __shfl_sync(FULLM, incl, 31);
-        }
-        const uint32_t c = lane < nwb ? s_fpre[lane + 1] : 0;
-        const uint32_t incl = wincl(c);
-        if (lane < nwb) s_fpre[lane + 1] = incl;
-        if (lane == 0) s_fpre[0] = 0;
-      }
-      CTA_SYNC();
-      for (uint32_t k = lane; k < nent; k += 32) {   // scatter into sorted order
-        const uint32_t e = fin[k];
-        const uint32_t p = atomicAdd(&s_fhist[min(m.ld[e & ((1u << 27) - 1)], FX_KEYS - 1)], 1u);
-        uint32_t o = 0;
-#pragma unroll
-        for (uint32_t step = 16; step; step >>= 1)
-          if (o + step < nwb && s_fpre[o + step] <= p) o += step;
-        s_fout[o][p - s_fpre[o]] = e;
-      }
-      CTA_SYNC();
-      const uint32_t total = s_fpre[nwb];
-      for (uint32_t c0 = 32 * wib; c0 < total; c0 += 32 * nwb) {
-        const uint32_t p = c0 + lane;
-        if (p >= total) continue;
-        uint32_t o = 0;
-#pragma unroll
-        for (uint32_t step = 16; step; step >>= 1)
-          if (o + step < nwb && s_fpre[o + step] <= p) o += step;
-        const uint32_t e = s_fout[o][p - s_fpre[o]];
-        const AsmMod& mm = all[e >> 27];
-        const uint32_t li = e & ((1u << 27) - 1);
-        const uint32_t w0 = mm.lwo[li] + 1;
-        encode_line(mm, X, li, mm.ld[li], M_COUNT, mm.sw + w0, mm.swr, w0, nullptr);
-      }
-      CTA_SYNC();
+      cta_dispatch(cs, fin, fout, nent,
+                   [&](uint32_t e) { return m.ld[e & CTA_ITEM]; },   // own entries only
+                   [&](uint32_t e) {
+                     const AsmMod& mm = all[e >> 27];
+                     const uint32_t li = e & CTA_ITEM;
+                     const uint32_t w0 = mm.lwo[li] + 1;
+                     encode_line(mm, X, li, mm.ld[li], M_COUNT, mm.sw + w0, mm.swr, w0, nullptr);
+                   });
     }
     if (!done && local) {
       // lanes take lines grouped by instruction (one code path per group instead of
@@ -2484,6 +2457,7 @@ end_i:
 __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(const __grid_constant__ AsmArgs a) {
   __shared__ uint32_t s_base[16];
   __shared__ AsmMod s_amod[32];   // the module descriptor, one per warp (not a per-thread local copy)
+  __shared__ CtaSort s_cs;        // cross-module work assignment (phases B, F)
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;                 // warps per barrier group
@@ -2502,7 +2476,7 @@ __global__ void __launch_bounds__(SKG_ASM_MAXT, SKG_ASM_MINB) asm_kernel(const _
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
     const uint32_t tk = base + gwarp_in;
-    assemble_module(s_args, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block], s_amod);
+    assemble_module(s_args, X, tk < a.n_mod ? a.order[tk] : a.n_mod, slot, gid, gw, s_amod[warp_in_block], s_amod, s_cs);
   }
 }
 

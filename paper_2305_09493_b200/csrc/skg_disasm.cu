@@ -743,63 +743,18 @@ __device__ __noinline__ void classify(Mod& m, const Tables& T) {
 }
 
 // Classification of the instructions of all modules of the CTA (every warp calls
-// it; `mine` = this warp's module takes part).  Entries (warp << 27 | instruction)
-// are counting-sorted by grammar entry in shared memory; the lists live in each
-// module's spill area (free until the name dedup).  Each instruction is walked
-// once with its own module's tables, as in classify().
-constexpr uint32_t CX_KEYS = 1024;
-__device__ __noinline__ void classify_cta(Mod* all, const Tables& T, bool mine, uint8_t* spill) {
-  __shared__ uint32_t s_hist[CX_KEYS];
-  __shared__ uint32_t s_pre[33];
-  __shared__ uint32_t* s_out[32];
-  const uint32_t lane = lane_id(), nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+// it; `mine` = this warp's module takes part): cta_dispatch sorts them by grammar
+// entry, the lists live in each module's spill area (free until the name dedup),
+// and each instruction is walked once with its own module's tables, as in classify().
+__device__ __noinline__ void classify_cta(Mod* all, const Tables& T, CtaSort& cs, bool mine, uint8_t* spill) {
+  const uint32_t wib = threadIdx.x >> 5;
   Mod& m = all[wib];
-  for (uint32_t k = threadIdx.x; k < CX_KEYS; k += blockDim.x) s_hist[k] = 0;
-  __syncthreads();
   const uint32_t n = mine ? m.I : 0;
   uint32_t* in = reinterpret_cast<uint32_t*>(spill);
   uint32_t* out = in + n + 4;
-  for (uint32_t i = lane; i < n; i += 32) {
-    in[i] = (wib << 27) | i;
-    atomicAdd(&s_hist[min((uint32_t)m.idef[i], CX_KEYS - 1)], 1u);
-  }
-  if (lane == 0) { s_out[wib] = out; s_pre[wib + 1] = n; }
-  __syncthreads();
-  if (wib == 0) {
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < CX_KEYS; base += 32) {
-      const uint32_t c = s_hist[base + lane];
-      const uint32_t incl = warp_incl_sum(c);
-      s_hist[base + lane] = carry + incl - c;
-      carry += __shfl_sync(FULL, incl, 31);
-    }
-    const uint32_t c = lane < nwb ? s_pre[lane + 1] : 0;
-    const uint32_t incl = warp_incl_sum(c);
-    if (lane < nwb) s_pre[lane + 1] = incl;
-    if (lane == 0) s_pre[0] = 0;
-  }
-  __syncthreads();
-  for (uint32_t i = lane; i < n; i += 32) {
-    const uint32_t p = atomicAdd(&s_hist[min((uint32_t)m.idef[i], CX_KEYS - 1)], 1u);
-    uint32_t o = 0;
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1)
-      if (o + step < nwb && s_pre[o + step] <= p) o += step;
-    s_out[o][p - s_pre[o]] = in[i];
-  }
-  __syncthreads();
-  const uint32_t total = s_pre[nwb];
-  for (uint32_t c0 = 32 * wib; c0 < total; c0 += 32 * nwb) {
-    const uint32_t p = c0 + lane;
-    if (p >= total) continue;
-    uint32_t o = 0;
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1)
-      if (o + step < nwb && s_pre[o + step] <= p) o += step;
-    const uint32_t e = s_out[o][p - s_pre[o]];
-    classify_one(all[e >> 27], T, e & ((1u << 27) - 1));
-  }
-  __syncthreads();
+  for (uint32_t i = lane_id(); i < n; i += 32) in[i] = (wib << 27) | i;
+  cta_dispatch(cs, in, out, n, [&](uint32_t e) { return (uint32_t)m.idef[e & CTA_ITEM]; },
+               [&](uint32_t e) { classify_one(all[e >> 27], T, e & CTA_ITEM); });
 }
 
 // referenced ids (A, disasm.py:221-240), word-parallel
@@ -1309,7 +1264,7 @@ __device__ unsigned long long g_dis_phase[16];
 template <bool VAL>
 __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, uint8_t* slab, uint8_t* gslot,
                                         uint8_t* stage, ErrSink& es, uint32_t gid, uint32_t gw, Mod& m,
-                                        uint64_t* veff, Mod* all) {
+                                        uint64_t* veff, Mod* all, CtaSort* cs) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   DPHASE_START();
@@ -1368,7 +1323,7 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
     // the barrier group is the whole CTA: the instructions of all its modules are
     // classified together, sorted by grammar entry, 32 consecutive ones per warp
     // (one walk per warp instead of a mix of a module's instructions)
-    classify_cta(all, T, status == ST_OK, m.spill);
+    classify_cta(all, T, *cs, status == ST_OK, m.spill);
   } else if (status == ST_OK) {
     classify(m, T);
   }
@@ -1548,6 +1503,7 @@ __device__ __forceinline__ void disasm_persistent(const DisasmArgs& a) {
   // take 32 x sizeof(Mod) of L1 per warp as local memory); all lanes write the
   // same values into it
   __shared__ Mod s_mod[32];
+  __shared__ CtaSort s_cs;   // cross-module work assignment (classification)
   __shared__ uint64_t s_eff[VAL ? 32 : 1][MAX_CAPW];   // VAL: effective capabilities per warp
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
@@ -1565,7 +1521,7 @@ __device__ __forceinline__ void disasm_persistent(const DisasmArgs& a) {
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
     disasm_one<VAL>(s_args, base + gwarp_in, slab, gslot, stage, es, gid, gw, s_mod[warp_in_block],
-                    VAL ? s_eff[warp_in_block] : nullptr, s_mod);
+                    VAL ? s_eff[warp_in_block] : nullptr, s_mod, &s_cs);
   }
 }
 

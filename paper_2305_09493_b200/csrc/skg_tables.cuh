@@ -29,6 +29,81 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
 }
 
+// ---------------------------------------------------------------------------
+// Cross-module work assignment inside one CTA (every warp of the CTA calls it;
+// CTA barriers inside).  Warp w offers n entries in `in`, each entry carrying its
+// warp in bits 27-31 and an item index below 2^27.  The entries of all warps are
+// counting-sorted by key(e) (< CTA_KEYS) into the warps' `out` arrays -- sorted
+// position p lives in the out array of the warp whose prefix range holds p, so a
+// warp needs room for its own entries only -- and then every warp runs work(e)
+// for 32 consecutive positions at a time: the lanes of a warp get items with equal
+// or adjacent keys, mostly of different modules, and warps with few items of
+// their own (or none: a finished module) take a share of the others'.
+constexpr uint32_t CTA_KEYS = 1024;
+constexpr uint32_t CTA_ITEM = (1u << 27) - 1;
+struct CtaSort {
+  uint32_t hist[CTA_KEYS];
+  uint32_t pre[33];
+  uint32_t* out[32];
+};
+
+__device__ __forceinline__ uint32_t cta_owner(const CtaSort& cs, uint32_t nwb, uint32_t p) {
+  uint32_t o = 0;   // the largest warp o with pre[o] <= p (the non-empty range holding p)
+#pragma unroll
+  for (uint32_t step = 16; step; step >>= 1)
+    if (o + step < nwb && cs.pre[o + step] <= p) o += step;
+  return o;
+}
+
+template <class Key, class Work>
+__device__ __forceinline__ void cta_dispatch(CtaSort& cs, const uint32_t* in, uint32_t* out, uint32_t n,
+                                             Key&& key, Work&& work) {
+  const uint32_t lane = threadIdx.x & 31, nwb = blockDim.x >> 5, wib = threadIdx.x >> 5;
+  for (uint32_t k = threadIdx.x; k < CTA_KEYS; k += blockDim.x) cs.hist[k] = 0;
+  __syncthreads();
+  for (uint32_t i = lane; i < n; i += 32) atomicAdd(&cs.hist[min(key(in[i]), CTA_KEYS - 1)], 1u);
+  if (lane == 0) { cs.out[wib] = out; cs.pre[wib + 1] = n; }
+  __syncthreads();
+  if (wib == 0) {   // bucket cursors (exclusive scan of the histogram), per-warp prefix
+    auto incl_sum = [&](uint32_t v) {
+#pragma unroll
+      for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, v, d);
+        if (lane >= d) v += t;
+      }
+      return v;
+    };
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < CTA_KEYS; base += 32) {
+      const uint32_t c = cs.hist[base + lane];
+      const uint32_t incl = incl_sum(c);
+      cs.hist[base + lane] = carry + incl - c;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    const uint32_t c = lane < nwb ? cs.pre[lane + 1] : 0;
+    const uint32_t incl = incl_sum(c);
+    if (lane < nwb) cs.pre[lane + 1] = incl;
+    if (lane == 0) cs.pre[0] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = lane; i < n; i += 32) {   // scatter into sorted order
+    const uint32_t e = in[i];
+    const uint32_t p = atomicAdd(&cs.hist[min(key(e), CTA_KEYS - 1)], 1u);
+    const uint32_t o = cta_owner(cs, nwb, p);
+    cs.out[o][p - cs.pre[o]] = e;
+  }
+  __syncthreads();
+  const uint32_t total = cs.pre[nwb];
+  for (uint32_t c0 = 32 * wib; c0 < total; c0 += 32 * nwb) {
+    const uint32_t p = c0 + lane;
+    if (p < total) {
+      const uint32_t o = cta_owner(cs, nwb, p);
+      work(cs.out[o][p - cs.pre[o]]);
+    }
+  }
+  __syncthreads();
+}
+
 // instruction special codes (tables.py SPECIAL)
 enum : uint32_t {
   SP_NONE = 0, SP_TYPEINT = 1, SP_TYPEFLOAT = 2, SP_EXTINSTIMPORT = 3, SP_NAME = 4, SP_SWITCH = 5,
