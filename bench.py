@@ -263,9 +263,13 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     t1 = time.perf_counter()
+    e2e_runs = []
     for _ in range(e2e_steps):
+        tr = time.perf_counter()
         text, tspan, tst, binv, bspan, bst = sess.run(h_batch, batch.offsets, batch.lengths)
+        e2e_runs.append(time.perf_counter() - tr)
     e2e_s = (time.perf_counter() - t1) / e2e_steps
+    log(f"[rank {rank}] e2e runs (ms): " + " ".join(f"{1e3 * r:.1f}" for r in e2e_runs))
     et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)

@@ -714,8 +714,11 @@ class DisasmPlan:
     """
 
     def __init__(self, batch: DeviceBatch, opts: int, spec=None, ext=None, text_cap=None,
-                 kind: str = "disasm", ws=None):
+                 kind: str = "disasm", ws=None, bufs=None):
+        """``bufs``: optional caller-owned device buffers (``text``, ``span``, ``status``,
+        ``errs``; grow-only pools of a session) used instead of fresh allocations."""
         torch = _torch()
+        bufs = bufs or {}
         self.kind = kind
         self.batch, self.opts = batch, opts
         self.th = tables_handle(spec, ext)
@@ -726,11 +729,17 @@ class DisasmPlan:
         else:
             self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.cap = text_cap if text_cap is not None else 6 * batch.total_bytes + 4096
-        self.text = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
-        self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
-        self.status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
         self.ecap = max(16, min(n, 1 << 16))
-        self.errs = torch.empty(self.ecap * 256, dtype=torch.uint8, device="cuda")
+
+        def buf(name, numel, dtype):
+            b = bufs.get(name)
+            if b is not None and b.numel() >= numel and b.dtype == dtype:
+                return b[:numel]
+            return torch.empty(numel, dtype=dtype, device="cuda")
+        self.text = buf("text", self.cap, torch.uint8)
+        self.span = buf("span", 2 * max(n, 1), torch.int64)
+        self.status = buf("status", max(n, 1), torch.int32)
+        self.errs = buf("errs", self.ecap * 256, torch.uint8)
         if kind == "pipeline":   # fused validation outputs (skg_disasm_validate)
             self.vcap = batch.total_bytes + 4096
             self.vtext = torch.empty(self.vcap, dtype=torch.uint8, device="cuda")
@@ -821,8 +830,10 @@ class AsmPlan:
     """Device buffers for repeated skg_asm launches over one resident text batch."""
 
     def __init__(self, batch: DeviceBatch, spec=None, ext=None, out_cap=None, slot_bytes=None,
-                 default_version=(1, 2), stride=1, ws=None):
+                 default_version=(1, 2), stride=1, ws=None, bufs=None):
+        """``bufs``: optional caller-owned device buffers (``out``, ``span``, ``status``)."""
         torch = _torch()
+        bufs = bufs or {}
         L = _bind_asm(lib())
         self.batch = batch
         self.stride = stride
@@ -836,9 +847,15 @@ class AsmPlan:
         else:
             self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device="cuda")
         self.cap = int(out_cap or (batch.total_bytes + 64 * n + 4096))
-        self.out = torch.empty(self.cap, dtype=torch.uint8, device="cuda")
-        self.span = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
-        self.status = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+
+        def buf(name, numel, dtype):
+            b = bufs.get(name)
+            if b is not None and b.numel() >= numel and b.dtype == dtype:
+                return b[:numel]
+            return torch.empty(numel, dtype=dtype, device="cuda")
+        self.out = buf("out", self.cap, torch.uint8)
+        self.span = buf("span", 2 * max(n, 1), torch.int64)
+        self.status = buf("status", max(n, 1), torch.int32)
         maj, mnr = default_version
         self.dv = ((int(maj) & 0xFFFF) << 16) | (int(mnr) & 0xFFFF)
 

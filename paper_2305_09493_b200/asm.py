@@ -152,7 +152,7 @@ class RoundTripSession:
         import torch
         b = self._buf.get(name)
         if b is None or b.numel() < n:
-            n = max(int(n), 16)
+            n = max(int(n) * 9 // 8, 16)   # headroom: the next batch's chunks may be a little larger
             b = torch.empty(n, dtype=dtype).pin_memory() if pinned else \
                 torch.empty(n, dtype=dtype, device="cuda")
             self._buf[name] = b
@@ -245,16 +245,27 @@ class RoundTripSession:
                 tcap, ocap = max(tcap, grow[0] + 16), max(ocap, grow[1] + 16)
                 max_text = max(max_text, grow[2])
             batch = _native.DeviceBatch(d_data, d_meta[a:b], d_meta[n + a:n + b], mw, cb)
-            dp = _native.DisasmPlan(batch, self.opts, self.spec, self.ext, text_cap=16,
-                                    ws=self._buf.get("ws_d"))
-            self._buf["ws_d"] = dp.ws
-            dp.text, dp.cap = self._get(f"text{k}", tcap, torch.uint8), tcap
+            # every device buffer is a grow-only pool of the session (per chunk slot): no
+            # allocator traffic, which would synchronise the pipeline, once warmed up
+            nb = b - a
+            dbufs = {"text": self._get(f"text{k}", tcap, torch.uint8),
+                     "span": self._get(f"dspan{k}", 2 * nb, torch.int64),
+                     "status": self._get(f"dst{k}", nb, torch.int32),
+                     "errs": self._get(f"derr{k}", 256 * max(16, min(nb, 1 << 16)), torch.uint8)}
+            dp = _native.DisasmPlan(batch, self.opts, self.spec, self.ext, text_cap=tcap,
+                                    ws=self._buf.get("ws_d"), bufs=dbufs)
+            if dp.ws is not self._buf.get("ws_d"):
+                self._buf["ws_d"] = dp.ws
             tb = _native.DeviceBatch(dp.text, dp.span[0::2], dp.span[1::2], 0, 0)
-            tb.n = b - a
+            tb.n = nb
             tb.max_words = (max_text + 3) // 4
-            ap = _native.AsmPlan(tb, self.spec, self.ext, out_cap=16, stride=2, ws=self._buf.get("ws_a"))
-            self._buf["ws_a"] = ap.ws
-            ap.out, ap.cap = self._get(f"out{k}", ocap, torch.uint8), ocap
+            abufs = {"out": self._get(f"out{k}", ocap, torch.uint8),
+                     "span": self._get(f"aspan{k}", 2 * nb, torch.int64),
+                     "status": self._get(f"ast{k}", nb, torch.int32)}
+            ap = _native.AsmPlan(tb, self.spec, self.ext, out_cap=ocap, stride=2, ws=self._buf.get("ws_a"),
+                                 bufs=abufs)
+            if ap.ws is not self._buf.get("ws_a"):
+                self._buf["ws_a"] = ap.ws
             if grow is None:
                 ev_in = torch.cuda.Event()
                 with torch.cuda.stream(s_in):
