@@ -224,13 +224,13 @@ __device__ __noinline__ void put_decode_msg(S& ew, const Mod& m, int64_t nbytes,
   }
 }
 
-// V2 (warp): module shape + effective capabilities (validate.py:101-136), per-instruction
-// diagnostic sizes, the first escaping exception (status, error record), then the
-// per-instruction offsets in m.ia; returns the module's diagnostics bytes
-__device__ __noinline__ uint64_t val_sizes(Mod& m, const Tables& T, uint64_t* eff, Shape& sh, int32_t& status,
-                                           ErrSink& es, int32_t t, uint32_t fast = 0) {
+// V2 (warp), in three parts: module shape + effective capabilities
+// (validate.py:101-136); the per-instruction diagnostic sizes (one grammar walk per
+// instruction: per warp here, or across the CTA's modules in val_walk_cta); then
+// the first escaping exception (status, error record) and the per-instruction
+// offsets in m.ia.  val_sizes returns the module's diagnostics bytes.
+__device__ __noinline__ void val_shape(const Mod& m, const Tables& T, uint64_t* eff, Shape& sh) {
   const uint32_t lane = lane_id();
-  uint64_t total = 0;
   bool fn = false, cap = false, ep = false;
   uint32_t mm = 0;
   for (uint32_t base = 0; base < m.I; base += 32) {
@@ -259,16 +259,18 @@ __device__ __noinline__ uint64_t val_sizes(Mod& m, const Tables& T, uint64_t* ef
     for (int dd = 16; dd > 0; dd >>= 1) eff[k] |= __shfl_xor_sync(FULL, eff[k], dd);
   }
   sh.linkage = T.linkage != NONE32 && ((eff[T.linkage / 64] >> (T.linkage % 64)) & 1);
-  for (uint32_t base = 0; base < m.I; base += 32) {
-    uint32_t i = base + lane;
-    if (i < m.I) {
-      CountSink cs;
-      WalkErr e = inst_diags(cs, m, T, i, eff, fast);
-      m.ierr[i] = (uint8_t)e.code;
-      m.ia[i] = cs.n;
-    }
-  }
-  __syncwarp();
+}
+
+__device__ __forceinline__ void val_walk_one(Mod& m, const Tables& T, uint32_t i, const uint64_t* eff, uint32_t fast) {
+  CountSink cs;
+  WalkErr e = inst_diags(cs, m, T, i, eff, fast);
+  m.ierr[i] = (uint8_t)e.code;
+  m.ia[i] = cs.n;
+}
+
+__device__ __noinline__ uint64_t val_finish(Mod& m, const Tables& T, const uint64_t* eff, const Shape& sh,
+                                            int32_t& status, ErrSink& es, int32_t t) {
+  const uint32_t lane = lane_id();
   uint32_t bad = NONE32;
   for (uint32_t base = 0; base < m.I && bad == NONE32; base += 32) {
     uint32_t i = base + lane;
@@ -302,8 +304,44 @@ __device__ __noinline__ uint64_t val_sizes(Mod& m, const Tables& T, uint64_t* ef
     run += __shfl_sync(FULL, incl, 31);
   }
   __syncwarp();
-  total = run;
-  return total;
+  return run;
+}
+
+__device__ __noinline__ uint64_t val_sizes(Mod& m, const Tables& T, uint64_t* eff, Shape& sh, int32_t& status,
+                                           ErrSink& es, int32_t t, uint32_t fast = 0) {
+  val_shape(m, T, eff, sh);
+  for (uint32_t base = 0; base < m.I; base += 32) {
+    uint32_t i = base + lane_id();
+    if (i < m.I) val_walk_one(m, T, i, eff, fast);
+  }
+  __syncwarp();
+  return val_finish(m, T, eff, sh, status, es, t);
+}
+
+// The V2 walks or the V3 writes of all the CTA's modules (every warp calls it;
+// `mine` = this warp's module takes part): instructions sorted by grammar entry
+// (cta_dispatch; lists in each module's spill area), each walked with its own
+// module's capabilities.  write == false: sizes (val_walk_one); write == true: the
+// diagnostics text at out[module] + m.ia[i] (val_write's per-instruction part).
+__device__ __noinline__ void val_walk_cta(Mod* all, const Tables& T, CtaSort& cs, const uint64_t (*effs)[MAX_CAPW],
+                                          const uint32_t* fasts, uint8_t* const* outs, bool mine, bool write) {
+  const uint32_t wib = threadIdx.x >> 5;
+  Mod& m = all[wib];
+  const uint32_t n = mine ? m.I : 0;
+  uint32_t* in = reinterpret_cast<uint32_t*>(m.spill);
+  uint32_t* out = in + n + 4;
+  for (uint32_t i = lane_id(); i < n; i += 32) in[i] = (wib << 27) | i;
+  cta_dispatch(cs, in, out, n, [&](uint32_t e) { return (uint32_t)m.idef[e & CTA_ITEM]; },
+               [&](uint32_t e) {
+                 const uint32_t mi = e >> 27, i = e & CTA_ITEM;
+                 Mod& mm = all[mi];
+                 if (write) {
+                   MemSink ms(outs[mi] + mm.ia[i]);
+                   inst_diags(ms, mm, T, i, effs[mi], fasts[mi]);
+                 } else {
+                   val_walk_one(mm, T, i, effs[mi], fasts[mi]);
+                 }
+               });
 }
 
 // V3 (warp): the diagnostics text at the offsets val_sizes left in m.ia
@@ -321,7 +359,7 @@ __device__ __noinline__ void val_write(uint8_t* out, const Mod& m, const Tables&
 // One module per warp; the CTA's warps run each phase together (CTA barrier
 // between phases), like disasm_kernel.  Scratch in the per-warp global slot.
 __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket, uint8_t* gslot, ErrSink& es,
-                                          uint32_t gid, uint32_t gw, Mod& m) {
+                                          uint32_t gid, uint32_t gw, Mod& m, Mod* all, CtaSort& cs) {
   const uint32_t lane = lane_id();
   const Tables& T = a.T;
   const bool live = ticket < a.n_mod;
@@ -367,9 +405,29 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
   group_sync(gid, gw);
   // -- V2: module shape + effective capabilities (validate.py:101-136), sizes,
   //        escaping exceptions, offsets
-  if (go && status == ST_OK) total = val_sizes(m, T, eff, sh, status, es, (int32_t)t);
+  // (the barrier group is the whole CTA: the per-instruction walks of V2 and V3 run
+  //  across the CTA's modules, sorted by grammar entry -- val_walk_cta)
+  __shared__ uint64_t s_veff[32][MAX_CAPW];
+  __shared__ uint32_t s_vfast[32];
+  __shared__ uint8_t* s_vout[32];
+  const uint32_t wib = threadIdx.x >> 5;
+  const bool vcross = gw == (blockDim.x >> 5);
+  const bool vgo = go && status == ST_OK;
+  if (vcross) {
+    if (vgo) val_shape(m, T, eff, sh);
+    if (lane == 0) {
+      for (int k = 0; k < MAX_CAPW; ++k) s_veff[wib][k] = eff[k];
+      s_vfast[wib] = 0;
+    }
+    val_walk_cta(all, T, cs, s_veff, s_vfast, nullptr, vgo, false);
+    if (vgo) total = val_finish(m, T, eff, sh, status, es, (int32_t)t);
+  } else if (vgo) {
+    total = val_sizes(m, T, eff, sh, status, es, (int32_t)t);
+  }
   group_sync(gid, gw);
   // -- V3: output
+  bool vwrite = false;
+  uint8_t* vout = nullptr;
   if (live && status == ST_OK && decode_status != ST_OK) {
     // the decode error of the module is its only diagnostic line
     const char* code = decode_code(decode_status);
@@ -404,7 +462,15 @@ __device__ __noinline__ void validate_one(const ValidateArgs& a, uint32_t ticket
       a.text_span[2 * t + 1] = (int64_t)total;
       a.status[t] = status;
     }
-    if (status == ST_OK && total > 0 && fits) val_write(a.text + off, m, T, eff, sh);
+    vwrite = status == ST_OK && total > 0 && fits;
+    vout = a.text + off;
+  }
+  if (vcross) {
+    if (vwrite && lane == 0) { MemSink ms(vout); shape_diags(ms, sh); }
+    if (lane == 0) s_vout[wib] = vout;
+    val_walk_cta(all, T, cs, s_veff, s_vfast, s_vout, vwrite, true);
+  } else if (vwrite) {
+    val_write(vout, m, T, eff, sh);
   }
   __syncwarp();
   group_sync(gid, gw);
@@ -419,6 +485,7 @@ __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(const __grid_con
   __syncthreads();
   __shared__ uint32_t s_base[16];
   __shared__ Mod s_mod[32];   // module descriptor, one per warp (not 32 per-thread local copies)
+  __shared__ CtaSort s_cs;    // cross-module work assignment (V2 / V3 walks)
   const uint32_t warps = blockDim.x >> 5;
   const uint32_t warp_in_block = threadIdx.x >> 5;
   const uint32_t gw = a.group_warps;
@@ -432,7 +499,7 @@ __global__ void __launch_bounds__(SKG_VAL_MAXT) validate_kernel(const __grid_con
     const uint32_t base = s_base[gid];
     group_sync(gid, gw);
     if (base >= a.n_mod) break;
-    validate_one(s_args, base + gwarp_in, gslot, es, gid, gw, s_mod[warp_in_block]);
+    validate_one(s_args, base + gwarp_in, gslot, es, gid, gw, s_mod[warp_in_block], s_mod, s_cs);
   }
 }
 

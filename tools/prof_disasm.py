@@ -17,7 +17,7 @@ def main():
     ap.add_argument("--modules", type=int, default=50000)
     ap.add_argument("--variants", type=int, default=2000)
     ap.add_argument("--launches", type=int, default=4)
-    ap.add_argument("--kind", default="disasm", choices=["disasm", "validate", "asm"])
+    ap.add_argument("--kind", default="disasm", choices=["disasm", "validate", "asm", "pipeline"])
     ap.add_argument("--opts", type=int, default=2)
     args = ap.parse_args()
     import torch
