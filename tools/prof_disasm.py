@@ -15,7 +15,7 @@ sys.path.insert(0, str(ROOT))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--modules", type=int, default=50000)
-    ap.add_argument("--variants", type=int, default=2000)
+    ap.add_argument("--variants", type=int, default=10000)   # the bench batch's diversity
     ap.add_argument("--launches", type=int, default=4)
     ap.add_argument("--kind", default="disasm", choices=["disasm", "validate", "asm", "pipeline"])
     ap.add_argument("--opts", type=int, default=2)
