@@ -188,17 +188,21 @@ class _PinnedStage:
     def __init__(self):
         self.buf = None
 
-    def to_bytes(self, dev_u8) -> bytes:
+    def to_bytes(self, dev_u8, view: bool = False):
+        """bytes of a device uint8 tensor; view=True: a numpy view of the pinned staging
+        buffer instead (no host-side copy into a new bytes object; valid until the next
+        staged copy)"""
         torch = _torch()
         n = int(dev_u8.numel())
         if n < (16 << 20) or dev_u8.dtype != torch.uint8 or not dev_u8.is_contiguous():
             # small results: the plain copy is cheaper than pinning
-            return dev_u8.cpu().numpy().tobytes()
+            out = dev_u8.cpu().numpy()
+            return out if view else out.tobytes()
         if self.buf is None or self.buf.numel() < n:
             self.buf = torch.empty(n + (n >> 3), dtype=torch.uint8).pin_memory()
         self.buf[:n].copy_(dev_u8, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return self.buf[:n].numpy().tobytes()
+        return self.buf[:n].numpy() if view else self.buf[:n].numpy().tobytes()
 
     def to_u32(self, dev_i32, count: int):
         """the first `count` elements of a device int32 tensor as a host uint32 array"""
@@ -436,8 +440,9 @@ def _header_bound(head: bytes) -> int:
     return int(np.frombuffer(head[:20], dtype=">u4")[3]) if w[0] == 0x03022307 else int(w[3])
 
 
-def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None):
-    """Shared driver of skg_validate_large / skg_disasm_large -> (rc, text bytes, errs)."""
+def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, view=False):
+    """Shared driver of skg_validate_large / skg_disasm_large -> (rc, text bytes, errs);
+    view=True: the text as a numpy view of the pinned staging buffer (see _PinnedStage)."""
     torch = _torch()
     L = lib()
     o = int(batch.off[i].item())
@@ -466,17 +471,18 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None):
         if rc != 2:
             break
     _check(rc if rc < 0 else 0, getattr(fn, "__name__", "large call"))
-    return rc, (_pinned.to_bytes(text[: int(need.value)]) if rc == 0 else None), errs
+    return rc, (_pinned.to_bytes(text[: int(need.value)], view) if rc == 0 else None), errs
 
 
-def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext):
-    """skg_disasm_large on module i -> text bytes | exception | None (= use the batch path)."""
+def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext, view=False):
+    """skg_disasm_large on module i -> text bytes | exception | None (= use the batch path);
+    view=True: the text as a numpy view of the pinned staging buffer."""
     L = lib()
     th = tables_handle(spec, ext)
 
     def disasm_large(*a):
         return L.skg_disasm_large(th, a[0], a[1], *a[2:])
-    rc, text, errs = _large_call(disasm_large, batch, i, nbytes, opts)
+    rc, text, errs = _large_call(disasm_large, batch, i, nbytes, opts, view=view)
     if rc == 2:
         return None
     if rc == 0:

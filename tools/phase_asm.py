@@ -30,7 +30,7 @@ def main():
     import torch
     from paper_2305_09493_b200 import _native
     from synth.families import sample_batch
-    b = sample_batch(n, 2000, 20261017)
+    b = sample_batch(n, min(n, 10000), 20261017)
     dev = _native.DeviceBatch.from_host(b.data, b.offsets, b.lengths)
     plan = _native.DisasmPlan(dev, 2)
     plan.fit()

@@ -34,7 +34,7 @@ def batch(n):
             words = len(m) // 4
         data = np.frombuffer(m + b"\0" * 16, dtype=np.uint8)
         return B, _native.DeviceBatch.from_host(data, np.array([0], np.int64), np.array([len(m)], np.int64))
-    b = sample_batch(n, min(n, 2000), 20261017)
+    b = sample_batch(n, min(n, 10000), 20261017)
     return b, _native.DeviceBatch.from_host(b.data, b.offsets, b.lengths)
 
 
