@@ -1669,168 +1669,8 @@ __global__ void bn_children(const Mod* mp, uint32_t* flags, uint32_t* clist, uin
   }
 }
 
-__global__ void bn_dedup(const Mod* mp, const uint32_t* clist, uint32_t nc, uint32_t nd) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  Mod m = *mp;
-  nm_dedup(m, nd, clist, nc);
-}
-
-// The same pass with the independent groups in parallel (one CTA of 1024).  A
-// group that neither has child groups nor is one ("involved" otherwise) only
-// sees its own members: its k-th member (D order) gets the base for k = 0 and
-// serial k - 1 after.  Per chunk of 1024 idents, such members are sorted by
-// (leader, position) in shared memory (bitonic), ranked within the chunk and
-// offset by the group's running count; the involved idents of the chunk go
-// through the exact sequential logic (nm_dedup's body) on thread 0, in order.
-__global__ void __launch_bounds__(1024) bn_dedup_par(const Mod* mp, const uint32_t* clist, uint32_t nc,
-                                                     uint32_t nd, uint32_t* gcount) {
-  __shared__ uint64_t key[1024];
-  __shared__ uint32_t segstart[1024];
-  __shared__ uint32_t inv[1024];
-  __shared__ uint32_t ninv;
-  // involved idents of the chunk, gathered in parallel for thread 0's ordered pass:
-  // group leader, leader's slot, own slot
-  __shared__ uint32_t q_g[1024], q_gs[1024], q_hs[1024], q_w[1024];   // q_w: warp of the ident's family
-  // thread 0's write-through cache of group state (nP, hfl) by slot: the ordered
-  // pass re-reads the same few groups, and a global store would evict them from L1
-  constexpr uint32_t GC = 512;
-  __shared__ uint32_t c_tag[GC], c_nP[GC], c_mx[GC];   // c_mx: largest child serial + 1 (0: none)
-  __shared__ uint8_t c_fl[GC];
-  Mod m = *mp;
-  const uint32_t t = threadIdx.x;
-  for (uint32_t e = t; e < GC; e += blockDim.x) c_tag[e] = NONE32;
-  auto child_of = [&](uint32_t g, uint32_t sv) -> uint32_t {
-    #pragma unroll 1
-    for (uint32_t q = 0; q < nc; ++q)
-      if (clist[3 * q] == g && clist[3 * q + 1] == sv) return clist[3 * q + 2];
-    return NONE32;
-  };
-  for (uint32_t base = 0; base < nd; base += 1024) {
-    const uint32_t k = base + t;
-    uint64_t kk = ~0ull;
-    bool involved = false;
-    uint32_t gk = 0, gks = 0;   // this ident's group leader and the leader's slot
-    if (k < nd) {
-      gk = (uint32_t)m.pos[k];
-      gks = m.ndl[gk];
-      involved = (m.hfl[gks] & HF_HASCHILD) || m.ib[gk] != NONE32;
-      if (!involved) kk = ((uint64_t)gk << 32) | t;
-    }
-    key[t] = kk;
-    if (t == 0) ninv = 0;
-    __syncthreads();
-    // involved idents of the chunk, in order
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, involved);
-    if ((t & 31) == 0) segstart[t >> 5] = __popc(b);
-    __syncthreads();
-    if (t == 0) {   // per-warp offsets (32 warps)
-      uint32_t run = 0;
-      for (uint32_t w = 0; w < 32; ++w) {
-        const uint32_t c = segstart[w];
-        segstart[w] = run;
-        run += c;
-      }
-      ninv = run;
-    }
-    __syncthreads();
-    if (involved) {
-      const uint32_t q = segstart[t >> 5] + __popc(b & ((1u << (t & 31)) - 1));
-      // family = the tree of groups linked by parent / child names: follow the parents to
-      // the root; families are independent, so each warp leader runs the ordered pass of
-      // the families hashed to it (each family still in D order)
-      uint32_t root = gk;
-      #pragma unroll 1
-      while (m.ib[root] != NONE32) root = m.ib[root];
-      inv[q] = k; q_g[q] = gk; q_gs[q] = gks; q_hs[q] = m.ndl[k]; q_w[q] = (root * 0x9E3779B1u) >> 27;
-    }
-    __syncthreads();
-    // bitonic sort of the independent members by (leader, position)
-    for (uint32_t size = 2; size <= 1024; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-        const uint32_t p = t ^ stride;
-        if (p > t) {
-          const bool up = (t & size) == 0;
-          const uint64_t a = key[t], c = key[p];
-          if ((a > c) == up) { key[t] = c; key[p] = a; }
-        }
-        __syncthreads();
-      }
-    }
-    const uint64_t me = key[t];
-    const uint32_t g = (uint32_t)(me >> 32);
-    const bool first = t == 0 || (uint32_t)(key[t - 1] >> 32) != g;
-    segstart[t] = first ? t : 0;
-    __syncthreads();
-    for (uint32_t d = 1; d < 1024; d <<= 1) {   // inclusive max-scan of segment starts
-      const uint32_t v = t >= d ? segstart[t - d] : 0;
-      __syncthreads();
-      segstart[t] = max(segstart[t], v);
-      __syncthreads();
-    }
-    // every member reads its group's running count before any segment's last member
-    // advances it (a segment can span warps)
-    const uint32_t gc0 = me != ~0ull ? gcount[g] : 0;
-    __syncthreads();
-    if (me != ~0ull) {
-      const uint32_t r = gc0 + (t - segstart[t]);
-      m.hser[m.ndl[base + (uint32_t)(me & 0xFFFF)]] = r == 0 ? NONE32 : r - 1;
-      const bool last = t == 1023 || (uint32_t)(key[t + 1] >> 32) != g;
-      if (last) gcount[g] = gc0 + t - segstart[t] + 1;
-    }
-    if ((t & 31) == 0) {   // involved idents: the exact sequential logic, in D order per family
-      const uint32_t wq = t >> 5;
-      auto slot_of = [&](uint32_t sl, uint32_t leader) -> uint32_t {   // cache entry of slot sl
-        const uint32_t e = wq * (GC / 32) + (sl & (GC / 32 - 1));     // this warp's part of the cache
-        if (c_tag[e] != sl) {
-          c_tag[e] = sl; c_nP[e] = m.nP[sl]; c_fl[e] = m.hfl[sl];
-          uint32_t mx = 0;   // serials past the largest child's never meet a child name
-          if (c_fl[e] & HF_HASCHILD) {
-            #pragma unroll 1
-            for (uint32_t q = 0; q < nc; ++q)
-              if (clist[3 * q] == leader) mx = max(mx, clist[3 * q + 1] + 1);
-          }
-          c_mx[e] = mx;
-        }
-        return e;
-      };
-      for (uint32_t q = 0; q < ninv; ++q) {
-        if (q_w[q] != wq) continue;
-        const uint32_t kq = inv[q];
-        const uint32_t gq = q_g[q];
-        const uint32_t gs = q_gs[q];
-        uint32_t ci = slot_of(gs, gq);
-        if (gq == kq) { c_nP[ci] = 0; m.nP[gs] = 0; }
-        uint32_t serial = NONE32;
-        const uint8_t fl = c_fl[ci];
-        if (!(fl & HF_TB)) {
-          c_fl[ci] = fl | HF_TB;
-          m.hfl[gs] = fl | HF_TB;
-        } else {
-          uint32_t sv = c_nP[ci];
-          if ((fl & HF_HASCHILD) && sv < c_mx[ci]) {
-            uint32_t c;
-            #pragma unroll 1
-            while ((c = child_of(gq, sv)) != NONE32) {   // first serial whose child name is free
-              const uint32_t cs = m.ndl[c];
-              const uint32_t cc = slot_of(cs, c);
-              if (!(c_fl[cc] & HF_TB)) { c_fl[cc] |= HF_TB; m.hfl[cs] = c_fl[cc]; break; }
-              ++sv;
-            }
-            ci = slot_of(gs, gq);   // (a child may have taken the parent's cache entry)
-          }
-          serial = sv;
-          c_nP[ci] = sv + 1;
-          m.nP[gs] = sv + 1;
-        }
-        m.hser[q_hs[q]] = serial;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---- name de-duplication of one large module in closed form (replaces the
-// ordered pass of bn_dedup_par).  disasm.py:173-185 gives the k-th named ident
+// ---- name de-duplication of one large module in closed form (replaced round 1's
+// ordered pass on one CTA).  disasm.py:173-185 gives the k-th named ident
 // (D order) the first free of base, base_0, base_1, ...  A candidate "B_s" of
 // group B (idents with sanitized base B) can only be taken by an earlier member of
 // B or by the bare name of the child group C whose literal base reads "B_s" (no
