@@ -50,6 +50,7 @@ __global__ void big_setup(Mod* mp, uint8_t* slot, uint32_t W, uint32_t* ctl, uin
   const uint32_t S = m.bound > min_table ? m.bound : min_table;
   if (S > 2 * m.W + 64) { ctl[BC_OVER] = 1; *mp = m; return; }   // not direct: host falls back
   layout_tables(m, true, S, 0, 0);
+  m.fpc = nullptr;
   m.work_shared = false;
   const uint32_t Imax = W > 5 ? W - 5 : 1;
   m.spill = slot + big_slot_bytes(W, S) - 256 - spill_bytes(Imax);

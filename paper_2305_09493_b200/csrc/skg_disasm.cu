@@ -896,7 +896,12 @@ __device__ __noinline__ uint32_t word_len(const Mod& m, const Tables& T, uint32_
     }
     case C_TYP: {
       const uint32_t pl = wk_pay(x), width_t = pl >> 2;
-      if (pl & 1) return n + 1 + repr_len(repr_parts(typed_float_bits(m, w, v, width_t)));
+      if (pl & 1) {   // the repr's digits (Ryu) once: kept for the write pass
+        const FloatParts fp = repr_parts(typed_float_bits(m, w, v, width_t));
+        if (m.fpc) m.fpc[w] = make_uint4((uint32_t)fp.digits, (uint32_t)(fp.digits >> 32), (uint32_t)fp.exp,
+                                         fp.kind | (fp.neg ? 0x100u : 0u));
+        return n + 1 + repr_len(fp);
+      }
       const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
       return n + 1 + (lv.neg ? 1 + dec_len_u64((uint64_t)0 - lv.bits) : dec_len_u64(lv.bits));
     }
@@ -1044,7 +1049,17 @@ __device__ __noinline__ void word_emit(uint8_t* __restrict__ p, const Mod& m, co
         const uint32_t pl = wk_pay(x), width_t = pl >> 2;
         Sink sk(p);
         sk.put(' ');
-        if (pl & 1) put_repr_double(sk, typed_float_bits(m, w, v, width_t));
+        if (pl & 1) {
+          FloatParts fp;
+          if (m.fpc) {   // parts computed by the size pass (word_len)
+            const uint4 c = m.fpc[w];
+            fp.digits = c.x | ((uint64_t)c.y << 32); fp.exp = (int32_t)c.z;
+            fp.kind = (uint8_t)(c.w & 0xFF); fp.neg = (c.w >> 8) & 1;
+          } else {
+            fp = repr_parts(typed_float_bits(m, w, v, width_t));
+          }
+          put_repr_parts(sk, fp);
+        }
         else {
           const LitVal lv = typed_int(m, w, v, width_t, pl & 2);
           if (lv.neg) put_i64(sk, (int64_t)lv.bits); else put_u64(sk, lv.bits);

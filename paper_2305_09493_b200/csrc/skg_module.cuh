@@ -76,6 +76,8 @@ struct Mod {
   uint32_t* ndl;          // named definitions in D order (slots)
   uint32_t* hnoff;        // friendly: offset of the sanitized base name in narena
   uint8_t* narena;        // sanitized base names of friendly ids (disassembler)
+  uint4* fpc;             // per word: the float repr parts of a typed float literal, computed by
+                          // the size pass for the write pass (nullptr: no room, recompute)
   uint32_t arena_need;    // bound on narena bytes: sum over OpName of 4 * string words + 1
   int32_t* pos;           // closed-form demotion scan, S + 2 entries
   uint16_t* hrl;          // friendly ref length
@@ -204,6 +206,8 @@ __device__ inline void layout_tables(Mod& m, bool direct, uint32_t S_or_C, size_
   m.pos = reinterpret_cast<int32_t*>(take(4ull * (S + 2)));
   m.hnoff = reinterpret_cast<uint32_t*>(take(4ull * S));
   m.narena = take(m.arena_need);
+  // the rest of the work region: the float repr cache, 16 bytes per word (disassembler)
+  m.fpc = (size_t)(m.work + m.work_bytes - p) >= 16ull * m.W ? reinterpret_cast<uint4*>(p) : nullptr;
 }
 
 // -- warp helpers -------------------------------------------------------------
