@@ -312,8 +312,13 @@ __device__ inline uint32_t nt_insert(const AsmMod& m, uint32_t t) {
       k = atomicCAS(e, EMPTYK, t);
       if (k == EMPTYK) { e[1] = h; return s; }
     }
-    const Tok o = tok_at(m, k);
-    if (o.n == me.n && bytes_eq(o.p, me.p, me.n)) return s;
+    // the entry's hash, once its inserter has written it, rules out most other keys
+    // without comparing bytes (0: not written yet -> compare)
+    const uint32_t eh = *(volatile uint32_t*)(e + 1);
+    if (eh == 0 || eh == h) {
+      const Tok o = tok_at(m, k);
+      if (o.n == me.n && bytes_eq(o.p, me.p, me.n)) return s;
+    }
     s = (s + 1) & (m.ncap - 1);
   }
   return NONE32;
@@ -2103,6 +2108,7 @@ end_c:
       const uint32_t rt = m.lt0[li];
       const Tok k = tok_at(m, rt);
       const uint32_t e = nt_insert(m, rt);
+      m.lgrp[li] = e;   // the line's result entry, for the binding pass and phase E (lgrp is free until G)
       if (!py_isdigit(k.p + 1, k.n - 1, X.U)) {
         if (k.n == 1) m.lfl[li] |= LF_RESOLVE_ERR;
         else if (e != NONE32) atomicMin(&m.nt[NT_W * e + 2], li);
@@ -2119,7 +2125,7 @@ end_c:
       if (li < L && (m.lfl[li] & LF_RESULT) && !(m.lfl[li] & LF_RESOLVE_ERR)) {
         const Tok k = tok_at(m, m.lt0[li]);
         if (!py_isdigit(k.p + 1, k.n - 1, X.U)) {
-          e = nt_find(m, k.p, k.n);
+          e = m.lgrp[li];
           first = e != NONE32 && m.nt[NT_W * e + 2] == li;
         }
       }
@@ -2163,7 +2169,7 @@ end_d:
     const uint32_t d = inst_by_name(X, on.p, on.n);
     m.ld[li] = d;
     if (!res || m.lnt[li] < 4) continue;
-    const uint32_t e = nt_find(m, tok_at(m, m.lt0[li]).p, tok_at(m, m.lt0[li]).n);
+    const uint32_t e = m.lgrp[li];   // the result token's entry (phase D's insert)
     if (e == NONE32) continue;
     const Tok o0 = tok_at(m, m.lt0[li] + 3);
     const bool ti = bytes_eq_z(on.p, on.n, "OpTypeInt"), tf = bytes_eq_z(on.p, on.n, "OpTypeFloat");
