@@ -211,6 +211,7 @@ int skg_tables_create(const uint32_t* host_blob, uint64_t n_words, skg_tables** 
   A.enhash = b + h[37]; A.enhash_cap = h[38];
   A.exhash = b + h[39]; A.exhash_cap = h[40];
   A.storage_fn = h[49]; A.op_label = h[50]; A.op_fnend = h[51];
+  A.op_typeint = h[53]; A.op_typefloat = h[54];
   t->u = skg::Uni{b + h[41], h[42], b + h[43], h[44], b + h[45], h[46], b + h[47], h[48]};
   *out = t;
   return 0;

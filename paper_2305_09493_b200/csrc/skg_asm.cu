@@ -30,6 +30,7 @@ struct AsmTables {
   const uint32_t* enhash; uint32_t enhash_cap;   // (hash, enum index, kind)
   const uint32_t* exhash; uint32_t exhash_cap;   // (hash, number, name off, name len)
   uint32_t storage_fn, op_label, op_fnend;
+  uint32_t op_typeint, op_typefloat;   // instruction indices of those names (NONE32: absent)
 };
 
 constexpr uint32_t ROUTE_SCOPE = 11, ROUTE_VARIABLE = 12, ROUTE_KEYERROR = 13;
@@ -2172,7 +2173,10 @@ end_d:
     const uint32_t e = m.lgrp[li];   // the result token's entry (phase D's insert)
     if (e == NONE32) continue;
     const Tok o0 = tok_at(m, m.lt0[li] + 3);
-    const bool ti = bytes_eq_z(on.p, on.n, "OpTypeInt"), tf = bytes_eq_z(on.p, on.n, "OpTypeFloat");
+    // opname text == "OpTypeInt" / "OpTypeFloat" (asm.py:223-227): an opname found in the
+    // grammar is that instruction exactly when its index is that name's; text otherwise
+    const bool ti = d != NONE32 ? d == X.A.op_typeint : bytes_eq_z(on.p, on.n, "OpTypeInt");
+    const bool tf = d != NONE32 ? d == X.A.op_typefloat : bytes_eq_z(on.p, on.n, "OpTypeFloat");
     if (ti || tf) {
       bool ok = parse_int(o0.p, o0.n, 0, X.U).status == INT_OK;
       if (ok && ti) {

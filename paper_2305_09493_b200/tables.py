@@ -468,6 +468,10 @@ def _asm_sections(spec, ext, insts, kinds, kind_index, header, put, strings):
     names = [i.name for i in insts]
     header[50] = names.index("OpLabel") if "OpLabel" in names else NONE32
     header[51] = names.index("OpFunctionEnd") if "OpFunctionEnd" in names else NONE32
+    # the assembler's width scan tests the opname text (asm.py:215-230); with these it
+    # compares instruction indices when the opname is in the grammar
+    header[53] = names.index("OpTypeInt") if "OpTypeInt" in names else NONE32
+    header[54] = names.index("OpTypeFloat") if "OpTypeFloat" in names else NONE32
 
 
 _UNI = None
