@@ -410,6 +410,7 @@ __device__ __noinline__ void nm_dedup(Mod& m, uint32_t nd, const uint32_t* clist
     if (k >= nd) break;
     const uint32_t g = gv[j];
     const uint32_t gs = gsv[j];
+    if (!(m.hfl[gs] & HF_HASCHILD) && m.ib[g] == NONE32) continue;   // independent group: nm_dedup_simple
     if (g == k) m.nP[gs] = 0;                       // group counter (nP no longer needed)
     uint32_t serial = NONE32;
     const uint8_t fl = m.hfl[gs];
@@ -428,6 +429,34 @@ __device__ __noinline__ void nm_dedup(Mod& m, uint32_t nd, const uint32_t* clist
     }
     m.hser[ksv[j]] = serial;
   }
+  }
+}
+
+// The groups that neither have child groups nor are one never meet another group's
+// candidates, so nm_dedup's rule reduces to: the group's r-th ident (D order) gets
+// the bare base for r = 0 and serial r - 1 after.  Warp-parallel, 32 idents at a
+// time (ranks by __match_any_sync plus a running count per group in nP); nm_dedup
+// then walks only the idents of the other groups, in order.
+__device__ __noinline__ void nm_dedup_simple(Mod& m, uint32_t nd) {
+  const uint32_t lane = lane_id();
+  #pragma unroll 1
+  for (uint32_t base = 0; base < nd; base += 32) {
+    const uint32_t k = base + lane;
+    uint32_t g = 0, gs = 0;
+    bool simple = false;
+    if (k < nd) {
+      g = (uint32_t)m.pos[k];
+      gs = m.ndl[g];
+      simple = !(m.hfl[gs] & HF_HASCHILD) && m.ib[g] == NONE32;
+    }
+    const unsigned peers = __match_any_sync(FULL, simple ? g : (0x80000000u | lane));
+    if (simple) {
+      const uint32_t r = (g >= base ? 0u : m.nP[gs]) + __popc(peers & ((1u << lane) - 1));
+      m.hser[m.ndl[k]] = r == 0 ? NONE32 : r - 1;
+      if (r == 0) m.hfl[gs] |= HF_TB;
+      if (lane == 31 - __clz(peers)) m.nP[gs] = r + 1;   // the group's count so far
+    }
+    __syncwarp();
   }
 }
 
@@ -546,6 +575,7 @@ __device__ __noinline__ void resolve_names(Mod& m, const Tables& T) {
     nc += __popc(b);
   }
   __syncwarp();
+  nm_dedup_simple(m, nd);
   if (lane == 0) nm_dedup(m, nd, clist, nc);
   __syncwarp();
   // 5. friendly = named definition that keeps its number; its sanitized base
