@@ -1418,13 +1418,13 @@ __device__ __noinline__ void disasm_one(const DisasmArgs& a, uint32_t ticket, ui
   group_sync(gid, gw);
   // -- P5 (VAL): the validator's shape, capabilities, diagnostic sizes and offsets
   //    (validate_one V2); m.ia is free once the friendly names are resolved
-  // The per-instruction walks of validate V2 / V3 stay per module here: with the
-  // classification status reused (VF_IERR_KNOWN) they are short, and running them
-  // across the CTA's modules (val_walk_cta, as validate_kernel does) measured 2.5%
-  // slower for the fused pass.
+  // The per-instruction walks of validate V2 / V3 run across the CTA's modules when the
+  // barrier group is the whole CTA (val_walk_cta, as in validate_kernel): fused pass
+  // on the bench's 1M-module batch 166 -> 149 ms (on a 200k batch of 2000 variants it
+  // measured 2.5% slower: fewer distinct instructions per CTA).
   __shared__ uint32_t s_vfast[32];
   __shared__ uint8_t* s_vout[32];
-  const bool vcross = false;
+  const bool vcross = gw == (blockDim.x >> 5);
   if (VAL) {
     const bool vmine = live && vstatus == ST_OK && decode_status == ST_OK;
     uint64_t eff[MAX_CAPW];
