@@ -2033,9 +2033,10 @@ end_a:
 
   PHASE_MARK(1);
   // -- B: tokenize + reservations ------------------------------------------------
-  // (lane per line within the module: a cross-module assignment of the lines,
-  // sorted by length or not, measured 2-3% slower -- the module's text stays in L1)
   uint32_t nres = 0;
+  // (lane per line within the module: a cross-module assignment of the lines measured
+  //  5% slower unsorted and 10% sorted by length on the bench batch -- the module's text
+  //  and token arrays stay in L1 when one warp tokenizes them)
   if (bready) {
     for (uint32_t base = 0; base < L; base += 32) {
       const uint32_t li = base + lane;
@@ -2158,35 +2159,65 @@ end_c:
 end_d:
   PHASE_MARK(4);
   CTA_SYNC();
-  if (done) goto end_e;
   // -- E: opname lookup, width / value-type scans ---------------------------------
-  for (uint32_t base = 0; base < L; base += 32) {
-    const uint32_t li = base + lane;
-    if (li >= L) continue;
-    const uint32_t fl = m.lfl[li];
-    if (fl & (LF_TOKERR | LF_EMPTY)) { m.ld[li] = NONE32; continue; }
-    const bool res = fl & LF_RESULT;
-    const Tok on = tok_at(m, m.lt0[li] + (res ? 2 : 0));
-    const uint32_t d = inst_by_name(X, on.p, on.n);
-    m.ld[li] = d;
-    if (!res || m.lnt[li] < 4) continue;
-    const uint32_t e = m.lgrp[li];   // the result token's entry (phase D's insert)
-    if (e == NONE32) continue;
-    const Tok o0 = tok_at(m, m.lt0[li] + 3);
-    // opname text == "OpTypeInt" / "OpTypeFloat" (asm.py:223-227): an opname found in the
-    // grammar is that instruction exactly when its index is that name's; text otherwise
-    const bool ti = d != NONE32 ? d == X.A.op_typeint : bytes_eq_z(on.p, on.n, "OpTypeInt");
-    const bool tf = d != NONE32 ? d == X.A.op_typefloat : bytes_eq_z(on.p, on.n, "OpTypeFloat");
-    if (ti || tf) {
-      bool ok = parse_int(o0.p, o0.n, 0, X.U).status == INT_OK;
-      if (ok && ti) {
-        if (m.lnt[li] < 5) ok = false;
-        else { const Tok o1 = tok_at(m, m.lt0[li] + 4); ok = parse_int(o1.p, o1.n, 0, X.U).status == INT_OK; }
+  {
+    auto e_line = [&](AsmMod& mm, uint32_t li) {
+      const uint32_t fl = mm.lfl[li];
+      const bool res = fl & LF_RESULT;
+      const Tok on = tok_at(mm, mm.lt0[li] + (res ? 2 : 0));
+      const uint32_t d = inst_by_name(X, on.p, on.n);
+      mm.ld[li] = d;
+      if (!res || mm.lnt[li] < 4) return;
+      const uint32_t e = mm.lgrp[li];   // the result token's entry (phase D's insert)
+      if (e == NONE32) return;
+      const Tok o0 = tok_at(mm, mm.lt0[li] + 3);
+      const bool ti = d != NONE32 ? d == X.A.op_typeint : bytes_eq_z(on.p, on.n, "OpTypeInt");
+      const bool tf = d != NONE32 ? d == X.A.op_typefloat : bytes_eq_z(on.p, on.n, "OpTypeFloat");
+      if (ti || tf) {
+        bool ok = parse_int(o0.p, o0.n, 0, X.U).status == INT_OK;
+        if (ok && ti) {
+          if (mm.lnt[li] < 5) ok = false;
+          else { const Tok o1 = tok_at(mm, mm.lt0[li] + 4); ok = parse_int(o1.p, o1.n, 0, X.U).status == INT_OK; }
+        }
+        if (ok) atomicMax(&mm.nt[NT_W * e + 4], li + 1);
       }
-      if (ok) atomicMax(&m.nt[NT_W * e + 4], li + 1);
+      if (d != NONE32 && X.T.has_rtype(d) && o0.n >= 1 && o0.p[0] == '%') atomicMax(&mm.nt[NT_W * e + 5], li + 1);
+    };
+    if (gw == (blockDim.x >> 5)) {
+      const uint32_t wib = threadIdx.x >> 5;
+      uint32_t ne = 0;
+      if (!done) {
+        for (uint32_t base = 0; base < L; base += 32) {
+          const uint32_t li = base + lane;
+          bool want = false;
+          if (li < L) {
+            if (m.lfl[li] & (LF_TOKERR | LF_EMPTY)) m.ld[li] = NONE32;
+            else want = true;
+          }
+          const unsigned bm = __ballot_sync(FULLM, want);
+          if (want) lperm[ne + __popc(bm & ((1u << lane) - 1))] = (wib << 27) | li;
+          ne += __popc(bm);
+        }
+      }
+      // the sorted share: m.loff (free until phase H)
+      cta_dispatch(cs, lperm, m.loff, ne,
+                   [&](uint32_t e) {
+                     const uint32_t li = e & CTA_ITEM;
+                     const Tok on = tok_at(m, m.lt0[li] + ((m.lfl[li] & LF_RESULT) ? 2 : 0));
+                     const uint32_t b2 = on.n > 2 ? on.p[2] : 0, b3 = on.n > 3 ? on.p[3] : 0;
+                     return ((b2 & 31) << 5 | (b3 & 31)) ^ (min(on.n, 31u) << 5);
+                   },
+                   [&](uint32_t e) { e_line(all[e >> 27], e & CTA_ITEM); });
+    } else if (!done) {
+      for (uint32_t base = 0; base < L; base += 32) {
+        const uint32_t li = base + lane;
+        if (li >= L) continue;
+        if (m.lfl[li] & (LF_TOKERR | LF_EMPTY)) { m.ld[li] = NONE32; continue; }
+        e_line(m, li);
+      }
     }
-    if (d != NONE32 && X.T.has_rtype(d) && o0.n >= 1 && o0.p[0] == '%') atomicMax(&m.nt[NT_W * e + 5], li + 1);
   }
+  if (done) goto end_e;
 end_e:
   PHASE_MARK(5);
   CTA_SYNC();
