@@ -429,10 +429,9 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
   uint32_t nsep = 0, ccarry = 0, prev_last = 0;   // prev_last: byte before this chunk (0 = text start)
   const uint32_t nw = (T + 3) / 4;
   const bool aligned = (reinterpret_cast<uintptr_t>(m.txt) & 3) == 0;
-  for (uint32_t base = 0; base < nw; base += 32) {
-    const uint32_t w = base + lane;
-    uint32_t cnt = 0;
-    uint32_t pos[4], len[4], cb[4];
+  // aligned text: each iteration's word is loaded one iteration ahead (the scan's
+  // carries make the iterations dependent; the loads need not be)
+  auto load_word = [&](uint32_t w) -> uint32_t {
     uint32_t word = 0;
     if (w < nw) {
       if (aligned) {
@@ -441,6 +440,15 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
         for (uint32_t b = 0; b < 4 && 4 * w + b < T; ++b) word |= (uint32_t)m.txt[4 * w + b] << (8 * b);
       }
     }
+    return word;
+  };
+  uint32_t next_word = load_word(lane);
+  for (uint32_t base = 0; base < nw; base += 32) {
+    const uint32_t w = base + lane;
+    uint32_t cnt = 0;
+    uint32_t pos[4], len[4], cb[4];
+    const uint32_t word = next_word;
+    next_word = load_word(w + 32);
     uint32_t pw = __shfl_up_sync(FULLM, word, 1);
     if (lane == 0) pw = prev_last << 24;
     const uint32_t prev = (word << 8) | (pw >> 24);          // previous byte of every byte
