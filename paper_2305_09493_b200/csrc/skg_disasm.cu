@@ -1196,17 +1196,22 @@ __device__ __noinline__ void text_write_range(const Mod& m, const Tables& T, uin
   uint32_t w0 = w_begin;
   const uint32_t* __restrict__ wk = m.wk;   // held in registers across the stage stores
   const uint16_t* __restrict__ wl = m.wl;
+  // each window's codes and lengths are loaded while the previous window is rendered
+  uint32_t x_next = 0, l_next = 0;
+  if (w0 + lane < w_end) { x_next = wk[w0 + lane]; l_next = wl[w0 + lane]; }
   while (w0 < w_end) {
     const uint32_t w = w0 + lane;
-    uint32_t x = 0, len = 0;
-    if (w < w_end) {
-      x = wk[w];
-      len = wl[w];
-      if (len == 0xFFFF) len = word_len(m, T, w, x, width, hl);
-    }
+    const uint32_t x = x_next;
+    uint32_t len = l_next;
+    if (w < w_end && len == 0xFFFF) len = word_len(m, T, w, x, width, hl);
     const uint32_t incl = warp_incl_sum(len);
     const uint32_t shift = (uint32_t)(reinterpret_cast<uintptr_t>(out + pos) & 15);
     const uint32_t take = __popc(__ballot_sync(FULL, w < w_end && shift + incl <= cap));
+    {
+      const uint32_t wn = w0 + (take ? take : 1) + lane;
+      x_next = 0; l_next = 0;
+      if (wn < w_end) { x_next = wk[wn]; l_next = wl[wn]; }
+    }
     if (take == 0) {   // one word longer than the stage
       if (lane == 0) word_emit(out + pos, m, T, w, x, width, hl, false);
       __syncwarp();
