@@ -1463,6 +1463,13 @@ __device__ __forceinline__ HdrLine header_line(const AsmMod& m, const AsmCtx& X,
   HdrLine r{0, 0, 0, 0, 0, 0};
   const uint8_t* p = m.txt + m.ls[li];
   const uint32_t n = m.le[li] - m.ls[li];
+  // an instruction line (the common case): after ASCII blanks, a printable ASCII byte
+  // other than ';' -- str.strip() then leaves it non-empty and not a comment
+  {
+    uint32_t i = 0;
+    while (i < n && (p[i] == ' ' || p[i] == '\t')) ++i;
+    if (i < n && p[i] > 0x20 && p[i] < 0x7F && p[i] != ';') { r.key = 5; return r; }
+  }
   uint32_t a, b;
   py_strip(p, n, U, a, b);
   if (b > a && p[a] != ';') { r.key = 5; return r; }
