@@ -426,9 +426,38 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   return check(cudaGetLastError());
 }
 
+namespace {
+// the link arrays after entry / count (skg_decode_large_workspace_bytes)
+void bd_link_layout(skg::BigDecode& b, uint32_t* q) {
+  const uint64_t N = (uint64_t)b.ntiles * skg::BD_K;
+  uint32_t levels = 1;
+  while ((1ull << levels) <= b.ntiles) ++levels;
+  b.levels = levels;
+  b.next = q; q += N;
+  b.tpos = q; q += N;
+  b.tcode = q; q += N;
+  b.jump = q;
+}
+// the tiles linked in parallel (successors, doubling, path); the sequential link only
+// if some speculative exit on the true chain landed on an unmarked position
+void bd_link(const skg::BigDecode& b, cudaStream_t s) {
+  const uint32_t N = b.ntiles * skg::BD_K;
+  skg::tile_entry_init<<<(b.ntiles + 255) / 256, 256, 0, s>>>(b);
+  skg::tile_land<<<(N + 127) / 128, 128, 0, s>>>(b);
+  for (uint32_t r = 1; r < b.levels; ++r) skg::tile_jump<<<(N + 255) / 256, 256, 0, s>>>(b, r);
+  skg::tile_path<<<(b.ntiles + 1 + 255) / 256, 256, 0, s>>>(b);
+  skg::tile_link_if_raw<<<1, 32, 0, s>>>(b);
+}
+}  // namespace
+
 uint64_t skg_decode_large_workspace_bytes(uint64_t n_words) {
   const uint64_t nt = (n_words + skg::BD_TILE - 1) / skg::BD_TILE;
-  return 256 + nt * skg::BD_TILE + 3 * 4 * skg::BD_K * nt + 3 * 4 * nt + 256;
+  uint64_t levels = 1;
+  while ((1ull << levels) <= nt) ++levels;
+  // chain maps, speculative exits / errors, entries + counts (+1 spare), then the
+  // parallel link's successor / terminal arrays and doubled maps (u32 per node per level)
+  return 256 + nt * skg::BD_TILE + 3 * 4 * skg::BD_K * nt + 3 * 4 * nt +
+         (3 + levels) * 4 * skg::BD_K * nt + 256;
 }
 
 int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, uint32_t* header,
@@ -451,12 +480,14 @@ int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, 
   b.spec_errc = q; q += (uint64_t)b.ntiles * skg::BD_K;
   b.entry = q; q += b.ntiles;
   b.count = q; q += b.ntiles;
+  q += b.ntiles;
+  bd_link_layout(b, q);
   const uint32_t tb = 128, tg = (b.ntiles + tb - 1) / tb;
   skg::big_prologue<<<1, 32, 0, s>>>(b);
   if (b.W >= 5) {
     skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
     skg::tile_spec<<<tg, tb, 0, s>>>(b);
-    skg::tile_link<<<1, 32, 0, s>>>(b);
+    bd_link(b, s);
     skg::tile_count<<<tg, tb, 0, s>>>(b);
     skg::tile_scan<<<1, 1024, 0, s>>>(b);
     skg::tile_write<<<tg, tb, 0, s>>>(b);
@@ -507,13 +538,15 @@ int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const
   b.spec_errc = q; q += (uint64_t)b.ntiles * skg::BD_K;
   b.entry = q; q += b.ntiles;
   b.count = q; q += b.ntiles;
+  q += b.ntiles;
+  bd_link_layout(b, q);
   const uint32_t tb = 128, tg = (b.ntiles + tb - 1) / tb;
   uint32_t* hdr = reinterpret_cast<uint32_t*>(l.dec);          // scratch for the epilogue outputs
   skg::big_prologue<<<1, 32, 0, s>>>(b);
   if (b.W >= 5) {
     skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
     skg::tile_spec<<<tg, tb, 0, s>>>(b);
-    skg::tile_link<<<1, 32, 0, s>>>(b);
+    bd_link(b, s);
     skg::tile_count<<<tg, tb, 0, s>>>(b);
     skg::tile_scan<<<1, 1024, 0, s>>>(b);
     skg::tile_write<<<tg, tb, 0, s>>>(b);

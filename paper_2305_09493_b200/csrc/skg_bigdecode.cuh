@@ -41,6 +41,12 @@ struct BigDecode {
   uint32_t* spec_errc;       // per tile and chain: ST_CORRUPT / ST_TRUNCATED
   uint32_t max_opcode;       // plausibility filter for speculative starts (0xFFFF: none)
   uint32_t* entry;           // per tile: first true-chain position in the tile (BD_NONE: none)
+  // parallel link (tile_land / tile_jump / tile_path): one node per (tile, chain)
+  uint32_t* next;            // node -> the node the true chain continues on, or BD_TERM | node
+  uint32_t* tpos;            // node: where the walk into the next tile ended (error position)
+  uint32_t* tcode;           // node: terminal kind (TK_END / TK_RAW / an error status)
+  uint32_t* jump;            // levels x nodes: next composed 2^r times
+  uint32_t levels;
   uint32_t* count;           // per tile: instructions, then exclusive offsets
   uint32_t* result;          // [0] status, [1] error position, [2] instruction count, [3] byte swap
   uint32_t* inst_off;
@@ -124,7 +130,15 @@ __global__ void tile_spec(BigDecode b) {
 // 16 bytes of their chain maps, where an entry nearly always lands) in one
 // round, then every lane runs the same walk, taking tile j's data from lane j by
 // shuffles; only an entry past those 16 bytes, or an unmarked one, reads memory.
-__global__ void tile_link(BigDecode b) {
+__device__ __forceinline__ void tile_link_body(BigDecode& b);
+__global__ void tile_link(BigDecode b) { tile_link_body(b); }
+__global__ void tile_link_if_raw(BigDecode b) {
+  if (b.result[4] == 0) return;   // the parallel link was complete
+  if (threadIdx.x < 32) b.result[0] = ST_OK;   // tile_path may have set nothing else
+  __syncwarp();
+  tile_link_body(b);
+}
+__device__ __forceinline__ void tile_link_body(BigDecode& b) {
   if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   if (b.result[0] != ST_OK) return;   // (the same value for every lane)
   const uint32_t lane = threadIdx.x;
@@ -189,6 +203,115 @@ __global__ void tile_link(BigDecode b) {
   }
   if (lane == 0) { b.result[0] = status; b.result[1] = errpos; }
 }
+
+// ---------------------------------------------------------------------------
+// Parallel link.  Node n = 4 t + k stands for "the true chain follows speculative
+// chain k of tile t".  tile_land computes each node's successor independently:
+// chain k's first error makes the node terminal (that is the true chain's first
+// error: it lies at or after any point where the true chain joins chain k); its
+// exit e (the first position past tile t, possibly several tiles on) is walked
+// by the exact rule in e's tile until it lands on a marked position (node of that
+// tile's chain), reaches the end of the stream (terminal END), hits a word count
+// 0 / overrun (terminal error) or leaves the tile unmarked (terminal RAW: the
+// sequential tile_link then does the whole link).  tile_jump composes the
+// successor map by doubling; tile_path gives thread d the d-th node of the chain
+// from node 0 (bits of d through the doubled maps), which sets that tile's entry
+// (the exit of node d-1) and, for the first terminal, the status.
+constexpr uint32_t BD_TERM = 0x80000000u;
+constexpr uint32_t TK_END = 100, TK_RAW = 101;
+
+constexpr uint32_t BD_MAXHOP = 16;   // tiles a successor walk may cross before giving up (TK_RAW)
+
+__global__ void tile_land(BigDecode b) {
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= b.ntiles * BD_K || b.result[0] != ST_OK) return;
+  const uint32_t er = b.spec_err[n], ex = b.spec_exit[n];
+  uint32_t nxt = BD_TERM | n, code = TK_RAW, pos = 0;
+  if (er != BD_NONE) {
+    code = b.spec_errc[n]; pos = er;
+  } else if (ex != BD_NONE) {
+    // the exact walk from the exit until it meets a marked position (chain maps are
+    // contiguous: chain[p] for absolute p), the stream end, or an error
+    uint32_t p = ex, t0 = ex / BD_TILE;
+    code = TK_END;
+    while (p < b.W) {
+      const uint32_t c = b.chain[p];
+      if (c) { nxt = BD_K * (p / BD_TILE) + c - 1; code = 0; break; }
+      const uint32_t wc = b.words[p] >> 16;
+      if (wc == 0) { code = ST_CORRUPT; pos = p; break; }
+      if ((uint64_t)p + wc > b.W) { code = ST_TRUNCATED; pos = p; break; }
+      p += wc;
+      if (p / BD_TILE > t0 + BD_MAXHOP) { code = TK_RAW; break; }
+    }
+  }
+  b.next[n] = nxt;
+  b.jump[n] = nxt;
+  b.tpos[n] = pos;
+  b.tcode[n] = code;
+}
+
+// level r from level r - 1 (a terminal maps to itself)
+__global__ void tile_jump(BigDecode b, uint32_t r) {
+  const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t N = b.ntiles * BD_K;
+  if (n >= N || b.result[0] != ST_OK) return;
+  const uint32_t* prev = b.jump + (uint64_t)(r - 1) * N;
+  const uint32_t x = prev[n];
+  b.jump[(uint64_t)r * N + n] = (x & BD_TERM) ? x : prev[x];
+}
+
+__device__ __forceinline__ uint32_t path_node(const BigDecode& b, uint32_t d) {
+  const uint32_t N = b.ntiles * BD_K;
+  uint32_t x = 0;
+  for (uint32_t r = 0; d && r < b.levels; ++r, d >>= 1)
+    if ((d & 1) && !(x & BD_TERM)) x = b.jump[(uint64_t)r * N + x];
+  return x;
+}
+
+// the tiles a true-chain walk from p enters before it meets a marked position or the
+// stream end: each gets its first position as entry (tile_land validated the walk)
+__device__ __forceinline__ void path_entries(const BigDecode& b, uint32_t p) {
+  uint32_t last = BD_NONE;
+  while (p < b.W) {
+    const uint32_t t = p / BD_TILE;
+    if (t != last) { b.entry[t] = p; last = t; }
+    if (b.chain[p]) return;
+    p += b.words[p] >> 16;
+  }
+}
+
+// thread d: the d-th node on the true chain (d <= ntiles: at most one node per tile)
+__global__ void tile_path(BigDecode b) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d > b.ntiles || b.result[0] != ST_OK) return;
+  const uint32_t x = path_node(b, d);
+  const uint32_t pv = d ? path_node(b, d - 1) : BD_TERM;
+  if (!(x & BD_TERM)) {   // node x: the walk into its tile from the previous node's exit
+    if (d == 0) b.entry[0] = 5u;
+    else path_entries(b, b.spec_exit[pv]);
+    return;
+  }
+  if (d && (pv & BD_TERM)) return;   // not the first terminal
+  const uint32_t n = x & ~BD_TERM;   // the node whose successor is terminal
+  const uint32_t code = b.tcode[n];
+  if (code == TK_END) {              // the chain ends with the stream: the tiles it still enters
+    if (b.spec_exit[n] != BD_NONE) path_entries(b, b.spec_exit[n]);
+    return;
+  }
+  if (code == TK_RAW) { b.result[4] = 1; return; }   // the sequential link decides
+  b.result[0] = code;
+  b.result[1] = b.tpos[n];
+}
+
+// entries default to BD_NONE before the path sets the tiles it visits
+__global__ void tile_entry_init(BigDecode b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < b.ntiles) b.entry[t] = BD_NONE;
+  if (t == 0) b.result[4] = 0;
+}
+
+// the sequential link only when the parallel one met an unmarked exit (TK_RAW)
+__global__ void tile_link_if_raw(BigDecode b);
 
 __global__ void tile_count(BigDecode b) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
