@@ -536,3 +536,36 @@ def test_f32_repr_exhaustive_on_device(sk):
                                                              no_header=True))[0]
     got = [ln.rsplit(" ", 1)[1] for ln in text.splitlines()[1:]]
     assert got == want
+
+
+def test_decode_large_long_unmarked_runs(sk):
+    """The parallel tile link gives up on a successor walk that crosses more than 16
+    tiles without meeting a speculative chain (runs of maximal OpStrings: 65535 words
+    each, their string words are not plausible instruction starts); the sequential
+    link then decides.  Instructions, and the exact first error after the runs, as the
+    oracle."""
+    import struct
+    from dataclasses import astuple
+    from oracle import core
+    words = [0x07230203, 0x00010100, 0, 100, 0]
+    for _ in range(8):                                   # small instructions
+        words += [(2 << 16) | 17, 11]                    # OpCapability 11
+    for r in range(3):                                   # a run of maximal OpStrings
+        for _ in range(5):
+            body = [0x61616161] * 65533 + [0]            # "aaaa..." + NUL word: 65534 words
+            words += [(65535 << 16) | 7, 1 + r] + body[:65533]
+    for _ in range(40):
+        words += [(2 << 16) | 17, 11]
+    data = struct.pack(f"<{len(words)}I", *words)
+    h, insts = sk.decode_module(data)
+    oh, oinsts = core.decode_module(data)
+    assert astuple(h) == tuple(oh)
+    assert [(i.opcode, tuple(i.operands)) for i in insts] == [(op, tuple(o)) for op, o in oinsts]
+    bad = list(words)
+    bad[-20] = 11                                        # word count 0 after the runs
+    data = struct.pack(f"<{len(bad)}I", *bad)
+    with pytest.raises(Exception) as e1:
+        sk.decode_module(data)
+    with pytest.raises(Exception) as e2:
+        core.decode_module(data)
+    assert (type(e1.value).__name__, str(e1.value)) == (type(e2.value).__name__, str(e2.value))
