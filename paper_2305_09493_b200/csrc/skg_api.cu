@@ -486,6 +486,7 @@ int skg_decode_large(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, 
   skg::big_prologue<<<1, 32, 0, s>>>(b);
   if (b.W >= 5) {
     skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
+    cudaMemsetAsync(b.chain, 0, (size_t)b.ntiles * skg::BD_TILE, s);   // chain maps (a memset beats a thread per tile)
     skg::tile_spec<<<tg, tb, 0, s>>>(b);
     bd_link(b, s);
     skg::tile_count<<<tg, tb, 0, s>>>(b);
@@ -545,6 +546,7 @@ int large_front(const uint8_t* data, uint64_t nbytes, uint32_t max_opcode, const
   skg::big_prologue<<<1, 32, 0, s>>>(b);
   if (b.W >= 5) {
     skg::big_copy<<<sm_count() * 8, 256, 0, s>>>(b);
+    cudaMemsetAsync(b.chain, 0, (size_t)b.ntiles * skg::BD_TILE, s);   // chain maps (a memset beats a thread per tile)
     skg::tile_spec<<<tg, tb, 0, s>>>(b);
     bd_link(b, s);
     skg::tile_count<<<tg, tb, 0, s>>>(b);

@@ -92,9 +92,7 @@ __global__ void tile_spec(BigDecode b) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= b.ntiles || b.result[0] != ST_OK) return;
   const uint32_t lo = t * BD_TILE, hi = min(lo + BD_TILE, b.W);
-  uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;
-  uint4* cm4 = reinterpret_cast<uint4*>(cm);
-  for (uint32_t k = 0; k < BD_TILE / 16; ++k) cm4[k] = make_uint4(0, 0, 0, 0);
+  uint8_t* cm = b.chain + (uint64_t)t * BD_TILE;   // zeroed by the host (cudaMemsetAsync)
   uint32_t* ex = b.spec_exit + (uint64_t)t * BD_K;
   uint32_t* er = b.spec_err + (uint64_t)t * BD_K;
   uint32_t* ec = b.spec_errc + (uint64_t)t * BD_K;
