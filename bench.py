@@ -255,7 +255,7 @@ def run_ours(args, rank, world, local_rank):
     # e2e through the host-buffer public API: RoundTripSession.run on the batch in pinned
     # host memory -- no sizing pass (capacity-bounded arenas, per-chunk counters read
     # back before each D2H), H2D of the binaries and D2H of text + binaries timed
-    sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "8")))   # pipeline depth (experiments)
+    sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "12")))   # pipeline depth (experiments)
     h_batch = torch.from_numpy(batch.data).pin_memory()
     sess.run(h_batch, batch.offsets, batch.lengths)          # warm-up: buffer allocation
     e2e_steps = max(1, min(args.steps, 3))

@@ -137,7 +137,7 @@ class RoundTripSession:
 
     TEXT_FACTOR = 6
 
-    def __init__(self, options=None, spec=None, ext=None, chunks=8):
+    def __init__(self, options=None, spec=None, ext=None, chunks=12):
         from .disasm import DisassemblerOptions, option_bits
         self.opts = option_bits(options if options is not None else DisassemblerOptions())
         self.spec, self.ext = spec, ext
