@@ -179,6 +179,7 @@ class _Workspace:
 
 
 _ws = _Workspace()
+_large_text = _Workspace()   # the large-module calls' text arena (grow-only, per device)
 
 
 class _PinnedStage:
@@ -460,7 +461,7 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, vi
         ws_bytes = int(L.skg_large_workspace_bytes(W, min(max(bound, min_table), 2 * W + 64)))
         ws = _ws.get(ws_bytes)
         for _ in range(3):
-            text = torch.empty(cap, dtype=torch.uint8, device="cuda")
+            text = _large_text.get(cap)   # grow-only (a fresh ~GB allocation per call stalls)
             need = ctypes.c_uint64(0)
             rc = fn(data, nbytes, *args, text.data_ptr(), cap, ctypes.byref(need), status.data_ptr(),
                     errs.data_ptr(), ws.data_ptr(), ws_bytes, _stream(), min_table)

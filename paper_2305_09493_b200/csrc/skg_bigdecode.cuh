@@ -25,7 +25,10 @@
 
 namespace skg {
 
-constexpr uint32_t BD_TILE = 4096;          // words per tile
+#ifndef SKG_BD_TILE
+#define SKG_BD_TILE 1024   // 4096 measured 2 ms slower per call (fewer threads in the per-tile passes)
+#endif
+constexpr uint32_t BD_TILE = SKG_BD_TILE;   // words per tile
 constexpr uint32_t BD_K = 4;                // speculative chains per tile
 constexpr uint32_t BD_SCAN = 64;            // words searched for plausible starts
 constexpr uint32_t BD_NONE = 0xFFFFFFFFu;
@@ -218,7 +221,8 @@ __device__ __forceinline__ void tile_link_body(BigDecode& b) {
 constexpr uint32_t BD_TERM = 0x80000000u;
 constexpr uint32_t TK_END = 100, TK_RAW = 101;
 
-constexpr uint32_t BD_MAXHOP = 16;   // tiles a successor walk may cross before giving up (TK_RAW)
+// tiles a successor walk may cross before giving up (TK_RAW): 64 K words, one maximal instruction
+constexpr uint32_t BD_MAXHOP = 65536 / BD_TILE;
 
 __global__ void tile_land(BigDecode b) {
   const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
