@@ -9,12 +9,14 @@
 //                    grammar's largest) to the tile end, marking the positions
 //                    each visits (a later chain stops where it joins an earlier
 //                    one) -> per chain the exit X and the first error on it
-//   3. tile_link     one thread, tiles in order: from the true entry e_t walk the
-//                    exact rule until the walk lands on a marked position (from
-//                    there that speculative chain IS the true chain: entry of
-//                    the next tile = its X, and its recorded error is the true
-//                    first error) or leaves the tile.  Typically a few steps per
-//                    tile; a tile whose speculation never merges is walked in full.
+//   3. tile_land / tile_jump / tile_path: the tiles linked in parallel -- every
+//                    (tile, chain) node's successor is the chain its exit lands on
+//                    (the exact walk from the exit to the next marked position: from
+//                    there that speculative chain IS the true chain, so its exit and
+//                    recorded first error are the true ones); the successor map is
+//                    doubled and thread d reads the d-th node of the true chain.  A walk
+//                    that crosses 64 K words unmarked sends the whole link to tile_link
+//                    (one warp, tiles in order, the same rule sequentially).
 //   4. tile_count    per tile: instructions on the true chain in the tile
 //   5. tile_scan     exclusive scan of the counts (one CTA)
 //   6. tile_write    per tile: the instruction offsets
