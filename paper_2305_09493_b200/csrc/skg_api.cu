@@ -4,6 +4,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
+#include <mutex>
 #include <cub/device/device_radix_sort.cuh>
 #ifdef W_OK   // <unistd.h> access() mode (via CUB): the walk status enum uses the name
 #undef W_OK
@@ -680,8 +681,24 @@ int name_dedup_closed(const LargeWs& l, uint32_t nd, const uint32_t* clist, uint
   // buffers: 4 x nd members, 6 x nd per-leader arrays, nd flags, 4 x nc children, skips
   // (+ 256-byte alignment of each of the 17 pieces)
   const size_t bytes = 16ull * nd + 24ull * nd + ((nd + 15) & ~15ull) + 24ull * ncx + 4ull * ncx + tmp + 17 * 256;
-  uint8_t* buf = nullptr;
-  if (int e = check(cudaMalloc(reinterpret_cast<void**>(&buf), bytes))) return e;   // (host-synchronous path)
+  // a per-device buffer kept across calls (grow-only): a cudaMalloc / cudaFree of a few
+  // hundred MB per call synchronises the device and costs milliseconds; the lock keeps
+  // concurrent host threads on one device from sharing it mid-call
+  int dev = 0;
+  if (int e = check(cudaGetDevice(&dev))) return e;
+  static std::mutex locks[64];
+  static uint8_t* bufs[64] = {};
+  static size_t caps[64] = {};
+  if (dev < 0 || dev >= 64) return -1;
+  std::lock_guard<std::mutex> guard(locks[dev]);
+  if (caps[dev] < bytes) {
+    if (bufs[dev]) cudaFree(bufs[dev]);
+    bufs[dev] = nullptr; caps[dev] = 0;
+    const size_t grow = bytes + bytes / 4;
+    if (int e = check(cudaMalloc(reinterpret_cast<void**>(&bufs[dev]), grow))) return e;
+    caps[dev] = grow;
+  }
+  uint8_t* buf = bufs[dev];
   uint8_t* p = buf;
   auto take = [&](size_t b) { uint8_t* r = p; p += (b + 255) & ~255ull; return r; };
   uint32_t* keys = reinterpret_cast<uint32_t*>(take(4ull * nd));
@@ -738,7 +755,6 @@ int name_dedup_closed(const LargeWs& l, uint32_t nd, const uint32_t* clist, uint
     step_ok("assign");
   } while (false);
   if (!rc) rc = check(cudaStreamSynchronize(s));
-  cudaFree(buf);
   return rc;
 }
 }  // namespace
