@@ -626,6 +626,84 @@ def run_config3(args, rank, world, local_rank):
     }
 
 
+def run_config1(args, rank, world, local_rank):
+    """BASELINE configs[0]: one saxpy-family module (synth/families.py, seed
+    --c1-seed) disassembled and re-assembled through the public single-module API,
+    assemble_module(disassemble_module(m)), one call pair per step: every step
+    copies the module to the device, launches both kernels, and reads the text
+    and the binary back (per-call latency, host buffers).  cpu_baseline: the
+    reference's own disassemble_module / assemble_module on one host core, same
+    module.  Replicas only: each rank makes its own calls."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    import paper_2305_09493_b200 as sk
+    from synth.families import build_module
+    m = build_module("saxpy", args.c1_seed)
+    W = len(m) // 4
+
+    def step():
+        return sk.assemble_module(sk.disassemble_module(m))
+
+    for _ in range(max(args.warmup, 20)):
+        out = step()
+    assert out == m, "config 1: round trip is not bit-identical"
+    text = sk.disassemble_module(m)
+    calls = max(args.steps, 200)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        t0 = time.perf_counter()
+        for _ in range(calls):
+            step()
+        t_host = time.perf_counter() - t0
+        e1.record()
+        torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_call = float(t.item()) / calls
+    if rank != 0:
+        return None
+    cpu = None
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    try:
+        import spirvkit as R
+        assert R.assemble_module(R.disassemble_module(m)) == m
+        n_ref = 0
+        r0 = time.perf_counter()
+        while time.perf_counter() - r0 < args.c1_cpu_seconds:
+            R.assemble_module(R.disassemble_module(m))
+            n_ref += 1
+        r_dt = (time.perf_counter() - r0) / n_ref
+        cpu = {"value": W / r_dt, "unit": "words/s", "cores": 1, "kind": "reference",
+               "sample": f"{n_ref} calls of spirvkit assemble_module(disassemble_module(m)) on the same "
+                         f"module, one core ({1e6 * r_dt:.0f} us per call)"}
+    except ImportError as exc:
+        log(f"config 1: reference not importable ({exc}); no cpu_baseline")
+    value = world * W / (ms_call / 1e3)
+    return {
+        "metric": METRIC, "value": value, "unit": "words/s", "n_gpus": world,
+        "steps": calls, "warmup": max(args.warmup, 20), "ms_per_step": ms_call, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: synth/families.py saxpy module (builder-canonical, seeded)",
+        "config": {"workload": "configs[0]: one saxpy module, assemble_module(disassemble_module(m)) per step "
+                               "through the public single-module API (per-call latency: H2D, both kernels, "
+                               "D2H of text and binary inside every call)",
+                   "seed": args.c1_seed, "words": W, "text_bytes": len(text),
+                   "us_per_call": 1e3 * ms_call, "host_us_per_call": 1e6 * t_host / calls,
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": len(m) + len(text),
+                "d2h_bytes_per_step": len(text) + len(m)},
+        "gpu_launches": 8 * calls,   # per call pair: 3 scheduling kernels + the main kernel, twice
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+
+
 def run_reference(args, rank):
     if rank != 0:
         return None
@@ -682,9 +760,11 @@ def main():
     ap.add_argument("--cpu-per-core", type=int, default=60)
     ap.add_argument("--ref-modules", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
-                    help="2: configs[1]+[3] round trip per GPU (default); 3: configs[2] one huge module; "
-                         "5: configs[4] sharded pipeline")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5],
+                    help="2: configs[1]+[3] round trip per GPU (default); 1: configs[0] one saxpy module "
+                         "per call (latency); 3: configs[2] one huge module; 5: configs[4] sharded pipeline")
+    ap.add_argument("--c1-seed", type=int, default=0, help="config 1: saxpy variant seed")
+    ap.add_argument("--c1-cpu-seconds", type=float, default=5.0, help="config 1: reference timing budget")
     ap.add_argument("--functions", type=int, default=55000, help="config 3: functions of the module")
     ap.add_argument("--chunk", type=int, default=1_000_000, help="config 5: modules per device chunk")
     args = ap.parse_args()
@@ -717,6 +797,8 @@ def main():
         line = run_config5(args, rank, world, local_rank)
     elif args.config == 3:
         line = run_config3(args, rank, world, local_rank)
+    elif args.config == 1:
+        line = run_config1(args, rank, world, local_rank)
     else:
         line = run_ours(args, rank, world, local_rank)
     if line is not None:

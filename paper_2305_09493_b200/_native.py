@@ -330,7 +330,7 @@ def run_texts_pipeline(batch: DeviceBatch, opts=0, spec=None, ext=None):
     if n == 0:
         return [], []
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
-    if batch.max_words >= LARGE_MODULE_WORDS or (n > 1 and need > WS_BUDGET):
+    if batch.max_words >= large_threshold(n) or (n > 1 and need > WS_BUDGET):
         return run_texts("disasm", batch, opts, spec, ext), run_texts("validate", batch, 0, spec)
     d, v = run_pipeline(batch, opts, spec, ext)
     return fetch_texts(d, n), fetch_texts(v, n)
@@ -390,16 +390,17 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None, refs=None):
     run = (lambda b: run_disasm(b, opts, spec, ext, refs=refs)) if kind == "disasm" else \
         (lambda b: run_validate(b, spec))
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
-    if (n == 1 or need <= WS_BUDGET) and batch.max_words < LARGE_MODULE_WORDS:
+    big = large_threshold(n) if refs is None else 1 << 62   # explicit refs: the batch kernel only
+    if (n == 1 or need <= WS_BUDGET) and batch.max_words < big:
         return fetch_texts(run(batch), n)
     lens = batch.len.cpu().numpy()
     words = lens // 4
-    if batch.max_words >= LARGE_MODULE_WORDS:   # single large modules: the whole GPU on one module
+    if batch.max_words >= big:   # single large modules: the whole GPU on one module
         out = [None] * n
         rest = []
         for i in range(n):
             r = None
-            if words[i] >= LARGE_MODULE_WORDS:
+            if words[i] >= big:
                 r = _validate_large(batch, i, int(lens[i]), spec) if kind == "validate" else \
                     _disasm_large(batch, i, int(lens[i]), opts, spec, ext)
             if r is None:
@@ -429,7 +430,17 @@ def run_texts(kind, batch: DeviceBatch, opts=0, spec=None, ext=None, refs=None):
     return out
 
 
-LARGE_MODULE_WORDS = 1 << 20   # validate: modules this size and up run grid-wide (skg_validate_large)
+LARGE_MODULE_WORDS = 1 << 20   # modules this size and up in a batch run grid-wide (skg_*_large)
+# A single-module call (n == 1) runs grid-wide from this size: one warp takes ~0.27 ms
+# (disasm) / ~0.09 ms (validate) per 1000 words, the grid-wide path ~1 ms + ~0.01 ms per
+# 1000 words (tools/large_threshold_probe.py on a B200: 13.6k words 3.8 vs 1.2 ms,
+# 850k words 291 vs 3.3 ms; 1.8k words 0.64 vs 0.98 ms).  In a batch the other modules
+# run beside the one warp, so only LARGE_MODULE_WORDS sends a module there.
+SINGLE_LARGE_WORDS = 4096
+
+
+def large_threshold(n: int) -> int:
+    return min(SINGLE_LARGE_WORDS, LARGE_MODULE_WORDS) if n == 1 else LARGE_MODULE_WORDS
 _DECODE_CODES = {ST_NOTSPIRV: "NotSpirv", ST_TRUNCATED: "TruncatedStream", ST_CORRUPT: "CorruptStream"}
 
 

@@ -168,12 +168,18 @@ def test_sharded_disasm_world1_gpu(sk):
         dist.destroy_process_group()
 
 
-def test_huge_single_module_vs_oracle(sk):
+@pytest.mark.parametrize("path", ["grid-wide", "one-warp"])
+def test_huge_single_module_vs_oracle(sk, monkeypatch, path):
     """Config-3 shape (one large module, dense OpName, long OpString, ids > 2^16)
     at a size the oracle finishes in seconds: disassembly (default options and
-    numeric refs) and validation identical."""
+    numeric refs) and validation identical, on the grid-wide path a single-module
+    call takes at this size (_native.SINGLE_LARGE_WORDS) and on the one-warp batch
+    path it takes inside a batch."""
     from oracle import disasm as odis, validate as oval
+    from paper_2305_09493_b200 import _native
     from synth.huge import build_huge
+    if path == "one-warp":
+        monkeypatch.setattr(_native, "SINGLE_LARGE_WORDS", 1 << 40)
     m = build_huge(400, chain=200, seed=3)          # ~740k words, ids up to ~81k
     assert len(m) // 4 > 500_000
     got = sk.disassemble_batch([m])[0]
@@ -182,6 +188,38 @@ def test_huge_single_module_vs_oracle(sk):
     assert sk.disassemble_batch([m], opts)[0] == odis.disassemble(m, opts)
     d = sk.validate_batch([m])[0]
     assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(m)]
+
+
+def test_single_module_routing_sizes(sk):
+    """Single-module calls on either side of _native.SINGLE_LARGE_WORDS (one-warp
+    batch kernel below, grid-wide kernels from it): every option set, the fused
+    disassemble+validate entry point and the decode errors equal the oracle's."""
+    import struct
+    from oracle import disasm as odis, validate as oval
+    from paper_2305_09493_b200 import _native
+    from synth.huge import build_huge
+    mods = [build_huge(k, chain=c, string_kib=s) for k, c, s in ((1, 20, ()), (4, 50, ()), (8, 200, (1,)))]
+    sizes = [len(m) // 4 for m in mods]
+    assert min(sizes) < _native.SINGLE_LARGE_WORDS <= max(sizes)
+    mods.append(mods[2][:-6])                                        # truncated mid-instruction
+    mods.append(mods[2][:20] + struct.pack("<I", 0x00000011) + mods[2][24:])   # word count 0
+    option_sets = [sk.DisassemblerOptions(), sk.DisassemblerOptions(inline_names=False),
+                   sk.DisassemblerOptions(highlight=True, group=True),
+                   sk.DisassemblerOptions(no_indent=True, no_header=True)]
+    for m in mods:
+        for o in option_sets:
+            try:
+                want = odis.disassemble(m, o)
+            except Exception as exc:  # noqa: BLE001
+                want = (type(exc).__name__, str(exc))
+            got = sk.disassemble_batch([m], o)[0]
+            got = (type(got).__name__, str(got)) if isinstance(got, BaseException) else got
+            assert got == want, (len(m), o)
+        want_v = [tuple(x) for x in oval.validate(m)]
+        got_v = sk.validate_batch([m])[0]
+        assert [(x.severity, x.code, x.location, x.message) for x in got_v] == want_v
+        _, v = sk.disassemble_validate_batch([m])[0]
+        assert [(x.severity, x.code, x.location, x.message) for x in v] == want_v
 
 
 def test_format_instruction_known_answers(sk):
