@@ -698,7 +698,7 @@ def run_config1(args, rank, world, local_rank):
                    "parallelism": f"replicas x{world}"},
         "e2e": {"value": value, "unit": "words/s", "h2d_bytes_per_step": len(m) + len(text),
                 "d2h_bytes_per_step": len(text) + len(m)},
-        "gpu_launches": 8 * calls,   # per call pair: 3 scheduling kernels + the main kernel, twice
+        "gpu_launches": 2 * calls,   # per call pair: disasm_kernel + asm_kernel (one module: no scheduling sort)
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

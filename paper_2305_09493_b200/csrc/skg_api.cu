@@ -79,6 +79,8 @@ int launch_sched(const int64_t* len, uint32_t stride, uint32_t n, uint8_t* sched
   uint32_t* hist = reinterpret_cast<uint32_t*>(sched);
   uint32_t* cursor = hist + skg::SCHED_BUCKETS;
   uint32_t* perm = cursor + skg::SCHED_BUCKETS;
+  if (n <= 1)   // one module (single-module calls): the order is [0], no sort kernels
+    return n ? (int)cudaMemsetAsync(perm, 0, 4, s) : 0;
   if (cudaError_t e = cudaMemsetAsync(hist, 0, 4 * skg::SCHED_BUCKETS, s)) return (int)e;
   uint32_t blocks = (n + 4095) / 4096;
   if (blocks > (uint32_t)sm_count() * 2) blocks = (uint32_t)sm_count() * 2;
