@@ -73,3 +73,29 @@ def test_grammar_disasm_validate_asm(sk, which):
     bad += [(r["name"], "asm") for (r, _), g in zip(texts, got)
             if not _same(_out(g.hex() if isinstance(g, bytes) else g), r[which]["asm"])]
     assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("which", ["1.2", "custom"])
+def test_grammar_grid_wide_single_module_path(sk, monkeypatch, which):
+    """The same goldens through the grid-wide single-module kernels (skg_disasm_large /
+    skg_validate_large), which single-module calls of _native.SINGLE_LARGE_WORDS words
+    and up take: forced here for every module, one call per module."""
+    from golden_io import modules
+    from paper_2305_09493_b200 import _native
+    monkeypatch.setattr(_native, "SINGLE_LARGE_WORDS", 1)
+    spec = _spec(sk, which)
+    data = {r["name"]: r["bytes"] for r in modules()}
+    from synth.families import FAMILIES, build_module
+    for f in FAMILIES:
+        for s in range(3):
+            data[f"fam_{f}_{s}"] = build_module(f, 100 + s)
+    bad = []
+    numeric = sk.DisassemblerOptions(inline_names=False)
+    for r in golden()["modules"]:
+        m = data[r["name"]]
+        for key, opts in (("disasm", None), ("numeric", numeric)):
+            if not _same(_out(sk.disassemble_batch([m], opts, spec=spec)[0]), r[which][key]):
+                bad.append((r["name"], key))
+        if not _same(_out(sk.validate_batch([m], spec=spec)[0], True), r[which]["validate"]):
+            bad.append((r["name"], "validate"))
+    assert not bad, bad[:10]

@@ -39,6 +39,29 @@ def test_disasm_golden_batch_all_options(sk):
     assert not bad, bad[:10]
 
 
+def test_golden_grid_wide_single_module_path(sk, monkeypatch):
+    """Every reference-recorded golden module, one call per module, through the
+    grid-wide kernels (skg_disasm_large / skg_validate_large) that single-module
+    calls of _native.SINGLE_LARGE_WORDS words and up take (forced here for all):
+    all six option sets, strict, and validation."""
+    from paper_2305_09493_b200 import _native
+    monkeypatch.setattr(_native, "SINGLE_LARGE_WORDS", 1)
+    bad = []
+    for r in CASES:
+        m = r["bytes"]
+        for key, opts in OPTION_SETS.items():
+            if not same(_as_outcome(sk.disassemble_batch([m], sk.DisassemblerOptions(**opts))[0]), r["disasm"][key]):
+                bad.append((r["name"], key))
+        if not same(_as_outcome(sk.disassemble_batch([m], strict=True)[0]), r["disasm_strict"]):
+            bad.append((r["name"], "strict"))
+        o = _as_outcome(sk.validate_batch([m])[0])
+        if "ok" in o:
+            o = {"ok": [[d.severity, d.code, d.location, d.message] for d in o["ok"]]}
+        if not same(o, r["validate"]):
+            bad.append((r["name"], "validate"))
+    assert not bad, bad[:10]
+
+
 @pytest.mark.parametrize("rec", CASES[:40], ids=[r["name"] for r in CASES[:40]])
 def test_disassemble_module_single(sk, rec):
     got = outcome(lambda: sk.disassemble_module(rec["bytes"]))
