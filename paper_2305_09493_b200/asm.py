@@ -11,6 +11,7 @@ ValueError, OverflowError, StructureError, SerializationError, CodecError).
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 
 from . import _native
@@ -136,6 +137,7 @@ class RoundTripSession:
     """
 
     TEXT_FACTOR = 6
+    TAPER = (0.25, 0.5, 0.75)   # relative sizes of the first / last chunks (short pipeline head / tail)
 
     def __init__(self, options=None, spec=None, ext=None, chunks=12):
         from .disasm import DisassemblerOptions, option_bits
@@ -186,6 +188,8 @@ class RoundTripSession:
         import numpy as np
         import torch
         n = len(offsets)
+        if self.kernel_events is not None:
+            self.marks = [("start", time.perf_counter())]
         if n == 0:
             z8, z32 = np.zeros(0, np.uint8), np.zeros(0, np.int32)
             zs = np.zeros((0, 2), np.int64)
@@ -196,32 +200,36 @@ class RoundTripSession:
         cum = np.cumsum(lengths)
         total = int(cum[-1])
         w = np.ones(self.nchunks)
-        if self.nchunks >= 3:
-            w[0] = w[-1] = 0.5
+        for j, t in enumerate(self.TAPER):          # short head and tail chunks
+            if self.nchunks >= 2 * j + 3:
+                w[j] = w[-1 - j] = t
         frac = np.cumsum(w) / w.sum()
-        cuts = [0] + [int(np.searchsorted(cum, total * frac[k - 1])) for k in range(1, self.nchunks)] + [n]
+        # integer targets: a float target would convert all of cum to float64 per search
+        cuts = [0] + [int(np.searchsorted(cum, int(total * frac[k - 1]))) for k in range(1, self.nchunks)] + [n]
         cuts = sorted(set(cuts))
         chunks = [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+        if self.kernel_events is not None:
+            self.marks.append(("chunks cut", time.perf_counter()))
         d_data = self._get("d_data", nbytes + 16, torch.uint8)
+        # module offsets / lengths go up per chunk with the chunk's bytes (the host fills
+        # chunk k's slice of the pinned staging while the GPU runs chunk k - 1)
         h_meta = self._get("h_meta", 2 * n, torch.int64, pinned=True)
-        h_meta.numpy()[:n] = offsets
-        h_meta.numpy()[n: 2 * n] = lengths
         d_meta = self._get("d_meta", 2 * n, torch.int64)
         h_tspan = self._get("h_tspan", 2 * n, torch.int64, pinned=True)
         h_bspan = self._get("h_bspan", 2 * n, torch.int64, pinned=True)
         h_tst = self._get("h_tst", n, torch.int32, pinned=True)
         h_bst = self._get("h_bst", n, torch.int32, pinned=True)
         h_cnt = self._get("h_cnt", 16 * len(chunks), torch.int32, pinned=True)
+        if self.kernel_events is not None:
+            self.marks.append(("buffers", time.perf_counter()))
         comp = torch.cuda.current_stream()
-        s_in = self._buf.setdefault("s_in", torch.cuda.Stream())
-        s_out = self._buf.setdefault("s_out", torch.cuda.Stream())
+        if "s_in" not in self._buf:
+            self._buf["s_in"], self._buf["s_out"] = torch.cuda.Stream(), torch.cuda.Stream()
+        s_in, s_out = self._buf["s_in"], self._buf["s_out"]
         cs = _native.ctypes.c_void_p(comp.cuda_stream)
-        with torch.cuda.stream(s_in):
-            d_meta[: 2 * n].copy_(h_meta[: 2 * n], non_blocking=True)
-        ev_meta = torch.cuda.Event()
-        ev_meta.record(s_in)
-        comp.wait_event(ev_meta)
         plans = []
+        if self.kernel_events is not None:
+            self.marks.append(("streams", time.perf_counter()))
 
         L = _native.lib()
 
@@ -267,8 +275,13 @@ class RoundTripSession:
             if ap.ws is not self._buf.get("ws_a"):
                 self._buf["ws_a"] = ap.ws
             if grow is None:
+                hm = h_meta.numpy()
+                hm[a:b] = offsets[a:b]
+                hm[n + a:n + b] = lengths[a:b]
                 ev_in = torch.cuda.Event()
                 with torch.cuda.stream(s_in):
+                    d_meta[a:b].copy_(h_meta[a:b], non_blocking=True)
+                    d_meta[n + a:n + b].copy_(h_meta[n + a:n + b], non_blocking=True)
                     d_data[b0:b1].copy_(h_data[b0:b1], non_blocking=True)
                     ev_in.record(s_in)
                 comp.wait_event(ev_in)
@@ -310,9 +323,23 @@ class RoundTripSession:
                 ho[pos[1]:pos[1] + oused].copy_(ap.out[:oused], non_blocking=True)
                 h_bspan[2 * a:2 * b].copy_(ap.span[: 2 * (b - a)], non_blocking=True)
                 h_bst[a:b].copy_(ap.status[: b - a], non_blocking=True)
-            parts[k] = (pos[0], tused, pos[1], oused)
+            ev_copy = torch.cuda.Event()
+            ev_copy.record(s_out)
+            parts[k] = (pos[0], tused, pos[1], oused, ev_copy)
+            rebased.discard(k)
             pos[0] += tused
             pos[1] += oused
+
+        def rebase(k):
+            """chunk k's spans -> offsets in the whole arenas (once its copies are done)"""
+            a, b = chunks[k]
+            tp, _, op, _, ev_copy = parts[k]
+            ev_copy.synchronize()
+            h_tspan[2 * a:2 * b:2].numpy()[:] += tp
+            h_bspan[2 * a:2 * b:2].numpy()[:] += op
+            if (h_bst[a:b].numpy() == _native.ST_INTERNAL).any():
+                internal.add(k)
+            rebased.add(k)
 
         def arena(name, used, need):
             """grow-only pinned host arena; growing keeps the bytes already copied"""
@@ -329,31 +356,41 @@ class RoundTripSession:
 
         total_in = int(lengths.sum())
         hint = {"h_text": total_in * self._ratio[0], "h_out": total_in * self._ratio[1]}
-        pos, parts = [0, 0], {}
+        pos, parts, rebased, internal = [0, 0], {}, set(), set()
         for k in range(len(chunks)):
             plans.append(launch(k))
+            if k == 0 and self.kernel_events is not None:
+                self.marks.append(("chunk 0 queued", time.perf_counter()))
             if k >= 1:
                 drain(k - 1)          # host one chunk behind: chunk k's kernels are queued
+            if k >= 2:
+                rebase(k - 2)         # its copies were queued a chunk ago: overlaps chunk k
         drain(len(chunks) - 1)
+        if self.kernel_events is not None:
+            self.marks.append(("last drain queued", time.perf_counter()))
         s_out.synchronize()
+        if self.kernel_events is not None:
+            self.marks.append(("copies done", time.perf_counter()))
+        for k in range(len(chunks)):
+            if k not in rebased:
+                rebase(k)
         # a module whose text outgrew the per-module bound the assembler slots were sized
         # for reports an internal status: re-run its chunk with slots for the real maximum
-        # (its results are appended to the arenas; spans are rebased below)
-        for k, (a, b) in enumerate(chunks):
-            if (h_bst[a:b].numpy() == _native.ST_INTERNAL).any():
-                mx = int(h_tspan[2 * a + 1:2 * b:2].numpy().max())
-                _, tused, _, oused = parts[k]
-                plans[k] = launch(k, grow=(tused, max(oused, 4 * mx), mx))
-                drain(k)
-                s_out.synchronize()
+        # (its results are appended to the arenas and its spans rebased again)
+        for k in sorted(internal):
+            a, b = chunks[k]
+            mx = int(h_tspan[2 * a + 1:2 * b:2].numpy().max())
+            _, tused, _, oused, _ = parts[k]
+            plans[k] = launch(k, grow=(tused, max(oused, 4 * mx), mx))
+            drain(k)
+            s_out.synchronize()
+            rebase(k)
         tspan = h_tspan[: 2 * n].numpy().reshape(n, 2)
         bspan = h_bspan[: 2 * n].numpy().reshape(n, 2)
-        for k, (a, b) in enumerate(chunks):
-            tp, _, op, _ = parts[k]
-            tspan[a:b, 0] += tp
-            bspan[a:b, 0] += op
         if total_in:
             self._ratio = (max(self._ratio[0], pos[0] / total_in), max(self._ratio[1], pos[1] / total_in))
+        if self.kernel_events is not None:
+            self.marks.append(("spans rebased", time.perf_counter()))
         text = self._buf["h_text"].numpy()[: pos[0]]
         binv = self._buf["h_out"].numpy()[: pos[1]]
         return text, tspan, h_tst[:n].numpy(), binv, bspan, h_bst[:n].numpy()

@@ -26,7 +26,9 @@ def shard_ranges(lengths, world: int) -> list[tuple[int, int]]:
     total = int(cum[-1]) if n else 0
     cuts = [0]
     for k in range(1, world):
-        cut = int(np.searchsorted(cum, total * k / world, side="left")) if total else n * k // world
+        # first module whose running byte total reaches k/world of the batch (integer
+        # target ceil(total*k/world): same cut, no float conversion of cum per search)
+        cut = int(np.searchsorted(cum, -(-total * k // world), side="left")) if total else n * k // world
         cuts.append(min(max(cut, cuts[-1]), n))
     cuts.append(n)
     return [(cuts[k], cuts[k + 1]) for k in range(world)]
