@@ -12,19 +12,33 @@ namespace skg {
 constexpr uint32_t SCHED_BUCKETS = 1024;
 constexpr uint32_t SCHED_SHIFT = 6;        // 64-byte size classes
 
-__device__ __forceinline__ uint32_t sched_bucket(int64_t len) {
-  const uint64_t c = len <= 0 ? 0 : ((uint64_t)len >> SCHED_SHIFT);
-  return SCHED_BUCKETS - 1 - (uint32_t)(c < SCHED_BUCKETS - 1 ? c : SCHED_BUCKETS - 1);
+// Region-major order (regions > 1): the modules are cut into `regions` contiguous
+// index ranges, processed one range after the other, each largest first (in
+// 1024/regions size classes of 2^shift bytes).  The modules in flight at any time
+// then come from one range of the input instead of from all of it.  Over the
+// bench's 1M-module (2.7 GB) batch: disassembly 133.1 -> 115.8 ms with 16 regions
+// of 128-byte classes (4: 127.2, 8: 119.6, 32: 118.4, 64: 119.7 ms; 16 regions of
+// 64-byte classes 121.6 ms), the fused disassemble+validate pass 156.5 -> 135.5 ms.
+// Used where the modules arrive in caller order (disassembler, fused pass).
+struct SchedKey {
+  uint32_t regions, n, shift;
+};
+
+__device__ __forceinline__ uint32_t sched_bucket(int64_t len, uint32_t i, SchedKey k) {
+  const uint64_t c = len <= 0 ? 0 : ((uint64_t)len >> k.shift);
+  const uint32_t per = SCHED_BUCKETS / k.regions;
+  const uint32_t r = (uint32_t)(((uint64_t)i * k.regions) / k.n);
+  return r * per + per - 1 - (uint32_t)(c < per - 1 ? c : per - 1);
 }
 
 // hist[b] += number of modules in bucket b
 __global__ void __launch_bounds__(1024) sched_hist(const int64_t* len, uint32_t stride, uint32_t n,
-                                                   uint32_t* hist) {
+                                                   uint32_t* hist, SchedKey k) {
   __shared__ uint32_t h[SCHED_BUCKETS];
   for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x) h[b] = 0;
   __syncthreads();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(&h[sched_bucket(len[(size_t)i * stride])], 1u);
+    atomicAdd(&h[sched_bucket(len[(size_t)i * stride], i, k)], 1u);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x)
     if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -58,19 +72,19 @@ __global__ void __launch_bounds__(1024) sched_scan(const uint32_t* hist, uint32_
 
 // perm[cursor[b]++] = i; each CTA owns a contiguous chunk of module indices
 __global__ void __launch_bounds__(1024) sched_scatter(const int64_t* len, uint32_t stride, uint32_t n,
-                                                      uint32_t* cursor, uint32_t* perm) {
+                                                      uint32_t* cursor, uint32_t* perm, SchedKey k) {
   __shared__ uint32_t h[SCHED_BUCKETS];
   const uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const uint32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x) h[b] = 0;
   __syncthreads();
-  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[sched_bucket(len[(size_t)i * stride])], 1u);
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[sched_bucket(len[(size_t)i * stride], i, k)], 1u);
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < SCHED_BUCKETS; b += blockDim.x)
     if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);
   __syncthreads();
   for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const uint32_t b = sched_bucket(len[(size_t)i * stride]);
+    const uint32_t b = sched_bucket(len[(size_t)i * stride], i, k);
     perm[atomicAdd(&h[b], 1u)] = i;
   }
 }
