@@ -36,8 +36,13 @@ def main():
             mt = int(dp.span[1::2].max().item())
             tb = _native.DeviceBatch(dp.text, dp.span[0::2], dp.span[1::2], (mt + 3) // 4, 0)
             tb.n = c - a
-            ap = _native.AsmPlan(tb, out_cap=int(lens.sum()) + 64 * (c - a) + 4096, stride=2)
+            import os
+            slot = int(os.environ.get("SLOT_KB", "0")) * 1024 or None
+            ap = _native.AsmPlan(tb, out_cap=int(lens.sum()) + 64 * (c - a) + 4096, stride=2, slot_bytes=slot)
             ap.fit()
+            st = ap.status[: c - a].cpu().numpy()
+            print(f"   asm slot {ap.slot} B, {(st == _native.ST_INTERNAL).sum()} modules over it, "
+                  f"{(st != 0).sum()} not ok", flush=True)
             plans.append((dp, ap))
         best_d = best_a = 1e9
         for _ in range(4):
