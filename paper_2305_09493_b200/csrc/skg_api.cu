@@ -72,7 +72,7 @@ struct WsLayout {
 };
 
 // scheduling region: hist[1024], cursor[1024], perm[n]
-uint64_t sched_bytes(uint32_t n_mod) { return (8192 + 4ull * n_mod + 255) & ~255ull; }
+uint64_t sched_bytes(uint32_t n_mod) { return (skg::SCHED_PERM_OFF + 4ull * n_mod + 255) & ~255ull; }
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -80,7 +80,7 @@ int env_int(const char* name, int dflt) {
 }
 
 // module processing order (largest first; region-major for big batches of modules
-// in caller order, see skg_sched.cuh) into sched + 8192
+// in caller order, see skg_sched.cuh) into sched + SCHED_PERM_OFF
 uint32_t sched_regions(uint32_t n) {
   const int want = env_int("SKG_SCHED_REGIONS", -1);         // experiments: fixed count
   uint32_t r = want > 0 ? (uint32_t)want : std::min<uint32_t>(16, n / 50000);
@@ -103,7 +103,7 @@ int launch_sched(const int64_t* len, uint32_t stride, uint32_t n, uint8_t* sched
   skg::SchedKey key{regions ? sched_regions(n) : 1u, n, skg::SCHED_SHIFT};
   if (key.regions > 1) key.shift = region_shift;   // 64 classes of 2^shift bytes per region (16 regions)
   skg::sched_hist<<<blocks, 1024, 0, s>>>(len, stride, n, hist, key);
-  skg::sched_scan<<<1, skg::SCHED_BUCKETS, 0, s>>>(hist, cursor);
+  skg::sched_scan<<<1, 1024, 0, s>>>(hist, cursor);
   skg::sched_scatter<<<blocks, 1024, 0, s>>>(len, stride, n, cursor, perm, key);
   return (int)cudaGetLastError();
 }
@@ -312,8 +312,8 @@ int disasm_launch(const skg_tables* t, const uint8_t* data, const int64_t* mod_o
   a.verrs = reinterpret_cast<skg::ErrRec*>(vo ? vo->errors : nullptr);
   a.verr_cap = vo ? vo->err_cap : 0;
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s, true,
-                                               (uint32_t)env_int("SKG_DIS_SHIFT", 7)))) return e;
-  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
+                                               (uint32_t)env_int("SKG_DIS_SHIFT", 6)))) return e;
+  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + skg::SCHED_PERM_OFF);
   a.stage_bytes = kDisStage;
   const Geom g = dis_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_DIS_GROUP", (int)g.warps));
@@ -382,7 +382,7 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   // size order only: region-major measured 53.3 -> 54.6 ms on the 1M-module batch here
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s, env_int("SKG_VAL_REGIONS", 0) != 0,
                                                (uint32_t)env_int("SKG_VAL_SHIFT", 7)))) return e;
-  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + 8192);
+  a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + skg::SCHED_PERM_OFF);
   const Geom g = val_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_VAL_GROUP", (int)g.warps));
   static uint64_t carve = 0;
@@ -434,7 +434,7 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   if (int e = check((cudaError_t)launch_sched(mod_len, a.mod_stride, n_mod, ws + 256, s,
                                                env_int("SKG_ASM_REGIONS", 0) != 0,
                                                (uint32_t)env_int("SKG_ASM_SHIFT", 11)))) return e;
-  a.order = reinterpret_cast<const uint32_t*>(ws + 256 + 8192);
+  a.order = reinterpret_cast<const uint32_t*>(ws + 256 + skg::SCHED_PERM_OFF);
   a.gscratch = ws + 256 + sched_bytes(n_mod);
   a.gslot_bytes = slot_bytes;
   a.default_version = default_version;

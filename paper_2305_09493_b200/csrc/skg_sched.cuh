@@ -9,16 +9,20 @@
 
 namespace skg {
 
-constexpr uint32_t SCHED_BUCKETS = 1024;
+constexpr uint32_t SCHED_BUCKETS = 4096;
+constexpr uint32_t SCHED_PER_THREAD = SCHED_BUCKETS / 1024;   // buckets per thread of sched_scan
+constexpr uint32_t SCHED_PERM_OFF = 8 * SCHED_BUCKETS;         // bytes: hist[], cursor[], then perm[]
 constexpr uint32_t SCHED_SHIFT = 6;        // 64-byte size classes
 
 // Region-major order (regions > 1): the modules are cut into `regions` contiguous
 // index ranges, processed one range after the other, each largest first (in
-// 1024/regions size classes of 2^shift bytes).  The modules in flight at any time
+// SCHED_BUCKETS/regions size classes of 2^shift bytes).  The modules in flight at any time
 // then come from one range of the input instead of from all of it.  Over the
 // bench's 1M-module (2.7 GB) batch: disassembly 133.1 -> 115.8 ms with 16 regions
-// of 128-byte classes (4: 127.2, 8: 119.6, 32: 118.4, 64: 119.7 ms; 16 regions of
-// 64-byte classes 121.6 ms), the fused disassemble+validate pass 156.5 -> 135.5 ms.
+// of 64 128-byte classes (4: 127.2, 8: 119.6, 32: 118.4, 64: 119.7 ms; 16 regions of
+// 64 64-byte classes, i.e. everything over 4 KB in one class: 121.6 ms), 115.2 ms
+// with 4096 buckets (16 regions of 256 64-byte classes); the fused
+// disassemble+validate pass 156.5 -> 135.4 ms.
 // Used where the modules arrive in caller order (disassembler, fused pass).
 struct SchedKey {
   uint32_t regions, n, shift;
@@ -44,12 +48,15 @@ __global__ void __launch_bounds__(1024) sched_hist(const int64_t* len, uint32_t 
     if (h[b]) atomicAdd(&hist[b], h[b]);
 }
 
-// cursor = exclusive scan of hist (one CTA of SCHED_BUCKETS threads)
+// cursor = exclusive scan of hist (one CTA of 1024 threads, SCHED_PER_THREAD
+// consecutive buckets each)
 __global__ void __launch_bounds__(1024) sched_scan(const uint32_t* hist, uint32_t* cursor) {
   __shared__ uint32_t wsum[32];
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const uint32_t v = hist[t];
-  uint32_t x = v;
+  uint32_t v[SCHED_PER_THREAD], own = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < SCHED_PER_THREAD; ++j) { v[j] = hist[t * SCHED_PER_THREAD + j]; own += v[j]; }
+  uint32_t x = own;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
@@ -67,7 +74,9 @@ __global__ void __launch_bounds__(1024) sched_scan(const uint32_t* hist, uint32_
     wsum[lane] = s;
   }
   __syncthreads();
-  cursor[t] = x - v + (warp ? wsum[warp - 1] : 0);
+  uint32_t c = x - own + (warp ? wsum[warp - 1] : 0);
+#pragma unroll
+  for (uint32_t j = 0; j < SCHED_PER_THREAD; ++j) { cursor[t * SCHED_PER_THREAD + j] = c; c += v[j]; }
 }
 
 // perm[cursor[b]++] = i; each CTA owns a contiguous chunk of module indices
