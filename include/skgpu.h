@@ -281,6 +281,14 @@ int skg_last_counts(const void* workspace, uint32_t* n_errors, uint32_t* text_ov
  * interface: plumbing of the host-buffer round-trip session. */
 int skg_store_counters(void* host_dst, const void* dev_src, uint32_t n_words, void* stream);
 
+/* Copy n_bytes from device memory into page-locked host memory (host_dst from
+ * cudaHostAlloc / a pinned tensor; both 16-byte aligned, else a plain async copy)
+ * with a kernel of n_ctas CTAs (0: 64) on `stream`: SM stores over PCIe, no copy
+ * engine, so small driver copies of concurrent calls do not queue behind it
+ * (skg_disasm_large's text while skg_validate_large runs).  Not a reference
+ * interface: plumbing of the single-large-module disassemble + validate call. */
+int skg_copy_to_host(void* host_dst, const void* dev_src, uint64_t n_bytes, uint32_t n_ctas, void* stream);
+
 /* Version / build info string. */
 const char* skg_version(void);
 

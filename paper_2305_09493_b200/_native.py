@@ -78,6 +78,8 @@ def lib():
         f.restype = I32
     L.skg_store_counters.argtypes = [P, P, U32, P]
     L.skg_store_counters.restype = I32
+    L.skg_copy_to_host.argtypes = [P, P, U64, U32, P]
+    L.skg_copy_to_host.restype = I32
     L.skg_version.restype = ctypes.c_char_p
     for f in (L.skg_tables_create, L.skg_disasm, L.skg_validate, L.skg_decode, L.skg_last_counts,
               L.skg_decode_large):
@@ -180,6 +182,7 @@ class _Workspace:
 
 _ws = _Workspace()
 _large_text = _Workspace()   # the large-module calls' text arena (grow-only, per device)
+_large_vtext = _Workspace()  # the validation's, when it runs while a disassembly is copied out
 
 
 class _PinnedStage:
@@ -219,11 +222,13 @@ class _PinnedStage:
 
 
 _pinned = _PinnedStage()
+_pinned_v = _PinnedStage()   # a validation's results while _pinned receives a disassembly
 
 
 def release_host_staging():
-    """Free the pinned host staging buffer (it grows to the largest result fetched)."""
+    """Free the pinned host staging buffers (they grow to the largest result fetched)."""
     _pinned.buf = None
+    _pinned_v.buf = None
 
 
 def _stream():
@@ -330,6 +335,13 @@ def run_texts_pipeline(batch: DeviceBatch, opts=0, spec=None, ext=None):
     if n == 0:
         return [], []
     need = int(lib().skg_workspace_bytes(n, max(batch.max_words, 1)))
+    if n == 1 and batch.max_words >= large_threshold(1):   # one large module: grid-wide, copy overlapped
+        t, v = _disasm_validate_large(batch, 0, int(batch.len[0].item()), opts, spec, ext)
+        if t is None:
+            t = run_texts("disasm", batch, opts, spec, ext)[0]
+        if v is None:
+            v = run_texts("validate", batch, 0, spec)[0]
+        return [t], [v]
     if batch.max_words >= large_threshold(n) or (n > 1 and need > WS_BUDGET):
         return run_texts("disasm", batch, opts, spec, ext), run_texts("validate", batch, 0, spec)
     d, v = run_pipeline(batch, opts, spec, ext)
@@ -452,9 +464,12 @@ def _header_bound(head: bytes) -> int:
     return int(np.frombuffer(head[:20], dtype=">u4")[3]) if w[0] == 0x03022307 else int(w[3])
 
 
-def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, view=False):
+def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, view=False, pool=None,
+                fetch=True, stage=None):
     """Shared driver of skg_validate_large / skg_disasm_large -> (rc, text bytes, errs);
-    view=True: the text as a numpy view of the pinned staging buffer (see _PinnedStage)."""
+    view=True: the text as a numpy view of the pinned staging buffer (see _PinnedStage);
+    pool: the device text arena (default _large_text); fetch=False: the text stays a
+    device tensor (a slice of the arena)."""
     torch = _torch()
     L = lib()
     o = int(batch.off[i].item())
@@ -472,7 +487,7 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, vi
         ws_bytes = int(L.skg_large_workspace_bytes(W, min(max(bound, min_table), 2 * W + 64)))
         ws = _ws.get(ws_bytes)
         for _ in range(3):
-            text = _large_text.get(cap)   # grow-only (a fresh ~GB allocation per call stalls)
+            text = (pool or _large_text).get(cap)   # grow-only (a fresh ~GB allocation per call stalls)
             need = ctypes.c_uint64(0)
             rc = fn(data, nbytes, *args, text.data_ptr(), cap, ctypes.byref(need), status.data_ptr(),
                     errs.data_ptr(), ws.data_ptr(), ws_bytes, _stream(), min_table)
@@ -483,7 +498,9 @@ def _large_call(fn, batch: DeviceBatch, i: int, nbytes: int, *args, cap=None, vi
         if rc != 2:
             break
     _check(rc if rc < 0 else 0, getattr(fn, "__name__", "large call"))
-    return rc, (_pinned.to_bytes(text[: int(need.value)], view) if rc == 0 else None), errs
+    if rc != 0:
+        return rc, None, errs
+    return rc, ((stage or _pinned).to_bytes(text[: int(need.value)], view) if fetch else text[: int(need.value)]), errs
 
 
 def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext, view=False):
@@ -502,14 +519,71 @@ def _disasm_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext,
     return decode_errors(errs.cpu().numpy())[0]
 
 
-def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec):
+def _disasm_validate_large(batch: DeviceBatch, i: int, nbytes: int, opts: int, spec, ext, view=False):
+    """Module i through skg_disasm_large then skg_validate_large, the disassembly's text
+    copied to the host on a side stream while the validation kernels run ->
+    (text | exception | None, diagnostics text | exception | None); None = use the batch
+    path.  view=True: the text as a numpy view of the pinned staging buffer."""
+    torch = _torch()
+    L = lib()
+    th = tables_handle(spec, ext)
+
+    def disasm_large(*a):
+        return L.skg_disasm_large(th, a[0], a[1], *a[2:])
+    rc, dtext, errs = _large_call(disasm_large, batch, i, nbytes, opts, fetch=False)
+    if rc == 2:
+        return None, _validate_large(batch, i, nbytes, spec)
+    if rc != 0:
+        return decode_errors(errs.cpu().numpy())[0], _validate_large(batch, i, nbytes, spec)
+    n = int(dtext.numel())
+    if n < (16 << 20):       # small text: the plain copy
+        return _pinned.to_bytes(dtext, view), _validate_large(batch, i, nbytes, spec, pool=_large_vtext)
+    stage = _pinned
+    if stage.buf is None or stage.buf.numel() < n:
+        stage.buf = torch.empty(n + (n >> 3), dtype=torch.uint8).pin_memory()
+    side = _side_stream()
+    ready = torch.cuda.Event()
+    ready.record(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        # SM stores into the mapped pinned buffer: a copy-engine D2H would hold up the
+        # validation's own small device->host reads queued behind it (config 3: 51.8 ms
+        # per step with the copy engine; 8 CTAs 40.7 ms, 4: 49, 16: 44.8, 64: 51.2 -- more
+        # CTAs take SMs from the validation kernels)
+        _check(L.skg_copy_to_host(ctypes.c_void_p(stage.buf.data_ptr()), ctypes.c_void_p(dtext.data_ptr()), n,
+                                  int(os.environ.get("SKG_D2H_CTAS", "8")), ctypes.c_void_p(side.cuda_stream)),
+               "copy_to_host")
+        copied = torch.cuda.Event()
+        copied.record(side)
+    # the validation writes its own arena (_large_vtext) and host staging (small: .cpu())
+    diags = _validate_large(batch, i, nbytes, spec, pool=_large_vtext, stage=_pinned_v)
+    copied.synchronize()
+    torch.cuda.current_stream().wait_event(copied)   # the arena is reused by the next call
+    host = stage.buf[:n].numpy()
+    return (host if view else host.tobytes()), diags
+
+
+_side_streams = {}
+
+
+def _side_stream():
+    """one side stream per device (result copies that overlap kernels)"""
+    torch = _torch()
+    dev = _device()
+    st = _side_streams.get(dev)
+    if st is None:
+        st = _side_streams[dev] = torch.cuda.Stream()
+    return st
+
+
+def _validate_large(batch: DeviceBatch, i: int, nbytes: int, spec, pool=None, stage=None):
     """skg_validate_large on module i of a device batch -> text bytes | exception | None (= not handled)."""
     L = lib()
     th = tables_handle(spec, None)
 
     def validate_large(*a):
         return L.skg_validate_large(th, *a)
-    rc, text, errs = _large_call(validate_large, batch, i, nbytes, cap=1 << 20)
+    rc, text, errs = _large_call(validate_large, batch, i, nbytes, cap=1 << 20, pool=pool, stage=stage)
     if rc == 2:
         return None
     if rc == 0:

@@ -177,6 +177,18 @@ __global__ void store_words_kernel(uint32_t* __restrict__ dst, const uint32_t* _
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   __threadfence_system();
 }
+// device -> mapped pinned host bytes by SM stores (skg_copy_to_host): 16-byte
+// loads and stores, a grid-stride loop over 16-byte blocks, the tail by bytes
+__global__ void __launch_bounds__(256) copy_to_host_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                           uint64_t n) {
+  const uint64_t nb = n >> 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += stride)
+    reinterpret_cast<uint4*>(dst)[k] = __ldcs(reinterpret_cast<const uint4*>(src) + k);
+  if (blockIdx.x == 0)
+    for (uint64_t i = (nb << 4) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
 }  // namespace skg
 
 extern "C" {
@@ -253,6 +265,21 @@ int skg_store_counters(void* host_dst, const void* dev_src, uint32_t n_words, vo
   }
   skg::store_words_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<uint32_t*>(dptr), static_cast<const uint32_t*>(dev_src), n_words);
+  return check(cudaGetLastError());
+}
+
+int skg_copy_to_host(void* host_dst, const void* dev_src, uint64_t n_bytes, uint32_t n_ctas, void* stream) {
+  if (!host_dst || !dev_src) return -1;
+  if (n_bytes == 0) return 0;
+  void* dptr = nullptr;
+  if ((reinterpret_cast<uintptr_t>(host_dst) | reinterpret_cast<uintptr_t>(dev_src)) & 15 ||
+      cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
+    cudaGetLastError();   // not mapped / not aligned: a plain async copy
+    return check(cudaMemcpyAsync(host_dst, dev_src, n_bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+  }
+  const uint32_t g = n_ctas ? n_ctas : 64;
+  skg::copy_to_host_kernel<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(dptr), static_cast<const uint8_t*>(dev_src), n_bytes);
   return check(cudaGetLastError());
 }
 

@@ -75,3 +75,8 @@ def test_config3_full_size(sk, n_fn, mut):
     got = sk.disassemble_module(m)
     want = fx["oracle_disasm_named" + mut]
     assert _digest(got) == (want["sha256"], want["bytes"])
+    del got
+    # the fused entry point: the text's host copy overlaps the validation kernels
+    t, v = sk.disassemble_validate_batch([m])[0]
+    assert _digest(t) == (want["sha256"], want["bytes"])
+    assert _digest(sk.diagnostics_text(v)) == (fx["ref_validate" + mut]["sha256"], fx["ref_validate" + mut]["bytes"])

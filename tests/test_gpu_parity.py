@@ -210,7 +210,12 @@ def test_huge_single_module_vs_oracle(sk, monkeypatch, path):
     opts = sk.DisassemblerOptions(inline_names=False)
     assert sk.disassemble_batch([m], opts)[0] == odis.disassemble(m, opts)
     d = sk.validate_batch([m])[0]
-    assert [(x.severity, x.code, x.location, x.message) for x in d] == [tuple(x) for x in oval.validate(m)]
+    want_v = [tuple(x) for x in oval.validate(m)]
+    assert [(x.severity, x.code, x.location, x.message) for x in d] == want_v
+    # the fused entry point (grid-wide: text copy overlapped with the validation kernels)
+    t, v = sk.disassemble_validate_batch([m])[0]
+    assert t == got
+    assert [(x.severity, x.code, x.location, x.message) for x in v] == want_v
 
 
 def test_single_module_routing_sizes(sk):
