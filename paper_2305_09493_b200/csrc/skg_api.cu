@@ -90,7 +90,7 @@ uint32_t sched_regions(uint32_t n) {
 }
 
 int launch_sched(const int64_t* len, uint32_t stride, uint32_t n, uint8_t* sched, cudaStream_t s,
-                 bool regions = false, uint32_t region_shift = 7) {
+                 bool regions = false, uint32_t shift = skg::SCHED_SHIFT) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(sched);
   uint32_t* cursor = hist + skg::SCHED_BUCKETS;
   uint32_t* perm = cursor + skg::SCHED_BUCKETS;
@@ -100,8 +100,7 @@ int launch_sched(const int64_t* len, uint32_t stride, uint32_t n, uint8_t* sched
   uint32_t blocks = (n + 4095) / 4096;
   if (blocks > (uint32_t)sm_count() * 2) blocks = (uint32_t)sm_count() * 2;
   if (blocks == 0) blocks = 1;
-  skg::SchedKey key{regions ? sched_regions(n) : 1u, n, skg::SCHED_SHIFT};
-  if (key.regions > 1) key.shift = region_shift;   // 64 classes of 2^shift bytes per region (16 regions)
+  const skg::SchedKey key{regions ? sched_regions(n) : 1u, n, shift};   // size classes of 2^shift units
   skg::sched_hist<<<blocks, 1024, 0, s>>>(len, stride, n, hist, key);
   skg::sched_scan<<<1, 1024, 0, s>>>(hist, cursor);
   skg::sched_scatter<<<blocks, 1024, 0, s>>>(len, stride, n, cursor, perm, key);
@@ -408,7 +407,7 @@ int skg_validate(const skg_tables* t, const uint8_t* data, const int64_t* mod_of
   a.smem_slab = 0;
   // size order only: region-major measured 53.3 -> 54.6 ms on the 1M-module batch here
   if (int e = check((cudaError_t)launch_sched(mod_len, 1, n_mod, ws + l.sched, s, env_int("SKG_VAL_REGIONS", 0) != 0,
-                                               (uint32_t)env_int("SKG_VAL_SHIFT", 7)))) return e;
+                                               (uint32_t)env_int("SKG_VAL_SHIFT", 6)))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + l.sched + skg::SCHED_PERM_OFF);
   const Geom g = val_geom(n_mod);
   a.group_warps = group_warps((int)g.warps, env_int("SKG_VAL_GROUP", (int)g.warps));
@@ -456,11 +455,13 @@ int skg_asm(const skg_tables* t, const uint8_t* text, const int64_t* mod_off, co
   a.mod_stride = mod_stride ? mod_stride : 1;
   a.out = out; a.out_cap = out_cap; a.out_span = out_span; a.status = status;
   a.counters = reinterpret_cast<uint32_t*>(ws);
-  // size order only: the texts already lie in the disassembler's processing order (region-
-  // major measured 159 -> 169 ms on the bench's 1M-module batch)
+  // Size order (text bytes), not region-major: the texts already lie in the disassembler's
+  // processing order (region-major measured 159 -> 169 ms on the bench's 1M-module batch).
+  // A work key of 4 x lines + tokens per text (counted by a SWAR kernel) balanced the CTAs'
+  // lines/tokens far better on paper (max/mean 1.41 -> 1.06) but measured 159 -> 161 ms.
   if (int e = check((cudaError_t)launch_sched(mod_len, a.mod_stride, n_mod, ws + 256, s,
                                                env_int("SKG_ASM_REGIONS", 0) != 0,
-                                               (uint32_t)env_int("SKG_ASM_SHIFT", 11)))) return e;
+                                               (uint32_t)env_int("SKG_ASM_SHIFT", 6)))) return e;
   a.order = reinterpret_cast<const uint32_t*>(ws + 256 + skg::SCHED_PERM_OFF);
   a.gscratch = ws + 256 + sched_bytes(n_mod);
   a.gslot_bytes = slot_bytes;
