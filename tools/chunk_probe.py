@@ -5,6 +5,7 @@ per-range launches (memory locality of the size-sorted order over GBs)?
 
 usage: python tools/chunk_probe.py [modules] [K,...]
 """
+import os
 import sys
 import time
 from pathlib import Path
@@ -30,13 +31,14 @@ def main():
         plans = []
         for a, c in zip(cuts[:-1], cuts[1:]):
             lens = b.lengths[a:c]
-            sub = _native.DeviceBatch(dev.data, dev.off[a:c], dev.len[a:c], int(lens.max()) // 4, int(lens.sum()))
+            mwf = float(os.environ.get("MAXW_FACTOR", "1"))   # experiments: scratch slot spacing
+            sub = _native.DeviceBatch(dev.data, dev.off[a:c], dev.len[a:c], int(int(lens.max()) // 4 * mwf),
+                                      int(lens.sum()))
             dp = _native.DisasmPlan(sub, opts)
             dp.fit()
             mt = int(dp.span[1::2].max().item())
             tb = _native.DeviceBatch(dp.text, dp.span[0::2], dp.span[1::2], (mt + 3) // 4, 0)
             tb.n = c - a
-            import os
             slot = int(os.environ.get("SLOT_KB", "0")) * 1024 or None
             ap = _native.AsmPlan(tb, out_cap=int(lens.sum()) + 64 * (c - a) + 4096, stride=2, slot_bytes=slot)
             ap.fit()
