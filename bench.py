@@ -174,6 +174,15 @@ def profile_traffic():
     return None
 
 
+def _issue_roofline(inst, ms):
+    if not inst or not ms:
+        return None
+    peak = 148 * 4 * 1.965e9
+    ach = inst / (ms / 1e3)
+    return {"warp_inst_per_launch": inst, "achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": peak,
+            "frac": ach / peak, "source": "profiles/traffic.json (ncu smsp__inst_executed.sum)"}
+
+
 # -- the GPU arm ---------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -322,6 +331,11 @@ def run_ours(args, rank, world, local_rank):
             "traffic": (traffic.get(dom) or {}).get("bytes_per_launch"),
             "frac_of_nominal_8TBs": achieved / 8000.0,
             "per_kernel": per_kernel,
+            # the bound these kernels actually sit against: instruction issue (warp instructions
+            # per launch from the ncu capture in profiles/, like traffic; the peak is 148 SMs x
+            # 4 schedulers x 1 warp instruction per cycle at 1965 MHz)
+            "issue": _issue_roofline((traffic.get(dom) or {}).get("warp_inst_per_launch"),
+                                     per_kernel[dom]["ms"]),
         },
         "e2e": {"value": total_words / e2e_s, "unit": "words/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -33,10 +33,20 @@ for k, name in (("disasm", "skg_disasm"), ("asm", "skg_asm")):
     rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
     traffic[name] = {"kernel": f"{k}_kernel", "bytes_per_launch": rd + wr, "dram_read_bytes": rd,
                      "dram_write_bytes": wr,
+                     "warp_inst_per_launch": int(float(d["smsp__inst_executed.sum"])),
+                     "ncu_ms": float(d["gpu__time_duration.sum"]) * {"ms": 1.0, "us": 1e-3, "ns": 1e-6,
+                                                                     "s": 1e3}[unit["gpu__time_duration.sum"]],
                      "source": f"profiles/{tag}_{k}_ncu_summary.txt (ncu --set full, 1M-module batch)"}
 (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 # the bench line was taken before this traffic.json existed: same figure bench.py reads from it
 bench = json.loads((PROF / f"{tag}_bench_roundtrip_1M.json").read_text())
 bench["roofline"]["traffic"] = traffic[bench["roofline"]["kernel"]]["bytes_per_launch"]
+t = traffic[bench["roofline"]["kernel"]]
+ms = bench["roofline"]["per_kernel"][bench["roofline"]["kernel"]]["ms"]
+peak_issue = 148 * 4 * 1.965e9
+bench["roofline"]["issue"] = {"warp_inst_per_launch": t["warp_inst_per_launch"],
+                              "achieved_warp_inst_per_s": t["warp_inst_per_launch"] / (ms / 1e3),
+                              "peak_warp_inst_per_s": peak_issue,
+                              "frac": t["warp_inst_per_launch"] / (ms / 1e3) / peak_issue}
 (PROF / f"{tag}_bench_roundtrip_1M.json").write_text(json.dumps(bench, indent=1) + "\n")
 print(json.dumps(traffic, indent=1))
