@@ -17,7 +17,7 @@ kernel; the dominant kernel is reported, both are listed), cpu_baseline (the
 reference's own CPU implementation, oracle/_ref, timed on this box's host cores
 on a bounded sample), e2e (host buffers through RoundTripSession: pinned H2D of
 the binaries + both kernels + D2H of the text and the binaries, pipelined over
-8 module chunks on three streams), gpu_launches,
+16 module chunks on three streams), gpu_launches,
 clocks.
 
 ``--impl reference`` times the reference's CPU implementation instead (rank 0
@@ -264,7 +264,7 @@ def run_ours(args, rank, world, local_rank):
     # e2e through the host-buffer public API: RoundTripSession.run on the batch in pinned
     # host memory -- no sizing pass (capacity-bounded arenas, per-chunk counters read
     # back before each D2H), H2D of the binaries and D2H of text + binaries timed
-    sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "12")))   # pipeline depth (experiments)
+    sess = RoundTripSession(chunks=int(os.environ.get("SKG_RT_CHUNKS", "16")))   # pipeline depth (experiments)
     h_batch = torch.from_numpy(batch.data).pin_memory()
     sess.run(h_batch, batch.offsets, batch.lengths)          # warm-up: buffer allocation
     e2e_steps = max(1, min(args.steps, 3))

@@ -137,9 +137,9 @@ class RoundTripSession:
     """
 
     TEXT_FACTOR = 6
-    TAPER = (0.25, 0.5, 0.75)   # relative sizes of the first / last chunks (short pipeline head / tail)
+    TAPER = (0.125, 0.25, 0.5, 0.75)   # relative sizes of the first / last chunks (short pipeline head / tail)
 
-    def __init__(self, options=None, spec=None, ext=None, chunks=12):
+    def __init__(self, options=None, spec=None, ext=None, chunks=16):
         from .disasm import DisassemblerOptions, option_bits
         self.opts = option_bits(options if options is not None else DisassemblerOptions())
         self.spec, self.ext = spec, ext
