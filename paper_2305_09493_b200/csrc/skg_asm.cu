@@ -428,19 +428,20 @@ __device__ __noinline__ uint32_t split_lines(AsmMod& m, const uint8_t* src, uint
   const uint32_t T = m.T;
   uint32_t nsep = 0, ccarry = 0, prev_last = 0;   // prev_last: byte before this chunk (0 = text start)
   const uint32_t nw = (T + 3) / 4;
-  const bool aligned = (reinterpret_cast<uintptr_t>(m.txt) & 3) == 0;
-  // aligned text: each iteration's word is loaded one iteration ahead (the scan's
-  // carries make the iterations dependent; the loads need not be)
+  // text word w (bytes 4w..4w+3; bytes past T are masked by `valid` below): aligned
+  // 32-bit loads, funnel-shifted together when the text does not start on a word
+  // (texts sit at arbitrary byte offsets of the disassembler's arena); only words
+  // holding text bytes are read.  Each iteration's word is loaded one iteration ahead
+  // (the scan's carries make the iterations dependent; the loads need not be).
+  const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(m.txt) & 3);
+  const uint32_t* A = reinterpret_cast<const uint32_t*>(m.txt - sh);
+  const uint32_t nA = (sh + T + 3) / 4;
   auto load_word = [&](uint32_t w) -> uint32_t {
-    uint32_t word = 0;
-    if (w < nw) {
-      if (aligned) {
-        word = __ldg(reinterpret_cast<const uint32_t*>(m.txt) + w);
-      } else {
-        for (uint32_t b = 0; b < 4 && 4 * w + b < T; ++b) word |= (uint32_t)m.txt[4 * w + b] << (8 * b);
-      }
-    }
-    return word;
+    if (w >= nw) return 0u;
+    const uint32_t lo = __ldg(A + w);
+    if (sh == 0) return lo;
+    const uint32_t hi = w + 1 < nA ? __ldg(A + w + 1) : 0u;
+    return __funnelshift_r(lo, hi, 8 * sh);
   };
   uint32_t next_word = load_word(lane);
   for (uint32_t base = 0; base < nw; base += 32) {
