@@ -892,6 +892,9 @@ __device__ __forceinline__ bool enc_one(EncCtx& c, uint32_t entry, uint32_t* st,
   const uint32_t t = enc_item(c, c.pos++);
   const Tok tk = tok_of(c, t);
   uint32_t kk = k;
+  // coerce(kind, token) sees the composite kind itself first: a string token there is
+  // reported under the composite's name (reference asm.py:293-295, ops.py:160-164)
+  if (tk.str && T.kcat(kk) == CAT_COMPOSITE) return enc_fail(c, E_STR_FOR, t, kk);
   // composite: value(bases[0], tok) then param(b) for the rest
   while (T.kcat(kk) == CAT_COMPOSITE) {
     const uint32_t nb = T.knbases(kk), bo = T.kbase_off(kk);

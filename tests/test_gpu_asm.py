@@ -259,3 +259,29 @@ def test_roundtrip_session_fresh_batches_and_regrowth(sk, monkeypatch):
             assert binv[bspan[i, 0]:bspan[i, 0] + bspan[i, 1]].tobytes() == m
             if i % 87 == 0:
                 assert text[tspan[i, 0]:tspan[i, 0] + tspan[i, 1]].tobytes().decode() == odis.disassemble(m)
+
+
+def test_composite_operand_string_literal(sk):
+    """A string token where a composite operand (PairIdRefIdRef of OpPhi) starts is
+    reported under the composite's kind; one in a later component under the
+    component's kind (reference asm.py:293-295 via ops.py:160-164).  Found by the
+    differential fuzz (tests/test_gpu_fuzz.py, seed 202)."""
+    from oracle import asm as oasm
+    from synth.families import build_module
+    texts = []
+    for fam in ("saxpy", "dft", "nbody"):
+        lines = sk.disassemble_module(build_module(fam, 7)).split("\n")
+        phi = next(i for i, ln in enumerate(lines) if " OpPhi " in ln)
+        for col in (4, 5, 6):          # first pair: first / second component; second pair: first
+            toks = lines[phi].split()
+            toks[col] = '"s"'
+            texts.append("\n".join(lines[:phi] + [" ".join(toks)] + lines[phi + 1:]))
+    got = sk.assemble_batch(texts)
+    for t, g in zip(texts, got):
+        try:
+            want = ("ok", oasm.assemble(t).hex())
+        except Exception as exc:  # noqa: BLE001
+            want = ("exc", type(exc).__name__, str(exc))
+        have = ("ok", g.hex()) if isinstance(g, bytes) else ("exc", type(g).__name__, str(g))
+        assert have == want
+    assert "PairIdRefIdRef operand" in str(got[0]) and "IdRef operand" in str(got[1])
