@@ -2,8 +2,9 @@
 
 Binary mutants (the mutation kinds of tools/make_golden.py: random words, word
 counts, opcodes, truncation, bit flips, header bounds) of the synthetic paper
-families go through disassemble_batch (default and numeric options),
-validate_batch and the fused disassemble_validate_batch; text mutants (the kinds
+families and of the reference-recorded golden modules go through
+disassemble_batch (default, numeric, no_indent, and highlight+group+no_header
+under strict), validate_batch and the fused disassemble_validate_batch; text mutants (the kinds
 of tests/test_gpu_asm.py) go through assemble_batch.  Every outcome -- text,
 words, diagnostics, exception class and message -- must equal the oracle's.
 
@@ -53,12 +54,24 @@ def _gpu(r):
     return ("ok", r)
 
 
-def _mutants(n, seed):
+def _seed_module(rng):
+    """a synthetic family module, or one of the reference-recorded golden modules (more
+    instruction kinds: switches, ext-inst sets, debug strings, decorations ...)"""
+    from golden_io import modules
     from synth.families import FAMILIES, build_module
+    if rng.random() < 0.5:
+        return build_module(rng.choice(FAMILIES), rng.randrange(1 << 20))
+    gold = modules()
+    return gold[rng.randrange(len(gold))]["bytes"]
+
+
+def _mutants(n, seed):
     rng = random.Random(seed)
     out = []
     while len(out) < n:
-        m = build_module(rng.choice(FAMILIES), rng.randrange(1 << 20))
+        m = _seed_module(rng)
+        if len(m) < 24 or len(m) % 4:
+            continue
         w = list(struct.unpack(f"<{len(m) // 4}I", m))
         for _ in range(rng.randrange(1, 3)):
             kind = rng.randrange(6)
@@ -79,12 +92,17 @@ def _mutants(n, seed):
     return out
 
 
+ALL_OPTS = {"highlight": True, "group": True, "no_header": True}
+
+
 def _oracle_binary(m):
     from oracle import disasm as odis, validate as oval
     from paper_2305_09493_b200.disasm import DisassemblerOptions
     return (_outcome(lambda: odis.disassemble(m)),
             _outcome(lambda: odis.disassemble(m, DisassemblerOptions(inline_names=False))),
-            _outcome(lambda: oval.validate(m)))
+            _outcome(lambda: oval.validate(m)),
+            _outcome(lambda: odis.disassemble(m, DisassemblerOptions(**ALL_OPTS), strict=True)),
+            _outcome(lambda: odis.disassemble(m, DisassemblerOptions(no_indent=True))))
 
 
 def _oracle_text(t):
@@ -105,6 +123,8 @@ def test_fuzz_binary_mutants(sk):
     got_n = sk.disassemble_batch(mods, sk.DisassemblerOptions(inline_names=False))
     got_v = sk.validate_batch(mods)
     fused = sk.disassemble_validate_batch(mods)
+    got_a = sk.disassemble_batch(mods, sk.DisassemblerOptions(**ALL_OPTS), strict=True)
+    got_i = sk.disassemble_batch(mods, sk.DisassemblerOptions(no_indent=True))
     bad = []
     for k, (m, w) in enumerate(zip(mods, want)):
         if _gpu(got_d[k]) != w[0]:
@@ -115,7 +135,11 @@ def test_fuzz_binary_mutants(sk):
             bad.append((k, "validate"))
         if _gpu(fused[k][0]) != w[0] or _gpu(fused[k][1]) != w[2]:
             bad.append((k, "fused"))
-    print(f"binary mutants: {len(mods)} modules x 4 outcomes, {len(bad)} mismatches")
+        if _gpu(got_a[k]) != w[3]:
+            bad.append((k, "highlight+group+no_header strict"))
+        if _gpu(got_i[k]) != w[4]:
+            bad.append((k, "no_indent"))
+    print(f"binary mutants: {len(mods)} modules x 6 outcomes, {len(bad)} mismatches")
     assert not bad, bad[:10]
 
 
@@ -125,12 +149,12 @@ def test_fuzz_text_mutants(sk):
     spec = importlib.util.spec_from_file_location("_asm_tests", Path(__file__).parent / "test_gpu_asm.py")
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    from synth.families import FAMILIES, build_module
     rng = random.Random(SEED + 1)
     texts = []
     while len(texts) < N_TXT:
-        t = sk.disassemble_module(build_module(rng.choice(FAMILIES), rng.randrange(1 << 20)),
-                                  sk.DisassemblerOptions(inline_names=rng.random() < 0.7))
+        t = sk.disassemble_batch([_seed_module(rng)], sk.DisassemblerOptions(inline_names=rng.random() < 0.7))[0]
+        if not isinstance(t, str) or not t:
+            continue
         for _ in range(rng.randrange(1, 4)):
             t = mod._mutate(t, rng)
         texts.append(t)
