@@ -165,3 +165,98 @@ def test_fuzz_text_mutants(sk):
            if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
     print(f"text mutants: {len(texts)} texts, {len(bad)} mismatches")
     assert not bad, bad[:10]
+
+
+_WORDS = ["Inline", "DontInline", "Kernel", "Float64", "Aligned", "None", "Volatile|Aligned", "OpNop", "OpLabel",
+          "CrossWorkgroup", "Function", "%", "%_", "%0", "%4294967295", "%name_0", "0x1p3", "1e400", "-0.0",
+          "inf", "-nan", "0x7fffffff", "-2147483648", "4294967295", "18446744073709551616", "0o17", "0b1_0",
+          "1__0", "00", "+1", "٣", "\"\"", "\"a\\\\b\"", "\"é\"", "=", ";", "OpExtInst", "sqrt", "exp", "12"]
+
+
+def _mutate_more(t, rng):
+    lines = t.split("\n")
+    k = rng.randrange(6)
+    i = rng.randrange(len(lines))
+    if k == 0:                                   # CRLF / other separators on some lines
+        sep = rng.choice(["\r\n", "\r", "\x0b", "\x0c", "\x1c", " ", "\x85"])
+        return "".join(ln + (sep if rng.random() < 0.2 else "\n") for ln in lines)
+    if k == 1:                                   # tabs / odd blanks as separators
+        lines[i] = lines[i].replace(" ", rng.choice(["\t", "  ", " \t "]))
+    elif k == 2:                                 # a token replaced by a grammar word / number form
+        toks = lines[i].split(" ")
+        toks[rng.randrange(len(toks))] = rng.choice(_WORDS)
+        lines[i] = " ".join(toks)
+    elif k == 3:                                 # a line duplicated
+        lines.insert(i, lines[i])
+    elif k == 4:                                 # trailing comment / blanks
+        lines[i] = lines[i] + rng.choice([" ; x", "\t", "   ", ";\"", " ;;"])
+    else:                                        # two tokens swapped
+        toks = lines[i].split(" ")
+        if len(toks) > 1:
+            a, b = rng.randrange(len(toks)), rng.randrange(len(toks))
+            toks[a], toks[b] = toks[b], toks[a]
+            lines[i] = " ".join(toks)
+    return "\n".join(lines)
+
+
+def test_fuzz_text_mutants_more(sk):
+    """text mutants with line separators other than LF, blanks, grammar words and number
+    forms in random operand positions, duplicated lines and swapped tokens"""
+    rng = random.Random(SEED + 2)
+    texts = []
+    while len(texts) < N_TXT:
+        t = sk.disassemble_batch([_seed_module(rng)], sk.DisassemblerOptions(inline_names=rng.random() < 0.7))[0]
+        if not isinstance(t, str) or not t:
+            continue
+        for _ in range(rng.randrange(1, 4)):
+            t = _mutate_more(t, rng)
+        texts.append(t)
+    with _pool() as ex:
+        want = list(ex.map(_oracle_text, texts, chunksize=8))
+    got = sk.assemble_batch(texts)
+    bad = [k for k, (g, w) in enumerate(zip(got, want))
+           if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
+    print(f"text mutants (separators, words, numbers): {len(texts)} texts, {len(bad)} mismatches")
+    assert not bad, bad[:10]
+
+
+def test_fuzz_grid_wide_single_modules(sk):
+    """binary mutants of mid-size modules (synth/huge.py) as single-module calls: the
+    grid-wide kernels (skg_disasm_large / skg_validate_large) against the oracle"""
+    from synth.huge import build_huge
+    rng = random.Random(SEED + 3)
+    n = max(8, N_TXT // 20)
+    mods = []
+    while len(mods) < n:
+        m = build_huge(rng.randrange(4, 12), chain=rng.randrange(150, 250), seed=rng.randrange(1 << 20),
+                       string_kib=(1,))
+        w = list(struct.unpack(f"<{len(m) // 4}I", m))
+        for _ in range(rng.randrange(0, 3)):
+            pos = rng.randrange(5, len(w))
+            kind = rng.randrange(4)
+            if kind == 0:
+                w[pos] = rng.getrandbits(32)
+            elif kind == 1:
+                w[pos] = (w[pos] & 0xFFFF) | (rng.randrange(0, 8) << 16)
+            elif kind == 2:
+                w = w[: rng.randrange(5, len(w) + 1)]
+            else:
+                w[pos] ^= 1 << rng.randrange(32)
+        mods.append(struct.pack(f"<{len(w)}I", *w))
+    with _pool() as ex:
+        want = list(ex.map(_oracle_binary, mods))
+    bad = []
+    for k, m in enumerate(mods):
+        if _gpu(sk.disassemble_batch([m])[0]) != want[k][0]:
+            bad.append((k, "disasm"))
+        if _gpu(sk.validate_batch([m])[0]) != want[k][2]:
+            bad.append((k, "validate"))
+        t, v = sk.disassemble_validate_batch([m])[0]
+        if _gpu(t) != want[k][0] or _gpu(v) != want[k][2]:
+            bad.append((k, "fused"))
+    from paper_2305_09493_b200 import _native
+    big = sum(len(m) // 4 >= _native.SINGLE_LARGE_WORDS for m in mods)
+    print(f"grid-wide single modules: {len(mods)} modules ({big} of {_native.SINGLE_LARGE_WORDS}+ words) "
+          f"x 3 outcomes, {len(bad)} mismatches")
+    assert 2 * big >= len(mods)     # most calls take the grid-wide kernels (truncations make some small)
+    assert not bad, bad[:10]
