@@ -260,3 +260,44 @@ def test_fuzz_grid_wide_single_modules(sk):
           f"x 3 outcomes, {len(bad)} mismatches")
     assert 2 * big >= len(mods)     # most calls take the grid-wide kernels (truncations make some small)
     assert not bad, bad[:10]
+
+
+def _oracle_binary_12(m):
+    from oracle import disasm as odis, validate as oval
+    from paper_2305_09493_b200 import grammar
+    spec = grammar.load_pinned("1.2")
+    return (_outcome(lambda: odis.disassemble(m, spec=spec)), _outcome(lambda: oval.validate(m, spec=spec)))
+
+
+def _oracle_text_12(t):
+    from oracle import asm as oasm
+    from paper_2305_09493_b200 import grammar
+    return _outcome(lambda: oasm.assemble(t, spec=grammar.load_pinned("1.2")).hex())
+
+
+def test_fuzz_pinned_12_grammar(sk):
+    """the same binary and text mutants under the pinned SPIR-V 1.2 grammar (empty
+    instruction classes, fewer opcodes / enumerants): disassembly, validation, assembly"""
+    spec = sk.load_pinned("1.2")
+    mods = _mutants(max(100, N_MOD // 4), SEED + 4)
+    with _pool() as ex:
+        want = list(ex.map(_oracle_binary_12, mods, chunksize=16))
+    got_d = sk.disassemble_batch(mods, spec=spec)
+    got_v = sk.validate_batch(mods, spec=spec)
+    bad = [(k, "disasm") for k in range(len(mods)) if _gpu(got_d[k]) != want[k][0]]
+    bad += [(k, "validate") for k in range(len(mods)) if _gpu(got_v[k]) != want[k][1]]
+    rng = random.Random(SEED + 5)
+    texts = []
+    while len(texts) < max(50, N_TXT // 4):
+        t = sk.disassemble_batch([_seed_module(rng)], spec=spec)[0]
+        if not isinstance(t, str) or not t:
+            continue
+        t = _mutate_more(t, rng) if rng.random() < 0.5 else t
+        texts.append(t)
+    with _pool() as ex:
+        want_t = list(ex.map(_oracle_text_12, texts, chunksize=8))
+    got_t = sk.assemble_batch(texts, spec=spec)
+    bad += [(k, "asm") for k, (g, w) in enumerate(zip(got_t, want_t))
+            if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
+    print(f"1.2 grammar: {len(mods)} binary mutants x 2, {len(texts)} texts, {len(bad)} mismatches")
+    assert not bad, bad[:10]
