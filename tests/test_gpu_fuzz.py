@@ -4,7 +4,8 @@ Binary mutants (the mutation kinds of tools/make_golden.py: random words, word
 counts, opcodes, truncation, bit flips, header bounds) of the synthetic paper
 families and of the reference-recorded golden modules go through
 disassemble_batch (default, numeric, no_indent, and highlight+group+no_header
-under strict), validate_batch and the fused disassemble_validate_batch; text mutants (the kinds
+under strict), validate_batch and the fused disassemble_validate_batch, also
+packed at unaligned offsets, some big-endian or not a whole number of words; text mutants (the kinds
 of tests/test_gpu_asm.py) go through assemble_batch.  Every outcome -- text,
 words, diagnostics, exception class and message -- must equal the oracle's.
 
@@ -88,7 +89,13 @@ def _mutants(n, seed):
                 w[pos] ^= 1 << rng.randrange(32)
             else:
                 w[3] = rng.randrange(0, 60)
-        out.append(struct.pack(f"<{len(w)}I", *w))
+        r = rng.random()
+        if r < 0.1:      # big-endian stream (the decoder reads all words byte-swapped)
+            out.append(struct.pack(f">{len(w)}I", *w))
+        elif r < 0.15:   # not a whole number of words
+            out.append(struct.pack(f"<{len(w)}I", *w) + bytes(rng.randrange(1, 4)))
+        else:
+            out.append(struct.pack(f"<{len(w)}I", *w))
     return out
 
 
@@ -124,6 +131,20 @@ def test_fuzz_binary_mutants(sk):
     got_v = sk.validate_batch(mods)
     fused = sk.disassemble_validate_batch(mods)
     got_a = sk.disassemble_batch(mods, sk.DisassemblerOptions(**ALL_OPTS), strict=True)
+    # the same modules packed back to back with 0-3 gap bytes: unaligned module offsets
+    import numpy as np
+    from paper_2305_09493_b200 import _native
+    rng = random.Random(SEED + 6)
+    offs, buf = [], bytearray()
+    for m in mods:
+        buf += bytes(rng.randrange(4))
+        offs.append(len(buf))
+        buf += m
+    packed = _native.DeviceBatch.from_host(np.frombuffer(bytes(buf + bytes(16)), dtype=np.uint8),
+                                           np.array(offs, dtype=np.int64),
+                                           np.array([len(m) for m in mods], dtype=np.int64))
+    got_u = sk.disassemble_batch(packed)
+    fused_u = sk.disassemble_validate_batch(packed)
     got_i = sk.disassemble_batch(mods, sk.DisassemblerOptions(no_indent=True))
     bad = []
     for k, (m, w) in enumerate(zip(mods, want)):
@@ -139,7 +160,9 @@ def test_fuzz_binary_mutants(sk):
             bad.append((k, "highlight+group+no_header strict"))
         if _gpu(got_i[k]) != w[4]:
             bad.append((k, "no_indent"))
-    print(f"binary mutants: {len(mods)} modules x 6 outcomes, {len(bad)} mismatches")
+        if _gpu(got_u[k]) != w[0] or _gpu(fused_u[k][0]) != w[0] or _gpu(fused_u[k][1]) != w[2]:
+            bad.append((k, "unaligned offsets"))
+    print(f"binary mutants: {len(mods)} modules x 9 outcomes, {len(bad)} mismatches")
     assert not bad, bad[:10]
 
 
