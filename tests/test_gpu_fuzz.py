@@ -324,3 +324,82 @@ def test_fuzz_pinned_12_grammar(sk):
             if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
     print(f"1.2 grammar: {len(mods)} binary mutants x 2, {len(texts)} texts, {len(bad)} mismatches")
     assert not bad, bad[:10]
+
+
+def _grammar_module(rng, spec):
+    """a module of random instructions drawn from the whole grammar, operands built from
+    each instruction's slot list (ids below a small bound, enumerants with their
+    parameters, literals, strings, context-dependent numbers), then mutated or not"""
+    insts = [d for d in spec.instructions if d.opcode < 0xFFFF]
+    words = []
+    for _ in range(rng.randrange(1, 12)):
+        d = rng.choice(insts)
+        ops = []
+
+        def value(kind_name, depth=0):
+            k = spec.kind(kind_name)
+            if k.category == "Id":
+                ops.append(rng.randrange(1, 40))
+            elif k.category in ("ValueEnum", "BitEnum") and k.enumerants:
+                if k.category == "BitEnum" and rng.random() < 0.5:
+                    es = [e for e in k.enumerants if e.value and rng.random() < 0.2]
+                    ops.append(sum({e.value for e in es}))
+                    for e in es:
+                        for p in e.parameters if depth < 2 else ():
+                            value(getattr(p, "kind", p), depth + 1)
+                else:
+                    e = rng.choice(k.enumerants)
+                    ops.append(e.value)
+                    for p in e.parameters if depth < 2 else ():
+                        value(getattr(p, "kind", p), depth + 1)
+            elif k.category == "Composite":
+                for b in k.bases or ():
+                    value(b, depth + 1)
+            elif k.kind == "LiteralString":
+                s = "".join(rng.choice(["a", "b", "_", " ", "\u00e9", "\\", '"']) for _ in range(rng.randrange(0, 9))).encode()
+                s += b"\0"
+                s += b"\0" * (-len(s) % 4)
+                ops.extend(struct.unpack(f"<{len(s) // 4}I", s))
+            else:
+                ops.append(rng.choice([0, 1, 7, 0xFFFFFFFF, 0x80000000, rng.getrandbits(32)]))
+                if k.kind == "LiteralContextDependentNumber" and rng.random() < 0.3:
+                    ops.append(rng.getrandbits(32))
+
+        for slot in d.operands:
+            q = getattr(slot, "quantifier", "")
+            reps = 1 if q not in ("?", "*") else (rng.randrange(0, 3) if q == "*" else rng.randrange(2))
+            for _ in range(reps):
+                value(slot.kind)
+        words += [((1 + len(ops)) << 16) | d.opcode, *ops]
+    w = [0x07230203, 0x00010200, 0, rng.choice([40, 20, 1 << 20]), 0] + words
+    return struct.pack(f"<{len(w)}I", *[x & 0xFFFFFFFF for x in w])
+
+
+def test_fuzz_grammar_random_instructions(sk):
+    """random instructions of every kind the grammar has (not only the ones the paper
+    families and the corpus use): disassembly (default, numeric, highlight+group
+    strict), validation; then their disassembly re-assembled"""
+    spec = sk.load_pinned()
+    rng = random.Random(SEED + 7)
+    mods = [_grammar_module(rng, spec) for _ in range(max(200, N_MOD // 2))]
+    with _pool() as ex:
+        want = list(ex.map(_oracle_binary, mods, chunksize=16))
+    got_d = sk.disassemble_batch(mods)
+    got_n = sk.disassemble_batch(mods, sk.DisassemblerOptions(inline_names=False))
+    got_v = sk.validate_batch(mods)
+    got_a = sk.disassemble_batch(mods, sk.DisassemblerOptions(**ALL_OPTS), strict=True)
+    bad = []
+    for k, w in enumerate(want):
+        for name, g, i in (("disasm", got_d, 0), ("numeric", got_n, 1), ("validate", got_v, 2), ("strict", got_a, 3)):
+            if _gpu(g[k]) != w[i]:
+                bad.append((k, name))
+    texts = [g for g in got_d if isinstance(g, str) and g]
+    with _pool() as ex:
+        want_t = list(ex.map(_oracle_text, texts, chunksize=8))
+    got_t = sk.assemble_batch(texts)
+    bad += [(k, "asm") for k, (g, w) in enumerate(zip(got_t, want_t))
+            if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
+    ok = sum(1 for w in want if w[0][0] == "ok")
+    print(f"grammar-random modules: {len(mods)} ({ok} disassemble) x 4 outcomes + {len(texts)} texts, "
+          f"{len(bad)} mismatches")
+    assert not bad, bad[:10]
