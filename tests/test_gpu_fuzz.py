@@ -326,6 +326,18 @@ def test_fuzz_pinned_12_grammar(sk):
     assert not bad, bad[:10]
 
 
+def mod_text_mutate(t, rng):
+    """tests/test_gpu_asm.py's text mutations"""
+    import importlib.util
+    from pathlib import Path
+    global _ASM_TESTS
+    if "_ASM_TESTS" not in globals():
+        spec = importlib.util.spec_from_file_location("_asm_tests", Path(__file__).parent / "test_gpu_asm.py")
+        _ASM_TESTS = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(_ASM_TESTS)
+    return _ASM_TESTS._mutate(t, rng)
+
+
 def _grammar_module(rng, spec):
     """a module of random instructions drawn from the whole grammar, operands built from
     each instruction's slot list (ids below a small bound, enumerants with their
@@ -399,7 +411,14 @@ def test_fuzz_grammar_random_instructions(sk):
     got_t = sk.assemble_batch(texts)
     bad += [(k, "asm") for k, (g, w) in enumerate(zip(got_t, want_t))
             if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
+    # the same texts mutated (assembler error paths over every opcode)
+    mut = [_mutate_more(t, rng) if rng.random() < 0.5 else mod_text_mutate(t, rng) for t in texts]
+    with _pool() as ex:
+        want_m = list(ex.map(_oracle_text, mut, chunksize=8))
+    got_m = sk.assemble_batch(mut)
+    bad += [(k, "asm mutated") for k, (g, w) in enumerate(zip(got_m, want_m))
+            if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
     ok = sum(1 for w in want if w[0][0] == "ok")
-    print(f"grammar-random modules: {len(mods)} ({ok} disassemble) x 4 outcomes + {len(texts)} texts, "
-          f"{len(bad)} mismatches")
+    print(f"grammar-random modules: {len(mods)} ({ok} disassemble) x 4 outcomes + {len(texts)} texts "
+          f"+ {len(mut)} mutated texts, {len(bad)} mismatches")
     assert not bad, bad[:10]
