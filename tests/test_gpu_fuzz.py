@@ -285,26 +285,47 @@ def test_fuzz_grid_wide_single_modules(sk):
     assert not bad, bad[:10]
 
 
-def _oracle_binary_12(m):
+_SPECS = {}
+
+
+def _spec_named(which):
+    """the pinned 1.2 grammar, or the custom GrammarSpec of tests/golden/grammars.json.gz
+    (an opcode removed, one renamed, a capability dependency and a mask enumerant added)"""
+    if which not in _SPECS:
+        import gzip
+        import json
+        from pathlib import Path
+        from paper_2305_09493_b200 import grammar
+        if which == "1.2":
+            _SPECS[which] = grammar.load_pinned("1.2")
+        else:
+            with gzip.open(Path(__file__).parent / "golden" / "grammars.json.gz", "rt", encoding="utf-8") as fh:
+                _SPECS[which] = grammar.load_core_grammar(json.load(fh)["custom_grammar"])
+    return _SPECS[which]
+
+
+def _oracle_binary_spec(arg):
+    which, m = arg
     from oracle import disasm as odis, validate as oval
-    from paper_2305_09493_b200 import grammar
-    spec = grammar.load_pinned("1.2")
+    spec = _spec_named(which)
     return (_outcome(lambda: odis.disassemble(m, spec=spec)), _outcome(lambda: oval.validate(m, spec=spec)))
 
 
-def _oracle_text_12(t):
+def _oracle_text_spec(arg):
+    which, t = arg
     from oracle import asm as oasm
-    from paper_2305_09493_b200 import grammar
-    return _outcome(lambda: oasm.assemble(t, spec=grammar.load_pinned("1.2")).hex())
+    return _outcome(lambda: oasm.assemble(t, spec=_spec_named(which)).hex())
 
 
-def test_fuzz_pinned_12_grammar(sk):
+@pytest.mark.parametrize("which", ["1.2", "custom"])
+def test_fuzz_other_grammars(sk, which):
     """the same binary and text mutants under the pinned SPIR-V 1.2 grammar (empty
-    instruction classes, fewer opcodes / enumerants): disassembly, validation, assembly"""
-    spec = sk.load_pinned("1.2")
+    instruction classes, fewer opcodes / enumerants) and a custom GrammarSpec:
+    disassembly, validation, assembly"""
+    spec = _spec_named(which)
     mods = _mutants(max(100, N_MOD // 4), SEED + 4)
     with _pool() as ex:
-        want = list(ex.map(_oracle_binary_12, mods, chunksize=16))
+        want = list(ex.map(_oracle_binary_spec, [(which, m) for m in mods], chunksize=16))
     got_d = sk.disassemble_batch(mods, spec=spec)
     got_v = sk.validate_batch(mods, spec=spec)
     bad = [(k, "disasm") for k in range(len(mods)) if _gpu(got_d[k]) != want[k][0]]
@@ -318,11 +339,11 @@ def test_fuzz_pinned_12_grammar(sk):
         t = _mutate_more(t, rng) if rng.random() < 0.5 else t
         texts.append(t)
     with _pool() as ex:
-        want_t = list(ex.map(_oracle_text_12, texts, chunksize=8))
+        want_t = list(ex.map(_oracle_text_spec, [(which, t) for t in texts], chunksize=8))
     got_t = sk.assemble_batch(texts, spec=spec)
     bad += [(k, "asm") for k, (g, w) in enumerate(zip(got_t, want_t))
             if (_gpu(g.hex()) if isinstance(g, bytes) else _gpu(g)) != w]
-    print(f"1.2 grammar: {len(mods)} binary mutants x 2, {len(texts)} texts, {len(bad)} mismatches")
+    print(f"{which} grammar: {len(mods)} binary mutants x 2, {len(texts)} texts, {len(bad)} mismatches")
     assert not bad, bad[:10]
 
 
